@@ -1,0 +1,150 @@
+/*
+ * ttg.h — C ABI of the B200-native TT-ICE / TT-ICE* per-increment update.
+ *
+ * This is the drop-in boundary.  Plain pointers and sizes
+ * only; no C++ or torch types cross it and no exception crosses it.  The C++
+ * host mirror of the reference API (include/ttstream/*.hpp) and the Python
+ * ctypes mirror (paper_2211_12487_b200/ttstream.py) both sit on top of it.
+ *
+ * Entry point  -> reference interface it replaces (reference = /root/reference/proj)
+ *   ttg_bootstrap                     -> tt_ice_bootstrap          include/ttstream/tt_ice.hpp:48-49
+ *                                        (tt_svd                   include/ttstream/tt_svd.hpp:13)
+ *   ttg_tt_ice_update                 -> tt_ice_update             include/ttstream/tt_ice.hpp:38-39
+ *   ttg_tt_ice_update_with_tolerances -> tt_ice_update_with_tolerances tt_ice.hpp:43-45
+ *   ttg_tt_ice_star_update            -> tt_ice_star_update        include/ttstream/tt_ice_star.hpp:57-59
+ *   ttg_per_obs_errors                -> per_obs_errors            include/ttstream/tt_ice_star.hpp:24
+ *   ttg_project                       -> tt_project                include/ttstream/tensor_train.hpp:103
+ *   ttg_reconstruct                   -> tt_reconstruct            include/ttstream/tensor_train.hpp:96-98
+ *   ttg_tt_upload / ttg_tt_download_* -> TensorTrain ctor / accessors tensor_train.hpp:59-93
+ *   status codes                      -> exception classes         include/ttstream/errors.hpp:9-55
+ *
+ * Semantics that differ from the reference by design:
+ *   - a device train (ttg_tt) is updated IN PLACE; earlier observations'
+ *     coefficients are never rewritten (Thm 3.3 holds bit-for-bit);
+ *   - UpdateReport.seconds is wall time from CUDA events, not std::clock.
+ */
+#ifndef TTG_H_
+#define TTG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TTG_MAX_CORES 32
+
+/* Status codes map 1:1 onto ttstream::*Error (errors.hpp:9-55). */
+enum ttg_status {
+  TTG_OK = 0,
+  TTG_E_DIMENSION = 1, /* DimensionError */
+  TTG_E_NUMERIC = 2,   /* NumericError   */
+  TTG_E_STATE = 3,     /* StateError     */
+  TTG_E_FORMAT = 4,    /* FormatError    */
+  TTG_E_INDEX = 5,     /* IndexError     */
+  TTG_E_CONFIG = 6,    /* ConfigError    */
+  TTG_E_RESOURCE = 7,  /* ResourceError  */
+  TTG_E_CUDA = 8,      /* CUDA runtime failure (no reference analogue) */
+  TTG_E_NCCL = 9,      /* NCCL failure (no reference analogue) */
+  TTG_E_ARGUMENT = 10  /* null pointer / bad enum at the ABI */
+};
+
+/* Where a data pointer lives. */
+enum ttg_where { TTG_HOST = 0, TTG_DEVICE = 1 };
+
+/* SkipStatistic (tt_ice_star.hpp:9-12). */
+enum ttg_skip_statistic { TTG_SKIP_MEAN = 0, TTG_SKIP_FULL_BATCH = 1 };
+
+typedef struct ttg_ctx ttg_ctx;
+typedef struct ttg_tt ttg_tt;
+
+/* Mirrors UpdateReport (tt_ice.hpp:10-20) with fixed-size rank arrays. */
+typedef struct ttg_report {
+  int64_t increment_index;
+  int64_t obs_in_batch;
+  int64_t obs_used;
+  int32_t n_ranks; /* D+1 entries used in the arrays below */
+  int32_t tolerance_clamped;
+  int64_t ranks_before[TTG_MAX_CORES + 1];
+  int64_t ranks_after[TTG_MAX_CORES + 1];
+  double eps_target;
+  double batch_rel_error_estimate;
+  double seconds; /* wall time (CUDA events) */
+  int32_t guard_reorthogonalised; /* number of modes whose 1e-10 Gram guard fired */
+  int32_t modes_updated;          /* modes whose basis grew */
+} ttg_report;
+
+/* Mirrors HeuristicConfig (tt_ice_star.hpp:14-20). */
+typedef struct ttg_heuristics {
+  double occupancy_threshold; /* default 0.8 */
+  int32_t skip_enabled;       /* default 1 */
+  int32_t subselect_enabled;  /* default 1 */
+  int32_t skip_statistic;     /* ttg_skip_statistic, default TTG_SKIP_MEAN */
+  int32_t use_approx_tolerance; /* default 0 */
+} ttg_heuristics;
+
+void ttg_heuristics_default(ttg_heuristics* h);
+
+/* ---- context ------------------------------------------------------------ */
+/* One context per stream (single logical writer).  Calls on a
+ * context are serialised on its CUDA stream. */
+int ttg_ctx_create(int device, ttg_ctx** out);
+/* Multi-GPU: one context per rank, batch axis sharded; Grams and scalars are
+ * all-reduced, coefficient columns all-gathered over NCCL.  `nccl_id` is the
+ * 128-byte ncclUniqueId produced by ttg_nccl_unique_id on rank 0. */
+int ttg_nccl_unique_id(uint8_t out[128]);
+int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[128], ttg_ctx** out);
+void ttg_ctx_destroy(ttg_ctx* ctx);
+const char* ttg_last_error(const ttg_ctx* ctx);
+int ttg_ctx_rank(const ttg_ctx* ctx);
+int ttg_ctx_world(const ttg_ctx* ctx);
+/* cudaStream_t the context launches on (as void*), for event timing. */
+void* ttg_ctx_stream(const ttg_ctx* ctx);
+/* Number of ttg kernels launched by this context so far. */
+int64_t ttg_ctx_launch_count(const ttg_ctx* ctx);
+int ttg_ctx_synchronize(ttg_ctx* ctx);
+
+/* ---- device train ------------------------------------------------------- */
+/* Upload a host train: cores[i] is r_left[i]*n[i]*r_right[i] doubles,
+ * first-index-fastest (TTCore layout, tensor_train.hpp:12-31). */
+int ttg_tt_upload(ttg_ctx* ctx, int n_cores, const int64_t* r_left, const int64_t* n,
+                  const int64_t* r_right, const double* const* cores, int64_t ortho_count,
+                  const int64_t* bounds, int64_t n_bounds, ttg_tt** out);
+void ttg_tt_destroy(ttg_tt* tt);
+int ttg_tt_num_cores(const ttg_tt* tt);
+/* ranks: n_cores+1 entries; modes: n_cores entries (last = local obs count). */
+int ttg_tt_shape(const ttg_tt* tt, int64_t* ranks, int64_t* modes, int64_t* ortho_count,
+                 int64_t* n_bounds);
+int ttg_tt_bounds(const ttg_tt* tt, int64_t* bounds);
+/* Copies core i (compact r_left*n*r_right, first-index-fastest) to host. */
+int ttg_tt_download_core(ttg_ctx* ctx, const ttg_tt* tt, int i, double* out);
+
+/* ---- the hot path ------------------------------------------------------- */
+/* y: shape[0..ndim-1] (spatial modes + observation mode), first-index-fastest.
+ * where: TTG_HOST (copied H2D inside the call) or TTG_DEVICE. */
+int ttg_bootstrap(ttg_ctx* ctx, const double* y, int where, const int64_t* shape, int ndim,
+                  double eps_des, ttg_tt** out, ttg_report* report);
+int ttg_tt_ice_update(ttg_ctx* ctx, ttg_tt* tt, const double* y, int where,
+                      const int64_t* shape, int ndim, double eps_des, ttg_report* report);
+int ttg_tt_ice_update_with_tolerances(ttg_ctx* ctx, ttg_tt* tt, const double* y, int where,
+                                      const int64_t* shape, int ndim, const double* deltas,
+                                      int n_deltas, ttg_report* report);
+int ttg_tt_ice_star_update(ttg_ctx* ctx, ttg_tt* tt, const double* y, int where,
+                           const int64_t* shape, int ndim, double eps_des,
+                           const ttg_heuristics* cfg, ttg_report* report);
+/* errs: host array of shape[ndim-1] doubles. */
+int ttg_per_obs_errors(ttg_ctx* ctx, const ttg_tt* tt, const double* y, int where,
+                       const int64_t* shape, int ndim, double* errs);
+/* coeffs: host array r_d x n_obs (first-index-fastest). */
+int ttg_project(ttg_ctx* ctx, const ttg_tt* tt, const double* y, int where,
+                const int64_t* shape, int ndim, double* coeffs);
+/* out: (n_1..n_d, obs_end-obs_begin) dense reconstruction; where = host or device. */
+int ttg_reconstruct(ttg_ctx* ctx, const ttg_tt* tt, int64_t obs_begin, int64_t obs_end,
+                    double* out, int where);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TTG_H_ */

@@ -1,0 +1,1176 @@
+// ttg.cu — host orchestration of the TT-ICE / TT-ICE* per-increment sweep on
+// B200 (sm_100a) and the C ABI declared in include/ttg.h.
+//
+// The sweep restates the reference's Algorithm 1 / 2 loops
+//   tt_ice_update_with_tolerances  tt_ice.cpp:60-129
+//   tt_ice_star_update             tt_ice_star.cpp:171-303
+//   tt_svd (bootstrap)             tt_svd.cpp:9-66
+// as a sequence of device passes over the increment:
+//   norms      per-observation |y_o|^2 and |Y|^2            (k_sumsq_obs)
+//   gram       residual Gram of cur_i vs U_pad (DMMA)        (k_gram_resid + k_gram_reduce)
+//   eig        one-sided Jacobi, rank rule, sign rule        (k_jacobi_eig)
+//   append     [U_pad U_R] with the 1e-10 guard              (k_append)
+//   project    cur_{i+1} = reshape(U_new^T cur_i) (DMMA)     (k_project)
+// Multi-GPU: the batch (observation) axis is sharded; the a_i x a_i Grams and
+// a handful of scalars are all-reduced and the coefficient columns
+// all-gathered with NCCL; every rank then runs the same deterministic eigen
+// solve on identical bytes.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ttg.h"
+#include "ttg_eig.cuh"
+#include "ttg_kernels.cuh"
+#include "ttg_misc.cuh"
+
+namespace {
+
+struct TtgError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw TtgError{code, msg}; }
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      fail(e_ == cudaErrorMemoryAllocation ? TTG_E_RESOURCE : TTG_E_CUDA,                       \
+           std::string(#x) + ": " + cudaGetErrorString(e_));                                    \
+  } while (0)
+
+#define NK(x)                                                                                   \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) fail(TTG_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));   \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFree(p);
+      p = o.p;
+      cap = o.cap;
+      o.p = nullptr;
+      o.cap = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { if (p) cudaFree(p); }
+  // grow-only; keep=true preserves the old contents
+  void ensure(size_t bytes, bool keep = false, cudaStream_t s = nullptr) {
+    if (bytes <= cap) return;
+    size_t nc = std::max(bytes, cap + cap / 2);
+    void* np = nullptr;
+    CK(cudaMalloc(&np, nc));
+    if (keep && p) {
+      CK(cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    if (p) cudaFree(p);
+    p = np;
+    cap = nc;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct ttg_ctx {
+  int device = 0;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 148;
+  size_t smem_optin = 232448;
+  // workspaces (grow-only)
+  DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, Uf, Upad, scratch, eigres, on2, sumsq_part,
+      scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2];
+  ttg::EigResult* h_eig = nullptr;
+  double* h_scal = nullptr;
+  ttg::StarStats* h_stats = nullptr;
+};
+
+struct ttg_tt {
+  int d = 0;                       // spatial modes
+  std::vector<int64_t> modes;      // n_1..n_d
+  std::vector<int64_t> ranks;      // r_0..r_d (r_0 = 1)
+  std::vector<DevBuf> cores;       // compact (r_{i-1} n_i) x r_i
+  DevBuf last;                     // r_d x n_obs, ld = rc
+  int64_t rc = 0, oc = 0, n_obs = 0;
+  int64_t ortho_count = 0;
+  std::vector<int64_t> bounds;
+};
+
+namespace {
+
+using ttg::EigResult;
+
+void post_launch(ttg_ctx* c) {
+  ++c->launches;
+  CK(cudaGetLastError());
+}
+
+int grid_for(long long n, int threads, int max_blocks) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+void allreduce_sum(ttg_ctx* c, double* d, size_t n) {
+  if (c->world <= 1) return;
+  NK(ncclAllReduce(d, d, n, ncclDouble, ncclSum, c->comm, c->stream));
+}
+
+// ---- norms ---------------------------------------------------------------
+// per-observation |y_o|^2 -> c->on2 (b), total -> c->scal[0] (global)
+void obs_norms(ttg_ctx* c, const double* Y, long long S, int b) {
+  int nchunk = (int)std::max<long long>(1, std::min<long long>((S + 65535) / 65536,
+                                                                (long long)c->num_sms * 8 / std::max(1, b) + 1));
+  c->sumsq_part.ensure(sizeof(double) * (size_t)nchunk * b);
+  c->on2.ensure(sizeof(double) * b);
+  c->scal.ensure(sizeof(double) * 16);
+  dim3 grid(nchunk, b);
+  ttg::k_sumsq_obs<<<grid, 256, 0, c->stream>>>(Y, S, nchunk, c->sumsq_part.as<double>());
+  post_launch(c);
+  ttg::k_sumsq_finalize<<<1, 256, 0, c->stream>>>(c->sumsq_part.as<double>(), nchunk, b,
+                                                   c->on2.as<double>(), c->scal.as<double>());
+  post_launch(c);
+  allreduce_sum(c, c->scal.as<double>(), 1);
+}
+
+double read_scalar(ttg_ctx* c, const double* d) {
+  CK(cudaMemcpyAsync(c->h_scal, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return c->h_scal[0];
+}
+
+// ---- fragments -------------------------------------------------------------
+void make_frags(ttg_ctx* c, const double* U, int a, int r, int ld, bool need_ut, bool need_u) {
+  int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
+  size_t n1 = (size_t)(r8 / 8) * (a8 / 4) * 32, n2 = (size_t)(a8 / 8) * (r8 / 4) * 32;
+  c->UTf.ensure(sizeof(double) * std::max<size_t>(n1, 1));
+  c->Uf.ensure(sizeof(double) * std::max<size_t>(n2, 1));
+  ttg::k_make_frags<<<grid_for(n1 + n2, 256, 1024), 256, 0, c->stream>>>(
+      U, a, r, ld, a8, r8, need_ut ? c->UTf.as<double>() : nullptr, need_u ? c->Uf.as<double>() : nullptr);
+  post_launch(c);
+}
+
+// ---- generic GEMM (any size) ------------------------------------------------
+template <bool TA, bool TB>
+void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
+          long long m, long long n, long long k, double alpha, double beta) {
+  if (m == 0 || n == 0) return;
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
+  if (grid.y > 65535) fail(TTG_E_RESOURCE, "generic gemm: m too large");
+  ttg::k_gemm<TA, TB><<<grid, dim3(32, 32), 0, c->stream>>>(A, lda, B, ldb, C, ldc, m, n, k, alpha, beta);
+  post_launch(c);
+}
+
+constexpr int kFastMax = 128;  // a8 / r8 limit of the fused DMMA tiles
+
+// ---- residual Gram -----------------------------------------------------------
+// G (a x a) = sum over selected columns x of X (a x L): (x - U U^T x)(...)^T
+template <int WBR, int WBC>
+void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem) {
+  auto kern = ttg::k_gram_resid<WBR, WBC>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem));
+  if (occ < 1) fail(TTG_E_RESOURCE, "gram kernel does not fit on an SM");
+  long long want = (long long)c->num_sms * occ;
+  int gx = (int)std::min<long long>(want, std::max<long long>(1, args.n_tiles));
+  constexpr int SBD = 8 * 4 * WBR;
+  c->partials.ensure(sizeof(double) * (size_t)gx * SBD * SBD);
+  ttg::GramArgs a2 = args;
+  a2.partials = c->partials.as<double>();
+  kern<<<gx, ttg::kThreads, smem, c->stream>>>(a2);
+  post_launch(c);
+  int a = args.src.a;
+  long long n = (long long)a * a;
+  ttg::k_gram_reduce<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, SBD, a,
+                                                                      c->G.as<double>());
+  post_launch(c);
+}
+
+void gram(ttg_ctx* c, const double* X, int a, long long L, const double* U, int r_old, int ldu,
+          const uint8_t* sel, long long cpo) {
+  int a8 = ttg::round_up(a, 8);
+  int r8 = r_old > 0 ? ttg::round_up(r_old, 8) : 0;
+  c->G.ensure(sizeof(double) * (size_t)a * a);
+  if (a8 <= kFastMax && r8 <= kFastMax) {
+    if (r_old > 0) make_frags(c, U, a, r_old, ldu, true, true);
+    ttg::GramArgs args{};
+    args.src = ttg::TileSrc{X, a, L, sel, cpo};
+    args.a8 = a8;
+    args.ldt = ttg::smem_ld(a8);
+    args.ldp = ttg::smem_ld(std::max(r8, 8));
+    args.UTf = c->UTf.as<double>();
+    args.Uf = c->Uf.as<double>();
+    args.r8 = r8;
+    args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+    size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+    int nb = a8 / 8;
+    if (nb <= 4) launch_gram_t<1, 2>(c, args, smem);
+    else if (nb <= 8) launch_gram_t<2, 4>(c, args, smem);
+    else if (nb <= 12) launch_gram_t<3, 6>(c, args, smem);
+    else launch_gram_t<4, 8>(c, args, smem);
+  } else {
+    // generic: R = X - U (U^T X) materialised, masked, then G = R R^T
+    c->scratch.ensure(sizeof(double) * (size_t)a * L);
+    double* R = c->scratch.as<double>();
+    CK(cudaMemcpyAsync(R, X, sizeof(double) * (size_t)a * L, cudaMemcpyDeviceToDevice, c->stream));
+    if (r_old > 0) {
+      c->W.ensure(sizeof(double) * (size_t)r_old * L);
+      double* P = c->W.as<double>();
+      gemm<true, false>(c, U, ldu, X, a, P, r_old, r_old, L, a, 1.0, 0.0);
+      gemm<false, false>(c, U, ldu, P, r_old, R, a, a, L, r_old, -1.0, 1.0);
+    }
+    if (sel) {
+      ttg::k_mask_cols<<<grid_for((long long)a * L, 256, 4096), 256, 0, c->stream>>>(R, a, L, sel, cpo);
+      post_launch(c);
+    }
+    gemm<false, true>(c, R, a, R, a, c->G.as<double>(), a, a, a, L, 1.0, 0.0);
+  }
+  allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+}
+
+// ---- eigen-solve -------------------------------------------------------------
+EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double delta_mult) {
+  c->UR.ensure(sizeof(double) * (size_t)a * a);
+  c->lam.ensure(sizeof(double) * a);
+  c->eigres.ensure(sizeof(EigResult));
+  size_t need_smem = sizeof(double) * ((size_t)a * a + a) + sizeof(int) * a + 64;
+  ttg::EigArgs args{};
+  args.G = c->G.as<double>();
+  args.a = a;
+  args.kmax = kmax;
+  args.delta_src = delta_src;
+  args.delta_mult = delta_mult;
+  args.tol = 2.220446049250313e-16 * std::max(8, a);
+  args.max_sweeps = 60;
+  args.UR = c->UR.as<double>();
+  args.lam = c->lam.as<double>();
+  args.res = c->eigres.as<EigResult>();
+  size_t smem;
+  if (need_smem <= c->smem_optin) {
+    args.in_smem = 1;
+    args.Wg = nullptr;
+    smem = need_smem;
+  } else {
+    args.in_smem = 0;
+    c->W.ensure(sizeof(double) * (size_t)a * a);
+    args.Wg = c->W.as<double>();
+    smem = sizeof(double) * a + sizeof(int) * a + 64;
+  }
+  CK(cudaFuncSetAttribute(ttg::k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ttg::k_jacobi_eig<<<1, ttg::kEigThreads, smem, c->stream>>>(args);
+  post_launch(c);
+  CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  EigResult r = *c->h_eig;
+  if (!r.converged) fail(TTG_E_NUMERIC, "svd_trunc: Jacobi eigen-solve failed to converge on " +
+                                            std::to_string(a) + "x" + std::to_string(a) + " Gram");
+  return r;
+}
+
+// [U_pad U_R] -> out (a x (r_old + r_R)) with the 1e-10 guard; returns guard flag
+int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* out) {
+  c->scratch.ensure(sizeof(double) * ((size_t)a * r_R + (size_t)(r_old + 1) * (r_R + 1) + 16));
+  ttg::AppendArgs args{Upad, c->UR.as<double>(), a, r_old, r_R, out, c->scratch.as<double>(),
+                       c->eigres.as<EigResult>()};
+  ttg::k_append<<<1, 1024, 0, c->stream>>>(args);
+  post_launch(c);
+  CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return c->h_eig->guard;
+}
+
+// ---- projection --------------------------------------------------------------
+void project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out) {
+  int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
+  if (a8 > kFastMax || r8 > kFastMax) {
+    gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
+    return;
+  }
+  make_frags(c, W, a, r, ldw, true, false);
+  ttg::ProjArgs args{};
+  args.src = ttg::TileSrc{X, a, L, nullptr, 1};
+  args.a8 = a8;
+  args.ldt = ttg::smem_ld(a8);
+  args.WTf = c->UTf.as<double>();
+  args.r = r;
+  args.r8 = r8;
+  args.out = out;
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)r * ttg::kTC);
+  CK(cudaFuncSetAttribute(ttg::k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttg::k_project, ttg::kThreads, smem));
+  occ = std::max(occ, 1);
+  int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  ttg::k_project<<<gx, ttg::kThreads, smem, c->stream>>>(args);
+  post_launch(c);
+}
+
+// ---- helpers -----------------------------------------------------------------
+int64_t prod(const std::vector<int64_t>& v) {
+  int64_t p = 1;
+  for (auto x : v) p *= x;
+  return p;
+}
+
+const double* stage_input(ttg_ctx* c, const double* y, int where, size_t n) {
+  if (where == TTG_DEVICE) return y;
+  if (where != TTG_HOST) fail(TTG_E_ARGUMENT, "where must be TTG_HOST or TTG_DEVICE");
+  c->ystage.ensure(sizeof(double) * n);
+  CK(cudaMemcpyAsync(c->ystage.p, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  return c->ystage.as<double>();
+}
+
+void check_shape_args(const int64_t* shape, int ndim) {
+  if (!shape || ndim < 1) fail(TTG_E_ARGUMENT, "shape must be non-null with ndim >= 1");
+  for (int i = 0; i < ndim; ++i)
+    if (shape[i] < 1) fail(TTG_E_DIMENSION, "tensor extent must be >= 1");
+}
+
+// preconditions of tt_ice.cpp:16-30 / tt_project tensor_train.cpp:196-208
+void check_train_vs_y(const ttg_tt* tt, const int64_t* shape, int ndim, bool state_first) {
+  if (state_first && tt->ortho_count != tt->d)
+    fail(TTG_E_STATE, "incremental update requires a fully orthonormal train");
+  if (ndim != tt->d + 1) fail(TTG_E_DIMENSION, "increment must carry the spatial shape plus an observation mode");
+  for (int i = 0; i < tt->d; ++i)
+    if (shape[i] != tt->modes[i]) fail(TTG_E_DIMENSION, "increment spatial shape does not match the train");
+}
+
+// make sure the observation counts are equal on all ranks (sharded batch)
+int64_t global_obs(ttg_ctx* c, int64_t b) {
+  if (c->world <= 1) return b;
+  c->scal.ensure(sizeof(double) * 16);
+  double* d = c->scal.as<double>() + 8;
+  double h[2] = {(double)b, (double)b * (double)b};
+  CK(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  allreduce_sum(c, d, 2);
+  CK(cudaMemcpyAsync(c->h_scal, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  double s = c->h_scal[0], s2 = c->h_scal[1];
+  if (s * s != s2 * c->world) fail(TTG_E_DIMENSION, "multi-GPU update needs the same batch shard size on every rank");
+  return (int64_t)s;
+}
+
+// coefficients (r x b_local, compact) -> last core columns [n_obs, n_obs + b_global)
+void append_last_core(ttg_ctx* c, ttg_tt* tt, const double* coeffs, int r, int64_t b_local) {
+  int64_t bg = b_local * c->world;
+  const double* src = coeffs;
+  if (c->world > 1) {
+    c->coeffs_all.ensure(sizeof(double) * (size_t)r * bg);
+    NK(ncclAllGather(coeffs, c->coeffs_all.p, (size_t)r * b_local, ncclDouble, c->comm, c->stream));
+    src = c->coeffs_all.as<double>();
+  }
+  int64_t need_rc = std::max<int64_t>(r, 1), need_oc = tt->n_obs + bg;
+  if (need_rc > tt->rc || need_oc > tt->oc) {
+    int64_t nrc = std::max(need_rc, tt->rc), noc = std::max(need_oc, tt->oc);
+    if (need_rc > tt->rc) nrc = std::max<int64_t>(need_rc + 8, tt->rc * 3 / 2);
+    if (need_oc > tt->oc) noc = std::max<int64_t>(need_oc, tt->oc * 2);
+    DevBuf nb;
+    nb.ensure(sizeof(double) * (size_t)nrc * noc);
+    CK(cudaMemsetAsync(nb.p, 0, sizeof(double) * (size_t)nrc * noc, c->stream));
+    if (tt->n_obs > 0)
+      CK(cudaMemcpy2DAsync(nb.p, sizeof(double) * nrc, tt->last.p, sizeof(double) * tt->rc,
+                           sizeof(double) * tt->rc, tt->n_obs, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    tt->last = std::move(nb);
+    tt->rc = nrc;
+    tt->oc = noc;
+  }
+  CK(cudaMemcpy2DAsync(tt->last.as<double>() + tt->rc * tt->n_obs, sizeof(double) * tt->rc, src,
+                       sizeof(double) * r, sizeof(double) * r, bg, cudaMemcpyDeviceToDevice, c->stream));
+  tt->n_obs += bg;
+  tt->bounds.push_back(tt->n_obs);
+}
+
+void set_core(ttg_ctx* c, ttg_tt* tt, int i, const double* src, size_t n) {
+  tt->cores[i].ensure(sizeof(double) * std::max<size_t>(n, 1), false, c->stream);
+  if (src != tt->cores[i].p)
+    CK(cudaMemcpyAsync(tt->cores[i].p, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+void fill_report_ranks(int64_t* dst, const ttg_tt* tt) {
+  for (int i = 0; i <= tt->d; ++i) dst[i] = tt->ranks[i];
+  dst[tt->d + 1] = 1;
+}
+
+double sumsq_device(ttg_ctx* c, const double* x, long long n) {
+  // reuse the per-observation kernel with one "observation"
+  c->sumsq_part.ensure(sizeof(double) * 64);
+  c->scal.ensure(sizeof(double) * 16);
+  dim3 grid(1, 1);
+  ttg::k_sumsq_obs<<<grid, 256, 0, c->stream>>>(x, n, 1, c->sumsq_part.as<double>());
+  post_launch(c);
+  return read_scalar(c, c->sumsq_part.as<double>());
+}
+
+// ---- the TT-ICE / TT-ICE* sweep -----------------------------------------------
+struct SweepOpts {
+  bool star = false;
+  double tau = 0.8;
+  const uint8_t* sel = nullptr;   // TT-ICE*: selected observations (local)
+  int64_t n_sel_global = 0;       // TT-ICE*: |D|
+  bool bootstrap = false;
+  const double* delta_src = nullptr;  // delta = mult * sqrt(*src) (uniform) ...
+  double delta_mult = 0.0;
+  const double* deltas = nullptr;     // ... or per-mode absolute deltas (host)
+  double y_norm = 0.0;
+};
+
+struct SweepOut {
+  double discarded_sq = 0.0;
+  int guards = 0;
+  int modes_updated = 0;
+  bool cores_changed = false;
+  const double* coeffs = nullptr;  // r_d x b_local (compact)
+  int r_d = 0;
+};
+
+SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o) {
+  SweepOut out;
+  const int d = tt->d;
+  const int64_t S = prod(tt->modes);
+  const int64_t bg = b * c->world;
+  std::vector<int64_t> old_ranks = tt->ranks;
+  const double* cur = Y;
+  int flip = 0;
+  int64_t r_left_new = 1;
+  int64_t total = S * b;
+  // U_pad of mode 0 is core 0 itself (r_left = 1 never grows)
+  const double* Upad = tt->cores.empty() ? nullptr : tt->cores[0].as<double>();
+  int64_t r_old = o.bootstrap ? 0 : old_ranks[1];
+  for (int i = 0; i < d; ++i) {
+    const int64_t n_i = tt->modes[i];
+    const int64_t a = r_left_new * n_i;
+    const int64_t L = total / a;
+    const int64_t cpo = L / b;
+    if (a > 4096) fail(TTG_E_RESOURCE, "unfolding rows a_i = " + std::to_string(a) + " exceed the device solver limit");
+    double delta_i = 0.0;
+    const double* dsrc = nullptr;
+    double dmult = 0.0;
+    if (o.deltas) {
+      dmult = o.deltas[i];
+    } else {
+      dsrc = o.delta_src;
+      dmult = o.delta_mult;
+    }
+    int64_t r_R = 0;
+    bool run_svd = true;
+    if (o.star) {
+      double occ = (double)r_old / (double)a;  // tt_ice_star.cpp:246-248 (padded core)
+      run_svd = occ < o.tau;
+    } else if (!o.bootstrap && r_old == a) {
+      // The residual of a square orthogonal basis is identically zero; the
+      // reference's SVD of the rounding noise returns rank 0 whenever
+      // delta > 1e-12 |Y|.  Keep the full computation below that.
+      double dl = dsrc ? dmult * o.y_norm : dmult;
+      run_svd = !(dl > 1e-12 * o.y_norm);
+    }
+    int64_t kmax = 0;
+    if (run_svd) {
+      const uint8_t* sel = o.star ? o.sel : nullptr;
+      gram(c, cur, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo);
+      kmax = o.star ? o.n_sel_global * cpo : L * c->world;
+      EigResult er = eig(c, (int)a, kmax, dsrc, dmult);
+      r_R = er.rank;
+      out.discarded_sq += er.tail_sq;
+      delta_i = er.delta;
+    }
+    (void)delta_i;
+    int64_t r_new;
+    // new core i
+    if (o.bootstrap) {
+      if (r_R == 0) {  // tt_svd.cpp:42-47 unit-column placeholder
+        r_new = 1;
+        std::vector<double> e1((size_t)a, 0.0);
+        e1[0] = 1.0;
+        tt->cores[i].ensure(sizeof(double) * a);
+        CK(cudaMemcpyAsync(tt->cores[i].p, e1.data(), sizeof(double) * a, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+      } else {
+        r_new = r_R;
+        set_core(c, tt, i, c->UR.as<double>(), (size_t)a * r_new);
+      }
+      out.cores_changed = true;
+    } else if (r_R > 0) {
+      r_new = r_old + r_R;
+      const bool alias = (Upad == tt->cores[i].p);
+      tt->cores[i].ensure(sizeof(double) * (size_t)a * r_new, /*keep=*/alias, c->stream);
+      if (alias) Upad = tt->cores[i].as<double>();  // keep aliasing valid after growth
+      out.guards += append(c, Upad, (int)a, (int)r_old, (int)r_R, tt->cores[i].as<double>());
+      out.cores_changed = true;
+      out.modes_updated++;
+    } else {
+      r_new = r_old;
+      set_core(c, tt, i, Upad, (size_t)a * r_new);
+    }
+    // projection
+    const double* W = tt->cores[i].as<double>();
+    double* dst;
+    int64_t next_total = r_new * L;
+    if (i + 1 < d) {
+      c->cur[flip].ensure(sizeof(double) * (size_t)std::max<int64_t>(next_total, 1));
+      dst = c->cur[flip].as<double>();
+    } else {
+      c->coeffs.ensure(sizeof(double) * (size_t)std::max<int64_t>(next_total, 1));
+      dst = c->coeffs.as<double>();
+    }
+    if (o.bootstrap && r_R == 0) {
+      CK(cudaMemsetAsync(dst, 0, sizeof(double) * next_total, c->stream));
+    } else {
+      project(c, cur, (int)a, L, W, (int)r_new, (int)a, dst);
+    }
+    if (i + 1 < d) {
+      // pad the next core (Eq. 3.4) unless the left rank is unchanged
+      const int64_t n_next = tt->modes[i + 1];
+      int64_t rl_old = o.bootstrap ? 1 : old_ranks[i + 1];
+      int64_t rr_old = o.bootstrap ? 0 : old_ranks[i + 2];
+      if (o.bootstrap) {
+        Upad = nullptr;
+        r_old = 0;
+      } else if (r_new != rl_old) {
+        int64_t tot = r_new * n_next * rr_old;
+        c->Upad.ensure(sizeof(double) * (size_t)std::max<int64_t>(tot, 1));
+        ttg::k_pad_core<<<grid_for(tot, 256, 1024), 256, 0, c->stream>>>(
+            tt->cores[i + 1].as<double>(), (int)rl_old, (int)n_next, (int)rr_old, (int)r_new, c->Upad.as<double>());
+        post_launch(c);
+        Upad = c->Upad.as<double>();
+        r_old = rr_old;
+      } else {
+        Upad = tt->cores[i + 1].as<double>();
+        r_old = rr_old;
+      }
+      cur = dst;
+      flip ^= 1;
+    }
+    total = next_total;
+    tt->ranks[i + 1] = r_new;
+    r_left_new = r_new;
+  }
+  out.coeffs = c->coeffs.as<double>();
+  out.r_d = (int)r_left_new;
+  return out;
+}
+
+// projection of Y through the train's current cores -> c->coeffs (r_d x b)
+void project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b) {
+  const int d = tt->d;
+  int64_t total = prod(tt->modes) * b;
+  const double* cur = Y;
+  int flip = 0;
+  for (int i = 0; i < d; ++i) {
+    int64_t a = tt->ranks[i] * tt->modes[i];
+    int64_t L = total / a;
+    int64_t r = tt->ranks[i + 1];
+    double* dst;
+    if (i + 1 < d) {
+      c->cur[flip].ensure(sizeof(double) * (size_t)(r * L));
+      dst = c->cur[flip].as<double>();
+    } else {
+      c->coeffs.ensure(sizeof(double) * (size_t)(r * L));
+      dst = c->coeffs.as<double>();
+    }
+    project(c, cur, (int)a, L, tt->cores[i].as<double>(), (int)r, (int)a, dst);
+    cur = dst;
+    flip ^= 1;
+    total = r * L;
+  }
+}
+
+// M = Phi^T Phi of the spatial chain -> returns device pointer (r_d x r_d)
+const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
+  int64_t rmax = 1;
+  for (auto r : tt->ranks) rmax = std::max(rmax, r);
+  int64_t nmax = 1;
+  for (auto n : tt->modes) nmax = std::max(nmax, n);
+  c->iface[0].ensure(sizeof(double) * rmax * rmax);
+  c->iface[1].ensure(sizeof(double) * rmax * rmax);
+  c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
+  double one = 1.0;
+  CK(cudaMemcpyAsync(c->iface[0].p, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int f = 0;
+  for (int i = 0; i < tt->d; ++i) {
+    int rl = (int)tt->ranks[i], n = (int)tt->modes[i], rr = (int)tt->ranks[i + 1];
+    long long t1 = (long long)rl * n * rr;
+    ttg::k_iface_step1<<<grid_for(t1, 256, 1024), 256, 0, c->stream>>>(c->iface[f].as<double>(),
+                                                                        tt->cores[i].as<double>(), rl, n, rr,
+                                                                        c->Mtmp.as<double>());
+    post_launch(c);
+    ttg::k_iface_step2<<<grid_for((long long)rr * rr, 128, 1024), 128, 0, c->stream>>>(
+        c->Mtmp.as<double>(), tt->cores[i].as<double>(), rl, n, rr, c->iface[f ^ 1].as<double>());
+    post_launch(c);
+    f ^= 1;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return c->iface[f].as<double>();
+}
+
+// per-observation statistics of TT-ICE* (norms already in c->on2)
+void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double eps) {
+  project_chain(c, tt, Y, b);
+  const double* M = interface_gram(c, tt);
+  int r = (int)tt->ranks[tt->d];
+  c->cn2.ensure(sizeof(double) * b);
+  c->cmc.ensure(sizeof(double) * b);
+  c->errs.ensure(sizeof(double) * b);
+  c->rn2.ensure(sizeof(double) * b);
+  c->stats.ensure(sizeof(ttg::StarStats));
+  ttg::k_coef_stats<<<grid_for(b, 128, 1024), 128, 0, c->stream>>>(c->coeffs.as<double>(), r, (int)b, M,
+                                                                   c->cn2.as<double>(), c->cmc.as<double>());
+  post_launch(c);
+  ttg::k_star_local<<<1, 32, 0, c->stream>>>(c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
+                                             (int)b, eps, c->errs.as<double>(), c->rn2.as<double>(),
+                                             c->stats.as<ttg::StarStats>());
+  post_launch(c);
+  allreduce_sum(c, c->stats.as<double>(), 9);
+}
+
+struct Timer {
+  ttg_ctx* c;
+  explicit Timer(ttg_ctx* cc) : c(cc) { CK(cudaEventRecord(c->ev0, c->stream)); }
+  double stop() {
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    return ms * 1e-3;
+  }
+};
+
+void check_finite_norm(double ysq) {
+  if (!std::isfinite(ysq)) fail(TTG_E_NUMERIC, "non-finite element rejected at tensor construction");
+}
+
+// ---- entry points (internal, throwing) ----------------------------------------
+
+void do_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t* shape, int ndim,
+               const double* deltas, int n_deltas, double eps_des, bool uniform, ttg_report* rep) {
+  if (!c || !tt || !y || !rep) fail(TTG_E_ARGUMENT, "null argument");
+  check_shape_args(shape, ndim);
+  if (uniform && !(eps_des > 0.0)) fail(TTG_E_NUMERIC, "eps_des must be positive");  // tt_ice.cpp:133-135
+  check_train_vs_y(tt, shape, ndim, true);
+  const int d = tt->d;
+  if (!uniform && n_deltas != d) fail(TTG_E_DIMENSION, "need one SVD tolerance per spatial dimension");
+  const int64_t b = shape[d];
+  const int64_t S = prod(tt->modes);
+  Timer tm(c);
+  const double* Y = stage_input(c, y, where, (size_t)(S * b));
+  int64_t bg = global_obs(c, b);
+  obs_norms(c, Y, S, (int)b);
+  double ysq = read_scalar(c, c->scal.as<double>());
+  check_finite_norm(ysq);
+  double y_norm = std::sqrt(ysq);
+  std::memset(rep, 0, sizeof(*rep));
+  rep->increment_index = (int64_t)tt->bounds.size();
+  rep->obs_in_batch = bg;
+  rep->obs_used = bg;
+  rep->n_ranks = d + 2;
+  fill_report_ranks(rep->ranks_before, tt);
+  SweepOpts o;
+  o.y_norm = y_norm;
+  if (uniform) {
+    o.delta_src = c->scal.as<double>();
+    o.delta_mult = eps_des / std::sqrt((double)d);  // tt_ice.cpp:137-138
+    rep->eps_target = eps_des * y_norm / std::sqrt((double)d);
+  } else {
+    for (int i = 0; i < d; ++i)
+      if (deltas[i] < 0.0) fail(TTG_E_NUMERIC, "svd_trunc: negative truncation threshold");
+    o.deltas = deltas;
+    rep->eps_target = d > 0 ? deltas[0] : 0.0;
+  }
+  SweepOut so = sweep(c, tt, Y, b, o);
+  append_last_core(c, tt, so.coeffs, so.r_d, b);
+  fill_report_ranks(rep->ranks_after, tt);
+  rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(so.discarded_sq) / y_norm;
+  rep->guard_reorthogonalised = so.guards;
+  rep->modes_updated = so.modes_updated;
+  rep->seconds = tm.stop();
+}
+
+void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t* shape, int ndim,
+                    double eps_des, const ttg_heuristics* cfgp, ttg_report* rep) {
+  if (!c || !tt || !y || !rep) fail(TTG_E_ARGUMENT, "null argument");
+  ttg_heuristics cfg;
+  ttg_heuristics_default(&cfg);
+  if (cfgp) cfg = *cfgp;
+  check_shape_args(shape, ndim);
+  if (!(eps_des > 0.0)) fail(TTG_E_NUMERIC, "eps_des must be positive");  // tt_ice_star.cpp:175-177
+  if (cfg.occupancy_threshold <= 0.0 || cfg.occupancy_threshold > 1.0)
+    fail(TTG_E_CONFIG, "occupancy threshold must lie in (0, 1]");       // :178-180
+  // per_obs_stats -> tt_project validates state and shape (tensor_train.cpp:196-208)
+  if (tt->ortho_count != tt->d) fail(TTG_E_STATE, "projection requires a fully orthonormal train");
+  check_train_vs_y(tt, shape, ndim, false);
+  const int d = tt->d;
+  const int64_t b = shape[d];
+  const int64_t S = prod(tt->modes);
+  Timer tm(c);
+  const double* Y = stage_input(c, y, where, (size_t)(S * b));
+  int64_t bg = global_obs(c, b);
+  obs_norms(c, Y, S, (int)b);
+  std::memset(rep, 0, sizeof(*rep));
+  rep->increment_index = (int64_t)tt->bounds.size();
+  rep->obs_in_batch = bg;
+  rep->n_ranks = d + 2;
+  fill_report_ranks(rep->ranks_before, tt);
+
+  star_stats(c, tt, Y, b, eps_des);
+  CK(cudaMemcpyAsync(c->h_stats, c->stats.p, sizeof(ttg::StarStats), cudaMemcpyDeviceToHost, c->stream));
+  double ysq = read_scalar(c, c->scal.as<double>());
+  check_finite_norm(ysq);
+  const double y_norm = std::sqrt(ysq);
+  const double* s = c->h_stats->sums;
+  // skip statistic (tt_ice_star.cpp:46-65)
+  double skip_stat;
+  if (cfg.skip_statistic == TTG_SKIP_MEAN) skip_stat = (s[1] == 0.0) ? 0.0 : s[0] / s[1];
+  else skip_stat = (s[3] == 0.0) ? 0.0 : std::sqrt(s[2] / s[3]);
+  int64_t n_sel = 0, n_rej = 0;
+  if (cfg.skip_enabled && skip_stat <= eps_des) {
+    n_sel = 0;
+  } else if (cfg.subselect_enabled) {
+    n_sel = (int64_t)s[6];
+    n_rej = (int64_t)s[7];
+  } else {
+    n_sel = bg;
+    n_rej = 0;
+  }
+  rep->obs_used = n_sel;
+  SweepOut so;
+  const double* coeffs = c->coeffs.as<double>();  // stats projection = projection through unchanged cores
+  int r_d = (int)tt->ranks[d];
+  if (n_sel > 0) {
+    double eps_upd = eps_des;
+    if (n_rej > 0) {
+      if (cfg.use_approx_tolerance) {  // Eq. 3.20, tt_ice_star.cpp:160-169
+        double mean_rej = s[8] / (double)n_rej;
+        eps_upd = (eps_des * (double)bg - mean_rej * (double)n_rej) / (double)n_sel;
+      } else {  // Eq. 3.19, tt_ice_star.cpp:121-158
+        double selected_sq = s[5];
+        if (selected_sq == 0.0) fail(TTG_E_NUMERIC, "selected observations carry no energy");
+        double budget = eps_des * y_norm;
+        double radicand = (budget * budget - s[4]) / selected_sq;
+        if (radicand < 0.0) {
+          radicand = 0.0;
+          rep->tolerance_clamped = 1;
+        }
+        eps_upd = std::sqrt(radicand);
+      }
+    }
+    double d_sq = cfg.subselect_enabled ? s[5] : s[3];
+    double delta = eps_upd / std::sqrt((double)d) * std::sqrt(d_sq);  // :235-236
+    rep->eps_target = delta;
+    c->sel.ensure((size_t)b);
+    ttg::k_star_mask<<<grid_for(b, 256, 64), 256, 0, c->stream>>>(c->errs.as<double>(), (int)b, eps_des,
+                                                                    cfg.subselect_enabled, c->sel.as<uint8_t>());
+    post_launch(c);
+    SweepOpts o;
+    o.star = true;
+    o.tau = cfg.occupancy_threshold;
+    o.sel = c->sel.as<uint8_t>();
+    o.n_sel_global = n_sel;
+    o.deltas = nullptr;
+    o.delta_src = nullptr;
+    o.delta_mult = delta;
+    o.y_norm = y_norm;
+    // the sweep mutates ranks/cores in place; TT-ICE* keeps the old cores when
+    // nothing grew (tt_ice_star.cpp:276-277), which in-place is the same bytes
+    so = sweep(c, tt, Y, b, o);
+    coeffs = so.coeffs;
+    r_d = so.r_d;
+    rep->guard_reorthogonalised = so.guards;
+    rep->modes_updated = so.modes_updated;
+  }
+  append_last_core(c, tt, coeffs, r_d, b);
+  fill_report_ranks(rep->ranks_after, tt);
+  // estimate: Pythagoras on the appended coefficients (tt_ice_star.cpp:297-300)
+  const double* csrc = c->world > 1 ? c->coeffs_all.as<double>() : coeffs;
+  double kept_sq = sumsq_device(c, csrc, (long long)r_d * bg);
+  double lost_sq = std::max(ysq - kept_sq, 0.0);
+  rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(lost_sq) / y_norm;
+  rep->seconds = tm.stop();
+}
+
+ttg_tt* do_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shape, int ndim, double eps,
+                     ttg_report* rep) {
+  if (!c || !y || !rep) fail(TTG_E_ARGUMENT, "null argument");
+  check_shape_args(shape, ndim);
+  if (eps < 0.0 || eps > 1.0) fail(TTG_E_NUMERIC, "tt_svd tolerance must lie in [0, 1]");  // tt_svd.cpp:10-12
+  if (ndim < 2) fail(TTG_E_DIMENSION, "bootstrap needs spatial modes plus an observation mode");
+  if (ndim - 1 > TTG_MAX_CORES - 1) fail(TTG_E_DIMENSION, "too many modes");
+  const int d = ndim - 1;
+  auto tt = new ttg_tt();
+  try {
+    tt->d = d;
+    tt->modes.assign(shape, shape + d);
+    tt->ranks.assign(d + 1, 1);
+    tt->cores.resize(d);
+    const int64_t b = shape[d];
+    const int64_t S = prod(tt->modes);
+    Timer tm(c);
+    const double* Y = stage_input(c, y, where, (size_t)(S * b));
+    int64_t bg = global_obs(c, b);
+    obs_norms(c, Y, S, (int)b);
+    double ysq = read_scalar(c, c->scal.as<double>());
+    check_finite_norm(ysq);
+    double y_norm = std::sqrt(ysq);
+    SweepOpts o;
+    o.bootstrap = true;
+    o.delta_src = c->scal.as<double>();
+    o.delta_mult = eps / std::sqrt((double)(ndim - 1));  // tt_svd.cpp:30
+    o.y_norm = y_norm;
+    SweepOut so = sweep(c, tt, Y, b, o);
+    append_last_core(c, tt, so.coeffs, so.r_d, b);
+    tt->ortho_count = d;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->increment_index = 0;
+    rep->obs_in_batch = bg;
+    rep->obs_used = bg;
+    rep->n_ranks = d + 2;
+    fill_report_ranks(rep->ranks_after, tt);
+    for (int i = 0; i <= d + 1; ++i) rep->ranks_before[i] = 1;
+    rep->eps_target = eps * y_norm / std::sqrt((double)(ndim - 1));
+    const double* src = c->world > 1 ? c->coeffs_all.as<double>() : so.coeffs;
+    double kept_sq = sumsq_device(c, src, (long long)so.r_d * bg);  // tt_norm (tensor_train.cpp:383-386)
+    double lost_sq = std::max(ysq - kept_sq, 0.0);
+    rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(lost_sq) / y_norm;
+    rep->seconds = tm.stop();
+  } catch (...) {
+    delete tt;
+    throw;
+  }
+  return tt;
+}
+
+int guard(ttg_ctx* c, auto&& fn) {
+  try {
+    fn();
+    return TTG_OK;
+  } catch (const TtgError& e) {
+    if (c) c->err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (c) c->err = "host allocation failed";
+    return TTG_E_RESOURCE;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return TTG_E_CUDA;
+  }
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+void ttg_heuristics_default(ttg_heuristics* h) {
+  if (!h) return;
+  h->occupancy_threshold = 0.8;
+  h->skip_enabled = 1;
+  h->subselect_enabled = 1;
+  h->skip_statistic = TTG_SKIP_MEAN;
+  h->use_approx_tolerance = 0;
+}
+
+static int ctx_init(ttg_ctx* c, int device) {
+  CK(cudaSetDevice(device));
+  c->device = device;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c->ev0));
+  CK(cudaEventCreate(&c->ev1));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  c->num_sms = prop.multiProcessorCount;
+  c->smem_optin = prop.sharedMemPerBlockOptin;
+  CK(cudaMallocHost((void**)&c->h_eig, sizeof(ttg::EigResult)));
+  CK(cudaMallocHost((void**)&c->h_scal, sizeof(double) * 16));
+  CK(cudaMallocHost((void**)&c->h_stats, sizeof(ttg::StarStats)));
+  return 0;
+}
+
+int ttg_ctx_create(int device, ttg_ctx** out) {
+  if (!out) return TTG_E_ARGUMENT;
+  auto c = new ttg_ctx();
+  int rc = guard(c, [&] { ctx_init(c, device); });
+  if (rc != TTG_OK) {
+    fprintf(stderr, "ttg_ctx_create: %s\n", c->err.c_str());
+    ttg_ctx_destroy(c);
+    *out = nullptr;
+    return rc;
+  }
+  *out = c;
+  return TTG_OK;
+}
+
+int ttg_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return TTG_E_ARGUMENT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return TTG_E_NCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+  return TTG_OK;
+}
+
+int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[128], ttg_ctx** out) {
+  if (!out || !nccl_id || world < 1 || rank < 0 || rank >= world) return TTG_E_ARGUMENT;
+  auto c = new ttg_ctx();
+  int rc = guard(c, [&] {
+    ctx_init(c, device);
+    c->rank = rank;
+    c->world = world;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, 128);
+    NK(ncclCommInitRank(&c->comm, world, id, rank));
+  });
+  if (rc != TTG_OK) {
+    fprintf(stderr, "ttg_ctx_create_dist: %s\n", c->err.c_str());
+    ttg_ctx_destroy(c);
+    *out = nullptr;
+    return rc;
+  }
+  *out = c;
+  return TTG_OK;
+}
+
+void ttg_ctx_destroy(ttg_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->h_eig) cudaFreeHost(c->h_eig);
+  if (c->h_scal) cudaFreeHost(c->h_scal);
+  if (c->h_stats) cudaFreeHost(c->h_stats);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  cudaStream_t s = c->stream;
+  delete c;  // frees workspaces
+  if (s) cudaStreamDestroy(s);
+}
+
+const char* ttg_last_error(const ttg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int ttg_ctx_rank(const ttg_ctx* c) { return c ? c->rank : -1; }
+int ttg_ctx_world(const ttg_ctx* c) { return c ? c->world : -1; }
+void* ttg_ctx_stream(const ttg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+int64_t ttg_ctx_launch_count(const ttg_ctx* c) { return c ? c->launches : -1; }
+int ttg_ctx_synchronize(ttg_ctx* c) {
+  return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int ttg_tt_upload(ttg_ctx* c, int n_cores, const int64_t* r_left, const int64_t* n, const int64_t* r_right,
+                  const double* const* cores, int64_t ortho_count, const int64_t* bounds, int64_t n_bounds,
+                  ttg_tt** out) {
+  if (!c || !out || !r_left || !n || !r_right || !cores) return TTG_E_ARGUMENT;
+  ttg_tt* tt = new ttg_tt();
+  int rc = guard(c, [&] {
+    // TensorTrain ctor validation (tensor_train.cpp:60-93)
+    if (n_cores < 2) fail(TTG_E_DIMENSION, "a streamed train needs spatial cores plus the observation core");
+    if (n_cores > TTG_MAX_CORES) fail(TTG_E_DIMENSION, "too many cores");
+    if (r_left[0] != 1 || r_right[n_cores - 1] != 1) fail(TTG_E_DIMENSION, "boundary ranks must be 1");
+    for (int i = 0; i < n_cores; ++i)
+      if (r_left[i] < 1 || n[i] < 1 || r_right[i] < 1) fail(TTG_E_DIMENSION, "core extents must be >= 1");
+    for (int i = 0; i + 1 < n_cores; ++i)
+      if (r_right[i] != r_left[i + 1]) fail(TTG_E_DIMENSION, "bond rank mismatch between cores");
+    if (ortho_count < 0 || ortho_count > n_cores - 1) fail(TTG_E_STATE, "ortho_count outside [0, D-1]");
+    const int d = n_cores - 1;
+    tt->d = d;
+    tt->modes.assign(n, n + d);
+    tt->ranks.resize(d + 1);
+    tt->ranks[0] = 1;
+    for (int i = 0; i < d; ++i) tt->ranks[i + 1] = r_right[i];
+    tt->cores.resize(d);
+    for (int i = 0; i < d; ++i) {
+      size_t cnt = (size_t)(r_left[i] * n[i] * r_right[i]);
+      tt->cores[i].ensure(sizeof(double) * cnt);
+      CK(cudaMemcpyAsync(tt->cores[i].p, cores[i], sizeof(double) * cnt, cudaMemcpyHostToDevice, c->stream));
+    }
+    int64_t nobs = n[d];
+    tt->rc = std::max<int64_t>(r_left[d] + 8, 16);
+    tt->oc = std::max<int64_t>(nobs * 2, 1024);
+    tt->last.ensure(sizeof(double) * (size_t)tt->rc * tt->oc);
+    CK(cudaMemsetAsync(tt->last.p, 0, sizeof(double) * (size_t)tt->rc * tt->oc, c->stream));
+    CK(cudaMemcpy2DAsync(tt->last.p, sizeof(double) * tt->rc, cores[d], sizeof(double) * r_left[d],
+                         sizeof(double) * r_left[d], nobs, cudaMemcpyHostToDevice, c->stream));
+    tt->n_obs = nobs;
+    tt->ortho_count = ortho_count;
+    if (n_bounds > 0 && bounds) tt->bounds.assign(bounds, bounds + n_bounds);
+    else tt->bounds.push_back(nobs);
+    int64_t prev = 0;
+    for (auto bnd : tt->bounds) {
+      if (bnd < prev) fail(TTG_E_DIMENSION, "batch boundaries must be nondecreasing");
+      prev = bnd;
+    }
+    if (tt->bounds.back() != nobs) fail(TTG_E_DIMENSION, "batch boundaries must end at the observation count");
+    CK(cudaStreamSynchronize(c->stream));
+  });
+  if (rc != TTG_OK) {
+    delete tt;
+    *out = nullptr;
+    return rc;
+  }
+  *out = tt;
+  return TTG_OK;
+}
+
+void ttg_tt_destroy(ttg_tt* tt) { delete tt; }
+int ttg_tt_num_cores(const ttg_tt* tt) { return tt ? tt->d + 1 : -1; }
+
+int ttg_tt_shape(const ttg_tt* tt, int64_t* ranks, int64_t* modes, int64_t* ortho_count, int64_t* n_bounds) {
+  if (!tt) return TTG_E_ARGUMENT;
+  if (ranks) {
+    for (int i = 0; i <= tt->d; ++i) ranks[i] = tt->ranks[i];
+    ranks[tt->d + 1] = 1;
+  }
+  if (modes) {
+    for (int i = 0; i < tt->d; ++i) modes[i] = tt->modes[i];
+    modes[tt->d] = tt->n_obs;
+  }
+  if (ortho_count) *ortho_count = tt->ortho_count;
+  if (n_bounds) *n_bounds = (int64_t)tt->bounds.size();
+  return TTG_OK;
+}
+
+int ttg_tt_bounds(const ttg_tt* tt, int64_t* bounds) {
+  if (!tt || !bounds) return TTG_E_ARGUMENT;
+  for (size_t i = 0; i < tt->bounds.size(); ++i) bounds[i] = tt->bounds[i];
+  return TTG_OK;
+}
+
+int ttg_tt_download_core(ttg_ctx* c, const ttg_tt* tt, int i, double* out) {
+  if (!c || !tt || !out) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    if (i < 0 || i > tt->d) fail(TTG_E_INDEX, "core index out of range");
+    if (i < tt->d) {
+      size_t cnt = (size_t)(tt->ranks[i] * tt->modes[i] * tt->ranks[i + 1]);
+      CK(cudaMemcpyAsync(out, tt->cores[i].p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->stream));
+    } else if (tt->n_obs > 0) {
+      int64_t r = tt->ranks[tt->d];
+      CK(cudaMemcpy2DAsync(out, sizeof(double) * r, tt->last.p, sizeof(double) * tt->rc, sizeof(double) * r,
+                           tt->n_obs, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ttg_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shape, int ndim, double eps_des,
+                  ttg_tt** out, ttg_report* report) {
+  if (!c || !out) return TTG_E_ARGUMENT;
+  *out = nullptr;
+  return guard(c, [&] { *out = do_bootstrap(c, y, where, shape, ndim, eps_des, report); });
+}
+
+int ttg_tt_ice_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t* shape, int ndim,
+                      double eps_des, ttg_report* report) {
+  if (!c) return TTG_E_ARGUMENT;
+  return guard(c, [&] { do_update(c, tt, y, where, shape, ndim, nullptr, 0, eps_des, true, report); });
+}
+
+int ttg_tt_ice_update_with_tolerances(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t* shape,
+                                      int ndim, const double* deltas, int n_deltas, ttg_report* report) {
+  if (!c || !deltas) return TTG_E_ARGUMENT;
+  return guard(c, [&] { do_update(c, tt, y, where, shape, ndim, deltas, n_deltas, 0.0, false, report); });
+}
+
+int ttg_tt_ice_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t* shape, int ndim,
+                           double eps_des, const ttg_heuristics* cfg, ttg_report* report) {
+  if (!c) return TTG_E_ARGUMENT;
+  return guard(c, [&] { do_star_update(c, tt, y, where, shape, ndim, eps_des, cfg, report); });
+}
+
+int ttg_per_obs_errors(ttg_ctx* c, const ttg_tt* tt, const double* y, int where, const int64_t* shape, int ndim,
+                       double* errs) {
+  if (!c || !tt || !y || !errs) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    check_shape_args(shape, ndim);
+    if (tt->ortho_count != tt->d) fail(TTG_E_STATE, "projection requires a fully orthonormal train");
+    check_train_vs_y(tt, shape, ndim, false);
+    const int64_t b = shape[tt->d];
+    const int64_t S = prod(tt->modes);
+    const double* Y = stage_input(c, y, where, (size_t)(S * b));
+    obs_norms(c, Y, S, (int)b);
+    star_stats(c, tt, Y, b, 0.0);
+    CK(cudaMemcpyAsync(errs, c->errs.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ttg_project(ttg_ctx* c, const ttg_tt* tt, const double* y, int where, const int64_t* shape, int ndim,
+                double* coeffs) {
+  if (!c || !tt || !y || !coeffs) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    check_shape_args(shape, ndim);
+    if (tt->ortho_count != tt->d) fail(TTG_E_STATE, "projection requires a fully orthonormal train");
+    check_train_vs_y(tt, shape, ndim, false);
+    const int64_t b = shape[tt->d];
+    const int64_t S = prod(tt->modes);
+    const double* Y = stage_input(c, y, where, (size_t)(S * b));
+    project_chain(c, tt, Y, b);
+    CK(cudaMemcpyAsync(coeffs, c->coeffs.p, sizeof(double) * b * tt->ranks[tt->d], cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ttg_reconstruct(ttg_ctx* c, const ttg_tt* tt, int64_t b0, int64_t e0, double* out, int where) {
+  if (!c || !tt || !out) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    if (b0 < 0 || e0 > tt->n_obs || b0 > e0) fail(TTG_E_INDEX, "observation range out of bounds");
+    if (where != TTG_HOST && where != TTG_DEVICE) fail(TTG_E_ARGUMENT, "bad where");
+    const int d = tt->d;
+    const int64_t m = e0 - b0;
+    const int64_t S = prod(tt->modes);
+    if (m == 0) return;
+    // spatial chain Phi (S x r_d), tensor_train.cpp:152-166
+    int64_t rows = tt->modes[0];
+    int64_t r = tt->ranks[1];
+    c->cur[0].ensure(sizeof(double) * (size_t)(rows * r));
+    CK(cudaMemcpyAsync(c->cur[0].p, tt->cores[0].p, sizeof(double) * rows * r, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    int f = 0;
+    for (int i = 1; i < d; ++i) {
+      int64_t n_i = tt->modes[i], rr = tt->ranks[i + 1];
+      c->cur[f ^ 1].ensure(sizeof(double) * (size_t)(rows * n_i * rr));
+      gemm<false, false>(c, c->cur[f].as<double>(), rows, tt->cores[i].as<double>(), r, c->cur[f ^ 1].as<double>(),
+                         rows, rows, n_i * rr, r, 1.0, 0.0);
+      rows *= n_i;
+      r = rr;
+      f ^= 1;
+    }
+    double* dst;
+    if (where == TTG_DEVICE) dst = out;
+    else {
+      c->cur[f ^ 1].ensure(sizeof(double) * (size_t)(S * m));
+      dst = c->cur[f ^ 1].as<double>();
+    }
+    gemm<false, false>(c, c->cur[f].as<double>(), S, tt->last.as<double>() + tt->rc * b0, tt->rc, dst, S, S, m, r,
+                       1.0, 0.0);
+    if (where == TTG_HOST)
+      CK(cudaMemcpyAsync(out, dst, sizeof(double) * S * m, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+// ttg_kernels.cuh — sm_100a kernels of the TT-ICE / TT-ICE* per-increment sweep.
+//
+// Every matrix is column-major ("first-index-fastest"), so an
+// unfolding  cur_i (a_i x L_i)  is the raw buffer: column q is a_i contiguous
+// doubles and the observation index is the slowest (observation o owns the
+// contiguous column range [o*cpo, (o+1)*cpo)).
+//
+// FP64 tensor-core math is DMMA (`mma.sync.aligned.m8n8k4 .f64`, SASS
+// DMMA.8x8x4): tcgen05 has no f64 kind.  Measured on this pool's B200:
+// DMMA 37.0 TF/s, DFMA 33.7 TF/s, cuBLAS DGEMM 35.5 TF/s (profiles/r01_box_probe.log).
+//
+// Fragment layouts of m8n8k4 (row.col), lane = 4*g + t:
+//   A (8x4):  A[g][t]          B (4x8): B[t][g]          C (8x8): C[g][2t], C[g][2t+1]
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ttg {
+
+constexpr int kTC = 64;        // columns of cur per smem tile
+constexpr int kThreads = 256;  // 8 warps; warp w owns tile columns [8w, 8w+8)
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int src_size = valid ? 8 : 0;  // 0 => zero-fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_size));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Leading dimension (in doubles) for an smem column-major tile with `rows`
+// rows: >= rows and == 4 (mod 16), which makes both m8n8k4 fragment patterns
+// (8 rows x 4 cols and 4 rows x 8 cols) hit every bank exactly twice.
+__host__ __device__ inline int smem_ld(int rows) {
+  int ld = rows;
+  int m = ((4 - ld) % 16 + 16) % 16;
+  return ld + m;
+}
+
+__host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// Tile loader: TC columns of X (a x L) starting at column q0 into smem T with
+// leading dimension ldt.  Rows a..a8 are pre-zeroed by the caller and never
+// touched.  Columns past L and columns of unselected observations are
+// zero-filled (cp.async src-size 0).
+// ---------------------------------------------------------------------------
+struct TileSrc {
+  const double* X;
+  int a;
+  long long L;
+  const uint8_t* sel;     // per-observation selection mask (nullable)
+  long long cols_per_obs;
+};
+
+__device__ __forceinline__ void load_tile_async(const TileSrc& s, long long q0, double* T, int ldt) {
+  const int n = s.a * kTC;
+  // incremental (row, col) walk avoids a division per element
+  int e = threadIdx.x;
+  int col = e / s.a;
+  int row = e - col * s.a;
+  const int step_c = kThreads / s.a;
+  const int step_r = kThreads - step_c * s.a;
+  const double* base = s.X + (long long)s.a * q0;
+  for (; e < n; e += kThreads) {
+    long long qc = q0 + col;
+    bool valid = qc < s.L;
+    if (valid && s.sel) valid = s.sel[qc / s.cols_per_obs] != 0;
+    cp_async8(&T[row + ldt * col], valid ? (const void*)(base + e) : (const void*)s.X, valid);
+    row += step_r;
+    col += step_c;
+    if (row >= s.a) {
+      row -= s.a;
+      ++col;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused residual + Gram:  for every selected column x of cur (a x L):
+//     r = x - U (U^T x);     G += r r^T
+// Fast path for a8 <= 128: one CTA accumulates the whole a8 x a8 Gram of a
+// grid-stride set of 64-column tiles in registers (DMMA) and writes it to its
+// own partial slot (deterministic fixed-order reduction follows).  Larger
+// unfoldings take the generic path (k_gemm).
+// U enters as pre-swizzled DMMA fragments (k_make_frags) read with coalesced
+// 256-byte loads.  WBR x WBC = 8x8 blocks per warp (warp grid 4 x 2).
+// ---------------------------------------------------------------------------
+struct GramArgs {
+  TileSrc src;
+  int a8;
+  int ldt, ldp;
+  const double* UTf;  // A-fragments of U^T: [r8/8][a8/4][32]
+  const double* Uf;   // A-fragments of U:   [a8/8][r8/4][32]
+  int r8;             // 0 => no residual (empty basis)
+  double* partials;   // [gridDim.x][SBD*SBD], SBD = 8*4*WBR >= a8
+  long long n_tiles;
+};
+
+template <int WBR, int WBC>
+__global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int SB = 4 * WBR;  // == 2*WBC blocks per super-tile side
+  constexpr int SBD = 8 * SB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ldt = p.ldt, ldp = p.ldp;
+  double* T0 = smem;
+  double* T1 = smem + ldt * kTC;
+  double* Pw = smem + 2 * ldt * kTC + warp * ldp * 8;
+
+  const int row_blk0 = (warp >> 1) * WBR;  // in 8-row blocks
+  const int col_blk0 = (warp & 1) * WBC;
+  const int nb = p.a8 >> 3;
+
+  // zero the whole tile area once: padded rows a..a8 stay zero forever
+  for (int i = threadIdx.x; i < 2 * ldt * kTC; i += kThreads) smem[i] = 0.0;
+  __syncthreads();
+
+  double acc[WBR][WBC][2];
+#pragma unroll
+  for (int i = 0; i < WBR; ++i)
+#pragma unroll
+    for (int j = 0; j < WBC; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KA = p.a8 >> 2, KR = p.r8 >> 2, MR = p.r8 >> 3;
+  long long tile = blockIdx.x;
+  if (tile < p.n_tiles) load_tile_async(p.src, tile * kTC, T0, ldt);
+  cp_async_commit();
+  int buf = 0;
+  for (; tile < p.n_tiles; tile += gridDim.x) {
+    double* T = buf ? T1 : T0;
+    double* Tn = buf ? T0 : T1;
+    long long nxt = tile + gridDim.x;
+    if (nxt < p.n_tiles) load_tile_async(p.src, nxt * kTC, Tn, ldt);
+    cp_async_commit();
+    cp_async_wait_1();
+    __syncthreads();
+
+    if (p.r8 > 0) {
+      const int c0 = warp * 8;
+      // P = U^T T_w   (r8 x 8)
+      for (int mb = 0; mb < MR; ++mb) {
+        double q0 = 0.0, q1 = 0.0;
+        const double* fa = p.UTf + ((long long)mb * KA) * 32 + lane;
+        for (int kb = 0; kb < KA; ++kb) {
+          double av = __ldg(fa + kb * 32);
+          double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+          dmma(q0, q1, av, bv);
+        }
+        Pw[(mb * 8 + g) + ldp * (2 * t)] = q0;
+        Pw[(mb * 8 + g) + ldp * (2 * t + 1)] = q1;
+      }
+      __syncwarp();
+      // T_w -= U P
+      for (int ib = 0; ib < nb; ++ib) {
+        double q0 = 0.0, q1 = 0.0;
+        const double* fa = p.Uf + ((long long)ib * KR) * 32 + lane;
+        for (int sb = 0; sb < KR; ++sb) {
+          double av = __ldg(fa + sb * 32);
+          double bv = Pw[(sb * 4 + t) + ldp * g];
+          dmma(q0, q1, av, bv);
+        }
+        T[(ib * 8 + g) + ldt * (c0 + 2 * t)] -= q0;
+        T[(ib * 8 + g) + ldt * (c0 + 2 * t + 1)] -= q1;
+      }
+      __syncthreads();
+    }
+
+    // G(super-tile) += T T^T over the tile's 64 columns
+#pragma unroll 4
+    for (int k0 = 0; k0 < kTC; k0 += 4) {
+      double af[WBR], bf[WBC];
+#pragma unroll
+      for (int i = 0; i < WBR; ++i) {
+        int rb = row_blk0 + i;
+        af[i] = (rb < nb) ? T[(rb * 8 + g) + ldt * (k0 + t)] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < WBC; ++j) {
+        int cb = col_blk0 + j;
+        bf[j] = (cb < nb) ? T[(cb * 8 + g) + ldt * (k0 + t)] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < WBR; ++i)
+#pragma unroll
+        for (int j = 0; j < WBC; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  cp_async_wait_0();
+
+  double* out = p.partials + (long long)blockIdx.x * SBD * SBD;
+#pragma unroll
+  for (int i = 0; i < WBR; ++i)
+#pragma unroll
+    for (int j = 0; j < WBC; ++j) {
+      int r = ((warp >> 1) * WBR + i) * 8 + g;
+      int c = ((warp & 1) * WBC + j) * 8 + 2 * t;
+      out[r + SBD * c] = acc[i][j][0];
+      out[r + SBD * (c + 1)] = acc[i][j][1];
+    }
+}
+
+// Fixed-order reduction of the per-CTA Gram partials into the full symmetric
+// a x a matrix G (column-major).
+__global__ void k_gram_reduce(const double* __restrict__ partials, int nx, int sbd, int a,
+                              double* __restrict__ G) {
+  long long n = (long long)a * a;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e % a), j = (int)(e / a);
+    const double* src = partials + i + (long long)sbd * j;
+    double s = 0.0;
+    for (int x = 0; x < nx; ++x) s += src[(long long)x * sbd * sbd];
+    G[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Projection  out (r x L) = W^T cur  with W (a x r) as DMMA fragments.  The
+// output is written compact (ld = r): exactly the next unfolding cur_{i+1}
+// (r*n_{i+1} x L/n_{i+1}) of the reference's reshape (tt_ice.cpp:100-104).
+// Optionally accumulates per-column squared norms of the output (coefficient
+// norms for TT-ICE*).
+// ---------------------------------------------------------------------------
+struct ProjArgs {
+  TileSrc src;
+  int a8, ldt;
+  const double* WTf;  // [r8/8][a8/4][32]
+  int r, r8;
+  double* out;
+  long long n_tiles;
+};
+
+__global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
+  extern __shared__ __align__(16) double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ldt = p.ldt;
+  double* T0 = smem;
+  double* T1 = smem + ldt * kTC;
+  double* O = smem + 2 * ldt * kTC;  // r x kTC staging (ld r)
+  for (int i = threadIdx.x; i < 2 * ldt * kTC; i += kThreads) smem[i] = 0.0;
+  __syncthreads();
+  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
+  long long tile = blockIdx.x;
+  if (tile < p.n_tiles) load_tile_async(p.src, tile * kTC, T0, ldt);
+  cp_async_commit();
+  int buf = 0;
+  for (; tile < p.n_tiles; tile += gridDim.x) {
+    double* T = buf ? T1 : T0;
+    double* Tn = buf ? T0 : T1;
+    long long nxt = tile + gridDim.x;
+    if (nxt < p.n_tiles) load_tile_async(p.src, nxt * kTC, Tn, ldt);
+    cp_async_commit();
+    cp_async_wait_1();
+    __syncthreads();
+    const int c0 = warp * 8;
+    for (int mb = 0; mb < MR; ++mb) {
+      double q0 = 0.0, q1 = 0.0;
+      const double* fa = p.WTf + ((long long)mb * KA) * 32 + lane;
+      for (int kb = 0; kb < KA; ++kb) {
+        double av = __ldg(fa + kb * 32);
+        double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+        dmma(q0, q1, av, bv);
+      }
+      int row = mb * 8 + g;
+      if (row < p.r) {
+        O[row + p.r * (c0 + 2 * t)] = q0;
+        O[row + p.r * (c0 + 2 * t + 1)] = q1;
+      }
+    }
+    __syncthreads();
+    long long q0c = tile * kTC;
+    long long ncols = p.src.L - q0c;
+    if (ncols > kTC) ncols = kTC;
+    long long nout = ncols * p.r;
+    double* dst = p.out + q0c * p.r;
+    for (long long e = threadIdx.x; e < nout; e += kThreads) dst[e] = O[e];
+    __syncthreads();
+    buf ^= 1;
+  }
+  cp_async_wait_0();
+}
+
+// ---------------------------------------------------------------------------
+// Generic path (any a): C = alpha op(A) op(B) + beta C, column-major, DFMA,
+// 32x32 smem tiles, one output per thread.  Fixed summation order, so results
+// are deterministic.  Used for unfoldings with a8 > 128 (and reconstruct).
+// grid = (ceil(n/32), ceil(m/32)), block = (32, 32).
+// ---------------------------------------------------------------------------
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(1024) k_gemm(const double* __restrict__ A, long long lda,
+                                               const double* __restrict__ B, long long ldb, double* C,
+                                               long long ldc, long long m, long long n, long long k,
+                                               double alpha, double beta) {
+  __shared__ double As[32][33];  // As[kk][i]
+  __shared__ double Bs[32][33];  // Bs[j][kk]
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long row0 = (long long)blockIdx.y * 32, col0 = (long long)blockIdx.x * 32;
+  double acc = 0.0;
+  for (long long k0 = 0; k0 < k; k0 += 32) {
+    if (!TA) {  // A[i + lda*kk]
+      long long i = row0 + tx, kk = k0 + ty;
+      As[ty][tx] = (i < m && kk < k) ? A[i + lda * kk] : 0.0;
+    } else {    // op(A)(i,kk) = A[kk + lda*i]
+      long long kk = k0 + tx, i = row0 + ty;
+      As[tx][ty] = (i < m && kk < k) ? A[kk + lda * i] : 0.0;
+    }
+    if (!TB) {  // B[kk + ldb*j]
+      long long kk = k0 + tx, j = col0 + ty;
+      Bs[ty][tx] = (kk < k && j < n) ? B[kk + ldb * j] : 0.0;
+    } else {    // op(B)(kk,j) = B[j + ldb*kk]
+      long long j = col0 + tx, kk = k0 + ty;
+      Bs[tx][ty] = (kk < k && j < n) ? B[j + ldb * kk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) acc = fma(As[kk][tx], Bs[ty][kk], acc);
+    __syncthreads();
+  }
+  long long i = row0 + tx, j = col0 + ty;
+  if (i < m && j < n) {
+    double v = alpha * acc;
+    if (beta != 0.0) v += beta * C[i + ldc * j];
+    C[i + ldc * j] = v;
+  }
+}
+
+// zero the columns of observations that are not selected
+__global__ void k_mask_cols(double* __restrict__ X, int a, long long L, const uint8_t* __restrict__ sel,
+                            long long cpo) {
+  long long n = (long long)a * L;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long q = e / a;
+    if (!sel[q / cpo]) X[e] = 0.0;
+  }
+}
+
+}  // namespace ttg

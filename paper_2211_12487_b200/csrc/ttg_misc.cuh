@@ -1,0 +1,182 @@
+// ttg_misc.cuh — small kernels of the sweep: fragment swizzle, norms,
+// core padding, TT-ICE* per-observation statistics and decisions, and the
+// expansion used by reconstruct.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ttg_eig.cuh"
+#include "ttg_kernels.cuh"
+
+namespace ttg {
+
+// U (a x r, ld) -> DMMA A-fragments of U^T ([r8/8][a8/4][32]) and of U
+// ([a8/8][r8/4][32]); zero outside the matrix.
+__global__ void k_make_frags(const double* __restrict__ U, int a, int r, int ld, int a8, int r8,
+                             double* __restrict__ UTf, double* __restrict__ Uf) {
+  const int KA = a8 / 4, KR = r8 / 4;
+  const long long n1 = (long long)(r8 / 8) * KA * 32;
+  const long long n2 = (long long)(a8 / 8) * KR * 32;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n1 + n2;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e < n1) {
+      if (!UTf) continue;
+      int lane = (int)(e & 31);
+      long long f = e >> 5;
+      int kb = (int)(f % KA), mb = (int)(f / KA);
+      int row = kb * 4 + (lane & 3), col = mb * 8 + (lane >> 2);  // A = U^T: A[m][k] = U[k][m]
+      UTf[e] = (row < a && col < r) ? U[row + (long long)ld * col] : 0.0;
+    } else {
+      if (!Uf) continue;
+      long long e2 = e - n1;
+      int lane = (int)(e2 & 31);
+      long long f = e2 >> 5;
+      int sb = (int)(f % KR), ib = (int)(f / KR);
+      int row = ib * 8 + (lane >> 2), col = sb * 4 + (lane & 3);
+      Uf[e2] = (row < a && col < r) ? U[row + (long long)ld * col] : 0.0;
+    }
+  }
+}
+
+// Per-observation partial sums of squares: block (chunk, obs).
+__global__ void k_sumsq_obs(const double* __restrict__ Y, long long S, int nchunk,
+                            double* __restrict__ part) {
+  __shared__ double red[33];
+  const int o = blockIdx.y, c = blockIdx.x;
+  long long cs = (S + nchunk - 1) / nchunk;
+  long long b = (long long)c * cs, e = b + cs;
+  if (e > S) e = S;
+  const double* y = Y + (long long)o * S;
+  double s = 0.0;
+  // 16-byte loads when aligned
+  if ((((uintptr_t)(y + b)) & 15) == 0) {
+    long long n2 = (e - b) / 2;
+    const double2* y2 = reinterpret_cast<const double2*>(y + b);
+    for (long long i = threadIdx.x; i < n2; i += blockDim.x) {
+      double2 v = y2[i];
+      s = fma(v.x, v.x, s);
+      s = fma(v.y, v.y, s);
+    }
+    for (long long i = b + 2 * n2 + threadIdx.x; i < e; i += blockDim.x) s = fma(y[i], y[i], s);
+  } else {
+    for (long long i = b + threadIdx.x; i < e; i += blockDim.x) s = fma(y[i], y[i], s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[(long long)o * nchunk + c] = s;
+}
+
+// on2[o] = sum of chunk partials (fixed order); out_total = sum_o on2[o].
+__global__ void k_sumsq_finalize(const double* __restrict__ part, int nchunk, int nobs,
+                                 double* __restrict__ on2, double* __restrict__ total) {
+  __shared__ double red[33];
+  double s = 0.0;
+  for (int o = threadIdx.x; o < nobs; o += blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < nchunk; ++c) v += part[(long long)o * nchunk + c];
+    on2[o] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int o = 0; o < nobs; ++o) s += on2[o];
+    *total = s;
+  }
+}
+
+// pad_core (tt_ice.cpp:43-58): core (r_old x n x r_right) -> (r_new x n x r_right)
+__global__ void k_pad_core(const double* __restrict__ core, int r_old, int n, int r_right, int r_new,
+                           double* __restrict__ out) {
+  long long tot = (long long)r_new * n * r_right;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    int p = (int)(e % r_new);
+    long long rest = e / r_new;  // j + n*q
+    out[e] = (p < r_old) ? core[p + (long long)r_old * rest] : 0.0;
+  }
+}
+
+// M_new = sum_j G_j^T M G_j  (G_j = core[:, j, :], r_l x r_r), two steps via scratch T.
+__global__ void k_iface_step1(const double* __restrict__ M, const double* __restrict__ core, int rl,
+                              int n, int rr, double* __restrict__ T) {
+  // T[p', j, q] = sum_p M[p', p] core[p, j, q]
+  long long tot = (long long)rl * n * rr;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    int pp = (int)(e % rl);
+    long long rest = e / rl;
+    double s = 0.0;
+    for (int p = 0; p < rl; ++p) s = fma(M[pp + (long long)rl * p], core[p + (long long)rl * rest], s);
+    T[e] = s;
+  }
+}
+__global__ void k_iface_step2(const double* __restrict__ T, const double* __restrict__ core, int rl,
+                              int n, int rr, double* __restrict__ Mn) {
+  // Mn[q, q'] = sum_{j, p'} core[p', j, q] T[p', j, q']
+  long long tot = (long long)rr * rr;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    int q = (int)(e % rr), q2 = (int)(e / rr);
+    double s = 0.0;
+    for (int j = 0; j < n; ++j)
+      for (int pp = 0; pp < rl; ++pp)
+        s = fma(core[pp + (long long)rl * (j + (long long)n * q)],
+                T[pp + (long long)rl * (j + (long long)n * q2)], s);
+    Mn[e] = s;
+  }
+}
+
+// cn2[o] = |c_o|^2, cmc[o] = c_o^T M c_o  (c: r x b, ld r)
+__global__ void k_coef_stats(const double* __restrict__ C, int r, int b, const double* __restrict__ M,
+                             double* __restrict__ cn2, double* __restrict__ cmc) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < b; o += gridDim.x * blockDim.x) {
+    const double* c = C + (long long)r * o;
+    double s = 0.0, m = 0.0;
+    for (int i = 0; i < r; ++i) {
+      s = fma(c[i], c[i], s);
+      double mi = 0.0;
+      for (int k = 0; k < r; ++k) mi = fma(M[i + (long long)r * k], c[k], mi);
+      m = fma(c[i], mi, m);
+    }
+    cn2[o] = s;
+    cmc[o] = m;
+  }
+}
+
+// TT-ICE* per-observation errors and the partial sums the decision needs
+// (tt_ice_star.cpp:22-65, 90-100, 121-158).  Single thread, observation order
+// = the reference's loop order.  sums[] layout:
+//  0 sum_err(on>0)  1 count(on>0)  2 sum_rn2  3 sum_on2  4 sum_rej_rn2(err<=eps)
+//  5 sum_sel_on2(err>eps)  6 n_sel  7 n_rej  8 sum_rej_err
+struct StarStats {
+  double sums[9];
+};
+__global__ void k_star_local(const double* __restrict__ on2, const double* __restrict__ cn2,
+                             const double* __restrict__ cmc, int b, double eps, double* __restrict__ errs,
+                             double* __restrict__ rn2_out, StarStats* st) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int o = 0; o < b; ++o) {
+    double on = sqrt(on2[o]);
+    // |y - Phi c|^2 = |y|^2 - 2|c|^2 + c^T (Phi^T Phi) c   (c = Phi^T y)
+    double rsq = on2[o] - 2.0 * cn2[o] + cmc[o];
+    if (rsq < 0.0) rsq = 0.0;
+    double rn = sqrt(rsq);
+    double err = (on == 0.0) ? 0.0 : rn / on;
+    errs[o] = err;
+    rn2_out[o] = rn * rn;
+    if (on > 0.0) { s[0] += err; s[1] += 1.0; }
+    s[2] += rn * rn;
+    s[3] += on * on;
+    if (err > eps) { s[5] += on2[o]; s[6] += 1.0; }
+    else { double r = err * on; s[4] += r * r; s[7] += 1.0; s[8] += err; }
+  }
+  for (int i = 0; i < 9; ++i) st->sums[i] = s[i];
+}
+
+// selection mask (err > eps, or all when subselect is off)
+__global__ void k_star_mask(const double* __restrict__ errs, int b, double eps, int subselect,
+                            uint8_t* __restrict__ sel) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < b; o += gridDim.x * blockDim.x)
+    sel[o] = subselect ? (errs[o] > eps ? 1 : 0) : 1;
+}
+
+}  // namespace ttg

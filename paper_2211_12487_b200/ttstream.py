@@ -1,0 +1,407 @@
+"""Python host mirror of the reference's public ingest/update/reconstruct API.
+
+Same names, argument meaning and error behaviour as /root/reference/proj:
+
+==============================  =============================================
+this module                     reference
+==============================  =============================================
+``tt_ice_bootstrap``            tt_ice.hpp:48-49  (tt_ice.cpp:143-165)
+``tt_ice_update``               tt_ice.hpp:38-39  (tt_ice.cpp:131-141)
+``tt_ice_update_with_tolerances`` tt_ice.hpp:43-45 (tt_ice.cpp:60-129)
+``tt_ice_star_update``          tt_ice_star.hpp:57-59 (tt_ice_star.cpp:171-303)
+``HeuristicConfig``             tt_ice_star.hpp:14-20
+``per_obs_errors``              tt_ice_star.hpp:24
+``tt_project``                  tensor_train.hpp:103
+``tt_reconstruct``              tensor_train.hpp:96-98
+``UpdateReport``                tt_ice.hpp:10-20
+``TensorTrain``                 tensor_train.hpp:51-93 (device-resident)
+==============================  =============================================
+
+Every call goes through the C ABI of ``libttg.so`` (include/ttg.h); there is
+no CPU path.  One deliberate difference: a device ``TensorTrain`` is updated
+IN PLACE (the reference returns a new train sharing buffers), and the update
+functions return that same object — earlier observations' coefficients are
+never rewritten, so Theorem 3.3 holds bit-for-bit.
+
+Increments ``y`` are either numpy arrays (host; copied H2D inside the call,
+first-index-fastest as the reference's DenseTensor) or torch CUDA tensors
+(device-resident).  A torch tensor must be float64 and either 1-D with an
+explicit ``shape=`` or N-D laid out first-index-fastest (``y.permute(*reversed
+dims)`` contiguous, e.g. ``torch.empty(shape[::-1]).permute(...)``).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from .errors import STATUS_TO_ERROR, Error
+
+TTG_HOST, TTG_DEVICE = 0, 1
+
+
+def _check(rc: int, ctx: Optional["Context"]) -> None:
+    if rc == 0:
+        return
+    msg = ""
+    if ctx is not None and ctx._h:
+        raw = _lib.load().ttg_last_error(ctx._h)
+        msg = raw.decode() if raw else ""
+    raise STATUS_TO_ERROR.get(rc, Error)(msg or f"ttg status {rc}")
+
+
+class Context:
+    """One context per stream and GPU (include/ttg.h ``ttg_ctx``)."""
+
+    def __init__(self, device: int = 0, *, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("multi-GPU context needs the 128-byte NCCL unique id")
+            rc = lib.ttg_ctx_create_dist(device, rank, world, nccl_id, ctypes.byref(h))
+        else:
+            rc = lib.ttg_ctx_create(device, ctypes.byref(h))
+        self._h = None
+        _check(rc, None)
+        self._h = h
+        self.device = device
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(_lib.load().ttg_nccl_unique_id(buf), None)
+        return buf.raw
+
+    @property
+    def rank(self) -> int:
+        return _lib.load().ttg_ctx_rank(self._h)
+
+    @property
+    def world(self) -> int:
+        return _lib.load().ttg_ctx_world(self._h)
+
+    @property
+    def stream_ptr(self) -> int:
+        return _lib.load().ttg_ctx_stream(self._h) or 0
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib.load().ttg_ctx_launch_count(self._h))
+
+    def synchronize(self) -> None:
+        _check(_lib.load().ttg_ctx_synchronize(self._h), self)
+
+    def close(self) -> None:
+        if self._h:
+            _lib.load().ttg_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_DEFAULT_CTX: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _DEFAULT_CTX
+    if _DEFAULT_CTX is None:
+        _DEFAULT_CTX = Context(0)
+    return _DEFAULT_CTX
+
+
+@dataclass
+class UpdateReport:
+    """tt_ice.hpp:10-20; ``seconds`` is wall time from CUDA events."""
+
+    increment_index: int = 0
+    obs_in_batch: int = 0
+    obs_used: int = 0
+    ranks_before: List[int] = field(default_factory=list)
+    ranks_after: List[int] = field(default_factory=list)
+    eps_target: float = 0.0
+    batch_rel_error_estimate: float = 0.0
+    seconds: float = 0.0
+    tolerance_clamped: bool = False
+    guard_reorthogonalised: int = 0
+    modes_updated: int = 0
+
+    @staticmethod
+    def _from(r: _lib.Report) -> "UpdateReport":
+        n = r.n_ranks
+        return UpdateReport(
+            increment_index=r.increment_index, obs_in_batch=r.obs_in_batch, obs_used=r.obs_used,
+            ranks_before=[int(r.ranks_before[i]) for i in range(n)],
+            ranks_after=[int(r.ranks_after[i]) for i in range(n)],
+            eps_target=r.eps_target, batch_rel_error_estimate=r.batch_rel_error_estimate,
+            seconds=r.seconds, tolerance_clamped=bool(r.tolerance_clamped),
+            guard_reorthogonalised=r.guard_reorthogonalised, modes_updated=r.modes_updated)
+
+
+@dataclass
+class HeuristicConfig:
+    """tt_ice_star.hpp:14-20 (``skip_statistic``: "mean" = kMean, "full" = kFullBatch)."""
+
+    occupancy_threshold: float = 0.8
+    skip_enabled: bool = True
+    subselect_enabled: bool = True
+    skip_statistic: str = "mean"
+    use_approx_tolerance: bool = False
+
+    def _to(self) -> _lib.Heuristics:
+        if self.skip_statistic not in ("mean", "full"):
+            raise ValueError("skip_statistic must be 'mean' or 'full'")
+        return _lib.Heuristics(float(self.occupancy_threshold), int(bool(self.skip_enabled)),
+                               int(bool(self.subselect_enabled)), 0 if self.skip_statistic == "mean" else 1,
+                               int(bool(self.use_approx_tolerance)))
+
+
+class _Input:
+    """Resolves y (numpy host array or torch CUDA tensor) to (pointer, where, shape)."""
+
+    def __init__(self, y, shape: Optional[Sequence[int]] = None):
+        self.keep = None
+        if isinstance(y, np.ndarray):
+            if y.dtype != np.float64:
+                raise TypeError("increments are float64 (SPEC.md:88)")
+            arr = np.asfortranarray(y)
+            self.keep = arr
+            self.shape = tuple(int(s) for s in (shape if shape is not None else arr.shape))
+            if int(np.prod(self.shape)) != arr.size:
+                raise ValueError("shape does not match the buffer")
+            self.ptr = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            self.where = TTG_HOST
+            return
+        # torch tensor (duck-typed so torch is not a hard dependency of the host mirror)
+        if not hasattr(y, "data_ptr") or not getattr(y, "is_cuda", False):
+            raise TypeError("y must be a numpy array or a CUDA torch tensor")
+        import torch
+
+        if y.dtype != torch.float64:
+            raise TypeError("increments are float64 (SPEC.md:88)")
+        if shape is not None:
+            if not y.is_contiguous():
+                raise ValueError("flat device buffer must be contiguous")
+            self.shape = tuple(int(s) for s in shape)
+            if int(np.prod(self.shape)) != y.numel():
+                raise ValueError("shape does not match the buffer")
+        else:
+            if not y.permute(*reversed(range(y.dim()))).is_contiguous():
+                raise ValueError("device tensor must be first-index-fastest (pass a flat tensor with shape=)")
+            self.shape = tuple(int(s) for s in y.shape)
+        self.keep = y
+        self.ptr = ctypes.cast(ctypes.c_void_p(y.data_ptr()), ctypes.POINTER(ctypes.c_double))
+        self.where = TTG_DEVICE
+
+    def shape_arr(self):
+        return (ctypes.c_int64 * len(self.shape))(*self.shape), len(self.shape)
+
+
+class TensorTrain:
+    """Device-resident accumulation (include/ttg.h ``ttg_tt``).
+
+    Accessors mirror tensor_train.hpp:51-93; ``core(i)`` downloads a compact
+    (r_left, n, r_right) copy (first-index-fastest) for inspection.
+    """
+
+    def __init__(self, handle: ctypes.c_void_p, ctx: Context):
+        self._h = handle
+        self.ctx = ctx
+
+    # -- construction from host data (TensorTrain ctor, tensor_train.cpp:60-93)
+    @staticmethod
+    def upload(cores: Sequence[np.ndarray], ortho_count: int, batch_boundaries: Sequence[int] = (),
+               ctx: Optional[Context] = None) -> "TensorTrain":
+        ctx = ctx or default_context()
+        n = len(cores)
+        rl = (ctypes.c_int64 * n)(*[c.shape[0] for c in cores])
+        nn = (ctypes.c_int64 * n)(*[c.shape[1] for c in cores])
+        rr = (ctypes.c_int64 * n)(*[c.shape[2] for c in cores])
+        keep = [np.asfortranarray(c, dtype=np.float64) for c in cores]
+        ptrs = (ctypes.POINTER(ctypes.c_double) * n)(*[k.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) for k in keep])
+        nb = len(batch_boundaries)
+        bnd = (ctypes.c_int64 * max(nb, 1))(*batch_boundaries) if nb else None
+        h = ctypes.c_void_p()
+        _check(_lib.load().ttg_tt_upload(ctx._h, n, rl, nn, rr, ptrs, int(ortho_count), bnd, nb, ctypes.byref(h)), ctx)
+        return TensorTrain(h, ctx)
+
+    def _shape(self):
+        nc = _lib.load().ttg_tt_num_cores(self._h)
+        ranks = (ctypes.c_int64 * (nc + 1))()
+        modes = (ctypes.c_int64 * nc)()
+        oc = ctypes.c_int64()
+        nb = ctypes.c_int64()
+        _check(_lib.load().ttg_tt_shape(self._h, ranks, modes, ctypes.byref(oc), ctypes.byref(nb)), self.ctx)
+        return list(ranks), list(modes), oc.value, nb.value
+
+    def num_cores(self) -> int:
+        return _lib.load().ttg_tt_num_cores(self._h)
+
+    def spatial_dims(self) -> int:
+        return self.num_cores() - 1
+
+    def ranks(self) -> List[int]:
+        return self._shape()[0]
+
+    def mode_sizes(self) -> List[int]:
+        return self._shape()[1]
+
+    def spatial_shape(self) -> List[int]:
+        return self._shape()[1][:-1]
+
+    @property
+    def ortho_count(self) -> int:
+        return self._shape()[2]
+
+    def fully_orthonormal(self) -> bool:
+        return self.ortho_count == self.num_cores() - 1
+
+    def obs_count(self) -> int:
+        return self._shape()[1][-1]
+
+    def batch_boundaries(self) -> List[int]:
+        nb = self._shape()[3]
+        out = (ctypes.c_int64 * max(nb, 1))()
+        _check(_lib.load().ttg_tt_bounds(self._h, out), self.ctx)
+        return list(out)[:nb]
+
+    def num_increments(self) -> int:
+        return self._shape()[3]
+
+    def core(self, i: int) -> np.ndarray:
+        ranks, modes, _, _ = self._shape()
+        shape = (ranks[i], modes[i], ranks[i + 1])
+        buf = np.empty(int(np.prod(shape)), dtype=np.float64)
+        _check(_lib.load().ttg_tt_download_core(self.ctx._h, self._h, i,
+                                                 buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), self.ctx)
+        return np.reshape(buf, shape, order="F")
+
+    def cores(self) -> List[np.ndarray]:
+        return [self.core(i) for i in range(self.num_cores())]
+
+    def param_count(self) -> int:
+        r, m, _, _ = self._shape()
+        return sum(r[i] * m[i] * r[i + 1] for i in range(len(m)))
+
+    def close(self) -> None:
+        if self._h:
+            _lib.load().ttg_tt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tt_ice_bootstrap(y, eps_des: float, ctx: Optional[Context] = None, shape=None) -> Tuple[TensorTrain, UpdateReport]:
+    """tt_ice.cpp:143-165: TT-SVD of the first increment (tt_svd.cpp:9-66), on device."""
+    ctx = ctx or default_context()
+    inp = _Input(y, shape)
+    sh, nd = inp.shape_arr()
+    h = ctypes.c_void_p()
+    rep = _lib.Report()
+    _check(_lib.load().ttg_bootstrap(ctx._h, inp.ptr, inp.where, sh, nd, float(eps_des), ctypes.byref(h),
+                                     ctypes.byref(rep)), ctx)
+    return TensorTrain(h, ctx), UpdateReport._from(rep)
+
+
+def tt_ice_update(tt: TensorTrain, y, eps_des: float, shape=None) -> Tuple[TensorTrain, UpdateReport]:
+    """tt_ice.cpp:131-141 (uniform delta = eps_des |y|_F / sqrt(d)); updates ``tt`` in place."""
+    inp = _Input(y, shape)
+    sh, nd = inp.shape_arr()
+    rep = _lib.Report()
+    _check(_lib.load().ttg_tt_ice_update(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, float(eps_des),
+                                         ctypes.byref(rep)), tt.ctx)
+    return tt, UpdateReport._from(rep)
+
+
+def tt_ice_update_with_tolerances(tt: TensorTrain, y, deltas: Sequence[float], shape=None):
+    """tt_ice.cpp:60-129 (one absolute threshold per spatial mode)."""
+    inp = _Input(y, shape)
+    sh, nd = inp.shape_arr()
+    rep = _lib.Report()
+    dl = (ctypes.c_double * max(len(deltas), 1))(*[float(x) for x in deltas])
+    _check(_lib.load().ttg_tt_ice_update_with_tolerances(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, dl,
+                                                         len(deltas), ctypes.byref(rep)), tt.ctx)
+    return tt, UpdateReport._from(rep)
+
+
+def tt_ice_star_update(tt: TensorTrain, y, eps_des: float, cfg: Optional[HeuristicConfig] = None, shape=None):
+    """tt_ice_star.cpp:171-303 (Algorithm 2); updates ``tt`` in place."""
+    cfg = cfg or HeuristicConfig()
+    inp = _Input(y, shape)
+    sh, nd = inp.shape_arr()
+    rep = _lib.Report()
+    h = cfg._to()
+    _check(_lib.load().ttg_tt_ice_star_update(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, float(eps_des),
+                                              ctypes.byref(h), ctypes.byref(rep)), tt.ctx)
+    return tt, UpdateReport._from(rep)
+
+
+def per_obs_errors(tt: TensorTrain, y, shape=None) -> np.ndarray:
+    """tt_ice_star.cpp:86-88."""
+    inp = _Input(y, shape)
+    sh, nd = inp.shape_arr()
+    out = np.empty(inp.shape[-1], dtype=np.float64)
+    _check(_lib.load().ttg_per_obs_errors(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd,
+                                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), tt.ctx)
+    return out
+
+
+def tt_project(tt: TensorTrain, y, shape=None) -> np.ndarray:
+    """tensor_train.cpp:195-226: r_d x n_obs latent coefficients."""
+    inp = _Input(y, shape)
+    sh, nd = inp.shape_arr()
+    r_d = tt.ranks()[-2]
+    out = np.empty((r_d, inp.shape[-1]), dtype=np.float64, order="F")
+    _check(_lib.load().ttg_project(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd,
+                                   out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), tt.ctx)
+    return out
+
+
+def tt_reconstruct(tt: TensorTrain, obs_begin: int = 0, obs_end: Optional[int] = None, out=None):
+    """tensor_train.cpp:182-193.  ``out`` may be a torch CUDA float64 tensor (device result)."""
+    if obs_end is None:
+        obs_end = tt.obs_count()
+    spatial = tt.spatial_shape()
+    m = obs_end - obs_begin
+    if out is None:
+        host = np.empty(int(np.prod(spatial)) * max(m, 0), dtype=np.float64)
+        _check(_lib.load().ttg_reconstruct(tt.ctx._h, tt._h, int(obs_begin), int(obs_end),
+                                           host.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), TTG_HOST), tt.ctx)
+        return np.reshape(host, tuple(spatial) + (m,), order="F")
+    ptr = ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_double))
+    _check(_lib.load().ttg_reconstruct(tt.ctx._h, tt._h, int(obs_begin), int(obs_end), ptr, TTG_DEVICE), tt.ctx)
+    return out
+
+
+def occupancy(core: np.ndarray) -> float:
+    """tensor_train.cpp:377-380 on a (r_left, n, r_right) core."""
+    return core.shape[2] / float(core.shape[0] * core.shape[1])
+
+
+def relaxed_tolerance_approx(n_batch: int, n_rejected: int, mean_rejected_error: float, eps_des: float) -> float:
+    """tt_ice_star.cpp:160-169 (Eq. 3.20); scalar host helper of the public API."""
+    from .errors import ConfigError
+
+    n_selected = n_batch - n_rejected
+    if n_selected < 1:
+        raise ConfigError("relaxed tolerance needs a nonempty selection")
+    return (eps_des * n_batch - mean_rejected_error * n_rejected) / n_selected
+
+
+def subselect(errs: Sequence[float], eps_des: float):
+    """tt_ice_star.cpp:90-100: (selected, rejected) with the strict '>' test."""
+    sel = [i for i, e in enumerate(errs) if e > eps_des]
+    rej = [i for i, e in enumerate(errs) if not (e > eps_des)]
+    return sel, rej

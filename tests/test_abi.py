@@ -1,0 +1,111 @@
+"""CPU: the C-ABI library loads and exports exactly what include/ttg.h declares
+(no compute calls without a GPU); the Python host mirror's pure-host logic."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ttg.h")
+LIB = os.path.join(ROOT, "paper_2211_12487_b200", "libttg.so")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(ttg_[a-z_0-9]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        import __graft_entry__
+
+        __graft_entry__.build()
+    return ctypes.CDLL(LIB)
+
+
+def test_header_declares_the_path(lib):
+    syms = declared_symbols()
+    for must in ["ttg_bootstrap", "ttg_tt_ice_update", "ttg_tt_ice_update_with_tolerances", "ttg_tt_ice_star_update",
+                 "ttg_project", "ttg_reconstruct", "ttg_per_obs_errors", "ttg_tt_upload", "ttg_ctx_create"]:
+        assert must in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), f"libttg.so does not export {s}"
+
+
+def test_exports_are_c_linkage():
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    for s in declared_symbols():
+        assert s in exported
+
+
+def test_ctypes_binding_covers_header():
+    from paper_2211_12487_b200 import _lib
+
+    bound = {name for name, _, _ in _lib.SIGNATURES}
+    assert bound == set(declared_symbols())
+
+
+def test_struct_layouts_match_header():
+    from paper_2211_12487_b200 import _lib
+
+    # ttg_report: 3 int64 + 2 int32 + 2*(33 int64) + 3 double + 2 int32
+    assert ctypes.sizeof(_lib.Report) == 3 * 8 + 2 * 4 + 2 * 33 * 8 + 3 * 8 + 2 * 4
+    assert ctypes.sizeof(_lib.Heuristics) == 8 + 4 * 4
+
+
+def test_heuristics_default_from_library(lib):
+    from paper_2211_12487_b200 import _lib
+
+    L = _lib.load()
+    h = _lib.Heuristics()
+    L.ttg_heuristics_default(ctypes.byref(h))
+    assert h.occupancy_threshold == 0.8 and h.skip_enabled == 1 and h.subselect_enabled == 1
+    assert h.skip_statistic == 0 and h.use_approx_tolerance == 0
+
+
+def test_null_arguments_return_status_without_gpu(lib):
+    from paper_2211_12487_b200 import _lib
+
+    L = _lib.load()
+    assert L.ttg_ctx_create(0, None) == 10  # TTG_E_ARGUMENT
+    assert L.ttg_tt_num_cores(None) == -1
+    assert L.ttg_last_error(None) == b"null context"
+
+
+def test_host_mirror_pure_helpers():
+    from paper_2211_12487_b200 import ConfigError, HeuristicConfig, occupancy, relaxed_tolerance_approx, subselect
+
+    assert subselect([0.2, 0.05, 0.1], 0.1) == ([0], [1, 2])
+    assert relaxed_tolerance_approx(10, 5, 0.05, 0.1) == pytest.approx(0.15)
+    with pytest.raises(ConfigError):
+        relaxed_tolerance_approx(3, 3, 0.0, 0.1)
+    assert occupancy(np.zeros((1, 4, 2))) == 0.5
+    h = HeuristicConfig(skip_statistic="full")._to()
+    assert h.skip_statistic == 1
+    with pytest.raises(ValueError):
+        HeuristicConfig(skip_statistic="median")._to()
+
+
+def test_status_codes_map_to_reference_exceptions():
+    from paper_2211_12487_b200 import errors
+
+    assert errors.STATUS_TO_ERROR[1] is errors.DimensionError
+    assert errors.STATUS_TO_ERROR[2] is errors.NumericError
+    assert errors.STATUS_TO_ERROR[3] is errors.StateError
+    assert errors.STATUS_TO_ERROR[6] is errors.ConfigError
+    for cls in errors.STATUS_TO_ERROR.values():
+        assert issubclass(cls, errors.Error)
+
+
+def test_sass_uses_fp64_tensor_cores():
+    """The fused Gram / projection kernels are DMMA (FP64 tensor core) code."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+    assert "DMMA.8x8x4" in out

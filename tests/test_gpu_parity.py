@@ -1,0 +1,264 @@
+"""GPU parity: the CUDA path (through the C ABI, libttg.so) against the CPU
+oracle (oracle/ttstream_oracle.py) on identical seeded inputs.
+
+Tolerances are stated in tests/parity_util.py (ranks identical; subspaces,
+reconstructions, per-increment relative errors within 1e-10).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ttstream_oracle as O
+from paper_2211_12487_b200 import (ConfigError, DimensionError, HeuristicConfig, NumericError, StateError,
+                                   TensorTrain, per_obs_errors, tt_ice_bootstrap, tt_ice_star_update,
+                                   tt_ice_update, tt_ice_update_with_tolerances, tt_project, tt_reconstruct)
+from paper_2211_12487_b200.streams import Stream
+from tests.parity_util import (TOL, compare_reconstructions, compare_reports, compare_trains, subspace_distance,
+                               to_oracle)
+
+pytestmark = pytest.mark.gpu
+
+
+def run_stream(ctx, stream, n_inc, algo="ice", cfg=None, check_every=1, eps=None):
+    eps = eps if eps is not None else stream.eps
+    y0 = stream.increment(0)
+    tg, rg = tt_ice_bootstrap(y0, eps, ctx=ctx)
+    tr, rr = O.tt_ice_bootstrap(y0, eps)
+    compare_reports(rg, rr)
+    compare_trains(tg, tr)
+    ys = [(0, y0)]
+    for k in range(1, n_inc):
+        y = stream.increment(k)
+        ys.append((k, y))
+        if algo == "ice":
+            tg, rg = tt_ice_update(tg, y, eps)
+            tr, rr = O.tt_ice_update(tr, y, eps)
+        else:
+            ocfg = O.HeuristicConfig(**vars(cfg)) if cfg else O.HeuristicConfig()
+            tg, rg = tt_ice_star_update(tg, y, eps, cfg)
+            tr, rr = O.tt_ice_star_update(tr, y, eps, ocfg)
+        compare_reports(rg, rr, star=(algo != "ice"))
+        if k % check_every == 0 or k == n_inc - 1:
+            compare_trains(tg, tr)
+    gh = to_oracle(tg)
+    compare_reconstructions(gh, tr, ys)
+    return tg, tr
+
+
+def test_cfg0_stream_tt_ice(ctx):
+    """BASELINE configs[0]: 64 increments of 8x8x8x8, batch 1, eps 0.1."""
+    run_stream(ctx, Stream(0, seed=0), 64, "ice")
+
+
+def test_cfg0_stream_tt_ice_star(ctx):
+    run_stream(ctx, Stream(0, seed=1), 64, "star")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_cfg3_small_ice_and_star(ctx, seed):
+    """cfg3 generator (drift TT, skip path on odd increments) at 4^6, batch 24."""
+    s = Stream(3, seed=seed, modes=(4,) * 6, batch=24, true_rank=6)
+    run_stream(ctx, s, 10, "ice")
+    run_stream(ctx, s, 10, "star")
+
+
+def test_cfg3_shape_star_midsize(ctx):
+    """cfg3 shape 8^7 at batch 4 (2.1M entries / observation), TT-ICE*."""
+    s = Stream(3, seed=2, batch=4)
+    run_stream(ctx, s, 5, "star")
+
+
+def test_cfg1_video_small_batch(ctx):
+    """BASELINE configs[1] shape (14,15,16,10,3) at batch 10, 6 increments."""
+    s = Stream(1, seed=0, batch=10)
+    run_stream(ctx, s, 6, "ice")
+
+
+def test_cfg2_simulation_small_grid(ctx):
+    """configs[2] generator on a 16^3 x 3 grid -> (4,4,4,4,4,4,3), batch 8."""
+    s = Stream(2, seed=0, batch=8, grid=16)
+    run_stream(ctx, s, 4, "ice")
+
+
+@pytest.mark.parametrize("variant", [
+    dict(skip_enabled=False),
+    dict(subselect_enabled=False),
+    dict(skip_statistic="full"),
+    dict(use_approx_tolerance=True),
+    dict(occupancy_threshold=0.3),
+    dict(occupancy_threshold=1.0),
+])
+def test_tt_ice_star_heuristic_variants(ctx, variant):
+    s = Stream(3, seed=3, modes=(4,) * 5, batch=12, true_rank=5)
+    run_stream(ctx, s, 7, "star", cfg=HeuristicConfig(**variant))
+
+
+def test_appendix_b_rank_recovery(ctx):
+    """SPEC.md:681 / PAPER Appendix B: noiseless 10x15x20, ranks [1,2,3,5,1], eps 1e-8."""
+    rng = np.random.default_rng(7)
+    modes, ranks = (10, 15, 20), [1, 2, 3, 5]
+    cores = []
+    for i, n in enumerate(modes):
+        q, _ = np.linalg.qr(rng.standard_normal((ranks[i] * n, ranks[i + 1])))
+        cores.append(q)
+    from paper_2211_12487_b200.streams import tt_chain
+    phi = tt_chain(cores)
+    eps = 1e-8
+    ys = [np.reshape(phi @ rng.standard_normal((5, 10)), modes + (10,), order="F") for _ in range(50)]
+    for algo in ("ice", "star"):
+        tg, rg = tt_ice_bootstrap(ys[0], eps, ctx=ctx)
+        tr, _ = O.tt_ice_bootstrap(ys[0], eps)
+        for k in range(1, 50):
+            if algo == "ice":
+                tg, rg = tt_ice_update(tg, ys[k], eps)
+                tr, rr = O.tt_ice_update(tr, ys[k], eps)
+            else:
+                tg, rg = tt_ice_star_update(tg, ys[k], eps)
+                tr, rr = O.tt_ice_star_update(tr, ys[k], eps)
+            assert rg.ranks_after == rr.ranks_after
+        assert tg.ranks() == [1, 2, 3, 5, 1]
+        gh = to_oracle(tg)
+        for k in range(50):
+            b, e = gh.increment_range(k)
+            rec = O.tt_reconstruct(gh, b, e)
+            assert np.linalg.norm(rec - ys[k]) <= (eps + 1e-9) * np.linalg.norm(ys[k])
+
+
+def test_in_span_increment_adds_no_directions(ctx):
+    """increment drawn from the current span -> all r_R = 0."""
+    s = Stream(0, seed=4)
+    tg, _ = tt_ice_bootstrap(s.increment(0, batch=8), 0.1, ctx=ctx)
+    th = to_oracle(tg)
+    coeff = np.random.default_rng(0).standard_normal((th.ranks()[-2], 5))
+    y = O.tt_expand(th, coeff)
+    before = tg.ranks()
+    tg, rep = tt_ice_update(tg, y, 0.1)
+    assert tg.ranks()[:-1] == before[:-1]
+    assert rep.modes_updated == 0
+    c = tt_project(tg, y)
+    assert np.allclose(c, coeff, atol=1e-12)
+
+
+def test_zero_increment(ctx):
+    s = Stream(0, seed=5)
+    tg, _ = tt_ice_bootstrap(s.increment(0, batch=4), 0.1, ctx=ctx)
+    tr, _ = O.tt_ice_bootstrap(s.increment(0, batch=4), 0.1)
+    z = np.zeros((8, 8, 8, 8, 3))
+    tg, rg = tt_ice_update(tg, z, 0.1)
+    tr, rr = O.tt_ice_update(tr, z, 0.1)
+    compare_reports(rg, rr)
+    tg, rg = tt_ice_star_update(tg, z, 0.1)
+    tr, rr = O.tt_ice_star_update(tr, z, 0.1)
+    compare_reports(rg, rr)
+    assert rg.obs_used == 0
+
+
+def test_bootstrap_rank_zero_placeholder(ctx):
+    """tt_svd.cpp:42-47: eps >= 1 -> every mode rank 0 -> unit-column placeholder."""
+    y = Stream(0, seed=6).increment(0, batch=3)
+    tg, rg = tt_ice_bootstrap(y, 1.0, ctx=ctx)
+    tr, rr = O.tt_ice_bootstrap(y, 1.0)
+    compare_reports(rg, rr)
+    compare_trains(tg, tr)
+
+
+def test_with_tolerances_and_project_reconstruct(ctx):
+    s = Stream(3, seed=8, modes=(4,) * 5, batch=9, true_rank=4)
+    y0 = s.increment(0)
+    tg, _ = tt_ice_bootstrap(y0, 0.05, ctx=ctx)
+    tr, _ = O.tt_ice_bootstrap(y0, 0.05)
+    y = s.increment(2)
+    deltas = [0.3, 0.2, 0.1, 0.05, 0.01]
+    tg, rg = tt_ice_update_with_tolerances(tg, y, deltas)
+    tr, rr = O.tt_ice_update_with_tolerances(tr, y, deltas)
+    compare_reports(rg, rr)
+    compare_trains(tg, tr)
+    y2 = s.increment(3)
+    cg = tt_project(tg, y2)
+    cr = O.tt_project(tr, y2)
+    assert np.linalg.norm(cg - cr) <= TOL * np.linalg.norm(cr)
+    eg = per_obs_errors(tg, y2)
+    er = O.per_obs_errors(tr, y2)
+    assert np.max(np.abs(eg - er)) <= 1e-9
+    rec = tt_reconstruct(tg, 3, 12)
+    rec_r = O.tt_reconstruct(tr, 3, 12)
+    assert np.linalg.norm(rec - rec_r) <= TOL * np.linalg.norm(rec_r)
+
+
+def test_device_resident_input_matches_host(ctx):
+    import torch
+
+    s = Stream(3, seed=9, modes=(4,) * 5, batch=6, true_rank=4)
+    y0, y1 = s.increment(0), s.increment(2)
+    ta, _ = tt_ice_bootstrap(y0, 0.01, ctx=ctx)
+    tb, _ = tt_ice_bootstrap(torch.from_numpy(np.ravel(y0, order="F")).cuda(), 0.01, ctx=ctx, shape=y0.shape)
+    ta, ra = tt_ice_update(ta, y1, 0.01)
+    tb, rb = tt_ice_update(tb, torch.from_numpy(np.ravel(y1, order="F")).cuda(), 0.01, shape=y1.shape)
+    assert ra.ranks_after == rb.ranks_after
+    for ca, cb in zip(ta.cores(), tb.cores()):
+        assert np.array_equal(ca, cb)  # deterministic: same bytes
+
+
+def test_determinism_bitwise(ctx):
+    s = Stream(0, seed=10)
+    outs = []
+    for _ in range(2):
+        tg, _ = tt_ice_bootstrap(s.increment(0, batch=2), 0.1, ctx=ctx)
+        for k in range(1, 6):
+            tg, _ = tt_ice_star_update(tg, s.increment(k, batch=2), 0.1)
+        outs.append([c.copy() for c in tg.cores()])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_theorem_3_3_no_regression(ctx):
+    """Earlier increments' reconstructions are unchanged (1e-12)."""
+    s = Stream(3, seed=11, modes=(4,) * 5, batch=5, true_rank=4)
+    tg, _ = tt_ice_bootstrap(s.increment(0), 0.01, ctx=ctx)
+    prev = tt_reconstruct(tg)
+    for k in range(1, 6):
+        tg, _ = tt_ice_update(tg, s.increment(k), 0.01)
+        now = tt_reconstruct(tg, 0, prev.shape[-1])
+        assert np.linalg.norm(now - prev) <= 1e-12 * max(1.0, np.linalg.norm(prev))
+        prev = tt_reconstruct(tg)
+
+
+def test_errors_mirror_reference(ctx):
+    s = Stream(0, seed=12)
+    y = s.increment(0, batch=2)
+    tg, _ = tt_ice_bootstrap(y, 0.1, ctx=ctx)
+    with pytest.raises(NumericError):
+        tt_ice_update(tg, y, 0.0)  # tt_ice.cpp:133-135
+    with pytest.raises(DimensionError):
+        tt_ice_update(tg, np.zeros((8, 8, 4, 8, 2)), 0.1)  # tt_ice.cpp:24-28
+    bad = y.copy()
+    bad[0, 0, 0, 0, 0] = np.nan
+    with pytest.raises(NumericError):
+        tt_ice_update(tg, bad, 0.1)
+    with pytest.raises(ConfigError):
+        tt_ice_star_update(tg, y, 0.1, HeuristicConfig(occupancy_threshold=1.5))
+    with pytest.raises(NumericError):
+        tt_ice_bootstrap(y, 1.5, ctx=ctx)  # tt_svd.cpp:10-12
+    with pytest.raises(DimensionError):
+        tt_ice_update_with_tolerances(tg, y, [0.1, 0.1])
+    cores = [c for c in tg.cores()]
+    nonortho = TensorTrain.upload(cores, 0, tg.batch_boundaries(), ctx=ctx)
+    with pytest.raises(StateError):
+        tt_ice_update(nonortho, y, 0.1)  # tt_ice.cpp:17-19
+    with pytest.raises(StateError):
+        tt_project(nonortho, y)
+
+
+def test_upload_roundtrip_and_update(ctx):
+    """A host train (oracle) uploaded through the ABI updates like the oracle."""
+    s = Stream(0, seed=13)
+    tr, _ = O.tt_ice_bootstrap(s.increment(0, batch=3), 0.1)
+    tg = TensorTrain.upload([c.data for c in tr.cores], tr.ortho_count, tr.batch_boundaries, ctx=ctx)
+    for a, b in zip(tg.cores(), tr.cores):
+        assert np.array_equal(a, b.data)
+    y = s.increment(1, batch=3)
+    tg, rg = tt_ice_star_update(tg, y, 0.1)
+    tr, rr = O.tt_ice_star_update(tr, y, 0.1)
+    compare_reports(rg, rr, star=True)
+    compare_trains(tg, tr)

@@ -1,0 +1,18 @@
+#!/bin/bash
+# Box probe: hardware, host cores, FP64 peaks (DFMA / DMMA / cuBLAS DGEMM), HBM copy.
+set -x
+nvidia-smi
+nproc; lscpu | head -20
+free -g
+./tools/probe/fp64_peak
+python - <<'PY'
+import torch, time
+a = torch.randn(8192, 8192, dtype=torch.float64, device='cuda'); b = torch.randn_like(a)
+for _ in range(3): c = a @ b
+torch.cuda.synchronize()
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+best = 1e9
+for _ in range(5):
+    e0.record(); c = a @ b; e1.record(); torch.cuda.synchronize(); best = min(best, e0.elapsed_time(e1))
+print("cuBLAS DGEMM 8192^3: %.2f TFLOP/s" % (2*8192**3/best/1e9))
+PY
