@@ -104,6 +104,17 @@ void* ttg_ctx_stream(const ttg_ctx* ctx);
 /* Number of ttg kernels launched by this context so far. */
 int64_t ttg_ctx_launch_count(const ttg_ctx* ctx);
 int ttg_ctx_synchronize(ttg_ctx* ctx);
+/* Per-kernel accounting.  Launch counts and ALGORITHMIC bytes / flops per
+ * launch are always kept; device time (CUDA events on the
+ * context stream around each launch) only while profiling is on. */
+int ttg_ctx_set_profiling(ttg_ctx* ctx, int on);
+void ttg_ctx_reset_stats(ttg_ctx* ctx);
+int ttg_ctx_num_kernel_stats(ttg_ctx* ctx);
+int ttg_ctx_kernel_stat(ttg_ctx* ctx, int idx, char* name, int name_len, int64_t* launches, double* ms,
+                        double* bytes, double* flops);
+/* Host<->device bytes moved by the context (H2D of host increments, D2H of
+ * scalars/decisions). */
+int ttg_ctx_io_bytes(const ttg_ctx* ctx, int64_t* h2d, int64_t* d2h);
 
 /* ---- device train ------------------------------------------------------- */
 /* Upload a host train: cores[i] is r_left[i]*n[i]*r_right[i] doubles,

@@ -107,6 +107,24 @@ struct ttg_ctx {
   ttg::EigResult* h_eig = nullptr;
   double* h_scal = nullptr;
   ttg::StarStats* h_stats = nullptr;
+  // per-kernel accounting (launches, algorithmic bytes/flops always; event
+  // time only while profiling is on)
+  struct KStat {
+    std::string name;
+    int64_t launches = 0;
+    double ms = 0.0, bytes = 0.0, flops = 0.0;
+  };
+  struct Pending {
+    int idx;
+    cudaEvent_t e0, e1;
+  };
+  bool profiling = false;
+  std::vector<KStat> kstats;
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> evpool;
+  int cur_idx = -1;
+  cudaEvent_t cur_e0 = nullptr;
+  int64_t h2d = 0, d2h = 0;
 };
 
 struct ttg_tt {
@@ -124,9 +142,60 @@ namespace {
 
 using ttg::EigResult;
 
+cudaEvent_t get_event(ttg_ctx* c) {
+  if (!c->evpool.empty()) {
+    cudaEvent_t e = c->evpool.back();
+    c->evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
+// Call before every kernel launch: accounts the launch under `name` with its
+// algorithmic bytes / flops and opens a timing event.
+void prof_begin(ttg_ctx* c, const char* name, double bytes, double flops) {
+  int idx = -1;
+  for (size_t i = 0; i < c->kstats.size(); ++i)
+    if (c->kstats[i].name == name) { idx = (int)i; break; }
+  if (idx < 0) {
+    c->kstats.push_back({name});
+    idx = (int)c->kstats.size() - 1;
+  }
+  auto& st = c->kstats[idx];
+  st.launches++;
+  st.bytes += bytes;
+  st.flops += flops;
+  c->cur_idx = idx;
+  if (c->profiling) {
+    c->cur_e0 = get_event(c);
+    CK(cudaEventRecord(c->cur_e0, c->stream));
+  }
+}
+
 void post_launch(ttg_ctx* c) {
   ++c->launches;
   CK(cudaGetLastError());
+  if (c->profiling && c->cur_idx >= 0) {
+    cudaEvent_t e1 = get_event(c);
+    CK(cudaEventRecord(e1, c->stream));
+    c->pending.push_back({c->cur_idx, c->cur_e0, e1});
+  }
+  c->cur_idx = -1;
+}
+
+void prof_flush(ttg_ctx* c) {
+  if (c->pending.empty()) return;
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.e0, p.e1));
+    c->kstats[p.idx].ms += ms;
+    c->evpool.push_back(p.e0);
+    c->evpool.push_back(p.e1);
+  }
+  c->pending.clear();
 }
 
 int grid_for(long long n, int threads, int max_blocks) {
@@ -150,8 +219,10 @@ void obs_norms(ttg_ctx* c, const double* Y, long long S, int b) {
   c->on2.ensure(sizeof(double) * b);
   c->scal.ensure(sizeof(double) * 16);
   dim3 grid(nchunk, b);
+  prof_begin(c, "k_sumsq_obs", 8.0 * S * b, 2.0 * S * b);
   ttg::k_sumsq_obs<<<grid, 256, 0, c->stream>>>(Y, S, nchunk, c->sumsq_part.as<double>());
   post_launch(c);
+  prof_begin(c, "k_sumsq_finalize", 8.0 * nchunk * b, 0.0);
   ttg::k_sumsq_finalize<<<1, 256, 0, c->stream>>>(c->sumsq_part.as<double>(), nchunk, b,
                                                    c->on2.as<double>(), c->scal.as<double>());
   post_launch(c);
@@ -159,6 +230,7 @@ void obs_norms(ttg_ctx* c, const double* Y, long long S, int b) {
 }
 
 double read_scalar(ttg_ctx* c, const double* d) {
+  c->d2h += sizeof(double);
   CK(cudaMemcpyAsync(c->h_scal, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return c->h_scal[0];
@@ -170,6 +242,7 @@ void make_frags(ttg_ctx* c, const double* U, int a, int r, int ld, bool need_ut,
   size_t n1 = (size_t)(r8 / 8) * (a8 / 4) * 32, n2 = (size_t)(a8 / 8) * (r8 / 4) * 32;
   c->UTf.ensure(sizeof(double) * std::max<size_t>(n1, 1));
   c->Uf.ensure(sizeof(double) * std::max<size_t>(n2, 1));
+  prof_begin(c, "k_make_frags", 8.0 * (n1 + n2), 0.0);
   ttg::k_make_frags<<<grid_for(n1 + n2, 256, 1024), 256, 0, c->stream>>>(
       U, a, r, ld, a8, r8, need_ut ? c->UTf.as<double>() : nullptr, need_u ? c->Uf.as<double>() : nullptr);
   post_launch(c);
@@ -182,6 +255,7 @@ void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long
   if (m == 0 || n == 0) return;
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
   if (grid.y > 65535) fail(TTG_E_RESOURCE, "generic gemm: m too large");
+  prof_begin(c, "k_gemm", 8.0 * (m * k + k * n + m * n), 2.0 * m * n * k);
   ttg::k_gemm<TA, TB><<<grid, dim3(32, 32), 0, c->stream>>>(A, lda, B, ldb, C, ldc, m, n, k, alpha, beta);
   post_launch(c);
 }
@@ -203,17 +277,23 @@ void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem) {
   c->partials.ensure(sizeof(double) * (size_t)gx * SBD * SBD);
   ttg::GramArgs a2 = args;
   a2.partials = c->partials.as<double>();
+  {
+    const double Ls = (double)args.src.L * args.sel_frac;
+    const double a_ = args.src.a, r_ = args.r_old;
+    prof_begin(c, "k_gram_resid", 8.0 * a_ * Ls, Ls * (4.0 * r_ * a_ + a_ * a_));
+  }
   kern<<<gx, ttg::kThreads, smem, c->stream>>>(a2);
   post_launch(c);
   int a = args.src.a;
   long long n = (long long)a * a;
+  prof_begin(c, "k_gram_reduce", 8.0 * gx * SBD * SBD, (double)gx * a * a);
   ttg::k_gram_reduce<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, SBD, a,
                                                                       c->G.as<double>());
   post_launch(c);
 }
 
 void gram(ttg_ctx* c, const double* X, int a, long long L, const double* U, int r_old, int ldu,
-          const uint8_t* sel, long long cpo) {
+          const uint8_t* sel, long long cpo, double sel_frac = 1.0) {
   int a8 = ttg::round_up(a, 8);
   int r8 = r_old > 0 ? ttg::round_up(r_old, 8) : 0;
   c->G.ensure(sizeof(double) * (size_t)a * a);
@@ -227,6 +307,8 @@ void gram(ttg_ctx* c, const double* X, int a, long long L, const double* U, int 
     args.UTf = c->UTf.as<double>();
     args.Uf = c->Uf.as<double>();
     args.r8 = r8;
+    args.r_old = r_old;
+    args.sel_frac = sel_frac;
     args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
     size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
     int nb = a8 / 8;
@@ -246,6 +328,7 @@ void gram(ttg_ctx* c, const double* X, int a, long long L, const double* U, int 
       gemm<false, false>(c, U, ldu, P, r_old, R, a, a, L, r_old, -1.0, 1.0);
     }
     if (sel) {
+      prof_begin(c, "k_mask_cols", 16.0 * a * L, 0.0);
       ttg::k_mask_cols<<<grid_for((long long)a * L, 256, 4096), 256, 0, c->stream>>>(R, a, L, sel, cpo);
       post_launch(c);
     }
@@ -255,7 +338,7 @@ void gram(ttg_ctx* c, const double* X, int a, long long L, const double* U, int 
 }
 
 // ---- eigen-solve -------------------------------------------------------------
-EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double delta_mult) {
+EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double delta_mult, int factor = 0) {
   c->UR.ensure(sizeof(double) * (size_t)a * a);
   c->lam.ensure(sizeof(double) * a);
   c->eigres.ensure(sizeof(EigResult));
@@ -263,6 +346,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
   ttg::EigArgs args{};
   args.G = c->G.as<double>();
   args.a = a;
+  args.factor = factor;
   args.kmax = kmax;
   args.delta_src = delta_src;
   args.delta_mult = delta_mult;
@@ -283,8 +367,10 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     smem = sizeof(double) * a + sizeof(int) * a + 64;
   }
   CK(cudaFuncSetAttribute(ttg::k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  prof_begin(c, "k_jacobi_eig", 16.0 * a * a, 0.0);
   ttg::k_jacobi_eig<<<1, ttg::kEigThreads, smem, c->stream>>>(args);
   post_launch(c);
+  c->d2h += sizeof(EigResult);
   CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   EigResult r = *c->h_eig;
@@ -293,13 +379,73 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
   return r;
 }
 
+
+// ---- accurate path: TSQR factor + Jacobi on T^T ---------------------------------
+bool accurate_supported(int a, int r_old) {
+  return ttg::round_up(a, 8) <= kFastMax && (r_old == 0 || ttg::round_up(r_old, 8) <= kFastMax);
+}
+
+// Replaces c->G by the a x a R-factor T of the residual (T^T T = R R^T) and
+// solves on T^T: singular values are resolved to eps_mach |R|.
+EigResult accurate_eig(ttg_ctx* c, const double* X, int a, long long L, const double* U, int r_old, int ldu,
+                       const uint8_t* sel, long long cpo, long long kmax, const double* dsrc, double dmult) {
+  int a8 = ttg::round_up(a, 8);
+  int r8 = r_old > 0 ? ttg::round_up(r_old, 8) : 0;
+  if (r_old > 0) make_frags(c, U, a, r_old, ldu, true, true);
+  ttg::TsqrArgs args{};
+  args.src = ttg::TileSrc{X, a, L, sel, cpo};
+  args.a8 = a8;
+  args.ldt = ttg::smem_ld(a8);
+  args.ldp = ttg::smem_ld(std::max(r8, 8));
+  args.UTf = c->UTf.as<double>();
+  args.Uf = c->Uf.as<double>();
+  args.r8 = r8;
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  size_t smem = sizeof(double) * ((size_t)a * a + (size_t)args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+  CK(cudaFuncSetAttribute(ttg::k_tsqr_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int gx = (int)std::min<long long>(c->num_sms, std::max<long long>(1, args.n_tiles));
+  c->partials.ensure(sizeof(double) * (size_t)gx * a * a);
+  args.Tout = c->partials.as<double>();
+  prof_begin(c, "k_tsqr_local", 8.0 * a * L, (double)L * (4.0 * r_old * a + 2.0 * a * a));
+  ttg::k_tsqr_local<<<gx, ttg::kThreads, smem, c->stream>>>(args);
+  post_launch(c);
+  c->scratch.ensure(sizeof(double) * (size_t)a * a);
+  c->G.ensure(sizeof(double) * (size_t)a * a);
+  size_t smem2 = sizeof(double) * (size_t)a * a;
+  CK(cudaFuncSetAttribute(ttg::k_tsqr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  prof_begin(c, "k_tsqr_combine", 16.0 * gx * a * a, 2.0 * gx * a * a * a);
+  ttg::k_tsqr_combine<<<1, 1024, smem2, c->stream>>>(c->partials.as<double>(), gx, a, c->scratch.as<double>(),
+                                                     c->G.as<double>());
+  post_launch(c);
+  if (c->world > 1) {
+    c->partials.ensure(sizeof(double) * (size_t)c->world * a * a);
+    NK(ncclAllGather(c->G.p, c->partials.p, (size_t)a * a, ncclDouble, c->comm, c->stream));
+    prof_begin(c, "k_tsqr_combine", 16.0 * c->world * a * a, 2.0 * c->world * a * a * a);
+    ttg::k_tsqr_combine<<<1, 1024, smem2, c->stream>>>(c->partials.as<double>(), c->world, a,
+                                                       c->scratch.as<double>(), c->G.as<double>());
+    post_launch(c);
+  }
+  return eig(c, a, kmax, dsrc, dmult, /*factor=*/1);
+}
+
+// The Gram floor resolves sigma only down to ~sqrt(eps_mach)|R|; fall back
+// to the factor path when the decision or a kept direction gets near it.
+bool needs_accurate(const EigResult& er) {
+  if (!(er.lam_max > 0.0)) return false;
+  if (er.delta * er.delta < 1e-9 * er.lam_max) return true;
+  if (er.rank > 0 && er.lam_min_kept < 1e-6 * er.lam_max) return true;
+  return false;
+}
+
 // [U_pad U_R] -> out (a x (r_old + r_R)) with the 1e-10 guard; returns guard flag
 int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* out) {
   c->scratch.ensure(sizeof(double) * ((size_t)a * r_R + (size_t)(r_old + 1) * (r_R + 1) + 16));
   ttg::AppendArgs args{Upad, c->UR.as<double>(), a, r_old, r_R, out, c->scratch.as<double>(),
                        c->eigres.as<EigResult>()};
+  prof_begin(c, "k_append", 8.0 * a * (2.0 * r_old + 2.0 * r_R), 2.0 * a * (r_old + r_R) * (r_old + r_R));
   ttg::k_append<<<1, 1024, 0, c->stream>>>(args);
   post_launch(c);
+  c->d2h += sizeof(EigResult);
   CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return c->h_eig->guard;
@@ -328,6 +474,7 @@ void project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttg::k_project, ttg::kThreads, smem));
   occ = std::max(occ, 1);
   int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  prof_begin(c, "k_project", 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
   ttg::k_project<<<gx, ttg::kThreads, smem, c->stream>>>(args);
   post_launch(c);
 }
@@ -344,6 +491,7 @@ const double* stage_input(ttg_ctx* c, const double* y, int where, size_t n) {
   if (where != TTG_HOST) fail(TTG_E_ARGUMENT, "where must be TTG_HOST or TTG_DEVICE");
   c->ystage.ensure(sizeof(double) * n);
   CK(cudaMemcpyAsync(c->ystage.p, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  c->h2d += (int64_t)(sizeof(double) * n);
   return c->ystage.as<double>();
 }
 
@@ -424,6 +572,7 @@ double sumsq_device(ttg_ctx* c, const double* x, long long n) {
   c->sumsq_part.ensure(sizeof(double) * 64);
   c->scal.ensure(sizeof(double) * 16);
   dim3 grid(1, 1);
+  prof_begin(c, "k_sumsq_obs", 8.0 * n, 2.0 * n);
   ttg::k_sumsq_obs<<<grid, 256, 0, c->stream>>>(x, n, 1, c->sumsq_part.as<double>());
   post_launch(c);
   return read_scalar(c, c->sumsq_part.as<double>());
@@ -446,6 +595,7 @@ struct SweepOut {
   double discarded_sq = 0.0;
   int guards = 0;
   int modes_updated = 0;
+  int accurate_modes = 0;
   bool cores_changed = false;
   const double* coeffs = nullptr;  // r_d x b_local (compact)
   int r_d = 0;
@@ -455,7 +605,6 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
   SweepOut out;
   const int d = tt->d;
   const int64_t S = prod(tt->modes);
-  const int64_t bg = b * c->world;
   std::vector<int64_t> old_ranks = tt->ranks;
   const double* cur = Y;
   int flip = 0;
@@ -470,7 +619,6 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     const int64_t L = total / a;
     const int64_t cpo = L / b;
     if (a > 4096) fail(TTG_E_RESOURCE, "unfolding rows a_i = " + std::to_string(a) + " exceed the device solver limit");
-    double delta_i = 0.0;
     const double* dsrc = nullptr;
     double dmult = 0.0;
     if (o.deltas) {
@@ -494,14 +642,18 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     int64_t kmax = 0;
     if (run_svd) {
       const uint8_t* sel = o.star ? o.sel : nullptr;
-      gram(c, cur, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo);
+      double sel_frac = o.star ? (double)o.n_sel_global / (double)(b * c->world) : 1.0;
+      gram(c, cur, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, sel_frac);
       kmax = o.star ? o.n_sel_global * cpo : L * c->world;
       EigResult er = eig(c, (int)a, kmax, dsrc, dmult);
+      if (needs_accurate(er) && accurate_supported((int)a, (int)r_old)) {
+        er = accurate_eig(c, cur, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, kmax,
+                          dsrc, dmult);
+        out.accurate_modes++;
+      }
       r_R = er.rank;
       out.discarded_sq += er.tail_sq;
-      delta_i = er.delta;
     }
-    (void)delta_i;
     int64_t r_new;
     // new core i
     if (o.bootstrap) {
@@ -556,6 +708,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       } else if (r_new != rl_old) {
         int64_t tot = r_new * n_next * rr_old;
         c->Upad.ensure(sizeof(double) * (size_t)std::max<int64_t>(tot, 1));
+        prof_begin(c, "k_pad_core", 16.0 * tot, 0.0);
         ttg::k_pad_core<<<grid_for(tot, 256, 1024), 256, 0, c->stream>>>(
             tt->cores[i + 1].as<double>(), (int)rl_old, (int)n_next, (int)rr_old, (int)r_new, c->Upad.as<double>());
         post_launch(c);
@@ -617,10 +770,12 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
   for (int i = 0; i < tt->d; ++i) {
     int rl = (int)tt->ranks[i], n = (int)tt->modes[i], rr = (int)tt->ranks[i + 1];
     long long t1 = (long long)rl * n * rr;
+    prof_begin(c, "k_iface", 8.0 * t1, 2.0 * t1 * rl);
     ttg::k_iface_step1<<<grid_for(t1, 256, 1024), 256, 0, c->stream>>>(c->iface[f].as<double>(),
                                                                         tt->cores[i].as<double>(), rl, n, rr,
                                                                         c->Mtmp.as<double>());
     post_launch(c);
+    prof_begin(c, "k_iface", 8.0 * rr * rr, 2.0 * rr * rr * n * rl);
     ttg::k_iface_step2<<<grid_for((long long)rr * rr, 128, 1024), 128, 0, c->stream>>>(
         c->Mtmp.as<double>(), tt->cores[i].as<double>(), rl, n, rr, c->iface[f ^ 1].as<double>());
     post_launch(c);
@@ -640,9 +795,11 @@ void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double
   c->errs.ensure(sizeof(double) * b);
   c->rn2.ensure(sizeof(double) * b);
   c->stats.ensure(sizeof(ttg::StarStats));
+  prof_begin(c, "k_coef_stats", 8.0 * r * b, 2.0 * r * r * b);
   ttg::k_coef_stats<<<grid_for(b, 128, 1024), 128, 0, c->stream>>>(c->coeffs.as<double>(), r, (int)b, M,
                                                                    c->cn2.as<double>(), c->cmc.as<double>());
   post_launch(c);
+  prof_begin(c, "k_star_local", 32.0 * b, 10.0 * b);
   ttg::k_star_local<<<1, 32, 0, c->stream>>>(c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
                                              (int)b, eps, c->errs.as<double>(), c->rn2.as<double>(),
                                              c->stats.as<ttg::StarStats>());
@@ -739,6 +896,7 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   fill_report_ranks(rep->ranks_before, tt);
 
   star_stats(c, tt, Y, b, eps_des);
+  c->d2h += sizeof(ttg::StarStats);
   CK(cudaMemcpyAsync(c->h_stats, c->stats.p, sizeof(ttg::StarStats), cudaMemcpyDeviceToHost, c->stream));
   double ysq = read_scalar(c, c->scal.as<double>());
   check_finite_norm(ysq);
@@ -784,6 +942,7 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
     double delta = eps_upd / std::sqrt((double)d) * std::sqrt(d_sq);  // :235-236
     rep->eps_target = delta;
     c->sel.ensure((size_t)b);
+    prof_begin(c, "k_star_mask", 9.0 * b, 0.0);
     ttg::k_star_mask<<<grid_for(b, 256, 64), 256, 0, c->stream>>>(c->errs.as<double>(), (int)b, eps_des,
                                                                     cfg.subselect_enabled, c->sel.as<uint8_t>());
     post_launch(c);
@@ -966,6 +1125,11 @@ void ttg_ctx_destroy(ttg_ctx* c) {
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (auto& p : c->pending) {
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
+  }
+  for (auto e : c->evpool) cudaEventDestroy(e);
   cudaStream_t s = c->stream;
   delete c;  // frees workspaces
   if (s) cudaStreamDestroy(s);
@@ -976,6 +1140,54 @@ int ttg_ctx_rank(const ttg_ctx* c) { return c ? c->rank : -1; }
 int ttg_ctx_world(const ttg_ctx* c) { return c ? c->world : -1; }
 void* ttg_ctx_stream(const ttg_ctx* c) { return c ? (void*)c->stream : nullptr; }
 int64_t ttg_ctx_launch_count(const ttg_ctx* c) { return c ? c->launches : -1; }
+int ttg_ctx_set_profiling(ttg_ctx* c, int on) {
+  if (!c) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    prof_flush(c);
+    c->profiling = on != 0;
+  });
+}
+
+void ttg_ctx_reset_stats(ttg_ctx* c) {
+  if (!c) return;
+  try {
+    prof_flush(c);
+  } catch (...) {
+  }
+  c->kstats.clear();
+  c->h2d = c->d2h = 0;
+}
+
+int ttg_ctx_num_kernel_stats(ttg_ctx* c) {
+  if (!c) return -1;
+  int rc = guard(c, [&] { prof_flush(c); });
+  return rc == TTG_OK ? (int)c->kstats.size() : -rc;
+}
+
+int ttg_ctx_kernel_stat(ttg_ctx* c, int idx, char* name, int name_len, int64_t* launches, double* ms,
+                        double* bytes, double* flops) {
+  if (!c) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    prof_flush(c);
+    if (idx < 0 || idx >= (int)c->kstats.size()) fail(TTG_E_INDEX, "kernel stat index out of range");
+    const auto& st = c->kstats[idx];
+    if (name && name_len > 0) {
+      std::snprintf(name, (size_t)name_len, "%s", st.name.c_str());
+    }
+    if (launches) *launches = st.launches;
+    if (ms) *ms = st.ms;
+    if (bytes) *bytes = st.bytes;
+    if (flops) *flops = st.flops;
+  });
+}
+
+int ttg_ctx_io_bytes(const ttg_ctx* c, int64_t* h2d, int64_t* d2h) {
+  if (!c) return TTG_E_ARGUMENT;
+  if (h2d) *h2d = c->h2d;
+  if (d2h) *d2h = c->d2h;
+  return TTG_OK;
+}
+
 int ttg_ctx_synchronize(ttg_ctx* c) {
   return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
 }

@@ -25,6 +25,7 @@ struct EigResult {
   double delta;
   double lam_max;
   double dev;     // append Gram deviation
+  double lam_min_kept;  // smallest kept sigma^2
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -41,6 +42,8 @@ struct EigArgs {
   long long kmax;     // number of singular values of R = min(a, #columns)
   double* Wg;         // global scratch a x a (used when !in_smem)
   int in_smem;
+  int factor;         // 1: G holds an upper-triangular factor T (T^T T = R R^T); solve on W = T^T,
+                      //    column norms are sigma (not sigma^2)
   const double* delta_src;  // if non-null: delta = delta_mult * sqrt(*delta_src)
   double delta_mult;
   double tol;
@@ -60,7 +63,14 @@ __global__ void __launch_bounds__(kEigThreads) k_jacobi_eig(EigArgs p) {
   __shared__ int s_rot;
   __shared__ int s_sweeps;
 
-  for (long long e = threadIdx.x; e < (long long)a * a; e += blockDim.x) W[e] = p.G[e];
+  for (long long e = threadIdx.x; e < (long long)a * a; e += blockDim.x) {
+    if (p.factor) {
+      long long i = e % a, j = e / a;
+      W[e] = p.G[j + (long long)a * i];  // W = T^T
+    } else {
+      W[e] = p.G[e];
+    }
+  }
   __syncthreads();
 
   const int n = a + (a & 1);
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(kEigThreads) k_jacobi_eig(EigArgs p) {
     double s = 0.0;
     for (int i = lane; i < a; i += 32) s = fma(W[(size_t)j * a + i], W[(size_t)j * a + i], s);
     s = warp_sum(s);
-    if (lane == 0) nrm[j] = sqrt(s);
+    if (lane == 0) nrm[j] = sqrt(s);  // lambda_j (Gram) or sigma_j (factor)
   }
   __syncthreads();
   // descending stable rank sort
@@ -125,7 +135,10 @@ __global__ void __launch_bounds__(kEigThreads) k_jacobi_eig(EigArgs p) {
     perm[pos] = j;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < a; j += blockDim.x) p.lam[j] = nrm[perm[j]];
+  for (int j = threadIdx.x; j < a; j += blockDim.x) {
+    double v = nrm[perm[j]];
+    p.lam[j] = p.factor ? v * v : v;  // sigma_j^2, descending
+  }
   __shared__ int s_rank;
   if (threadIdx.x == 0) {
     double delta = p.delta_src ? p.delta_mult * sqrt(*p.delta_src) : p.delta_mult;
@@ -133,7 +146,8 @@ __global__ void __launch_bounds__(kEigThreads) k_jacobi_eig(EigArgs p) {
     double tail_sq = 0.0;
     long long rank = k;
     for (long long j = k - 1; j >= 0; --j) {  // truncated_svd.cpp:74-81
-      double next = tail_sq + nrm[perm[j]];   // sigma_j^2 = lambda_j
+      double sj = nrm[perm[j]];
+      double next = tail_sq + (p.factor ? sj * sj : sj);  // sigma_j^2
       if (sqrt(next) > delta) break;
       tail_sq = next;
       rank = j;
@@ -144,7 +158,10 @@ __global__ void __launch_bounds__(kEigThreads) k_jacobi_eig(EigArgs p) {
     p.res->delta = delta;
     p.res->converged = (s_sweeps < p.max_sweeps);
     p.res->sweeps = s_sweeps;
-    p.res->lam_max = a > 0 ? nrm[perm[0]] : 0.0;
+    double l0 = a > 0 ? nrm[perm[0]] : 0.0;
+    double lr = rank > 0 ? nrm[perm[rank - 1]] : 0.0;
+    p.res->lam_max = p.factor ? l0 * l0 : l0;
+    p.res->lam_min_kept = p.factor ? lr * lr : lr;
   }
   __syncthreads();
   const int rank = s_rank;
@@ -223,7 +240,7 @@ __global__ void __launch_bounds__(1024) k_append(AppendArgs p) {
   const int a = p.a, r0 = p.r_old, rr = p.r_R, rn = r0 + rr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (long long e = threadIdx.x; e < (long long)a * rn; e += blockDim.x) {
-    long long c = e / a, i = e - c * a;
+    long long c = e / a;
     p.out[e] = (c < r0) ? p.Upad[e] : p.UR[e - (long long)r0 * a];
   }
   __syncthreads();

@@ -87,6 +87,39 @@ __device__ __forceinline__ void load_tile_async(const TileSrc& s, long long q0, 
   }
 }
 
+// In-place residual of the warp's 8 tile columns: T_w -= U (U^T T_w), with U
+// given as DMMA A-fragments (k_make_frags); Pw is the warp's r8 x 8 scratch.
+__device__ __forceinline__ void tile_residual(double* T, int ldt, double* Pw, int ldp, const double* UTf,
+                                              const double* Uf, int KA, int KR, int MR, int nb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = warp * 8;
+  for (int mb = 0; mb < MR; ++mb) {  // P = U^T T_w   (r8 x 8)
+    double q0 = 0.0, q1 = 0.0;
+    const double* fa = UTf + ((long long)mb * KA) * 32 + lane;
+    for (int kb = 0; kb < KA; ++kb) {
+      double av = __ldg(fa + kb * 32);
+      double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+      dmma(q0, q1, av, bv);
+    }
+    Pw[(mb * 8 + g) + ldp * (2 * t)] = q0;
+    Pw[(mb * 8 + g) + ldp * (2 * t + 1)] = q1;
+  }
+  __syncwarp();
+  for (int ib = 0; ib < nb; ++ib) {  // T_w -= U P
+    double q0 = 0.0, q1 = 0.0;
+    const double* fa = Uf + ((long long)ib * KR) * 32 + lane;
+    for (int sb = 0; sb < KR; ++sb) {
+      double av = __ldg(fa + sb * 32);
+      double bv = Pw[(sb * 4 + t) + ldp * g];
+      dmma(q0, q1, av, bv);
+    }
+    T[(ib * 8 + g) + ldt * (c0 + 2 * t)] -= q0;
+    T[(ib * 8 + g) + ldt * (c0 + 2 * t + 1)] -= q1;
+  }
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------------------
 // Fused residual + Gram:  for every selected column x of cur (a x L):
 //     r = x - U (U^T x);     G += r r^T
@@ -106,6 +139,8 @@ struct GramArgs {
   int r8;             // 0 => no residual (empty basis)
   double* partials;   // [gridDim.x][SBD*SBD], SBD = 8*4*WBR >= a8
   long long n_tiles;
+  int r_old;          // host-side accounting only
+  double sel_frac;    // host-side accounting only
 };
 
 template <int WBR, int WBC>
@@ -149,32 +184,7 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
     __syncthreads();
 
     if (p.r8 > 0) {
-      const int c0 = warp * 8;
-      // P = U^T T_w   (r8 x 8)
-      for (int mb = 0; mb < MR; ++mb) {
-        double q0 = 0.0, q1 = 0.0;
-        const double* fa = p.UTf + ((long long)mb * KA) * 32 + lane;
-        for (int kb = 0; kb < KA; ++kb) {
-          double av = __ldg(fa + kb * 32);
-          double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
-          dmma(q0, q1, av, bv);
-        }
-        Pw[(mb * 8 + g) + ldp * (2 * t)] = q0;
-        Pw[(mb * 8 + g) + ldp * (2 * t + 1)] = q1;
-      }
-      __syncwarp();
-      // T_w -= U P
-      for (int ib = 0; ib < nb; ++ib) {
-        double q0 = 0.0, q1 = 0.0;
-        const double* fa = p.Uf + ((long long)ib * KR) * 32 + lane;
-        for (int sb = 0; sb < KR; ++sb) {
-          double av = __ldg(fa + sb * 32);
-          double bv = Pw[(sb * 4 + t) + ldp * g];
-          dmma(q0, q1, av, bv);
-        }
-        T[(ib * 8 + g) + ldt * (c0 + 2 * t)] -= q0;
-        T[(ib * 8 + g) + ldt * (c0 + 2 * t + 1)] -= q1;
-      }
+      tile_residual(T, ldt, Pw, ldp, p.UTf, p.Uf, KA, KR, MR, nb);
       __syncthreads();
     }
 
@@ -227,6 +237,116 @@ __global__ void k_gram_reduce(const double* __restrict__ partials, int nx, int s
     for (int x = 0; x < nx; ++x) s += src[(long long)x * sbd * sbd];
     G[e] = s;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Accurate path (small delta): TSQR R-factor of the residual.  With
+// R^T = Q T (T a x a upper triangular), T^T T = R R^T but T carries the
+// singular values of R unsquared, so the Jacobi solve on T^T resolves sigma
+// down to eps_mach |R| instead of sqrt(eps_mach) |R| (the Gram floor).
+// qr_update: T <- R-factor of [T; C] with C an m x a block given by strides
+// C(q, j) = C[q*sq + j*sj]; Householder per column (Eigen/LAPACK sign rule).
+// T is a x a column-major with leading dimension ldT (shared or global).
+// ---------------------------------------------------------------------------
+__device__ void qr_update(double* T, int ldT, double* C, int m, long long sq, long long sj, int a, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int j = 0; j < a; ++j) {
+    double ss = 0.0;
+    for (int q = threadIdx.x; q < m; q += blockDim.x) {
+      double v = C[q * sq + j * sj];
+      ss = fma(v, v, ss);
+    }
+    // block sum (deterministic)
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += red[w];
+      red[32] = s;
+    }
+    __syncthreads();
+    ss = red[32];
+    const double alpha = T[j + (long long)ldT * j];
+    if (ss == 0.0) {  // nothing below the diagonal: H = I
+      __syncthreads();
+      continue;
+    }
+    double beta = sqrt(alpha * alpha + ss);
+    if (alpha >= 0.0) beta = -beta;
+    const double tau = (beta - alpha) / beta;
+    const double scale = 1.0 / (alpha - beta);
+    // apply to columns c > j: w = T[j][c] + sum_q v_q C[q][c]; T[j][c] -= tau w; C[q][c] -= tau w v_q
+    for (int c = j + 1 + warp; c < a; c += nwarps) {
+      double w = 0.0;
+      for (int q = lane; q < m; q += 32) w = fma(C[q * sq + j * sj] * scale, C[q * sq + c * sj], w);
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      w += T[j + (long long)ldT * c];
+      const double f = tau * w;
+      if (lane == 0) T[j + (long long)ldT * c] -= f;
+      for (int q = lane; q < m; q += 32) C[q * sq + c * sj] -= f * (C[q * sq + j * sj] * scale);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) T[j + (long long)ldT * j] = beta;
+    for (int q = threadIdx.x; q < m; q += blockDim.x) C[q * sq + j * sj] = 0.0;
+    __syncthreads();
+  }
+}
+
+struct TsqrArgs {
+  TileSrc src;
+  int a8, ldt, ldp;
+  const double* UTf;
+  const double* Uf;
+  int r8;
+  double* Tout;  // [gridDim.x][a*a]
+  long long n_tiles;
+};
+
+// per-CTA T of the residual columns it owns (grid-stride over 64-column tiles)
+__global__ void __launch_bounds__(kThreads) k_tsqr_local(TsqrArgs p) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red[33];
+  const int a = p.src.a, ldt = p.ldt, ldp = p.ldp;
+  const int warp = threadIdx.x >> 5;
+  double* Tf = smem;                       // a x a factor (ld a)
+  double* Tl = smem + (size_t)a * a;       // tile a8 x 64 (ld ldt)
+  double* Pw = Tl + (size_t)ldt * kTC + warp * ldp * 8;
+  for (int i = threadIdx.x; i < a * a + ldt * kTC; i += kThreads) smem[i] = 0.0;
+  __syncthreads();
+  const int KA = p.a8 >> 2, KR = p.r8 >> 2, MR = p.r8 >> 3, nb = p.a8 >> 3;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    load_tile_async(p.src, tile * kTC, Tl, ldt);
+    cp_async_commit();
+    cp_async_wait_0();
+    __syncthreads();
+    if (p.r8 > 0) {
+      tile_residual(Tl, ldt, Pw, ldp, p.UTf, p.Uf, KA, KR, MR, nb);
+      __syncthreads();
+    }
+    // rows of R^T are the tile's columns: C(q, j) = Tl[j + ldt*q]
+    qr_update(Tf, a, Tl, kTC, ldt, 1, a, red);
+  }
+  double* out = p.Tout + (long long)blockIdx.x * a * a;
+  for (int i = threadIdx.x; i < a * a; i += kThreads) out[i] = Tf[i];
+}
+
+// T <- R-factor of the stacked factors Ts[0..n-1] (each a x a), fixed order.
+__global__ void __launch_bounds__(1024) k_tsqr_combine(const double* __restrict__ Ts, int n, int a,
+                                                      double* __restrict__ scratch, double* __restrict__ T) {
+  extern __shared__ __align__(16) double sm2[];
+  __shared__ double red[33];
+  double* Tf = sm2;  // a x a
+  for (int i = threadIdx.x; i < a * a; i += blockDim.x) Tf[i] = Ts[i];
+  __syncthreads();
+  for (int k = 1; k < n; ++k) {
+    double* C = scratch;  // copy (qr_update overwrites the block)
+    for (int i = threadIdx.x; i < a * a; i += blockDim.x) C[i] = Ts[(long long)k * a * a + i];
+    __syncthreads();
+    qr_update(Tf, a, C, a, 1, a, a, red);  // C(q, j) = C[q + a*j]
+  }
+  for (int i = threadIdx.x; i < a * a; i += blockDim.x) T[i] = Tf[i];
 }
 
 // ---------------------------------------------------------------------------

@@ -68,7 +68,6 @@ __global__ void k_sumsq_obs(const double* __restrict__ Y, long long S, int nchun
 // on2[o] = sum of chunk partials (fixed order); out_total = sum_o on2[o].
 __global__ void k_sumsq_finalize(const double* __restrict__ part, int nchunk, int nobs,
                                  double* __restrict__ on2, double* __restrict__ total) {
-  __shared__ double red[33];
   double s = 0.0;
   for (int o = threadIdx.x; o < nobs; o += blockDim.x) {
     double v = 0.0;

@@ -93,6 +93,32 @@ class Context:
     def launch_count(self) -> int:
         return int(_lib.load().ttg_ctx_launch_count(self._h))
 
+    def set_profiling(self, on: bool) -> None:
+        _check(_lib.load().ttg_ctx_set_profiling(self._h, int(bool(on))), self)
+
+    def reset_stats(self) -> None:
+        _lib.load().ttg_ctx_reset_stats(self._h)
+
+    def kernel_stats(self) -> list:
+        """[{name, launches, ms, bytes, flops}] accumulated since reset_stats()."""
+        lib = _lib.load()
+        n = lib.ttg_ctx_num_kernel_stats(self._h)
+        if n < 0:
+            _check(-n, self)
+        out = []
+        for i in range(n):
+            name = ctypes.create_string_buffer(64)
+            la, ms, by, fl = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+            _check(lib.ttg_ctx_kernel_stat(self._h, i, name, 64, ctypes.byref(la), ctypes.byref(ms), ctypes.byref(by),
+                                           ctypes.byref(fl)), self)
+            out.append(dict(name=name.value.decode(), launches=la.value, ms=ms.value, bytes=by.value, flops=fl.value))
+        return out
+
+    def io_bytes(self):
+        h, d = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.load().ttg_ctx_io_bytes(self._h, ctypes.byref(h), ctypes.byref(d)), self)
+        return h.value, d.value
+
     def synchronize(self) -> None:
         _check(_lib.load().ttg_ctx_synchronize(self._h), self)
 
