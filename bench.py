@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: stream GB/s ingested (FP64) by the TT-ICE* per-increment update.
+
+Workload (BASELINE.json configs[3] per GPU, configs[4] at 8 GPUs): the cfg3
+generator (8^7 spatial modes, eps 0.01, TT-ICE* with default heuristics,
+odd increments in-span -> skip path, even increments add a new direction ->
+update path), batch 256 observations per GPU (weak scaling: the global batch
+is 256*N, = configs[4]'s 2048 at N=8).  A "step" is one TT-ICE* update of
+one increment; increments are pre-generated in HBM before the timed region
+(4.29 GB each per GPU, > L2, so no flush is needed).
+
+``--impl reference`` times the CPU oracle (oracle/, the reference restated;
+the reference itself cannot be built here) on the same stream
+with a bounded batch per step, on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stream GB/s ingested (FP64)"
+MODES = (8,) * 7
+EPS = 0.01
+PEAK_FP64_TFLOPS = 37.0  # measured DMMA m8n8k4 peak on this pool (profiles/r01_box_probe.log)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                bits = int(r[2], 16)
+                for b, name in REASON_BITS.items():
+                    if bits & b and name != "gpu_idle":
+                        reasons.add(name)
+            except ValueError:
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle on the host
+# ---------------------------------------------------------------------------
+def cpu_oracle_run(steps: int, warmup: int, batch: int, seed: int, budget_s: float = None):
+    """Oracle TT-ICE* on the cfg3 stream with `batch` observations per step.
+    Returns (GB/s, seconds, n_steps_timed, bytes)."""
+    from oracle import ttstream_oracle as O
+    from paper_2211_12487_b200.streams import Stream
+
+    s = Stream(3, seed=seed, batch=batch)
+    tt, _ = O.tt_ice_bootstrap(s.increment(0), EPS)
+    k = 1
+    for _ in range(warmup):
+        tt, _ = O.tt_ice_star_update(tt, s.increment(k), EPS)
+        k += 1
+    tot_t, tot_b, n = 0.0, 0, 0
+    for _ in range(steps):
+        y = s.increment(k)
+        t0 = time.perf_counter()
+        tt, _ = O.tt_ice_star_update(tt, y, EPS)
+        tot_t += time.perf_counter() - t0
+        tot_b += y.nbytes
+        n += 1
+        k += 1
+        if budget_s is not None and tot_t >= budget_s and n >= 2:
+            break
+    return tot_b / tot_t / 1e9, tot_t, n, tot_b
+
+
+def reference_arm(args):
+    cores = os.cpu_count()
+    batch = args.ref_batch
+    gbs, secs, n, nbytes = cpu_oracle_run(args.steps, args.warmup, batch, args.seed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(n, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, batch_override=batch),
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle (numpy/OpenBLAS restatement of the reference) TT-ICE* on the cfg3 stream, "
+                                   f"batch {batch} per step (bounded sample of the 256-obs increment), "
+                                   f"{n} timed steps after {args.warmup} warm-up"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, batch_override=None, world=1):
+    b = batch_override or args.batch
+    return {"workload": "cfg3 TT-ICE* stream (BASELINE configs[3]; configs[4] at 8 GPUs)",
+            "modes": list(MODES), "batch_per_gpu": b, "global_batch": b * world, "eps_des": EPS,
+            "algo": "tt_ice_star", "heuristics": "default (tau 0.8, skip, subselect, mean)",
+            "seed": args.seed, "increment_bytes_per_gpu": 8 * int(np.prod(MODES)) * b,
+            "l2": "inputs larger than L2 (one 4.29 GB increment per step per GPU), no flush",
+            "parallelism": f"dp{world} (batch sharded; Grams all-reduced over NCCL)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def our_arm(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2211_12487_b200 import Context, tt_ice_bootstrap, tt_ice_star_update
+    from paper_2211_12487_b200.streams import DeviceStream
+
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(Context.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        ctx = Context(local_rank, rank=rank, world=world, nccl_id=bytes(idt.cpu().numpy().tobytes()))
+    else:
+        ctx = Context(local_rank)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    b = args.batch
+    S = int(np.prod(MODES))
+    inc_bytes = 8 * S * b
+    gen = DeviceStream(seed=args.seed, modes=MODES, rank_shard=rank)
+    free, _total = torch.cuda.mem_get_info()
+    reserve = 24 << 30
+    cap = max(2, int((free - reserve) // inc_bytes))
+    n_inc = 1 + args.warmup + args.steps
+    pool = min(n_inc, cap)
+    ys = [gen.increment(k, b) for k in range(pool)]
+    torch.cuda.synchronize()
+
+    def inc(k):
+        return ys[k % pool] if k >= pool else ys[k]
+
+    shape = MODES + (b,)
+    tt, _ = tt_ice_bootstrap(ys[0], EPS, ctx=ctx, shape=shape)
+    k = 1
+    for _ in range(args.warmup):
+        tt, _ = tt_ice_star_update(tt, inc(k), EPS, shape=shape)
+        k += 1
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    launches0 = ctx.launch_count
+    sampler = ClockSampler(local_rank)
+    barrier()
+    sampler.start()
+    time.sleep(0.3)
+    ev0.record(stream)
+    reports = []
+    for _ in range(args.steps):
+        tt, rep = tt_ice_star_update(tt, inc(k), EPS, shape=shape)
+        reports.append(rep)
+        k += 1
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count - launches0
+    kstats = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_bytes = inc_bytes * world * args.steps
+    value = total_bytes / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (largest device time in the timed region)
+    peaks = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    dom = max(kstats, key=lambda s: s["ms"]) if kstats else None
+    roof = None
+    if dom and dom["ms"] > 0:
+        t_hbm = dom["bytes"] / (hbm * 1e9)
+        t_fp = dom["flops"] / (PEAK_FP64_TFLOPS * 1e12)
+        sec = dom["ms"] * 1e-3
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(dom["name"])
+            except Exception:
+                traffic = None
+        if t_hbm >= t_fp:
+            ach = dom["bytes"] / sec / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+        else:
+            ach = dom["flops"] / sec / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / PEAK_FP64_TFLOPS,
+                    "peak_source": "measured FP64 DMMA peak (profiles/r01_box_probe.log); MEASURED_PEAKS.json has no FP64"}
+        roof.update({"kernel": dom["name"], "launches": dom["launches"], "kernel_ms_total": dom["ms"],
+                     "share_of_step": dom["ms"] / ms, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": dom["bytes"] / dom["launches"],
+                     "algorithmic_flops_per_launch": dom["flops"] / dom["launches"]})
+        # whole-step roofline: sum over kernels of max(bytes/BW, flops/peak)
+        t_roof = sum(max(s["bytes"] / (hbm * 1e9), s["flops"] / (PEAK_FP64_TFLOPS * 1e12)) for s in kstats)
+        roof["step_roofline_frac"] = t_roof / (ms * 1e-3)
+
+    # end-to-end through the public API with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.e2e_steps, args.steps))
+        hosts = []
+        for j in range(e2e_steps):
+            d = gen.increment(k + j, b)
+            h = torch.empty(d.numel(), dtype=torch.float64, pin_memory=True)
+            h.copy_(d)
+            hosts.append(np.reshape(h.numpy(), shape, order="F"))
+            del d
+        torch.cuda.synchronize()
+        for y in ys:  # release device pool before the host-buffer phase
+            del y
+        ys.clear()
+        io0 = ctx.io_bytes()
+        barrier()
+        t0 = time.perf_counter()
+        for j in range(e2e_steps):
+            tt, rep = tt_ice_star_update(tt, hosts[j], EPS)
+            _ = rep.batch_rel_error_estimate  # result read back on the host
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        io1 = ctx.io_bytes()
+        e2e = {"value": inc_bytes * world * e2e_steps / el / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": (io1[0] - io0[0]) // e2e_steps, "d2h_bytes_per_step": (io1[1] - io0[1]) // e2e_steps,
+               "steps": e2e_steps, "path": "ttstream.tt_ice_star_update(numpy pinned host array) -> ttg C ABI (TTG_HOST)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gbs, secs, n, nbytes = cpu_oracle_run(steps=6, warmup=1, batch=args.cpu_batch, seed=args.seed, budget_s=20.0)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"oracle TT-ICE* on the cfg3 stream at batch {args.cpu_batch} (of 256), {n} steps, "
+                         f"{secs:.1f} s, numpy/OpenBLAS on all host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg3 generator, DESIGN.md §6)",
+            "config": workload_config(args, world=world),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "per_gpu_gbs": value / world,
+            "steps_detail": [{"obs_used": r.obs_used, "ranks": r.ranks_after, "modes_updated": r.modes_updated}
+                             for r in reports],
+            "kernels": sorted([{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in s.items()}
+                               for s in kstats], key=lambda s: -s["ms"])[:8],
+            "pool_increments": pool,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--cpu-batch", type=int, default=8)
+    ap.add_argument("--ref-batch", type=int, default=4)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        reference_arm(args)
+        return
+    our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

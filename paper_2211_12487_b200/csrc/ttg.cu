@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -374,6 +375,9 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
   CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   EigResult r = *c->h_eig;
+  if (std::getenv("TTG_DEBUG"))
+    std::fprintf(stderr, "[ttg] eig a=%d factor=%d smem=%d rank=%d sweeps=%d lam_max=%.3e delta=%.3e\n", a, factor,
+                 args.in_smem, r.rank, r.sweeps, r.lam_max, r.delta);
   if (!r.converged) fail(TTG_E_NUMERIC, "svd_trunc: Jacobi eigen-solve failed to converge on " +
                                             std::to_string(a) + "x" + std::to_string(a) + " Gram");
   return r;
