@@ -30,6 +30,7 @@
 #include "ttg_eig.cuh"
 #include "ttg_kernels.cuh"
 #include "ttg_misc.cuh"
+#include "ttg_syev.cuh"
 
 namespace {
 
@@ -104,7 +105,10 @@ struct ttg_ctx {
   size_t smem_optin = 232448;
   // workspaces (grow-only)
   DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, Uf, Upad, scratch, eigres, on2, sumsq_part,
-      scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2];
+      scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2], tsq, psif, wcomb, psi[2],
+      spsi[2], scoeffs, matbuf;
+  std::vector<DevBuf> scur;       // TT-ICE* stats-chain intermediates (reused by the sweep)
+  std::vector<bool> stat_has;
   ttg::EigResult* h_eig = nullptr;
   double* h_scal = nullptr;
   ttg::StarStats* h_stats = nullptr;
@@ -264,125 +268,227 @@ void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long
 constexpr int kFastMax = 128;  // a8 / r8 limit of the fused DMMA tiles
 
 // ---- residual Gram -----------------------------------------------------------
-// G (a x a) = sum over selected columns x of X (a x L): (x - U U^T x)(...)^T
-template <int WBR, int WBC>
-void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem) {
-  auto kern = ttg::k_gram_resid<WBR, WBC>;
+constexpr int kFastMax1 = 256;  // a8 limit of the single-buffered DMMA tiles
+
+template <int WBR, int WBC, bool PRE, bool DB>
+void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem, int npairs) {
+  auto kern = ttg::k_gram_resid<WBR, WBC, PRE, DB>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem));
   if (occ < 1) fail(TTG_E_RESOURCE, "gram kernel does not fit on an SM");
-  long long want = (long long)c->num_sms * occ;
+  long long want = std::max<long long>(1, (long long)c->num_sms * occ / npairs);
   int gx = (int)std::min<long long>(want, std::max<long long>(1, args.n_tiles));
+  if (args.tsumsq) gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
   constexpr int SBD = 8 * 4 * WBR;
-  c->partials.ensure(sizeof(double) * (size_t)gx * SBD * SBD);
+  c->partials.ensure(sizeof(double) * (size_t)npairs * gx * SBD * SBD);
   ttg::GramArgs a2 = args;
   a2.partials = c->partials.as<double>();
   {
     const double Ls = (double)args.src.L * args.sel_frac;
-    const double a_ = args.src.a, r_ = args.r_old;
-    prof_begin(c, "k_gram_resid", 8.0 * a_ * Ls, Ls * (4.0 * r_ * a_ + a_ * a_));
+    const double a_ = args.a, r_ = args.r_old;
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "%s[a=%d,r=%d]", PRE ? "k_gram_resid_pre" : "k_gram_resid", args.a, args.r_old);
+    prof_begin(c, nm, 8.0 * args.src.a * Ls, Ls * (4.0 * r_ * a_ + a_ * a_));
   }
-  kern<<<gx, ttg::kThreads, smem, c->stream>>>(a2);
+  kern<<<dim3(gx, npairs), ttg::kThreads, smem, c->stream>>>(a2);
   post_launch(c);
-  int a = args.src.a;
-  long long n = (long long)a * a;
-  prof_begin(c, "k_gram_reduce", 8.0 * gx * SBD * SBD, (double)gx * a * a);
+  const int a = args.a;
+  const long long n = (long long)a * a;
+  prof_begin(c, "k_gram_reduce", 8.0 * npairs * gx * SBD * SBD, (double)gx * a * a);
   ttg::k_gram_reduce<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, SBD, a,
                                                                       c->G.as<double>());
   post_launch(c);
 }
 
-void gram(ttg_ctx* c, const double* X, int a, long long L, const double* U, int r_old, int ldu,
-          const uint8_t* sel, long long cpo, double sel_frac = 1.0) {
-  int a8 = ttg::round_up(a, 8);
-  int r8 = r_old > 0 ? ttg::round_up(r_old, 8) : 0;
+// The current unfolding cur_i (a_i x L_i) over a stored buffer:
+//   cur_i = (I_n (x) Psi^T) (S viewed as (As*n) x (Ls/n)),   a_i = r*n, L_i = Ls/n.
+// Psi == nullptr means identity (r == As): cur_i is S itself.  Mode 1 is
+// {Y, As = 1, Ls = N}.  Keeping Psi pending instead of materialising cur_i
+// lets mode i be read straight from the buffer of an earlier mode.
+struct Src {
+  const double* S = nullptr;
+  int64_t As = 1, Ls = 0;
+  const double* Psi = nullptr;
+  int64_t r = 1;
+};
+
+// per-tile sums of squares are only usable when tiles never straddle observations
+bool tiles_align(int64_t rows, int64_t obs_elems) { return obs_elems % (rows * ttg::kTC) == 0; }
+
+// Fused residual Gram of cur_i into c->G.  `tsq` (nullable): per-tile sums of
+// squares of the source tiles (only when the fast path runs; returns whether
+// they were produced).
+bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, const uint8_t* sel, long long cpo,
+              double sel_frac, double* tsq) {
+  const int a = (int)(s.r * n);
+  const long long L = s.Ls / n;
+  const int a8 = ttg::round_up(a, 8);
+  const int r8 = r_old > 0 ? ttg::round_up(r_old, 8) : 0;
   c->G.ensure(sizeof(double) * (size_t)a * a);
-  if (a8 <= kFastMax && r8 <= kFastMax) {
-    if (r_old > 0) make_frags(c, U, a, r_old, ldu, true, true);
-    ttg::GramArgs args{};
-    args.src = ttg::TileSrc{X, a, L, sel, cpo};
-    args.a8 = a8;
-    args.ldt = ttg::smem_ld(a8);
-    args.ldp = ttg::smem_ld(std::max(r8, 8));
+  ttg::GramArgs args{};
+  args.a = a;
+  args.a8 = a8;
+  args.r8 = r8;
+  args.r_old = r_old;
+  args.sel_frac = sel_frac;
+  args.ldt = ttg::smem_ld(a8);
+  args.ldp = ttg::smem_ld(std::max(r8, 8));
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  args.tsumsq = tsq;
+  if (s.Psi) {
+    const int src_rows = (int)(s.As * n);
+    if (src_rows > kFastMax || a8 > kFastMax || r8 > kFastMax)
+      fail(TTG_E_RESOURCE, "internal: pre-projected Gram outside the fast path");
+    if (r_old > 0) make_frags(c, U, a, r_old, a, true, true);
+    // Psi^T fragments into their own buffer
+    const int As8 = ttg::round_up((int)s.As, 8), rc8 = ttg::round_up((int)s.r, 8);
+    const size_t nf = (size_t)(rc8 / 8) * (As8 / 4) * 32;
+    c->psif.ensure(sizeof(double) * nf);
+    prof_begin(c, "k_make_frags", 8.0 * nf, 0.0);
+    ttg::k_make_frags<<<grid_for((long long)nf, 256, 1024), 256, 0, c->stream>>>(
+        s.Psi, (int)s.As, (int)s.r, (int)s.As, As8, rc8, c->psif.as<double>(), nullptr);
+    post_launch(c);
+    args.src = ttg::TileSrc{s.S, src_rows, L, sel, cpo};
+    args.lds = ttg::smem_ld(src_rows + As8 + 8);
+    args.As = (int)s.As;
+    args.nblk = (int)n;
+    args.rc = (int)s.r;
+    args.MRC = rc8 / 8;
+    args.KS = As8 / 4;
+    args.PsiTf = c->psif.as<double>();
     args.UTf = c->UTf.as<double>();
     args.Uf = c->Uf.as<double>();
-    args.r8 = r8;
-    args.r_old = r_old;
-    args.sel_frac = sel_frac;
-    args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
-    size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
-    int nb = a8 / 8;
-    if (nb <= 4) launch_gram_t<1, 2>(c, args, smem);
-    else if (nb <= 8) launch_gram_t<2, 4>(c, args, smem);
-    else if (nb <= 12) launch_gram_t<3, 6>(c, args, smem);
-    else launch_gram_t<4, 8>(c, args, smem);
-  } else {
-    // generic: R = X - U (U^T X) materialised, masked, then G = R R^T
-    c->scratch.ensure(sizeof(double) * (size_t)a * L);
-    double* R = c->scratch.as<double>();
-    CK(cudaMemcpyAsync(R, X, sizeof(double) * (size_t)a * L, cudaMemcpyDeviceToDevice, c->stream));
-    if (r_old > 0) {
-      c->W.ensure(sizeof(double) * (size_t)r_old * L);
-      double* P = c->W.as<double>();
-      gemm<true, false>(c, U, ldu, X, a, P, r_old, r_old, L, a, 1.0, 0.0);
-      gemm<false, false>(c, U, ldu, P, r_old, R, a, a, L, r_old, -1.0, 1.0);
-    }
-    if (sel) {
-      prof_begin(c, "k_mask_cols", 16.0 * a * L, 0.0);
-      ttg::k_mask_cols<<<grid_for((long long)a * L, 256, 4096), 256, 0, c->stream>>>(R, a, L, sel, cpo);
-      post_launch(c);
-    }
-    gemm<false, true>(c, R, a, R, a, c->G.as<double>(), a, a, a, L, 1.0, 0.0);
+    const size_t smem = sizeof(double) * ((size_t)2 * args.lds * ttg::kTC + (size_t)args.ldt * ttg::kTC +
+                                          (size_t)8 * args.ldp * 8);
+    const int nb = a8 / 8;
+    if (nb <= 4) launch_gram_t<1, 2, true, true>(c, args, smem, 1);
+    else if (nb <= 8) launch_gram_t<2, 4, true, true>(c, args, smem, 1);
+    else if (nb <= 12) launch_gram_t<3, 6, true, true>(c, args, smem, 1);
+    else launch_gram_t<4, 8, true, true>(c, args, smem, 1);
+    allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+    return tsq != nullptr;
   }
+  const double* X = s.S;
+  args.src = ttg::TileSrc{X, a, L, sel, cpo};
+  if (a8 <= kFastMax1 && r8 <= kFastMax) {
+    if (r_old > 0) make_frags(c, U, a, r_old, a, true, true);
+    args.UTf = c->UTf.as<double>();
+    args.Uf = c->Uf.as<double>();
+    const int nb = a8 / 8;
+    if (a8 <= kFastMax) {
+      const size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+      if (nb <= 4) launch_gram_t<1, 2, false, true>(c, args, smem, 1);
+      else if (nb <= 8) launch_gram_t<2, 4, false, true>(c, args, smem, 1);
+      else if (nb <= 12) launch_gram_t<3, 6, false, true>(c, args, smem, 1);
+      else launch_gram_t<4, 8, false, true>(c, args, smem, 1);
+    } else {
+      const int ns = (nb + 15) / 16;
+      const size_t smem = sizeof(double) * ((size_t)args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+      launch_gram_t<4, 8, false, false>(c, args, smem, ns * (ns + 1) / 2);
+    }
+    allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+    return tsq != nullptr;
+  }
+  // generic: R = X - U (U^T X) materialised, masked, then G = R R^T
+  c->scratch.ensure(sizeof(double) * (size_t)a * L);
+  double* R = c->scratch.as<double>();
+  CK(cudaMemcpyAsync(R, X, sizeof(double) * (size_t)a * L, cudaMemcpyDeviceToDevice, c->stream));
+  if (r_old > 0) {
+    c->W.ensure(sizeof(double) * (size_t)r_old * L);
+    double* P = c->W.as<double>();
+    gemm<true, false>(c, U, a, X, a, P, r_old, r_old, L, a, 1.0, 0.0);
+    gemm<false, false>(c, U, a, P, r_old, R, a, a, L, r_old, -1.0, 1.0);
+  }
+  if (sel) {
+    prof_begin(c, "k_mask_cols", 16.0 * a * L, 0.0);
+    ttg::k_mask_cols<<<grid_for((long long)a * L, 256, 4096), 256, 0, c->stream>>>(R, a, L, sel, cpo);
+    post_launch(c);
+  }
+  gemm<false, true>(c, R, a, R, a, c->G.as<double>(), a, a, a, L, 1.0, 0.0);
   allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+  return false;
 }
 
 // ---- eigen-solve -------------------------------------------------------------
+// factor == 0: G is the residual Gram -> tridiagonal solver (k_syev).
+// factor == 1: G holds the TSQR factor T -> one-sided Jacobi on T^T (k_jacobi_eig).
 EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double delta_mult, int factor = 0) {
   c->UR.ensure(sizeof(double) * (size_t)a * a);
   c->lam.ensure(sizeof(double) * a);
   c->eigres.ensure(sizeof(EigResult));
-  size_t need_smem = sizeof(double) * ((size_t)a * a + a) + sizeof(int) * a + 64;
-  ttg::EigArgs args{};
-  args.G = c->G.as<double>();
-  args.a = a;
-  args.factor = factor;
-  args.kmax = kmax;
-  args.delta_src = delta_src;
-  args.delta_mult = delta_mult;
-  args.tol = 2.220446049250313e-16 * std::max(8, a);
-  args.max_sweeps = 60;
-  args.UR = c->UR.as<double>();
-  args.lam = c->lam.as<double>();
-  args.res = c->eigres.as<EigResult>();
-  size_t smem;
-  if (need_smem <= c->smem_optin) {
-    args.in_smem = 1;
-    args.Wg = nullptr;
-    smem = need_smem;
+  if (!factor) {
+    ttg::SyevArgs args{};
+    args.G = c->G.as<double>();
+    args.a = a;
+    args.kmax = kmax;
+    args.delta_src = delta_src;
+    args.delta_mult = delta_mult;
+    args.UR = c->UR.as<double>();
+    args.lam = c->lam.as<double>();
+    c->Mtmp.ensure(sizeof(double) * (size_t)32 * 6 * a);
+    args.zbuf = c->Mtmp.as<double>();
+    args.res = c->eigres.as<EigResult>();
+    size_t vec = sizeof(double) * (size_t)7 * a;
+    size_t smem = sizeof(double) * (size_t)a * a + vec;
+    if (smem <= c->smem_optin) {
+      args.in_smem = 1;
+    } else {
+      args.in_smem = 0;
+      c->W.ensure(sizeof(double) * (size_t)a * a);
+      args.Ag = c->W.as<double>();
+      smem = vec;
+    }
+    CK(cudaFuncSetAttribute(ttg::k_syev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "k_syev[a=%d]", a);
+    prof_begin(c, nm, 16.0 * a * a, 4.0 / 3.0 * a * a * a);
+    ttg::k_syev<<<1, ttg::kSyevThreads, smem, c->stream>>>(args);
+    post_launch(c);
   } else {
-    args.in_smem = 0;
-    c->W.ensure(sizeof(double) * (size_t)a * a);
-    args.Wg = c->W.as<double>();
-    smem = sizeof(double) * a + sizeof(int) * a + 64;
+    size_t need_smem = sizeof(double) * ((size_t)a * a + a) + sizeof(int) * a + 64;
+    ttg::EigArgs args{};
+    args.G = c->G.as<double>();
+    args.a = a;
+    args.factor = factor;
+    args.kmax = kmax;
+    args.delta_src = delta_src;
+    args.delta_mult = delta_mult;
+    args.tol = 2.220446049250313e-16 * std::max(8, a);
+    args.max_sweeps = 60;
+    args.UR = c->UR.as<double>();
+    args.lam = c->lam.as<double>();
+    args.res = c->eigres.as<EigResult>();
+    size_t smem;
+    if (need_smem <= c->smem_optin) {
+      args.in_smem = 1;
+      args.Wg = nullptr;
+      smem = need_smem;
+    } else {
+      args.in_smem = 0;
+      c->W.ensure(sizeof(double) * (size_t)a * a);
+      args.Wg = c->W.as<double>();
+      smem = sizeof(double) * a + sizeof(int) * a + 64;
+    }
+    CK(cudaFuncSetAttribute(ttg::k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    prof_begin(c, "k_jacobi_eig", 16.0 * a * a, 0.0);
+    ttg::k_jacobi_eig<<<1, ttg::kEigThreads, smem, c->stream>>>(args);
+    post_launch(c);
   }
-  CK(cudaFuncSetAttribute(ttg::k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  prof_begin(c, "k_jacobi_eig", 16.0 * a * a, 0.0);
-  ttg::k_jacobi_eig<<<1, ttg::kEigThreads, smem, c->stream>>>(args);
-  post_launch(c);
   c->d2h += sizeof(EigResult);
   CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   EigResult r = *c->h_eig;
   if (std::getenv("TTG_DEBUG"))
-    std::fprintf(stderr, "[ttg] eig a=%d factor=%d smem=%d rank=%d sweeps=%d lam_max=%.3e delta=%.3e\n", a, factor,
-                 args.in_smem, r.rank, r.sweeps, r.lam_max, r.delta);
+    std::fprintf(stderr,
+                 "[ttg] eig a=%d factor=%d rank=%d sweeps=%d lam_max=%.3e lam_min_kept=%.3e delta=%.3e "
+                 "cycles tri=%lld val=%lld vec=%lld n_lam=%lld\n",
+                 a, factor, r.rank, r.sweeps, r.lam_max, r.lam_min_kept, r.delta, r.t_phase[0], r.t_phase[1],
+                 r.t_phase[2], r.t_phase[3]);
   if (!r.converged) fail(TTG_E_NUMERIC, "svd_trunc: Jacobi eigen-solve failed to converge on " +
-                                            std::to_string(a) + "x" + std::to_string(a) + " Gram");
+                                            std::to_string(a) + "x" + std::to_string(a) + " matrix");
   return r;
 }
-
 
 // ---- accurate path: TSQR factor + Jacobi on T^T ---------------------------------
 bool accurate_supported(int a, int r_old) {
@@ -456,11 +562,13 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
 }
 
 // ---- projection --------------------------------------------------------------
-void project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out) {
-  int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
-  if (a8 > kFastMax || r8 > kFastMax) {
+// out (r x L) = W^T X  (X: a x L, W: a x r with leading dimension ldw)
+bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
+             double* tsq = nullptr) {
+  const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
+  if (a8 > kFastMax1 || r8 > kFastMax) {
     gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
-    return;
+    return false;
   }
   make_frags(c, W, a, r, ldw, true, false);
   ttg::ProjArgs args{};
@@ -471,16 +579,54 @@ void project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   args.r = r;
   args.r8 = r8;
   args.out = out;
+  args.tsumsq = tsq;
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
-  size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)r * ttg::kTC);
-  CK(cudaFuncSetAttribute(ttg::k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const bool db = a8 <= kFastMax;
+  const size_t smem = sizeof(double) * ((size_t)(db ? 2 : 1) * args.ldt * ttg::kTC + (size_t)r * ttg::kTC);
+  auto kern = db ? ttg::k_project<true> : ttg::k_project<false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttg::k_project, ttg::kThreads, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem));
   occ = std::max(occ, 1);
-  int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
-  prof_begin(c, "k_project", 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
-  ttg::k_project<<<gx, ttg::kThreads, smem, c->stream>>>(args);
+  const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
+  prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
+  kern<<<gx, ttg::kThreads, smem, c->stream>>>(args);
   post_launch(c);
+  return tsq != nullptr;
+}
+
+// W' = (I_n (x) Psi) U : (As*n) x rn, the combined interface matrix of the
+// pending pre-projection and U (a = r*n rows).  One small GEMM:
+// Psi (As x r) * U viewed as r x (n*rn)  ->  As x (n*rn) == (As*n) x rn.
+const double* combine_psi(ttg_ctx* c, const Src& s, int64_t n, const double* U, int64_t rn, DevBuf& dst) {
+  dst.ensure(sizeof(double) * (size_t)(s.As * n * rn));
+  gemm<false, false>(c, s.Psi, s.As, U, s.r, dst.as<double>(), s.As, s.As, n * rn, s.r, 1.0, 0.0);
+  return dst.as<double>();
+}
+
+// out (rn x L_i) = U^T cur_i   (U: a_i x rn, ld a_i), through the pending Psi
+bool project_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int64_t rn, double* out, double* tsq) {
+  const long long L = s.Ls / n;
+  if (!s.Psi) return project(c, s.S, (int)(s.As * n), L, U, (int)rn, (int)(s.As * n), out, tsq);
+  const double* W = combine_psi(c, s, n, U, rn, c->wcomb);
+  return project(c, s.S, (int)(s.As * n), L, W, (int)rn, (int)(s.As * n), out, tsq);
+}
+
+// materialise cur_i itself (accurate path on a pre-projected source)
+const double* materialise(ttg_ctx* c, const Src& s, int64_t n, DevBuf& dst) {
+  if (!s.Psi) return s.S;
+  const int64_t rows = s.As * n, a = s.r * n;
+  c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
+  prof_begin(c, "k_kron_eye", 8.0 * rows * a, 0.0);
+  ttg::k_kron_eye<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, (int)s.As, (int)s.r, (int)n,
+                                                                         c->wcomb.as<double>());
+  post_launch(c);
+  const long long L = s.Ls / n;
+  dst.ensure(sizeof(double) * (size_t)(a * L));
+  project(c, s.S, (int)rows, L, c->wcomb.as<double>(), (int)a, (int)rows, dst.as<double>());
+  return dst.as<double>();
 }
 
 // ---- helpers -----------------------------------------------------------------
@@ -592,7 +738,9 @@ struct SweepOpts {
   const double* delta_src = nullptr;  // delta = mult * sqrt(*src) (uniform) ...
   double delta_mult = 0.0;
   const double* deltas = nullptr;     // ... or per-mode absolute deltas (host)
-  double y_norm = 0.0;
+  double y_norm = 0.0;                // known only for the per-mode-delta API
+  bool need_norms = false;            // fuse |y_o|^2 into the first pass over Y
+  bool reuse_stats = false;           // TT-ICE*: intermediates of the stats chain are valid
 };
 
 struct SweepOut {
@@ -605,74 +753,124 @@ struct SweepOut {
   int r_d = 0;
 };
 
-SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o) {
+// Norms of the increment: fused into the first kernel that streams Y (per-tile
+// sums of squares, then a fixed-order per-observation reduction), or a
+// separate pass when tiles would straddle observations.
+struct Norms {
+  bool pending = false;
+  const double* Y = nullptr;
+  int64_t S = 0, b = 0;
+};
+
+double* norms_tiles_for(ttg_ctx* c, Norms& nm, const double* src, int64_t rows, long long L) {
+  if (!nm.pending || src != nm.Y) return nullptr;
+  if (!tiles_align(rows, nm.S)) {
+    obs_norms(c, nm.Y, nm.S, (int)nm.b);
+    nm.pending = false;
+    return nullptr;
+  }
+  const long long nt = (L + ttg::kTC - 1) / ttg::kTC;
+  c->tsq.ensure(sizeof(double) * (size_t)nt);
+  return c->tsq.as<double>();
+}
+
+void norms_finish(ttg_ctx* c, Norms& nm, int64_t rows, bool produced) {
+  if (!produced) {
+    obs_norms(c, nm.Y, nm.S, (int)nm.b);
+  } else {
+    c->on2.ensure(sizeof(double) * nm.b);
+    c->scal.ensure(sizeof(double) * 16);
+    const long long tpo = nm.S / (rows * ttg::kTC);
+    prof_begin(c, "k_tiles_to_obs", 8.0 * tpo * nm.b, 0.0);
+    ttg::k_tiles_to_obs<<<1, 256, 0, c->stream>>>(c->tsq.as<double>(), tpo, (int)nm.b, c->on2.as<double>(),
+                                                  c->scal.as<double>());
+    post_launch(c);
+    allreduce_sum(c, c->scal.as<double>(), 1);
+  }
+  nm.pending = false;
+}
+
+void check_finite_norm(double ysq) {
+  if (!std::isfinite(ysq)) fail(TTG_E_NUMERIC, "non-finite element rejected at tensor construction");
+}
+
+// next-mode fusion rule: the next Gram / projection reads the same buffer
+// through the combined pre-projection when its tile still fits the fast path
+bool can_fuse(const Src& s, int64_t n_i, int64_t r_new, int64_t n_next, int64_t r_old_next) {
+  return s.As * n_i * n_next <= kFastMax && ttg::round_up((int)(r_new * n_next), 8) <= kFastMax &&
+         ttg::round_up((int)std::max<int64_t>(r_old_next, 1), 8) <= kFastMax;
+}
+
+SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm) {
   SweepOut out;
   const int d = tt->d;
   const int64_t S = prod(tt->modes);
   std::vector<int64_t> old_ranks = tt->ranks;
-  const double* cur = Y;
-  int flip = 0;
-  int64_t r_left_new = 1;
-  int64_t total = S * b;
+  Src src{Y, 1, S * b, nullptr, 1};
+  int flip = 0, pf = 0;
+  bool unchanged = true;
+  bool norm_checked = !o.need_norms;
   // U_pad of mode 0 is core 0 itself (r_left = 1 never grows)
   const double* Upad = tt->cores.empty() ? nullptr : tt->cores[0].as<double>();
   int64_t r_old = o.bootstrap ? 0 : old_ranks[1];
   for (int i = 0; i < d; ++i) {
     const int64_t n_i = tt->modes[i];
-    const int64_t a = r_left_new * n_i;
-    const int64_t L = total / a;
-    const int64_t cpo = L / b;
+    const int64_t a = src.r * n_i;
+    const long long L = src.Ls / n_i;
+    const long long cpo = L / b;
     if (a > 4096) fail(TTG_E_RESOURCE, "unfolding rows a_i = " + std::to_string(a) + " exceed the device solver limit");
-    const double* dsrc = nullptr;
-    double dmult = 0.0;
-    if (o.deltas) {
-      dmult = o.deltas[i];
-    } else {
-      dsrc = o.delta_src;
-      dmult = o.delta_mult;
-    }
+    const double* dsrc = o.deltas ? nullptr : o.delta_src;
+    const double dmult = o.deltas ? o.deltas[i] : o.delta_mult;
     int64_t r_R = 0;
     bool run_svd = true;
     if (o.star) {
-      double occ = (double)r_old / (double)a;  // tt_ice_star.cpp:246-248 (padded core)
-      run_svd = occ < o.tau;
+      run_svd = (double)r_old / (double)a < o.tau;  // occupancy on the padded core, tt_ice_star.cpp:246-248
     } else if (!o.bootstrap && r_old == a) {
-      // The residual of a square orthogonal basis is identically zero; the
-      // reference's SVD of the rounding noise returns rank 0 whenever
-      // delta > 1e-12 |Y|.  Keep the full computation below that.
-      double dl = dsrc ? dmult * o.y_norm : dmult;
-      run_svd = !(dl > 1e-12 * o.y_norm);
+      // A square orthogonal basis leaves an identically zero residual; the
+      // reference's SVD of its rounding noise returns rank 0 whenever
+      // delta > 1e-12 |Y|; below that, run the full computation.
+      const bool big = o.deltas ? (dmult > 1e-12 * o.y_norm) : (dmult > 1e-12);
+      run_svd = !big;
     }
-    int64_t kmax = 0;
     if (run_svd) {
       const uint8_t* sel = o.star ? o.sel : nullptr;
-      double sel_frac = o.star ? (double)o.n_sel_global / (double)(b * c->world) : 1.0;
-      gram(c, cur, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, sel_frac);
-      kmax = o.star ? o.n_sel_global * cpo : L * c->world;
+      const int64_t rows = src.Psi ? src.As * n_i : a;
+      double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
+      const double sel_frac = o.star ? (double)o.n_sel_global / (double)(b * c->world) : 1.0;
+      const bool did = gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq);
+      if (tsq) norms_finish(c, nm, rows, did);
+      if (!norm_checked && !nm.pending) {  // reject non-finite input before anything is mutated
+        check_finite_norm(read_scalar(c, c->scal.as<double>()));
+        norm_checked = true;
+      }
+      const long long kmax = o.star ? o.n_sel_global * cpo : L * c->world;
       EigResult er = eig(c, (int)a, kmax, dsrc, dmult);
       if (needs_accurate(er) && accurate_supported((int)a, (int)r_old)) {
-        er = accurate_eig(c, cur, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, kmax,
-                          dsrc, dmult);
+        const double* X = materialise(c, src, n_i, c->matbuf);
+        er = accurate_eig(c, X, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, kmax, dsrc,
+                          dmult);
         out.accurate_modes++;
       }
       r_R = er.rank;
       out.discarded_sq += er.tail_sq;
     }
     int64_t r_new;
-    // new core i
+    bool zero_next = false;
     if (o.bootstrap) {
-      if (r_R == 0) {  // tt_svd.cpp:42-47 unit-column placeholder
+      if (r_R == 0) {  // tt_svd.cpp:42-47 unit-column placeholder, next carry = 0
         r_new = 1;
         std::vector<double> e1((size_t)a, 0.0);
         e1[0] = 1.0;
         tt->cores[i].ensure(sizeof(double) * a);
         CK(cudaMemcpyAsync(tt->cores[i].p, e1.data(), sizeof(double) * a, cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+        zero_next = true;
       } else {
         r_new = r_R;
         set_core(c, tt, i, c->UR.as<double>(), (size_t)a * r_new);
       }
       out.cores_changed = true;
+      unchanged = false;
     } else if (r_R > 0) {
       r_new = r_old + r_R;
       const bool alias = (Upad == tt->cores[i].p);
@@ -681,36 +879,43 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       out.guards += append(c, Upad, (int)a, (int)r_old, (int)r_R, tt->cores[i].as<double>());
       out.cores_changed = true;
       out.modes_updated++;
+      unchanged = false;
     } else {
       r_new = r_old;
+      if (Upad != tt->cores[i].p) unchanged = false;  // padded core (an earlier mode grew)
       set_core(c, tt, i, Upad, (size_t)a * r_new);
     }
-    // projection
-    const double* W = tt->cores[i].as<double>();
-    double* dst;
-    int64_t next_total = r_new * L;
+    const double* Ui = tt->cores[i].as<double>();
     if (i + 1 < d) {
-      c->cur[flip].ensure(sizeof(double) * (size_t)std::max<int64_t>(next_total, 1));
-      dst = c->cur[flip].as<double>();
-    } else {
-      c->coeffs.ensure(sizeof(double) * (size_t)std::max<int64_t>(next_total, 1));
-      dst = c->coeffs.as<double>();
-    }
-    if (o.bootstrap && r_R == 0) {
-      CK(cudaMemsetAsync(dst, 0, sizeof(double) * next_total, c->stream));
-    } else {
-      project(c, cur, (int)a, L, W, (int)r_new, (int)a, dst);
-    }
-    if (i + 1 < d) {
-      // pad the next core (Eq. 3.4) unless the left rank is unchanged
       const int64_t n_next = tt->modes[i + 1];
-      int64_t rl_old = o.bootstrap ? 1 : old_ranks[i + 1];
-      int64_t rr_old = o.bootstrap ? 0 : old_ranks[i + 2];
+      const int64_t rl_old = o.bootstrap ? 1 : old_ranks[i + 1];
+      const int64_t rr_old = o.bootstrap ? 0 : old_ranks[i + 2];
+      if (zero_next) {
+        c->cur[flip].ensure(sizeof(double) * (size_t)std::max<long long>(L, 1));
+        CK(cudaMemsetAsync(c->cur[flip].p, 0, sizeof(double) * L, c->stream));
+        src = Src{c->cur[flip].as<double>(), 1, L, nullptr, 1};
+        flip ^= 1;
+      } else if (can_fuse(src, n_i, r_new, n_next, rr_old)) {
+        const double* psi = src.Psi ? combine_psi(c, src, n_i, Ui, r_new, c->psi[pf]) : Ui;
+        if (src.Psi) pf ^= 1;
+        src = Src{src.S, src.As * n_i, L, psi, r_new};
+      } else if (o.reuse_stats && unchanged && c->stat_has.size() > (size_t)(i + 1) && c->stat_has[i + 1]) {
+        src = Src{c->scur[i + 1].as<double>(), r_new, L, nullptr, r_new};
+      } else {
+        c->cur[flip].ensure(sizeof(double) * (size_t)std::max<long long>(r_new * L, 1));
+        const int64_t rows = src.Psi ? src.As * n_i : a;
+        double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
+        const bool did = project_src(c, src, n_i, Ui, r_new, c->cur[flip].as<double>(), tsq);
+        if (tsq) norms_finish(c, nm, rows, did);
+        src = Src{c->cur[flip].as<double>(), r_new, L, nullptr, r_new};
+        flip ^= 1;
+      }
+      // pad the next core (Eq. 3.4) unless the left rank is unchanged
       if (o.bootstrap) {
         Upad = nullptr;
         r_old = 0;
       } else if (r_new != rl_old) {
-        int64_t tot = r_new * n_next * rr_old;
+        const int64_t tot = r_new * n_next * rr_old;
         c->Upad.ensure(sizeof(double) * (size_t)std::max<int64_t>(tot, 1));
         prof_begin(c, "k_pad_core", 16.0 * tot, 0.0);
         ttg::k_pad_core<<<grid_for(tot, 256, 1024), 256, 0, c->stream>>>(
@@ -722,41 +927,72 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         Upad = tt->cores[i + 1].as<double>();
         r_old = rr_old;
       }
-      cur = dst;
-      flip ^= 1;
+    } else {
+      c->coeffs.ensure(sizeof(double) * (size_t)std::max<long long>(r_new * L, 1));
+      if (zero_next) {
+        CK(cudaMemsetAsync(c->coeffs.p, 0, sizeof(double) * r_new * L, c->stream));
+        out.coeffs = c->coeffs.as<double>();
+      } else if (o.reuse_stats && unchanged) {
+        out.coeffs = c->scoeffs.as<double>();  // projection through unchanged cores
+      } else {
+        const int64_t rows = src.Psi ? src.As * n_i : a;
+        double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
+        const bool did = project_src(c, src, n_i, Ui, r_new, c->coeffs.as<double>(), tsq);
+        if (tsq) norms_finish(c, nm, rows, did);
+        out.coeffs = c->coeffs.as<double>();
+      }
     }
-    total = next_total;
     tt->ranks[i + 1] = r_new;
-    r_left_new = r_new;
+    if (i + 1 == d) out.r_d = (int)r_new;
   }
-  out.coeffs = c->coeffs.as<double>();
-  out.r_d = (int)r_left_new;
   return out;
 }
 
-// projection of Y through the train's current cores -> c->coeffs (r_d x b)
-void project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b) {
+// Projection of Y through the train's current cores (same fusion plan as the
+// sweep).  cache=true keeps the materialised intermediates (c->scur) and the
+// coefficients (c->scoeffs) for reuse by a following TT-ICE* sweep.
+const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, bool cache, Norms& nm) {
   const int d = tt->d;
-  int64_t total = prod(tt->modes) * b;
-  const double* cur = Y;
-  int flip = 0;
-  for (int i = 0; i < d; ++i) {
-    int64_t a = tt->ranks[i] * tt->modes[i];
-    int64_t L = total / a;
-    int64_t r = tt->ranks[i + 1];
-    double* dst;
-    if (i + 1 < d) {
-      c->cur[flip].ensure(sizeof(double) * (size_t)(r * L));
-      dst = c->cur[flip].as<double>();
-    } else {
-      c->coeffs.ensure(sizeof(double) * (size_t)(r * L));
-      dst = c->coeffs.as<double>();
-    }
-    project(c, cur, (int)a, L, tt->cores[i].as<double>(), (int)r, (int)a, dst);
-    cur = dst;
-    flip ^= 1;
-    total = r * L;
+  const int64_t S = prod(tt->modes);
+  Src src{Y, 1, S * b, nullptr, 1};
+  int flip = 0, pf = 0;
+  if (cache) {
+    if ((int)c->scur.size() < d + 1) c->scur.resize(d + 1);
+    c->stat_has.assign(d + 1, false);
   }
+  for (int i = 0; i < d; ++i) {
+    const int64_t n_i = tt->modes[i];
+    const long long L = src.Ls / n_i;
+    const int64_t r = tt->ranks[i + 1];
+    const double* Ui = tt->cores[i].as<double>();
+    const int64_t rows = src.Psi ? src.As * n_i : src.r * n_i;
+    if (i + 1 < d) {
+      const int64_t n_next = tt->modes[i + 1];
+      const int64_t rr = tt->ranks[i + 2];
+      if (can_fuse(src, n_i, r, n_next, rr)) {
+        const double* psi = src.Psi ? combine_psi(c, src, n_i, Ui, r, c->spsi[pf]) : Ui;
+        if (src.Psi) pf ^= 1;
+        src = Src{src.S, src.As * n_i, L, psi, r};
+        continue;
+      }
+      DevBuf& dst = cache ? c->scur[i + 1] : c->cur[flip];
+      dst.ensure(sizeof(double) * (size_t)std::max<long long>(r * L, 1));
+      double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
+      const bool did = project_src(c, src, n_i, Ui, r, dst.as<double>(), tsq);
+      if (tsq) norms_finish(c, nm, rows, did);
+      if (cache) c->stat_has[i + 1] = true;
+      src = Src{dst.as<double>(), r, L, nullptr, r};
+      flip ^= 1;
+    } else {
+      DevBuf& dst = cache ? c->scoeffs : c->coeffs;
+      dst.ensure(sizeof(double) * (size_t)std::max<long long>(r * L, 1));
+      double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
+      const bool did = project_src(c, src, n_i, Ui, r, dst.as<double>(), tsq);
+      if (tsq) norms_finish(c, nm, rows, did);
+      return dst.as<double>();
+    }
+  }
+  return nullptr;
 }
 
 // M = Phi^T Phi of the spatial chain -> returns device pointer (r_d x r_d)
@@ -768,12 +1004,12 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
   c->iface[0].ensure(sizeof(double) * rmax * rmax);
   c->iface[1].ensure(sizeof(double) * rmax * rmax);
   c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
-  double one = 1.0;
+  const double one = 1.0;
   CK(cudaMemcpyAsync(c->iface[0].p, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
   int f = 0;
   for (int i = 0; i < tt->d; ++i) {
-    int rl = (int)tt->ranks[i], n = (int)tt->modes[i], rr = (int)tt->ranks[i + 1];
-    long long t1 = (long long)rl * n * rr;
+    const int rl = (int)tt->ranks[i], n = (int)tt->modes[i], rr = (int)tt->ranks[i + 1];
+    const long long t1 = (long long)rl * n * rr;
     prof_begin(c, "k_iface", 8.0 * t1, 2.0 * t1 * rl);
     ttg::k_iface_step1<<<grid_for(t1, 256, 1024), 256, 0, c->stream>>>(c->iface[f].as<double>(),
                                                                         tt->cores[i].as<double>(), rl, n, rr,
@@ -785,23 +1021,25 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
     post_launch(c);
     f ^= 1;
   }
-  CK(cudaStreamSynchronize(c->stream));
   return c->iface[f].as<double>();
 }
 
-// per-observation statistics of TT-ICE* (norms already in c->on2)
+// TT-ICE* per-observation statistics: norms (fused) + projection through the
+// current cores (cached for the sweep) + decisions' partial sums
 void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double eps) {
-  project_chain(c, tt, Y, b);
+  Norms nm{true, Y, prod(tt->modes), b};
+  const double* coeffs = project_chain(c, tt, Y, b, /*cache=*/true, nm);
+  if (nm.pending) norms_finish(c, nm, 0, false);
   const double* M = interface_gram(c, tt);
-  int r = (int)tt->ranks[tt->d];
+  const int r = (int)tt->ranks[tt->d];
   c->cn2.ensure(sizeof(double) * b);
   c->cmc.ensure(sizeof(double) * b);
   c->errs.ensure(sizeof(double) * b);
   c->rn2.ensure(sizeof(double) * b);
   c->stats.ensure(sizeof(ttg::StarStats));
   prof_begin(c, "k_coef_stats", 8.0 * r * b, 2.0 * r * r * b);
-  ttg::k_coef_stats<<<grid_for(b, 128, 1024), 128, 0, c->stream>>>(c->coeffs.as<double>(), r, (int)b, M,
-                                                                   c->cn2.as<double>(), c->cmc.as<double>());
+  ttg::k_coef_stats<<<grid_for(b, 128, 1024), 128, 0, c->stream>>>(coeffs, r, (int)b, M, c->cn2.as<double>(),
+                                                                   c->cmc.as<double>());
   post_launch(c);
   prof_begin(c, "k_star_local", 32.0 * b, 10.0 * b);
   ttg::k_star_local<<<1, 32, 0, c->stream>>>(c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
@@ -823,10 +1061,6 @@ struct Timer {
   }
 };
 
-void check_finite_norm(double ysq) {
-  if (!std::isfinite(ysq)) fail(TTG_E_NUMERIC, "non-finite element rejected at tensor construction");
-}
-
 // ---- entry points (internal, throwing) ----------------------------------------
 
 void do_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t* shape, int ndim,
@@ -837,15 +1071,14 @@ void do_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t
   check_train_vs_y(tt, shape, ndim, true);
   const int d = tt->d;
   if (!uniform && n_deltas != d) fail(TTG_E_DIMENSION, "need one SVD tolerance per spatial dimension");
+  if (!uniform)
+    for (int i = 0; i < d; ++i)
+      if (deltas[i] < 0.0) fail(TTG_E_NUMERIC, "svd_trunc: negative truncation threshold");
   const int64_t b = shape[d];
   const int64_t S = prod(tt->modes);
   Timer tm(c);
   const double* Y = stage_input(c, y, where, (size_t)(S * b));
-  int64_t bg = global_obs(c, b);
-  obs_norms(c, Y, S, (int)b);
-  double ysq = read_scalar(c, c->scal.as<double>());
-  check_finite_norm(ysq);
-  double y_norm = std::sqrt(ysq);
+  const int64_t bg = global_obs(c, b);
   std::memset(rep, 0, sizeof(*rep));
   rep->increment_index = (int64_t)tt->bounds.size();
   rep->obs_in_batch = bg;
@@ -853,18 +1086,25 @@ void do_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t
   rep->n_ranks = d + 2;
   fill_report_ranks(rep->ranks_before, tt);
   SweepOpts o;
-  o.y_norm = y_norm;
+  Norms nm{true, Y, S, b};
   if (uniform) {
     o.delta_src = c->scal.as<double>();
     o.delta_mult = eps_des / std::sqrt((double)d);  // tt_ice.cpp:137-138
-    rep->eps_target = eps_des * y_norm / std::sqrt((double)d);
+    o.need_norms = true;
   } else {
-    for (int i = 0; i < d; ++i)
-      if (deltas[i] < 0.0) fail(TTG_E_NUMERIC, "svd_trunc: negative truncation threshold");
+    obs_norms(c, Y, S, (int)b);  // per-mode thresholds are absolute: |Y| only for the shortcut and report
+    nm.pending = false;
+    const double ysq0 = read_scalar(c, c->scal.as<double>());
+    check_finite_norm(ysq0);
     o.deltas = deltas;
-    rep->eps_target = d > 0 ? deltas[0] : 0.0;
+    o.y_norm = std::sqrt(ysq0);
   }
-  SweepOut so = sweep(c, tt, Y, b, o);
+  SweepOut so = sweep(c, tt, Y, b, o, nm);
+  if (nm.pending) norms_finish(c, nm, 0, false);
+  const double ysq = read_scalar(c, c->scal.as<double>());
+  check_finite_norm(ysq);
+  const double y_norm = std::sqrt(ysq);
+  rep->eps_target = uniform ? eps_des * y_norm / std::sqrt((double)d) : (d > 0 ? deltas[0] : 0.0);
   append_last_core(c, tt, so.coeffs, so.r_d, b);
   fill_report_ranks(rep->ranks_after, tt);
   rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(so.discarded_sq) / y_norm;
@@ -891,18 +1131,17 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   const int64_t S = prod(tt->modes);
   Timer tm(c);
   const double* Y = stage_input(c, y, where, (size_t)(S * b));
-  int64_t bg = global_obs(c, b);
-  obs_norms(c, Y, S, (int)b);
+  const int64_t bg = global_obs(c, b);
   std::memset(rep, 0, sizeof(*rep));
   rep->increment_index = (int64_t)tt->bounds.size();
   rep->obs_in_batch = bg;
   rep->n_ranks = d + 2;
   fill_report_ranks(rep->ranks_before, tt);
 
-  star_stats(c, tt, Y, b, eps_des);
+  star_stats(c, tt, Y, b, eps_des);  // norms fused into the stats projection
   c->d2h += sizeof(ttg::StarStats);
   CK(cudaMemcpyAsync(c->h_stats, c->stats.p, sizeof(ttg::StarStats), cudaMemcpyDeviceToHost, c->stream));
-  double ysq = read_scalar(c, c->scal.as<double>());
+  const double ysq = read_scalar(c, c->scal.as<double>());
   check_finite_norm(ysq);
   const double y_norm = std::sqrt(ysq);
   const double* s = c->h_stats->sums;
@@ -922,18 +1161,18 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   }
   rep->obs_used = n_sel;
   SweepOut so;
-  const double* coeffs = c->coeffs.as<double>();  // stats projection = projection through unchanged cores
+  const double* coeffs = c->scoeffs.as<double>();  // stats projection = projection through unchanged cores
   int r_d = (int)tt->ranks[d];
   if (n_sel > 0) {
     double eps_upd = eps_des;
     if (n_rej > 0) {
       if (cfg.use_approx_tolerance) {  // Eq. 3.20, tt_ice_star.cpp:160-169
-        double mean_rej = s[8] / (double)n_rej;
+        const double mean_rej = s[8] / (double)n_rej;
         eps_upd = (eps_des * (double)bg - mean_rej * (double)n_rej) / (double)n_sel;
       } else {  // Eq. 3.19, tt_ice_star.cpp:121-158
-        double selected_sq = s[5];
+        const double selected_sq = s[5];
         if (selected_sq == 0.0) fail(TTG_E_NUMERIC, "selected observations carry no energy");
-        double budget = eps_des * y_norm;
+        const double budget = eps_des * y_norm;
         double radicand = (budget * budget - s[4]) / selected_sq;
         if (radicand < 0.0) {
           radicand = 0.0;
@@ -942,8 +1181,8 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
         eps_upd = std::sqrt(radicand);
       }
     }
-    double d_sq = cfg.subselect_enabled ? s[5] : s[3];
-    double delta = eps_upd / std::sqrt((double)d) * std::sqrt(d_sq);  // :235-236
+    const double d_sq = cfg.subselect_enabled ? s[5] : s[3];
+    const double delta = eps_upd / std::sqrt((double)d) * std::sqrt(d_sq);  // :235-236
     rep->eps_target = delta;
     c->sel.ensure((size_t)b);
     prof_begin(c, "k_star_mask", 9.0 * b, 0.0);
@@ -955,13 +1194,12 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
     o.tau = cfg.occupancy_threshold;
     o.sel = c->sel.as<uint8_t>();
     o.n_sel_global = n_sel;
-    o.deltas = nullptr;
-    o.delta_src = nullptr;
     o.delta_mult = delta;
-    o.y_norm = y_norm;
+    o.reuse_stats = true;
+    Norms nm;  // norms already known
     // the sweep mutates ranks/cores in place; TT-ICE* keeps the old cores when
     // nothing grew (tt_ice_star.cpp:276-277), which in-place is the same bytes
-    so = sweep(c, tt, Y, b, o);
+    so = sweep(c, tt, Y, b, o, nm);
     coeffs = so.coeffs;
     r_d = so.r_d;
     rep->guard_reorthogonalised = so.guards;
@@ -971,8 +1209,8 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   fill_report_ranks(rep->ranks_after, tt);
   // estimate: Pythagoras on the appended coefficients (tt_ice_star.cpp:297-300)
   const double* csrc = c->world > 1 ? c->coeffs_all.as<double>() : coeffs;
-  double kept_sq = sumsq_device(c, csrc, (long long)r_d * bg);
-  double lost_sq = std::max(ysq - kept_sq, 0.0);
+  const double kept_sq = sumsq_device(c, csrc, (long long)r_d * bg);
+  const double lost_sq = std::max(ysq - kept_sq, 0.0);
   rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(lost_sq) / y_norm;
   rep->seconds = tm.stop();
 }
@@ -995,17 +1233,20 @@ ttg_tt* do_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shap
     const int64_t S = prod(tt->modes);
     Timer tm(c);
     const double* Y = stage_input(c, y, where, (size_t)(S * b));
-    int64_t bg = global_obs(c, b);
-    obs_norms(c, Y, S, (int)b);
-    double ysq = read_scalar(c, c->scal.as<double>());
-    check_finite_norm(ysq);
-    double y_norm = std::sqrt(ysq);
+    const int64_t bg = global_obs(c, b);
     SweepOpts o;
     o.bootstrap = true;
     o.delta_src = c->scal.as<double>();
     o.delta_mult = eps / std::sqrt((double)(ndim - 1));  // tt_svd.cpp:30
-    o.y_norm = y_norm;
-    SweepOut so = sweep(c, tt, Y, b, o);
+    o.need_norms = true;
+    c->scal.ensure(sizeof(double) * 16);
+    o.delta_src = c->scal.as<double>();
+    Norms nm{true, Y, S, b};
+    SweepOut so = sweep(c, tt, Y, b, o, nm);
+    if (nm.pending) norms_finish(c, nm, 0, false);
+    const double ysq = read_scalar(c, c->scal.as<double>());
+    check_finite_norm(ysq);
+    const double y_norm = std::sqrt(ysq);
     append_last_core(c, tt, so.coeffs, so.r_d, b);
     tt->ortho_count = d;
     std::memset(rep, 0, sizeof(*rep));
@@ -1017,8 +1258,8 @@ ttg_tt* do_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shap
     for (int i = 0; i <= d + 1; ++i) rep->ranks_before[i] = 1;
     rep->eps_target = eps * y_norm / std::sqrt((double)(ndim - 1));
     const double* src = c->world > 1 ? c->coeffs_all.as<double>() : so.coeffs;
-    double kept_sq = sumsq_device(c, src, (long long)so.r_d * bg);  // tt_norm (tensor_train.cpp:383-386)
-    double lost_sq = std::max(ysq - kept_sq, 0.0);
+    const double kept_sq = sumsq_device(c, src, (long long)so.r_d * bg);  // tt_norm (tensor_train.cpp:383-386)
+    const double lost_sq = std::max(ysq - kept_sq, 0.0);
     rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(lost_sq) / y_norm;
     rep->seconds = tm.stop();
   } catch (...) {
@@ -1326,7 +1567,6 @@ int ttg_per_obs_errors(ttg_ctx* c, const ttg_tt* tt, const double* y, int where,
     const int64_t b = shape[tt->d];
     const int64_t S = prod(tt->modes);
     const double* Y = stage_input(c, y, where, (size_t)(S * b));
-    obs_norms(c, Y, S, (int)b);
     star_stats(c, tt, Y, b, 0.0);
     CK(cudaMemcpyAsync(errs, c->errs.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1343,9 +1583,9 @@ int ttg_project(ttg_ctx* c, const ttg_tt* tt, const double* y, int where, const 
     const int64_t b = shape[tt->d];
     const int64_t S = prod(tt->modes);
     const double* Y = stage_input(c, y, where, (size_t)(S * b));
-    project_chain(c, tt, Y, b);
-    CK(cudaMemcpyAsync(coeffs, c->coeffs.p, sizeof(double) * b * tt->ranks[tt->d], cudaMemcpyDeviceToHost,
-                       c->stream));
+    Norms nm;  // not needed
+    const double* cf = project_chain(c, tt, Y, b, /*cache=*/false, nm);
+    CK(cudaMemcpyAsync(coeffs, cf, sizeof(double) * b * tt->ranks[tt->d], cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   });
 }

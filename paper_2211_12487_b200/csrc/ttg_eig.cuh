@@ -26,6 +26,7 @@ struct EigResult {
   double lam_max;
   double dev;     // append Gram deviation
   double lam_min_kept;  // smallest kept sigma^2
+  long long t_phase[4];  // clock64 stamps of the solver phases (diagnostics)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -87,6 +87,80 @@ __device__ __forceinline__ void load_tile_async(const TileSrc& s, long long q0, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA tile pipeline (sm_100a cp.async.bulk + mbarrier).  A tile = kTC
+// consecutive columns of X (a x L, column-major): each column is one
+// contiguous a*8-byte run, copied by one bulk instruction into the padded smem
+// tile (ld = ldt).  Warp 0 is the producer: it evaluates the 64 column flags
+// (inside L, observation selected) once per tile, posts the expected bytes on
+// the buffer's mbarrier, issues the bulk copies and zero-fills the invalid
+// columns.  Requires a even (16-byte runs); odd a falls back to cp.async.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// Issue the loads of tile [q0, q0+kTC) into T.  Uniform call by all threads.
+// tma: bulk path (a even); else cp.async 8-byte path (caller commits/waits).
+__device__ __forceinline__ void tile_issue(const TileSrc& s, long long q0, double* T, int ldt, uint64_t* bar,
+                                           bool tma) {
+  if (!tma) {
+    load_tile_async(s, q0, T, ldt);
+    return;
+  }
+  if ((threadIdx.x >> 5) != 0) return;
+  const int lane = threadIdx.x & 31;
+  bool v[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const long long q = q0 + lane + 32 * h;
+    bool ok = q < s.L;
+    if (ok && s.sel) ok = s.sel[q / s.cols_per_obs] != 0;
+    v[h] = ok;
+  }
+  const unsigned m0 = __ballot_sync(0xffffffffu, v[0]), m1 = __ballot_sync(0xffffffffu, v[1]);
+  const unsigned nvalid = __popc(m0) + __popc(m1);
+  const unsigned colbytes = (unsigned)s.a * 8u;
+  fence_proxy_async();  // earlier generic-proxy writes to this buffer precede the async copies
+  if (lane == 0) mbar_expect_tx(bar, nvalid * colbytes);
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (v[h]) {
+      bulk_g2s(T + (size_t)ldt * c, s.X + (size_t)s.a * (q0 + c), colbytes, bar);
+    } else {
+      for (int r = 0; r < s.a; ++r) T[r + (size_t)ldt * c] = 0.0;
+    }
+  }
+}
+
 // In-place residual of the warp's 8 tile columns: T_w -= U (U^T T_w), with U
 // given as DMMA A-fragments (k_make_frags); Pw is the warp's r8 x 8 scratch.
 __device__ __forceinline__ void tile_residual(double* T, int ldt, double* Pw, int ldp, const double* UTf,
@@ -94,74 +168,158 @@ __device__ __forceinline__ void tile_residual(double* T, int ldt, double* Pw, in
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int c0 = warp * 8;
-  for (int mb = 0; mb < MR; ++mb) {  // P = U^T T_w   (r8 x 8)
-    double q0 = 0.0, q1 = 0.0;
-    const double* fa = UTf + ((long long)mb * KA) * 32 + lane;
+  // P = U^T T_w (r8 x 8): 4 m-blocks in flight (independent DMMA chains)
+  for (int mb0 = 0; mb0 < MR; mb0 += 4) {
+    double q[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     for (int kb = 0; kb < KA; ++kb) {
-      double av = __ldg(fa + kb * 32);
-      double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
-      dmma(q0, q1, av, bv);
+      const double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (mb0 + u < MR) dmma(q[u][0], q[u][1], __ldg(UTf + ((long long)(mb0 + u) * KA + kb) * 32 + lane), bv);
     }
-    Pw[(mb * 8 + g) + ldp * (2 * t)] = q0;
-    Pw[(mb * 8 + g) + ldp * (2 * t + 1)] = q1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (mb0 + u < MR) {
+        Pw[((mb0 + u) * 8 + g) + ldp * (2 * t)] = q[u][0];
+        Pw[((mb0 + u) * 8 + g) + ldp * (2 * t + 1)] = q[u][1];
+      }
   }
   __syncwarp();
-  for (int ib = 0; ib < nb; ++ib) {  // T_w -= U P
-    double q0 = 0.0, q1 = 0.0;
-    const double* fa = Uf + ((long long)ib * KR) * 32 + lane;
+  // T_w -= U P: 4 row-blocks in flight
+  for (int ib0 = 0; ib0 < nb; ib0 += 4) {
+    double q[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     for (int sb = 0; sb < KR; ++sb) {
-      double av = __ldg(fa + sb * 32);
-      double bv = Pw[(sb * 4 + t) + ldp * g];
-      dmma(q0, q1, av, bv);
+      const double bv = Pw[(sb * 4 + t) + ldp * g];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ib0 + u < nb) dmma(q[u][0], q[u][1], __ldg(Uf + ((long long)(ib0 + u) * KR + sb) * 32 + lane), bv);
     }
-    T[(ib * 8 + g) + ldt * (c0 + 2 * t)] -= q0;
-    T[(ib * 8 + g) + ldt * (c0 + 2 * t + 1)] -= q1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ib0 + u < nb) {
+        T[((ib0 + u) * 8 + g) + ldt * (c0 + 2 * t)] -= q[u][0];
+        T[((ib0 + u) * 8 + g) + ldt * (c0 + 2 * t + 1)] -= q[u][1];
+      }
   }
   __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
-// Fused residual + Gram:  for every selected column x of cur (a x L):
-//     r = x - U (U^T x);     G += r r^T
-// Fast path for a8 <= 128: one CTA accumulates the whole a8 x a8 Gram of a
-// grid-stride set of 64-column tiles in registers (DMMA) and writes it to its
-// own partial slot (deterministic fixed-order reduction follows).  Larger
-// unfoldings take the generic path (k_gemm).
-// U enters as pre-swizzled DMMA fragments (k_make_frags) read with coalesced
-// 256-byte loads.  WBR x WBC = 8x8 blocks per warp (warp grid 4 x 2).
+// Sum of squares of an smem tile (rows x kTC, ld) -> block total on thread 0.
+// Fixed thread/element assignment and tree: deterministic.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double tile_sumsq(const double* T, int rows, int ld, double* red8) {
+  double s = 0.0;
+  for (int e = threadIdx.x; e < rows * kTC; e += kThreads) {
+    const int c = e / rows, r = e - c * rows;
+    const double v = T[r + ld * c];
+    s = fma(v, v, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red8[warp] = s;
+  __syncthreads();
+  double tot = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kThreads / 32; ++w) tot += red8[w];
+  return tot;
+}
+
+// Pre-projection of the warp's 8 tile columns: the current unfolding's column
+// is (I_nblk (x) Psi^T) applied to the source column (rows As*nblk):
+//   Tc[p + rc*j][c] = sum_k Psi[k][p] * Ts[k + As*j][c]
+__device__ __forceinline__ void tile_preproject(const double* Ts, int lds, double* Tc, int ldt, const double* PsiTf,
+                                                int As, int nblk, int rc, int MRC, int KS) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = warp * 8;
+  for (int mb = 0; mb < MRC; ++mb) {
+    const int row = mb * 8 + g;
+    for (int j0 = 0; j0 < nblk; j0 += 4) {
+      double q[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int kb = 0; kb < KS; ++kb) {
+        const double av = __ldg(PsiTf + ((long long)mb * KS + kb) * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + u < nblk) dmma(q[u][0], q[u][1], av, Ts[(As * (j0 + u) + kb * 4 + t) + lds * (c0 + g)]);
+      }
+      if (row < rc) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + u < nblk) {
+            Tc[(row + rc * (j0 + u)) + ldt * (c0 + 2 * t)] = q[u][0];
+            Tc[(row + rc * (j0 + u)) + ldt * (c0 + 2 * t + 1)] = q[u][1];
+          }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// Fused (pre-projection +) residual + Gram:  for every selected column x of
+// the current unfolding cur_i (a x L):  r = x - U (U^T x);  G += r r^T.
+// WBR x WBC 8x8 blocks per warp (warp grid 4 x 2) -> one 8*4*WBR super-tile
+// (I, J), I >= J, per blockIdx.y; a grid-stride set of 64-column tiles per
+// blockIdx.x; per-CTA partial written for a fixed-order reduction.
+// PRE: the tile is loaded from the source S (rows As*nblk) and projected by
+//      Psi (I_nblk (x) Psi^T) into the cur tile (mode i read straight from the
+//      buffer of mode i-1 or earlier, no intermediate in HBM).
+// DB : cp.async double-buffered source tiles (else single-buffered, for
+//      a8 up to 256).
+// U enters as pre-swizzled DMMA fragments read with coalesced 256-byte loads.
 // ---------------------------------------------------------------------------
 struct GramArgs {
-  TileSrc src;
-  int a8;
-  int ldt, ldp;
+  TileSrc src;        // tile source: rows src.a (= As*nblk when PRE, = a otherwise)
+  int a, a8;          // rows of the current unfolding
+  int ldt, lds, ldp;
+  int As, nblk, rc, MRC, KS;  // pre-projection geometry (PRE)
+  const double* PsiTf;        // A-fragments of Psi^T: [MRC][KS][32]
   const double* UTf;  // A-fragments of U^T: [r8/8][a8/4][32]
   const double* Uf;   // A-fragments of U:   [a8/8][r8/4][32]
   int r8;             // 0 => no residual (empty basis)
-  double* partials;   // [gridDim.x][SBD*SBD], SBD = 8*4*WBR >= a8
+  double* partials;   // [gridDim.y][gridDim.x][SBD*SBD]
+  double* tsumsq;     // per-tile sum of squares of the source tile (nullable)
   long long n_tiles;
   int r_old;          // host-side accounting only
   double sel_frac;    // host-side accounting only
 };
 
-template <int WBR, int WBC>
+template <int WBR, int WBC, bool PRE, bool DB>
 __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
   extern __shared__ __align__(16) double smem[];
+  __shared__ double red8[kThreads / 32];
   constexpr int SB = 4 * WBR;  // == 2*WBC blocks per super-tile side
   constexpr int SBD = 8 * SB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int ldt = p.ldt, ldp = p.ldp;
-  double* T0 = smem;
-  double* T1 = smem + ldt * kTC;
-  double* Pw = smem + 2 * ldt * kTC + warp * ldp * 8;
+  const int lds = PRE ? p.lds : ldt;
+  // smem: source buffers S0 [S1], cur tile Tc (PRE only), per-warp P scratch
+  double* S0 = smem;
+  double* S1 = DB ? S0 + (size_t)lds * kTC : S0;
+  double* Tc = PRE ? S1 + (size_t)lds * kTC : nullptr;
+  double* Pw = (PRE ? Tc + (size_t)ldt * kTC : S0 + (size_t)(DB ? 2 : 1) * lds * kTC) + warp * ldp * 8;
+  const int n_zero = (int)((PRE ? (DB ? 2 : 1) * lds + ldt : (DB ? 2 : 1) * ldt) * kTC);
 
-  const int row_blk0 = (warp >> 1) * WBR;  // in 8-row blocks
-  const int col_blk0 = (warp & 1) * WBC;
+  int I = 0, J = blockIdx.y;
+  while (J > I) { J -= I + 1; ++I; }
+  const int row_blk0 = I * SB + (warp >> 1) * WBR;  // in 8-row blocks
+  const int col_blk0 = J * SB + (warp & 1) * WBC;
   const int nb = p.a8 >> 3;
 
-  // zero the whole tile area once: padded rows a..a8 stay zero forever
-  for (int i = threadIdx.x; i < 2 * ldt * kTC; i += kThreads) smem[i] = 0.0;
+  for (int i = threadIdx.x; i < n_zero; i += kThreads) smem[i] = 0.0;  // padded rows stay zero
   __syncthreads();
+
+  __shared__ __align__(8) uint64_t bars[2];
+  const bool tma = (p.src.a & 1) == 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  __syncthreads();
+  unsigned phase[2] = {0u, 0u};
 
   double acc[WBR][WBC][2];
 #pragma unroll
@@ -171,35 +329,60 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
 
   const int KA = p.a8 >> 2, KR = p.r8 >> 2, MR = p.r8 >> 3;
   long long tile = blockIdx.x;
-  if (tile < p.n_tiles) load_tile_async(p.src, tile * kTC, T0, ldt);
-  cp_async_commit();
+  if (DB) {
+    if (tile < p.n_tiles) tile_issue(p.src, tile * kTC, S0, lds, &bars[0], tma);
+    if (!tma) cp_async_commit();
+  }
   int buf = 0;
   for (; tile < p.n_tiles; tile += gridDim.x) {
-    double* T = buf ? T1 : T0;
-    double* Tn = buf ? T0 : T1;
-    long long nxt = tile + gridDim.x;
-    if (nxt < p.n_tiles) load_tile_async(p.src, nxt * kTC, Tn, ldt);
-    cp_async_commit();
-    cp_async_wait_1();
+    double* Ssrc = (DB && buf) ? S1 : S0;
+    const int cb = DB ? buf : 0;
+    if (DB) {
+      double* Sn = buf ? S0 : S1;
+      const long long nxt = tile + gridDim.x;
+      if (nxt < p.n_tiles) tile_issue(p.src, nxt * kTC, Sn, lds, &bars[buf ^ 1], tma);
+      if (!tma) {
+        cp_async_commit();
+        cp_async_wait_1();
+      }
+    } else {
+      tile_issue(p.src, tile * kTC, S0, lds, &bars[0], tma);
+      if (!tma) {
+        cp_async_commit();
+        cp_async_wait_0();
+      }
+    }
+    if (tma) {
+      mbar_wait(&bars[cb], phase[cb]);
+      phase[cb] ^= 1u;
+    }
     __syncthreads();
-
+    if (p.tsumsq) {
+      const double ts = tile_sumsq(Ssrc, p.src.a, lds, red8);
+      if (threadIdx.x == 0) p.tsumsq[tile] = ts;
+    }
+    double* T = Ssrc;
+    if (PRE) {
+      tile_preproject(Ssrc, lds, Tc, ldt, p.PsiTf, p.As, p.nblk, p.rc, p.MRC, p.KS);
+      T = Tc;
+      __syncthreads();
+    }
     if (p.r8 > 0) {
       tile_residual(T, ldt, Pw, ldp, p.UTf, p.Uf, KA, KR, MR, nb);
       __syncthreads();
     }
-
     // G(super-tile) += T T^T over the tile's 64 columns
 #pragma unroll 4
     for (int k0 = 0; k0 < kTC; k0 += 4) {
       double af[WBR], bf[WBC];
 #pragma unroll
       for (int i = 0; i < WBR; ++i) {
-        int rb = row_blk0 + i;
+        const int rb = row_blk0 + i;
         af[i] = (rb < nb) ? T[(rb * 8 + g) + ldt * (k0 + t)] : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < WBC; ++j) {
-        int cb = col_blk0 + j;
+        const int cb = col_blk0 + j;
         bf[j] = (cb < nb) ? T[(cb * 8 + g) + ldt * (k0 + t)] : 0.0;
       }
 #pragma unroll
@@ -210,15 +393,15 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
     __syncthreads();
     buf ^= 1;
   }
-  cp_async_wait_0();
+  if (!tma) cp_async_wait_0();
 
-  double* out = p.partials + (long long)blockIdx.x * SBD * SBD;
+  double* out = p.partials + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * SBD * SBD;
 #pragma unroll
   for (int i = 0; i < WBR; ++i)
 #pragma unroll
     for (int j = 0; j < WBC; ++j) {
-      int r = ((warp >> 1) * WBR + i) * 8 + g;
-      int c = ((warp & 1) * WBC + j) * 8 + 2 * t;
+      const int r = ((warp >> 1) * WBR + i) * 8 + g;
+      const int c = ((warp & 1) * WBC + j) * 8 + 2 * t;
       out[r + SBD * c] = acc[i][j][0];
       out[r + SBD * (c + 1)] = acc[i][j][1];
     }
@@ -232,7 +415,11 @@ __global__ void k_gram_reduce(const double* __restrict__ partials, int nx, int s
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
     int i = (int)(e % a), j = (int)(e / a);
-    const double* src = partials + i + (long long)sbd * j;
+    int ii = i, jj = j;
+    if (jj > ii) { const int tmp = ii; ii = jj; jj = tmp; }  // lower-triangle source
+    const int I = ii / sbd, J = jj / sbd;
+    const int py = I * (I + 1) / 2 + J;
+    const double* src = partials + (long long)py * nx * sbd * sbd + (ii - I * sbd) + (long long)sbd * (jj - J * sbd);
     double s = 0.0;
     for (int x = 0; x < nx; ++x) s += src[(long long)x * sbd * sbd];
     G[e] = s;
@@ -362,58 +549,110 @@ struct ProjArgs {
   const double* WTf;  // [r8/8][a8/4][32]
   int r, r8;
   double* out;
+  double* tsumsq;     // per-tile sum of squares of the input tile (nullable)
   long long n_tiles;
 };
 
+// DB: cp.async double-buffered input tiles (a8 <= 128); single-buffered for a8 <= 256.
+template <bool DB>
 __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
   extern __shared__ __align__(16) double smem[];
+  __shared__ double red8[kThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int ldt = p.ldt;
   double* T0 = smem;
-  double* T1 = smem + ldt * kTC;
-  double* O = smem + 2 * ldt * kTC;  // r x kTC staging (ld r)
-  for (int i = threadIdx.x; i < 2 * ldt * kTC; i += kThreads) smem[i] = 0.0;
+  double* T1 = DB ? smem + ldt * kTC : T0;
+  double* O = smem + (DB ? 2 : 1) * ldt * kTC;  // r x kTC staging (ld r)
+  for (int i = threadIdx.x; i < (DB ? 2 : 1) * ldt * kTC; i += kThreads) smem[i] = 0.0;
   __syncthreads();
+  __shared__ __align__(8) uint64_t bars[2];
+  const bool tma = (p.src.a & 1) == 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  __syncthreads();
+  unsigned phase[2] = {0u, 0u};
   const int KA = p.a8 >> 2, MR = p.r8 >> 3;
   long long tile = blockIdx.x;
-  if (tile < p.n_tiles) load_tile_async(p.src, tile * kTC, T0, ldt);
-  cp_async_commit();
+  if (DB) {
+    if (tile < p.n_tiles) tile_issue(p.src, tile * kTC, T0, ldt, &bars[0], tma);
+    if (!tma) cp_async_commit();
+  }
   int buf = 0;
   for (; tile < p.n_tiles; tile += gridDim.x) {
-    double* T = buf ? T1 : T0;
-    double* Tn = buf ? T0 : T1;
-    long long nxt = tile + gridDim.x;
-    if (nxt < p.n_tiles) load_tile_async(p.src, nxt * kTC, Tn, ldt);
-    cp_async_commit();
-    cp_async_wait_1();
-    __syncthreads();
-    const int c0 = warp * 8;
-    for (int mb = 0; mb < MR; ++mb) {
-      double q0 = 0.0, q1 = 0.0;
-      const double* fa = p.WTf + ((long long)mb * KA) * 32 + lane;
-      for (int kb = 0; kb < KA; ++kb) {
-        double av = __ldg(fa + kb * 32);
-        double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
-        dmma(q0, q1, av, bv);
+    double* T = (DB && buf) ? T1 : T0;
+    const int cb = DB ? buf : 0;
+    if (DB) {
+      double* Tn = buf ? T0 : T1;
+      const long long nxt = tile + gridDim.x;
+      if (nxt < p.n_tiles) tile_issue(p.src, nxt * kTC, Tn, ldt, &bars[buf ^ 1], tma);
+      if (!tma) {
+        cp_async_commit();
+        cp_async_wait_1();
       }
-      int row = mb * 8 + g;
-      if (row < p.r) {
-        O[row + p.r * (c0 + 2 * t)] = q0;
-        O[row + p.r * (c0 + 2 * t + 1)] = q1;
+    } else {
+      tile_issue(p.src, tile * kTC, T0, ldt, &bars[0], tma);
+      if (!tma) {
+        cp_async_commit();
+        cp_async_wait_0();
+      }
+    }
+    if (tma) {
+      mbar_wait(&bars[cb], phase[cb]);
+      phase[cb] ^= 1u;
+    }
+    __syncthreads();
+    if (p.tsumsq) {
+      const double ts = tile_sumsq(T, p.src.a, ldt, red8);
+      if (threadIdx.x == 0) p.tsumsq[tile] = ts;
+    }
+    const int c0 = warp * 8;
+    for (int mb0 = 0; mb0 < MR; mb0 += 4) {
+      double q[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int kb = 0; kb < KA; ++kb) {
+        const double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (mb0 + u < MR) dmma(q[u][0], q[u][1], __ldg(p.WTf + ((long long)(mb0 + u) * KA + kb) * 32 + lane), bv);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int row = (mb0 + u) * 8 + g;
+        if (mb0 + u < MR && row < p.r) {
+          O[row + p.r * (c0 + 2 * t)] = q[u][0];
+          O[row + p.r * (c0 + 2 * t + 1)] = q[u][1];
+        }
       }
     }
     __syncthreads();
-    long long q0c = tile * kTC;
+    const long long q0c = tile * kTC;
     long long ncols = p.src.L - q0c;
     if (ncols > kTC) ncols = kTC;
-    long long nout = ncols * p.r;
+    const long long nout = ncols * p.r;
     double* dst = p.out + q0c * p.r;
     for (long long e = threadIdx.x; e < nout; e += kThreads) dst[e] = O[e];
     __syncthreads();
     buf ^= 1;
   }
-  cp_async_wait_0();
+  if (!tma) cp_async_wait_0();
+}
+
+// per-observation sums from per-tile partials (tiles never straddle observations)
+__global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_per_obs, int nobs,
+                               double* __restrict__ on2, double* __restrict__ total) {
+  for (int o = threadIdx.x; o < nobs; o += blockDim.x) {
+    double s = 0.0;
+    for (long long k = 0; k < tiles_per_obs; ++k) s += ts[(long long)o * tiles_per_obs + k];
+    on2[o] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int o = 0; o < nobs; ++o) s += on2[o];
+    *total = s;
+  }
 }
 
 // ---------------------------------------------------------------------------

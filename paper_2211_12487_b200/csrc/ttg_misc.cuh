@@ -171,6 +171,18 @@ __global__ void k_star_local(const double* __restrict__ on2, const double* __res
   for (int i = 0; i < 9; ++i) st->sums[i] = s[i];
 }
 
+// W = I_n (x) Psi  ((As*n) x (r*n), block diagonal)
+__global__ void k_kron_eye(const double* __restrict__ Psi, int As, int r, int n, double* __restrict__ W) {
+  const long long rows = (long long)As * n, tot = rows * r * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e % rows, col = e / rows;
+    const int j = (int)(row / As), k = (int)(row % As);
+    const int j2 = (int)(col / r), p = (int)(col % r);
+    W[e] = (j == j2) ? Psi[k + (long long)As * p] : 0.0;
+  }
+}
+
 // selection mask (err > eps, or all when subselect is off)
 __global__ void k_star_mask(const double* __restrict__ errs, int b, double eps, int subselect,
                             uint8_t* __restrict__ sel) {
