@@ -429,22 +429,50 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     c->Mtmp.ensure(sizeof(double) * (size_t)32 * 6 * a);
     args.zbuf = c->Mtmp.as<double>();
     args.res = c->eigres.as<EigResult>();
-    size_t vec = sizeof(double) * (size_t)7 * a;
-    size_t smem = sizeof(double) * (size_t)a * a + vec;
-    if (smem <= c->smem_optin) {
-      args.in_smem = 1;
-    } else {
-      args.in_smem = 0;
-      c->W.ensure(sizeof(double) * (size_t)a * a);
-      args.Ag = c->W.as<double>();
-      smem = vec;
+    // fast path: block subspace iteration for the few kept directions
+    bool done = false;
+    if (!std::getenv("TTG_FULL_EIG")) {
+      const size_t sub_vec = sizeof(double) * (size_t)2 * a * ttg::kSubK;
+      size_t smem_s = sizeof(double) * (size_t)a * a + sub_vec;
+      ttg::SyevArgs sa = args;
+      if (smem_s <= c->smem_optin) {
+        sa.in_smem = 1;
+      } else {
+        sa.in_smem = 0;
+        smem_s = sub_vec;
+      }
+      CK(cudaFuncSetAttribute(ttg::k_syev_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+      char nm[64];
+      std::snprintf(nm, sizeof nm, "k_syev_top[a=%d]", a);
+      prof_begin(c, nm, 16.0 * a * a, 2.0 * a * a * ttg::kSubK);
+      ttg::k_syev_top<<<1, ttg::kSubThreads, smem_s, c->stream>>>(sa);
+      post_launch(c);
+      c->d2h += sizeof(EigResult);
+      CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      done = c->h_eig->converged != 0;
+      if (std::getenv("TTG_DEBUG"))
+        std::fprintf(stderr, "[ttg] eig_top a=%d conv=%d iters=%d rank=%d\n", a, c->h_eig->converged,
+                     c->h_eig->sweeps, c->h_eig->rank);
     }
-    CK(cudaFuncSetAttribute(ttg::k_syev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    char nm[64];
-    std::snprintf(nm, sizeof nm, "k_syev[a=%d]", a);
-    prof_begin(c, nm, 16.0 * a * a, 4.0 / 3.0 * a * a * a);
-    ttg::k_syev<<<1, ttg::kSyevThreads, smem, c->stream>>>(args);
-    post_launch(c);
+    if (!done) {
+      size_t vec = sizeof(double) * (size_t)7 * a;
+      size_t smem = sizeof(double) * (size_t)a * a + vec;
+      if (smem <= c->smem_optin) {
+        args.in_smem = 1;
+      } else {
+        args.in_smem = 0;
+        c->W.ensure(sizeof(double) * (size_t)a * a);
+        args.Ag = c->W.as<double>();
+        smem = vec;
+      }
+      CK(cudaFuncSetAttribute(ttg::k_syev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      char nm[64];
+      std::snprintf(nm, sizeof nm, "k_syev[a=%d]", a);
+      prof_begin(c, nm, 16.0 * a * a, 4.0 / 3.0 * a * a * a);
+      ttg::k_syev<<<1, ttg::kSyevThreads, smem, c->stream>>>(args);
+      post_launch(c);
+    }
   } else {
     size_t need_smem = sizeof(double) * ((size_t)a * a + a) + sizeof(int) * a + 64;
     ttg::EigArgs args{};

@@ -386,3 +386,296 @@ __global__ void __launch_bounds__(kSyevThreads) k_syev(SyevArgs p) {
 }
 
 }  // namespace ttg
+
+namespace ttg {
+
+// ---------------------------------------------------------------------------
+// Fast path for the common case "few kept directions": block subspace
+// iteration with Rayleigh–Ritz on G (a x a, shared memory when it fits),
+// block size kSubK.  The rank rule uses trace(G) - sum_{j<r} theta_j (Ritz
+// values are lower bounds of the eigenvalues, so an unconverged estimate can
+// only over-state the rank; convergence is certified by the Ritz residuals
+// |G u_j - theta_j u_j| <= 64 eps theta_0 for every kept j and the next one).
+// If that does not happen within kSubIters, or r >= kSubK - 1, res->converged
+// = 0 and the host falls back to the full tridiagonal solver (k_syev).
+// ---------------------------------------------------------------------------
+constexpr int kSubK = 8;
+constexpr int kSubIters = 40;
+constexpr int kSubThreads = 256;
+
+// one warp: parallel cyclic Jacobi on the symmetric k x k H (k <= 8, ld k),
+// eigenvectors into W.  Round-robin pairs, one lane per pair; all row
+// rotations of a round, then all column rotations (disjoint supports commute).
+// A rotation is skipped when |h_pq| <= 1e-18 sqrt(|h_pp h_qq|); stops after a
+// sweep without rotations.
+__device__ void small_sym_eig(double* H, double* W, int k) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < k * k; i += 32) W[i] = ((i % k) == (i / k)) ? 1.0 : 0.0;
+  __syncwarp();
+  const int n = k + (k & 1);
+  for (int sweep = 0; sweep < 20; ++sweep) {
+    int rotated = 0;
+    for (int rnd = 0; rnd < n - 1; ++rnd) {
+      int pp = -1, qq = -1;
+      double c = 1.0, sn = 0.0;
+      bool act = false;
+      if (lane < n / 2) {
+        pp = (lane == 0) ? 0 : ((lane - 1 + rnd) % (n - 1)) + 1;
+        qq = ((n - 2 - lane + rnd) % (n - 1)) + 1;
+        if (pp > qq) { const int tq = pp; pp = qq; qq = tq; }
+        if (qq < k) {
+          const double hpq = H[pp + k * qq], hpp = H[pp + k * pp], hqq = H[qq + k * qq];
+          if (hpq != 0.0 && fabs(hpq) > 1e-18 * sqrt(fabs(hpp * hqq))) {
+            const double zeta = (hqq - hpp) / (2.0 * hpq);
+            const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
+            c = 1.0 / sqrt(1.0 + t * t);
+            sn = c * t;
+            act = true;
+          }
+        }
+      }
+      rotated |= __any_sync(0xffffffffu, act);
+      __syncwarp();
+      if (act)
+        for (int r = 0; r < k; ++r) {  // rows p, q
+          const double hp = H[pp + k * r], hq = H[qq + k * r];
+          H[pp + k * r] = c * hp - sn * hq;
+          H[qq + k * r] = sn * hp + c * hq;
+        }
+      __syncwarp();
+      if (act) {
+        for (int r = 0; r < k; ++r) {  // columns p, q
+          const double hp = H[r + k * pp], hq = H[r + k * qq];
+          H[r + k * pp] = c * hp - sn * hq;
+          H[r + k * qq] = sn * hp + c * hq;
+        }
+        for (int r = 0; r < k; ++r) {
+          const double wp = W[r + k * pp], wq = W[r + k * qq];
+          W[r + k * pp] = c * wp - sn * wq;
+          W[r + k * qq] = sn * wp + c * wq;
+        }
+      }
+      __syncwarp();
+    }
+    if (!rotated) break;
+  }
+}
+
+// block MGS (twice) of the k columns of X (a x k, ld a); warp-per-column dots,
+// sequential over columns; all threads participate, returns after a barrier.
+__device__ void block_mgs2(double* X, int a, int k, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int j = 0; j < k; ++j) {
+      double* xj = X + (size_t)a * j;
+      // dots with earlier columns: warp i computes <x_i, x_j>
+      for (int i = warp; i < j; i += nw) {
+        const double* xi = X + (size_t)a * i;
+        double s = 0.0;
+        for (int r = lane; r < a; r += 32) s = fma(xi[r], xj[r], s);
+        s = warp_sum(s);
+        if (lane == 0) red[i] = s;
+      }
+      __syncthreads();
+      for (int r = threadIdx.x; r < a; r += blockDim.x) {
+        double v = xj[r];
+        for (int i = 0; i < j; ++i) v -= red[i] * X[r + (size_t)a * i];
+        xj[r] = v;
+      }
+      __syncthreads();
+      double s = 0.0;
+      for (int r = threadIdx.x; r < a; r += blockDim.x) s = fma(xj[r], xj[r], s);
+      s = warp_sum(s);
+      if (lane == 0) red[32 + warp] = s;
+      __syncthreads();
+      double nn = 0.0;
+      for (int w = 0; w < nw; ++w) nn += red[32 + w];
+      const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+      for (int r = threadIdx.x; r < a; r += blockDim.x) xj[r] *= inv;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[64];
+  __shared__ double H[kSubK * kSubK], Wv[kSubK * kSubK], theta[kSubK], resn[kSubK];
+  __shared__ int s_state, s_rank;
+  __shared__ double s_tail;
+  const int a = p.a;
+  const int k = a < kSubK ? a : kSubK;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double* G = p.in_smem ? sm : const_cast<double*>(p.G);
+  double* X = p.in_smem ? sm + (size_t)a * a : sm;
+  double* Z = X + (size_t)a * kSubK;
+  if (p.in_smem)
+    for (long long i = tid; i < (long long)a * a; i += blockDim.x) G[i] = p.G[i];
+  // deterministic pseudo-random start block
+  for (int e = tid; e < a * k; e += blockDim.x) {
+    unsigned long long h = 0x9E3779B97F4A7C15ull * (unsigned long long)(e + 1);
+    h ^= h >> 31; h *= 0xbf58476d1ce4e5b9ull; h ^= h >> 27;
+    X[e] = (double)(h >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+  __syncthreads();
+  double trace = 0.0;
+  for (int i = 0; i < a; ++i) trace += G[i + (size_t)a * i];
+  const double delta = p.delta_src ? p.delta_mult * sqrt(*p.delta_src) : p.delta_mult;
+  const long long kcap = p.kmax < a ? p.kmax : a;
+  if (tid == 0) { s_state = 0; s_rank = 0; s_tail = trace; }
+  if (!(sqrt(fmax(trace, 0.0)) > delta) || kcap == 0) {  // everything fits under delta: rank 0
+    if (tid == 0) {
+      p.res->rank = 0; p.res->tail_sq = fmax(trace, 0.0); p.res->delta = delta; p.res->converged = 1;
+      p.res->sweeps = 0; p.res->lam_max = 0.0; p.res->lam_min_kept = 0.0;
+    }
+    return;
+  }
+  block_mgs2(X, a, k, red);
+  double prev_res = 1e300;
+  int it = 0;
+  for (; it < kSubIters; ++it) {
+    // Z = G X  (thread-consecutive rows i: G[i + a*j] is bank-conflict free)
+    for (int e = tid; e < a * k; e += blockDim.x) {
+      const int i = e % a, c = e / a;
+      const double* xc = X + (size_t)a * c;
+      double s0 = 0.0, s1 = 0.0;
+      int j = 0;
+      for (; j + 1 < a; j += 2) {
+        s0 = fma(G[i + (size_t)a * j], xc[j], s0);
+        s1 = fma(G[i + (size_t)a * (j + 1)], xc[j + 1], s1);
+      }
+      if (j < a) s0 = fma(G[i + (size_t)a * j], xc[j], s0);
+      Z[e] = s0 + s1;
+    }
+    __syncthreads();
+    // H = X^T Z (k x k), symmetrised
+    for (int e = warp; e < k * k; e += nw) {
+      const int i = e % k, j = e / k;
+      double s = 0.0;
+      for (int r = lane; r < a; r += 32) s = fma(X[r + (size_t)a * i], Z[r + (size_t)a * j], s);
+      s = warp_sum(s);
+      if (lane == 0) H[e] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int e = lane; e < k * k; e += 32) {
+        const int i = e % k, j = e / k;
+        if (i < j) {
+          const double m = 0.5 * (H[i + k * j] + H[j + k * i]);
+          H[i + k * j] = m;
+          H[j + k * i] = m;
+        }
+      }
+      __syncwarp();
+      small_sym_eig(H, Wv, k);
+      if (lane == 0) {  // sort descending (selection sort on k <= 8), permute W
+        for (int i = 0; i < k; ++i) theta[i] = H[i + k * i];
+        for (int i = 0; i < k; ++i) {
+          int m = i;
+          for (int j = i + 1; j < k; ++j)
+            if (theta[j] > theta[m]) m = j;
+          if (m != i) {
+            const double tv = theta[i]; theta[i] = theta[m]; theta[m] = tv;
+            for (int r = 0; r < k; ++r) { const double w = Wv[r + k * i]; Wv[r + k * i] = Wv[r + k * m]; Wv[r + k * m] = w; }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // residuals |Z w_j - theta_j X w_j|
+    for (int j = warp; j < k; j += nw) {
+      double s = 0.0;
+      for (int r = lane; r < a; r += 32) {
+        double zw = 0.0, xw = 0.0;
+        for (int c = 0; c < k; ++c) {
+          zw = fma(Z[r + (size_t)a * c], Wv[c + k * j], zw);
+          xw = fma(X[r + (size_t)a * c], Wv[c + k * j], xw);
+        }
+        const double d = zw - theta[j] * xw;
+        s = fma(d, d, s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) resn[j] = sqrt(s);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // rank from the Ritz values (lower bounds => rank can only be over-stated)
+      double pre = 0.0;
+      int r = -1;
+      for (int q = 0; q <= k; ++q) {
+        if (q <= kcap && !(sqrt(fmax(trace - pre, 0.0)) > delta)) { r = q; break; }
+        if (q < k) pre += fmax(theta[q], 0.0);
+      }
+      const double tol = 64.0 * 2.220446049250313e-16 * fmax(theta[0], 1e-300);
+      double worst = 0.0;
+      if (r >= 1 && r < k) {
+        // only the kept Ritz pairs enter the tail and U_R: certify those
+        for (int q = 0; q < r; ++q) worst = fmax(worst, resn[q]);
+        if (worst <= tol || (worst <= 1e-12 * theta[0] && worst >= 0.9 * prev_res)) {
+          double pre2 = 0.0;
+          for (int q = 0; q < r; ++q) pre2 += theta[q];
+          s_rank = r;
+          s_tail = fmax(trace - pre2, 0.0);
+          s_state = 1;  // converged
+        }
+      } else {
+        worst = resn[0];
+        if (it >= 5) s_state = 2;  // more kept directions than the block holds: full solver
+      }
+      prev_res = worst;
+      red[63] = worst;
+    }
+    __syncthreads();
+    if (s_state) break;
+    prev_res = red[63];
+    // next block: X = orth(Z W)   (Ritz-rotated power step)
+    for (int e = tid; e < a * k; e += blockDim.x) {
+      const int i = e % a, j = e / a;
+      double s = 0.0;
+      for (int c = 0; c < k; ++c) s = fma(Z[i + (size_t)a * c], Wv[c + k * j], s);
+      X[e] = s;
+    }
+    __syncthreads();
+    block_mgs2(X, a, k, red);
+  }
+  const int rank = s_rank;
+  if (tid == 0) {
+    p.res->converged = (s_state == 1) ? 1 : 0;
+    p.res->sweeps = it;
+    p.res->rank = rank;
+    p.res->tail_sq = s_tail;
+    p.res->delta = delta;
+    p.res->lam_max = theta[0];
+    p.res->lam_min_kept = rank > 0 ? theta[rank - 1] : 0.0;
+  }
+  if (s_state != 1) return;
+  for (int j = tid; j < k; j += blockDim.x) p.lam[j] = theta[j];
+  // U_R = X W[:, :rank], normalised, sign rule
+  for (int j = warp; j < rank; j += nw) {
+    double* out = p.UR + (size_t)a * j;
+    double nn = 0.0, best = -1.0;
+    int bi = a;
+    for (int r = lane; r < a; r += 32) {
+      double u = 0.0;
+      for (int c = 0; c < k; ++c) u = fma(X[r + (size_t)a * c], Wv[c + k * j], u);
+      out[r] = u;
+      nn = fma(u, u, nn);
+    }
+    nn = warp_sum(nn);
+    const double inv = 1.0 / sqrt(nn);
+    for (int r = lane; r < a; r += 32) {
+      const double v = fabs(out[r]);
+      if (v > best) { best = v; bi = r; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double sgn = (out[bi] < 0.0) ? -inv : inv;
+    __syncwarp();
+    for (int r = lane; r < a; r += 32) out[r] *= sgn;
+  }
+}
+
+}  // namespace ttg

@@ -191,7 +191,7 @@ class Stream:
         else:  # simulation
             s = self._simulation(k, b)
         s = _add_noise(g, s, self.noise)
-        return np.reshape(s, self.modes + (b,), order="F")
+        return np.asfortranarray(np.reshape(s, self.modes + (b,), order="F"))
 
     def _simulation(self, k: int, b: int) -> np.ndarray:
         t0 = k * b
