@@ -54,17 +54,21 @@ REASON_BITS = {
 
 
 class ClockSampler:
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval_ms: int = 100, enabled: bool = True):
         self.index = index
+        self.interval_ms = interval_ms
+        self.enabled = enabled
         self.rows = []
         self.proc = None
         self.thread = None
 
     def start(self):
+        if not self.enabled:
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -198,7 +202,7 @@ def our_arm(args):
     inc_bytes = 8 * S * b
     gen = DeviceStream(seed=args.seed, modes=MODES, rank_shard=rank)
     free, _total = torch.cuda.mem_get_info()
-    reserve = 24 << 30
+    reserve = 48 << 30  # library workspaces grow with the ranks; keep allocations cheap
     cap = max(2, int((free - reserve) // inc_bytes))
     n_inc = 1 + args.warmup + args.steps
     pool = min(n_inc, cap)
@@ -220,14 +224,18 @@ def our_arm(args):
     ctx.reset_stats()
     ctx.set_profiling(True)
     launches0 = ctx.launch_count
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(local_rank, args.clock_interval_ms, not args.no_clocks)
     barrier()
     sampler.start()
     time.sleep(0.3)
     ev0.record(stream)
     reports = []
+    step_evs = []
     for _ in range(args.steps):
         tt, rep = tt_ice_star_update(tt, inc(k), EPS, shape=shape)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        step_evs.append(e)
         reports.append(rep)
         k += 1
     ev1.record(stream)
@@ -235,6 +243,8 @@ def our_arm(args):
     barrier()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
+    step_ms = [ (step_evs[0] if i == 0 else step_evs[i - 1]).elapsed_time(step_evs[i]) if i > 0
+                else ev0.elapsed_time(step_evs[0]) for i in range(len(step_evs))]
     launches = ctx.launch_count - launches0
     kstats = ctx.kernel_stats()
     ctx.set_profiling(False)
@@ -325,8 +335,9 @@ def our_arm(args):
             "config": workload_config(args, world=world),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "per_gpu_gbs": value / world,
-            "steps_detail": [{"obs_used": r.obs_used, "ranks": r.ranks_after, "modes_updated": r.modes_updated}
-                             for r in reports],
+            "steps_detail": [{"obs_used": r.obs_used, "ranks": r.ranks_after, "modes_updated": r.modes_updated,
+                              "device_ms": round(dt, 3), "call_ms": round(r.seconds * 1e3, 3)}
+                             for r, dt in zip(reports, step_ms)],
             "kernels": sorted([{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in s.items()}
                                for s in kstats], key=lambda s: -s["ms"])[:8],
             "pool_increments": pool,
@@ -350,6 +361,8 @@ def main():
     ap.add_argument("--ref-batch", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--clock-interval-ms", type=int, default=100)
+    ap.add_argument("--no-clocks", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

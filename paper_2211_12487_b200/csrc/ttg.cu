@@ -76,7 +76,7 @@ struct DevBuf {
   // grow-only; keep=true preserves the old contents
   void ensure(size_t bytes, bool keep = false, cudaStream_t s = nullptr) {
     if (bytes <= cap) return;
-    size_t nc = std::max(bytes, cap + cap / 2);
+    size_t nc = std::max(bytes + bytes / 4, cap + cap / 2);  // headroom: ranks grow by a few per increment
     void* np = nullptr;
     CK(cudaMalloc(&np, nc));
     if (keep && p) {
@@ -106,7 +106,7 @@ struct ttg_ctx {
   // workspaces (grow-only)
   DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, Uf, Upad, scratch, eigres, on2, sumsq_part,
       scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2], tsq, psif, wcomb, psi[2],
-      spsi[2], scoeffs, matbuf;
+      spsi[2], scoeffs, matbuf, tmp, Craw, small[4];
   std::vector<DevBuf> scur;       // TT-ICE* stats-chain intermediates (reused by the sweep)
   std::vector<bool> stat_has;
   ttg::EigResult* h_eig = nullptr;
@@ -203,6 +203,35 @@ void prof_flush(ttg_ctx* c) {
   c->pending.clear();
 }
 
+// cudaFuncSetAttribute / occupancy queries are driver calls: cache them per
+// (kernel, dynamic smem) so the per-increment host path stays short.
+template <class K>
+int kernel_occupancy(const void* key, K kern, int threads, size_t smem) {
+  struct Entry {
+    const void* k;
+    size_t smem;
+    int occ;
+  };
+  static std::vector<Entry> cache;
+  static std::vector<std::pair<const void*, size_t>> attr;
+  for (const auto& e : cache)
+    if (e.k == key && e.smem == smem) return e.occ;
+  size_t have = 0;
+  for (const auto& a : attr)
+    if (a.first == key) have = a.second;
+  if (smem > have) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bool found = false;
+    for (auto& a : attr)
+      if (a.first == key) { a.second = smem; found = true; }
+    if (!found) attr.push_back({key, smem});
+  }
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  cache.push_back({key, smem, occ});
+  return occ;
+}
+
 int grid_for(long long n, int threads, int max_blocks) {
   long long b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -254,6 +283,7 @@ void make_frags(ttg_ctx* c, const double* U, int a, int r, int ld, bool need_ut,
 }
 
 // ---- generic GEMM (any size) ------------------------------------------------
+// (defined below; forward declaration for the raw-Gram path)
 template <bool TA, bool TB>
 void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
           long long m, long long n, long long k, double alpha, double beta) {
@@ -273,9 +303,7 @@ constexpr int kFastMax1 = 256;  // a8 limit of the single-buffered DMMA tiles
 template <int WBR, int WBC, bool PRE, bool DB>
 void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem, int npairs) {
   auto kern = ttg::k_gram_resid<WBR, WBC, PRE, DB>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem));
+  const int occ = kernel_occupancy((const void*)kern, kern, ttg::kThreads, smem);
   if (occ < 1) fail(TTG_E_RESOURCE, "gram kernel does not fit on an SM");
   long long want = std::max<long long>(1, (long long)c->num_sms * occ / npairs);
   int gx = (int)std::min<long long>(want, std::max<long long>(1, args.n_tiles));
@@ -350,7 +378,7 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
         s.Psi, (int)s.As, (int)s.r, (int)s.As, As8, rc8, c->psif.as<double>(), nullptr);
     post_launch(c);
     args.src = ttg::TileSrc{s.S, src_rows, L, sel, cpo};
-    args.lds = ttg::smem_ld(src_rows + As8 + 8);
+    args.lds = ttg::smem_ld(src_rows + (As8 - (int)s.As) + 4);
     args.As = (int)s.As;
     args.nblk = (int)n;
     args.rc = (int)s.r;
@@ -359,8 +387,13 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
     args.PsiTf = c->psif.as<double>();
     args.UTf = c->UTf.as<double>();
     args.Uf = c->Uf.as<double>();
-    const size_t smem = sizeof(double) * ((size_t)2 * args.lds * ttg::kTC + (size_t)args.ldt * ttg::kTC +
-                                          (size_t)8 * args.ldp * 8);
+    size_t smem = sizeof(double) * ((size_t)args.lds * ttg::kTC + (size_t)args.ldt * ttg::kTC +
+                                    (size_t)8 * args.ldp * 8);
+    const size_t nfr = (size_t)(r8 / 8) * (a8 / 4) * 32 + (size_t)(a8 / 8) * (r8 / 4) * 32 + nf;
+    if (smem + sizeof(double) * nfr <= 110 * 1024) {  // keep 2 CTAs / SM
+      args.frag_smem = 1;
+      smem += sizeof(double) * nfr;
+    }
     const int nb = a8 / 8;
     if (nb <= 4) launch_gram_t<1, 2, true, true>(c, args, smem, 1);
     else if (nb <= 8) launch_gram_t<2, 4, true, true>(c, args, smem, 1);
@@ -376,15 +409,24 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
     args.UTf = c->UTf.as<double>();
     args.Uf = c->Uf.as<double>();
     const int nb = a8 / 8;
+    const size_t nfr = (size_t)(r8 / 8) * (a8 / 4) * 32 + (size_t)(a8 / 8) * (r8 / 4) * 32;
     if (a8 <= kFastMax) {
-      const size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+      size_t smem = sizeof(double) * ((size_t)2 * args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+      if (smem + sizeof(double) * nfr <= 200 * 1024) {
+        args.frag_smem = 1;
+        smem += sizeof(double) * nfr;
+      }
       if (nb <= 4) launch_gram_t<1, 2, false, true>(c, args, smem, 1);
       else if (nb <= 8) launch_gram_t<2, 4, false, true>(c, args, smem, 1);
       else if (nb <= 12) launch_gram_t<3, 6, false, true>(c, args, smem, 1);
       else launch_gram_t<4, 8, false, true>(c, args, smem, 1);
     } else {
       const int ns = (nb + 15) / 16;
-      const size_t smem = sizeof(double) * ((size_t)args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+      size_t smem = sizeof(double) * ((size_t)args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
+      if (smem + sizeof(double) * nfr <= 200 * 1024) {
+        args.frag_smem = 1;
+        smem += sizeof(double) * nfr;
+      }
       launch_gram_t<4, 8, false, false>(c, args, smem, ns * (ns + 1) / 2);
     }
     allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
@@ -408,6 +450,59 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
   gemm<false, true>(c, R, a, R, a, c->G.as<double>(), a, a, a, L, 1.0, 0.0);
   allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
   return false;
+}
+
+
+// Residual Gram of a pre-projected unfolding from the RAW Gram of its source:
+// cur_i = K s with K = I_n (x) Psi^T (orthonormal rows), so
+//   G_i = P K C K^T P,   C = sum_{selected s} s s^T,   P = I - U U^T.
+// The streaming kernel is then a plain SYRK of the source columns (no
+// residual, no pre-projection); the rest is (a x a)-sized.  trace(C) is left
+// in c->scal[4] for the accuracy guard (see sweep()).
+bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, const uint8_t* sel,
+                  long long cpo, double sel_frac, double* tsq) {
+  const int64_t rows = s.As * n, a = s.r * n;
+  const long long L = s.Ls / n;
+  const Src plain{s.S, rows, L, nullptr, rows};
+  const bool did = gram_src(c, plain, 1, nullptr, 0, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
+  c->Craw.ensure(sizeof(double) * (size_t)(rows * rows));
+  CK(cudaMemcpyAsync(c->Craw.p, c->G.p, sizeof(double) * rows * rows, cudaMemcpyDeviceToDevice, c->stream));
+  c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
+  prof_begin(c, "k_kron_eye", 8.0 * rows * a, 0.0);
+  ttg::k_kron_eye<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, (int)s.As, (int)s.r, (int)n,
+                                                                         c->wcomb.as<double>());
+  post_launch(c);
+  c->small[0].ensure(sizeof(double) * (size_t)(rows * a));
+  c->small[1].ensure(sizeof(double) * (size_t)(a * a));
+  double* T1 = c->small[0].as<double>();
+  double* M = c->small[1].as<double>();
+  gemm<false, false>(c, c->Craw.as<double>(), rows, c->wcomb.as<double>(), rows, T1, rows, rows, a, rows, 1.0, 0.0);
+  gemm<true, false>(c, c->wcomb.as<double>(), rows, T1, rows, M, a, a, a, rows, 1.0, 0.0);  // K C K^T
+  c->G.ensure(sizeof(double) * (size_t)(a * a));
+  double* G = c->G.as<double>();
+  if (r_old > 0) {
+    c->small[2].ensure(sizeof(double) * (size_t)(r_old * a));
+    c->small[3].ensure(sizeof(double) * (size_t)(a * a));
+    double* T2 = c->small[2].as<double>();
+    double* R1 = c->small[3].as<double>();
+    gemm<true, false>(c, U, a, M, a, T2, r_old, r_old, a, a, 1.0, 0.0);  // U^T M
+    CK(cudaMemcpyAsync(R1, M, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
+    gemm<false, false>(c, U, a, T2, r_old, R1, a, a, a, r_old, -1.0, 1.0);  // R1 = M - U U^T M
+    gemm<false, false>(c, R1, a, U, a, T2, a, a, r_old, a, 1.0, 0.0);      // T3 = R1 U   (a x r_old, reuse)
+    CK(cudaMemcpyAsync(G, R1, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
+    gemm<false, true>(c, T2, a, U, a, G, a, a, a, r_old, -1.0, 1.0);       // G = R1 - T3 U^T
+  } else {
+    CK(cudaMemcpyAsync(G, M, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  // trace(C) for the guard, then symmetrise G
+  c->scal.ensure(sizeof(double) * 16);
+  prof_begin(c, "k_symmetrize_trace", 16.0 * rows * rows, 0.0);
+  ttg::k_symmetrize_trace<<<1, 256, 0, c->stream>>>(c->Craw.as<double>(), (int)rows, c->scal.as<double>() + 4);
+  post_launch(c);
+  prof_begin(c, "k_symmetrize_trace", 16.0 * a * a, 0.0);
+  ttg::k_symmetrize_trace<<<1, 256, 0, c->stream>>>(G, (int)a, nullptr);
+  post_launch(c);
+  return did;
 }
 
 // ---- eigen-solve -------------------------------------------------------------
@@ -441,7 +536,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         sa.in_smem = 0;
         smem_s = sub_vec;
       }
-      CK(cudaFuncSetAttribute(ttg::k_syev_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+      kernel_occupancy((const void*)ttg::k_syev_top, ttg::k_syev_top, ttg::kSubThreads, smem_s);
       char nm[64];
       std::snprintf(nm, sizeof nm, "k_syev_top[a=%d]", a);
       prof_begin(c, nm, 16.0 * a * a, 2.0 * a * a * ttg::kSubK);
@@ -466,7 +561,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         args.Ag = c->W.as<double>();
         smem = vec;
       }
-      CK(cudaFuncSetAttribute(ttg::k_syev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kernel_occupancy((const void*)ttg::k_syev, ttg::k_syev, ttg::kSyevThreads, smem);
       char nm[64];
       std::snprintf(nm, sizeof nm, "k_syev[a=%d]", a);
       prof_begin(c, nm, 16.0 * a * a, 4.0 / 3.0 * a * a * a);
@@ -498,7 +593,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
       args.Wg = c->W.as<double>();
       smem = sizeof(double) * a + sizeof(int) * a + 64;
     }
-    CK(cudaFuncSetAttribute(ttg::k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kernel_occupancy((const void*)ttg::k_jacobi_eig, ttg::k_jacobi_eig, ttg::kEigThreads, smem);
     prof_begin(c, "k_jacobi_eig", 16.0 * a * a, 0.0);
     ttg::k_jacobi_eig<<<1, ttg::kEigThreads, smem, c->stream>>>(args);
     post_launch(c);
@@ -540,7 +635,7 @@ EigResult accurate_eig(ttg_ctx* c, const double* X, int a, long long L, const do
   args.r8 = r8;
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
   size_t smem = sizeof(double) * ((size_t)a * a + (size_t)args.ldt * ttg::kTC + (size_t)8 * args.ldp * 8);
-  CK(cudaFuncSetAttribute(ttg::k_tsqr_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kernel_occupancy((const void*)ttg::k_tsqr_local, ttg::k_tsqr_local, ttg::kThreads, smem);
   int gx = (int)std::min<long long>(c->num_sms, std::max<long long>(1, args.n_tiles));
   c->partials.ensure(sizeof(double) * (size_t)gx * a * a);
   args.Tout = c->partials.as<double>();
@@ -550,7 +645,7 @@ EigResult accurate_eig(ttg_ctx* c, const double* X, int a, long long L, const do
   c->scratch.ensure(sizeof(double) * (size_t)a * a);
   c->G.ensure(sizeof(double) * (size_t)a * a);
   size_t smem2 = sizeof(double) * (size_t)a * a;
-  CK(cudaFuncSetAttribute(ttg::k_tsqr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  kernel_occupancy((const void*)ttg::k_tsqr_combine, ttg::k_tsqr_combine, 1024, smem2);
   prof_begin(c, "k_tsqr_combine", 16.0 * gx * a * a, 2.0 * gx * a * a * a);
   ttg::k_tsqr_combine<<<1, 1024, smem2, c->stream>>>(c->partials.as<double>(), gx, a, c->scratch.as<double>(),
                                                      c->G.as<double>());
@@ -610,12 +705,19 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   args.tsumsq = tsq;
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
   const bool db = a8 <= kFastMax;
-  const size_t smem = sizeof(double) * ((size_t)(db ? 2 : 1) * args.ldt * ttg::kTC + (size_t)r * ttg::kTC);
-  auto kern = db ? ttg::k_project<true> : ttg::k_project<false>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem));
-  occ = std::max(occ, 1);
+  const size_t nfr = (size_t)(r8 / 8) * (a8 / 4) * 32;
+  size_t smem = sizeof(double) * ((size_t)(db ? 2 : 1) * args.ldt * ttg::kTC + (size_t)2 * r * ttg::kTC);
+  if (smem > c->smem_optin - 1024) {  // does not fit the tile pipeline: generic path
+    gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
+    return false;
+  }
+  if (smem + sizeof(double) * nfr <= std::min<size_t>(c->smem_optin - 1024, 110 * 1024)) {
+    args.frag_smem = 1;
+    smem += sizeof(double) * nfr;
+  }
+  const bool regw = db && a8 <= 64 && r8 <= 16;
+  auto kern = regw ? ttg::k_project<true, true> : (db ? ttg::k_project<true, false> : ttg::k_project<false, false>);
+  const int occ = std::max(kernel_occupancy((const void*)kern, kern, ttg::kThreads, smem), 1);
   const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
   char nm[64];
   std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
@@ -776,6 +878,7 @@ struct SweepOut {
   int guards = 0;
   int modes_updated = 0;
   int accurate_modes = 0;
+  int raw_fallbacks = 0;
   bool cores_changed = false;
   const double* coeffs = nullptr;  // r_d x b_local (compact)
   int r_d = 0;
@@ -846,6 +949,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     const int64_t a = src.r * n_i;
     const long long L = src.Ls / n_i;
     const long long cpo = L / b;
+    const bool was_unchanged = unchanged;
     if (a > 4096) fail(TTG_E_RESOURCE, "unfolding rows a_i = " + std::to_string(a) + " exceed the device solver limit");
     const double* dsrc = o.deltas ? nullptr : o.delta_src;
     const double dmult = o.deltas ? o.deltas[i] : o.delta_mult;
@@ -865,7 +969,9 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       const int64_t rows = src.Psi ? src.As * n_i : a;
       double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
       const double sel_frac = o.star ? (double)o.n_sel_global / (double)(b * c->world) : 1.0;
-      const bool did = gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq);
+      const bool raw = src.Psi != nullptr && !std::getenv("TTG_NO_RAW_GRAM");
+      const bool did = raw ? gram_raw_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq)
+                           : gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq);
       if (tsq) norms_finish(c, nm, rows, did);
       if (!norm_checked && !nm.pending) {  // reject non-finite input before anything is mutated
         check_finite_norm(read_scalar(c, c->scal.as<double>()));
@@ -873,6 +979,16 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       }
       const long long kmax = o.star ? o.n_sel_global * cpo : L * c->world;
       EigResult er = eig(c, (int)a, kmax, dsrc, dmult);
+      if (raw && er.rank > 0) {
+        // raw-Gram cancellation costs ~eps*tr(C)/gap in the kept vectors: keep
+        // it only for directions carrying >= 1e-3 of the source energy
+        const double trC = read_scalar(c, c->scal.as<double>() + 4);
+        if (er.lam_min_kept < 1e-3 * trC) {
+          gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, nullptr);
+          er = eig(c, (int)a, kmax, dsrc, dmult);
+          out.raw_fallbacks++;
+        }
+      }
       if (needs_accurate(er) && accurate_supported((int)a, (int)r_old)) {
         const double* X = materialise(c, src, n_i, c->matbuf);
         er = accurate_eig(c, X, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, kmax, dsrc,
@@ -929,6 +1045,19 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         src = Src{src.S, src.As * n_i, L, psi, r_new};
       } else if (o.reuse_stats && unchanged && c->stat_has.size() > (size_t)(i + 1) && c->stat_has[i + 1]) {
         src = Src{c->scur[i + 1].as<double>(), r_new, L, nullptr, r_new};
+      } else if (o.reuse_stats && was_unchanged && r_R > 0 && c->stat_has.size() > (size_t)(i + 1) &&
+                 c->stat_has[i + 1] && r_old > 0) {
+        // only mode i grew (appended columns): cur_{i+1} = [stats rows ; r_R new rows]
+        c->tmp.ensure(sizeof(double) * (size_t)std::max<long long>(r_R * L, 1));
+        project_src(c, src, n_i, Ui + (size_t)a * r_old, r_R, c->tmp.as<double>(), nullptr);
+        c->cur[flip].ensure(sizeof(double) * (size_t)std::max<long long>(r_new * L, 1));
+        const long long tot = r_new * L;
+        prof_begin(c, "k_merge_rows", 8.0 * (double)(2 * r_new) * L, 0.0);
+        ttg::k_merge_rows<<<grid_for(tot, 256, 8 * c->num_sms), 256, 0, c->stream>>>(
+            c->scur[i + 1].as<double>(), (int)r_old, c->tmp.as<double>(), (int)r_new, L, c->cur[flip].as<double>());
+        post_launch(c);
+        src = Src{c->cur[flip].as<double>(), r_new, L, nullptr, r_new};
+        flip ^= 1;
       } else {
         c->cur[flip].ensure(sizeof(double) * (size_t)std::max<long long>(r_new * L, 1));
         const int64_t rows = src.Psi ? src.As * n_i : a;
@@ -1339,6 +1468,27 @@ static int ctx_init(ttg_ctx* c, int device) {
   CK(cudaGetDeviceProperties(&prop, device));
   c->num_sms = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
+  // eager-load every kernel variant (CUDA lazy loading would otherwise stall
+  // the first increment that needs a new shape class, mid-stream)
+  {
+    cudaFuncAttributes fa;
+    const void* ks[] = {
+        (const void*)ttg::k_gram_resid<1, 2, false, true>, (const void*)ttg::k_gram_resid<2, 4, false, true>,
+        (const void*)ttg::k_gram_resid<3, 6, false, true>, (const void*)ttg::k_gram_resid<4, 8, false, true>,
+        (const void*)ttg::k_gram_resid<4, 8, false, false>, (const void*)ttg::k_gram_resid<1, 2, true, true>,
+        (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
+        (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
+        (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
+        (const void*)ttg::k_gram_reduce, (const void*)ttg::k_syev, (const void*)ttg::k_syev_top,
+        (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
+        (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
+        (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,
+        (const void*)ttg::k_iface_step1, (const void*)ttg::k_iface_step2, (const void*)ttg::k_coef_stats,
+        (const void*)ttg::k_star_local, (const void*)ttg::k_star_mask, (const void*)ttg::k_mask_cols,
+        (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
+        (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>};
+    for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));
+  }
   CK(cudaMallocHost((void**)&c->h_eig, sizeof(ttg::EigResult)));
   CK(cudaMallocHost((void**)&c->h_scal, sizeof(double) * 16));
   CK(cudaMallocHost((void**)&c->h_stats, sizeof(ttg::StarStats)));

@@ -175,7 +175,7 @@ __device__ __forceinline__ void tile_residual(double* T, int ldt, double* Pw, in
       const double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (mb0 + u < MR) dmma(q[u][0], q[u][1], __ldg(UTf + ((long long)(mb0 + u) * KA + kb) * 32 + lane), bv);
+        if (mb0 + u < MR) dmma(q[u][0], q[u][1], UTf[((long long)(mb0 + u) * KA + kb) * 32 + lane], bv);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -192,7 +192,7 @@ __device__ __forceinline__ void tile_residual(double* T, int ldt, double* Pw, in
       const double bv = Pw[(sb * 4 + t) + ldp * g];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (ib0 + u < nb) dmma(q[u][0], q[u][1], __ldg(Uf + ((long long)(ib0 + u) * KR + sb) * 32 + lane), bv);
+        if (ib0 + u < nb) dmma(q[u][0], q[u][1], Uf[((long long)(ib0 + u) * KR + sb) * 32 + lane], bv);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -239,7 +239,7 @@ __device__ __forceinline__ void tile_preproject(const double* Ts, int lds, doubl
     for (int j0 = 0; j0 < nblk; j0 += 4) {
       double q[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
       for (int kb = 0; kb < KS; ++kb) {
-        const double av = __ldg(PsiTf + ((long long)mb * KS + kb) * 32 + lane);
+        const double av = PsiTf[((long long)mb * KS + kb) * 32 + lane];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (j0 + u < nblk) dmma(q[u][0], q[u][1], av, Ts[(As * (j0 + u) + kb * 4 + t) + lds * (c0 + g)]);
@@ -282,6 +282,7 @@ struct GramArgs {
   double* partials;   // [gridDim.y][gridDim.x][SBD*SBD]
   double* tsumsq;     // per-tile sum of squares of the source tile (nullable)
   long long n_tiles;
+  int frag_smem;      // stage UTf / Uf / PsiTf in shared memory
   int r_old;          // host-side accounting only
   double sel_frac;    // host-side accounting only
 };
@@ -290,30 +291,45 @@ template <int WBR, int WBC, bool PRE, bool DB>
 __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red8[kThreads / 32];
+  __shared__ __align__(8) uint64_t bars[2];
   constexpr int SB = 4 * WBR;  // == 2*WBC blocks per super-tile side
   constexpr int SBD = 8 * SB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int ldt = p.ldt, ldp = p.ldp;
   const int lds = PRE ? p.lds : ldt;
-  // smem: source buffers S0 [S1], cur tile Tc (PRE only), per-warp P scratch
+  const bool tma = (p.src.a & 1) == 0;
+  // PRE: one source buffer (prefetched right after the pre-projection) + cur tile.
+  // !PRE: DB ? two tiles : one tile (the residual is computed in place).
+  const int nsrc = PRE ? 1 : (DB ? 2 : 1);
   double* S0 = smem;
-  double* S1 = DB ? S0 + (size_t)lds * kTC : S0;
-  double* Tc = PRE ? S1 + (size_t)lds * kTC : nullptr;
-  double* Pw = (PRE ? Tc + (size_t)ldt * kTC : S0 + (size_t)(DB ? 2 : 1) * lds * kTC) + warp * ldp * 8;
-  const int n_zero = (int)((PRE ? (DB ? 2 : 1) * lds + ldt : (DB ? 2 : 1) * ldt) * kTC);
+  double* S1 = (!PRE && DB) ? S0 + (size_t)lds * kTC : S0;
+  double* Tc = PRE ? S0 + (size_t)lds * kTC : nullptr;
+  double* Pw0 = S0 + (size_t)nsrc * lds * kTC + (PRE ? (size_t)ldt * kTC : 0);
+  double* Pw = Pw0 + warp * ldp * 8;
+  double* fr = Pw0 + 8 * ldp * 8;  // fragment staging (when p.frag_smem)
+  const int n_zero = (int)((nsrc * lds + (PRE ? ldt : 0)) * kTC);
 
   int I = 0, J = blockIdx.y;
   while (J > I) { J -= I + 1; ++I; }
   const int row_blk0 = I * SB + (warp >> 1) * WBR;  // in 8-row blocks
   const int col_blk0 = J * SB + (warp & 1) * WBC;
   const int nb = p.a8 >> 3;
+  const int KA = p.a8 >> 2, KR = p.r8 >> 2, MR = p.r8 >> 3;
 
+  const double* UTf = p.UTf;
+  const double* Uf = p.Uf;
+  const double* PsiTf = p.PsiTf;
+  if (p.frag_smem) {  // stage the (small) fragment arrays once per CTA
+    const int n1 = MR * KA * 32, n2 = nb * KR * 32, n3 = PRE ? p.MRC * p.KS * 32 : 0;
+    for (int i = threadIdx.x; i < n1; i += kThreads) fr[i] = p.UTf[i];
+    for (int i = threadIdx.x; i < n2; i += kThreads) fr[n1 + i] = p.Uf[i];
+    for (int i = threadIdx.x; i < n3; i += kThreads) fr[n1 + n2 + i] = p.PsiTf[i];
+    UTf = fr;
+    Uf = fr + n1;
+    PsiTf = fr + n1 + n2;
+  }
   for (int i = threadIdx.x; i < n_zero; i += kThreads) smem[i] = 0.0;  // padded rows stay zero
-  __syncthreads();
-
-  __shared__ __align__(8) uint64_t bars[2];
-  const bool tma = (p.src.a & 1) == 0;
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -327,25 +343,26 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
 #pragma unroll
     for (int j = 0; j < WBC; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int KA = p.a8 >> 2, KR = p.r8 >> 2, MR = p.r8 >> 3;
+  // early-prefetch scheme (PRE, or DB): the first tile is issued before the loop
+  const bool pre_issue = PRE ? tma : DB;
   long long tile = blockIdx.x;
-  if (DB) {
+  if (pre_issue) {
     if (tile < p.n_tiles) tile_issue(p.src, tile * kTC, S0, lds, &bars[0], tma);
     if (!tma) cp_async_commit();
   }
   int buf = 0;
   for (; tile < p.n_tiles; tile += gridDim.x) {
-    double* Ssrc = (DB && buf) ? S1 : S0;
-    const int cb = DB ? buf : 0;
-    if (DB) {
+    const long long nxt = tile + gridDim.x;
+    double* Ssrc = (!PRE && DB && buf) ? S1 : S0;
+    const int cb = (!PRE && DB) ? buf : 0;
+    if (!PRE && DB) {
       double* Sn = buf ? S0 : S1;
-      const long long nxt = tile + gridDim.x;
       if (nxt < p.n_tiles) tile_issue(p.src, nxt * kTC, Sn, lds, &bars[buf ^ 1], tma);
       if (!tma) {
         cp_async_commit();
         cp_async_wait_1();
       }
-    } else {
+    } else if (!pre_issue) {
       tile_issue(p.src, tile * kTC, S0, lds, &bars[0], tma);
       if (!tma) {
         cp_async_commit();
@@ -363,12 +380,14 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
     }
     double* T = Ssrc;
     if (PRE) {
-      tile_preproject(Ssrc, lds, Tc, ldt, p.PsiTf, p.As, p.nblk, p.rc, p.MRC, p.KS);
+      tile_preproject(Ssrc, lds, Tc, ldt, PsiTf, p.As, p.nblk, p.rc, p.MRC, p.KS);
       T = Tc;
       __syncthreads();
+      // the source buffer is free: fetch the next tile while residual + Gram run
+      if (tma && nxt < p.n_tiles) tile_issue(p.src, nxt * kTC, S0, lds, &bars[0], tma);
     }
     if (p.r8 > 0) {
-      tile_residual(T, ldt, Pw, ldp, p.UTf, p.Uf, KA, KR, MR, nb);
+      tile_residual(T, ldt, Pw, ldp, UTf, Uf, KA, KR, MR, nb);
       __syncthreads();
     }
     // G(super-tile) += T T^T over the tile's 64 columns
@@ -382,13 +401,15 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
       }
 #pragma unroll
       for (int j = 0; j < WBC; ++j) {
-        const int cb = col_blk0 + j;
-        bf[j] = (cb < nb) ? T[(cb * 8 + g) + ldt * (k0 + t)] : 0.0;
+        const int cb2 = col_blk0 + j;
+        bf[j] = (cb2 < nb) ? T[(cb2 * 8 + g) + ldt * (k0 + t)] : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < WBR; ++i)
 #pragma unroll
-        for (int j = 0; j < WBC; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < WBC; ++j)
+          if (col_blk0 + j <= row_blk0 + i)  // lower triangle only (the reduction reads row >= col)
+            dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
     buf ^= 1;
@@ -551,36 +572,64 @@ struct ProjArgs {
   double* out;
   double* tsumsq;     // per-tile sum of squares of the input tile (nullable)
   long long n_tiles;
+  int frag_smem;      // stage W^T fragments in shared memory
 };
 
-// DB: cp.async double-buffered input tiles (a8 <= 128); single-buffered for a8 <= 256.
-template <bool DB>
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+// Projection out (r x L) = W^T X.  Each warp owns 8 tile columns; its m-blocks
+// are computed 4 at a time with a 2-way K split (8 independent DMMA chains).
+// W^T fragments are staged once per CTA in shared memory.  The r x kTC output
+// tile is staged in smem (double-buffered) and written back by one TMA bulk
+// store per tile.  DB: double-buffered input tiles (a8 <= 128), else single
+// (a8 <= 256).
+template <bool DB, bool REGW>
 __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red8[kThreads / 32];
+  __shared__ __align__(8) uint64_t bars[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int ldt = p.ldt;
+  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
+  const int nfr = MR * KA * 32;
   double* T0 = smem;
   double* T1 = DB ? smem + ldt * kTC : T0;
-  double* O = smem + (DB ? 2 : 1) * ldt * kTC;  // r x kTC staging (ld r)
-  for (int i = threadIdx.x; i < (DB ? 2 : 1) * ldt * kTC; i += kThreads) smem[i] = 0.0;
-  __syncthreads();
-  __shared__ __align__(8) uint64_t bars[2];
+  double* Wfs = smem + (DB ? 2 : 1) * ldt * kTC;
+  const double* Wf = p.frag_smem ? Wfs : p.WTf;
+  double* O0 = Wfs + (p.frag_smem ? nfr : 0);
+  double* O1 = O0 + p.r * kTC;
   const bool tma = (p.src.a & 1) == 0;
+  for (int i = threadIdx.x; i < (DB ? 2 : 1) * ldt * kTC; i += kThreads) smem[i] = 0.0;
+  if (p.frag_smem)
+    for (int i = threadIdx.x; i < nfr; i += kThreads) Wfs[i] = p.WTf[i];
+  double wreg[REGW ? 32 : 1];
+  if (REGW) {  // requires MR <= 2 and KA <= 16 (a8 <= 64, r8 <= 16)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb)
+        wreg[u * 16 + kb] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
   }
   __syncthreads();
   unsigned phase[2] = {0u, 0u};
-  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
   long long tile = blockIdx.x;
   if (DB) {
     if (tile < p.n_tiles) tile_issue(p.src, tile * kTC, T0, ldt, &bars[0], tma);
     if (!tma) cp_async_commit();
   }
-  int buf = 0;
+  int buf = 0, obuf = 0;
   for (; tile < p.n_tiles; tile += gridDim.x) {
     double* T = (DB && buf) ? T1 : T0;
     const int cb = DB ? buf : 0;
@@ -603,39 +652,87 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
       mbar_wait(&bars[cb], phase[cb]);
       phase[cb] ^= 1u;
     }
+    // the output staging buffer of two tiles ago must have been read by its bulk store
+    if (threadIdx.x == 0) bulk_wait_read1();
     __syncthreads();
     if (p.tsumsq) {
       const double ts = tile_sumsq(T, p.src.a, ldt, red8);
       if (threadIdx.x == 0) p.tsumsq[tile] = ts;
     }
+    double* O = obuf ? O1 : O0;
     const int c0 = warp * 8;
+    if (REGW) {
+      // W^T fragments live in registers (MR*KA <= 32): one smem load per DMMA pair
+      double q[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb) {
+        if (kb < KA) {
+          const double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (u < MR) dmma(q[u][kb & 1][0], q[u][kb & 1][1], wreg[u * 16 + kb], bv);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int row = u * 8 + g;
+        if (u < MR && row < p.r) {
+          O[row + p.r * (c0 + 2 * t)] = q[u][0][0] + q[u][1][0];
+          O[row + p.r * (c0 + 2 * t + 1)] = q[u][0][1] + q[u][1][1];
+        }
+      }
+    } else
     for (int mb0 = 0; mb0 < MR; mb0 += 4) {
-      double q[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-      for (int kb = 0; kb < KA; ++kb) {
-        const double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+      double q[4][2][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u][0][0] = q[u][0][1] = q[u][1][0] = q[u][1][1] = 0.0;
+      const int nu = min(4, MR - mb0);
+      int kb = 0;
+      for (; kb + 1 < KA; kb += 2) {
+        const double b0 = T[(kb * 4 + t) + ldt * (c0 + g)];
+        const double b1 = T[(kb * 4 + 4 + t) + ldt * (c0 + g)];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (mb0 + u < MR) dmma(q[u][0], q[u][1], __ldg(p.WTf + ((long long)(mb0 + u) * KA + kb) * 32 + lane), bv);
+          if (u < nu) {
+            const double* wf = Wf + ((mb0 + u) * KA + kb) * 32 + lane;
+            dmma(q[u][0][0], q[u][0][1], wf[0], b0);
+            dmma(q[u][1][0], q[u][1][1], wf[32], b1);
+          }
+      }
+      if (kb < KA) {
+        const double b0 = T[(kb * 4 + t) + ldt * (c0 + g)];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < nu) dmma(q[u][0][0], q[u][0][1], Wf[((mb0 + u) * KA + kb) * 32 + lane], b0);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int row = (mb0 + u) * 8 + g;
-        if (mb0 + u < MR && row < p.r) {
-          O[row + p.r * (c0 + 2 * t)] = q[u][0];
-          O[row + p.r * (c0 + 2 * t + 1)] = q[u][1];
+        if (u < nu && row < p.r) {
+          O[row + p.r * (c0 + 2 * t)] = q[u][0][0] + q[u][1][0];
+          O[row + p.r * (c0 + 2 * t + 1)] = q[u][0][1] + q[u][1][1];
         }
       }
     }
+    fence_proxy_async();  // generic writes of O -> visible to the bulk store
     __syncthreads();
     const long long q0c = tile * kTC;
     long long ncols = p.src.L - q0c;
     if (ncols > kTC) ncols = kTC;
     const long long nout = ncols * p.r;
     double* dst = p.out + q0c * p.r;
-    for (long long e = threadIdx.x; e < nout; e += kThreads) dst[e] = O[e];
-    __syncthreads();
+    if (((nout * 8) & 15) == 0 && (((uintptr_t)dst) & 15) == 0) {
+      if (threadIdx.x == 0) {
+        bulk_s2g(dst, O, (unsigned)(nout * 8));
+        bulk_commit();
+      }
+    } else {
+      for (long long e = threadIdx.x; e < nout; e += kThreads) dst[e] = O[e];
+    }
     buf ^= 1;
+    obuf ^= 1;
   }
+  if (threadIdx.x == 0) bulk_wait_all();
   if (!tma) cp_async_wait_0();
 }
 

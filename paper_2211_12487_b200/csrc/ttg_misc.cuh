@@ -183,6 +183,37 @@ __global__ void k_kron_eye(const double* __restrict__ Psi, int As, int r, int n,
   }
 }
 
+// out (rn x L) = [old (ro x L) ; add ((rn - ro) x L)] row-interleaved per column
+__global__ void k_merge_rows(const double* __restrict__ old, int ro, const double* __restrict__ add, int rn,
+                             long long L, double* __restrict__ out) {
+  const int ra = rn - ro;
+  const long long tot = (long long)rn * L;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long q = e / rn;
+    const int p = (int)(e - q * rn);
+    out[e] = (p < ro) ? old[p + (long long)ro * q] : add[(p - ro) + (long long)ra * q];
+  }
+}
+
+// G <- (G + G^T) / 2 and trace -> *tr (fixed order, one block)
+__global__ void k_symmetrize_trace(double* __restrict__ G, int a, double* __restrict__ tr) {
+  for (long long e = threadIdx.x; e < (long long)a * a; e += blockDim.x) {
+    const int i = (int)(e % a), j = (int)(e / a);
+    if (i < j) {
+      const double m = 0.5 * (G[i + (long long)a * j] + G[j + (long long)a * i]);
+      G[i + (long long)a * j] = m;
+      G[j + (long long)a * i] = m;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && tr) {
+    double s = 0.0;
+    for (int i = 0; i < a; ++i) s += G[i + (long long)a * i];
+    *tr = s;
+  }
+}
+
 // selection mask (err > eps, or all when subselect is off)
 __global__ void k_star_mask(const double* __restrict__ errs, int b, double eps, int subselect,
                             uint8_t* __restrict__ sel) {
