@@ -208,6 +208,9 @@ def our_arm(args):
     pool = min(n_inc, cap)
     ys = [gen.increment(k, b) for k in range(pool)]
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    # workspaces grow with the ranks: map them up front (outside the timed region)
+    ctx.reserve(int(min(torch.cuda.mem_get_info()[0] - (8 << 30), 12 * inc_bytes)))
 
     def inc(k):
         return ys[k % pool] if k >= pool else ys[k]
@@ -342,6 +345,9 @@ def our_arm(args):
                                for s in kstats], key=lambda s: -s["ms"])[:8],
             "pool_increments": pool,
         }
+        if args.kernels_out:
+            with open(args.kernels_out, "w") as f:
+                json.dump(sorted(kstats, key=lambda s: -s["ms"]), f, indent=1)
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist is not None:
@@ -363,6 +369,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--clock-interval-ms", type=int, default=100)
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--kernels-out", default=None, help="write the full per-kernel table (JSON) here")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

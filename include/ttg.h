@@ -112,6 +112,10 @@ void ttg_ctx_reset_stats(ttg_ctx* ctx);
 int ttg_ctx_num_kernel_stats(ttg_ctx* ctx);
 int ttg_ctx_kernel_stat(ttg_ctx* ctx, int idx, char* name, int name_len, int64_t* launches, double* ms,
                         double* bytes, double* flops);
+/* Pre-map `bytes` of device memory into the context's stream-ordered workspace
+ * pool, so workspace growth during a stream (ranks grow) never maps new
+ * pages mid-update. */
+int ttg_ctx_reserve(ttg_ctx* ctx, int64_t bytes);
 /* Host<->device bytes moved by the context (H2D of host increments, D2H of
  * scalars/decisions). */
 int ttg_ctx_io_bytes(const ttg_ctx* ctx, int64_t* h2d, int64_t* d2h);

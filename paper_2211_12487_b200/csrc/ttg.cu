@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -55,6 +56,11 @@ struct TtgError {
     if (r_ != ncclSuccess) fail(TTG_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));   \
   } while (0)
 
+// Workspaces come from the device's stream-ordered memory pool on the
+// calling context's stream (no device-wide sync on growth; freed blocks stay
+// cached in the pool).  g_alloc_stream is set at every ABI entry.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
@@ -64,7 +70,7 @@ struct DevBuf {
   DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
-      if (p) cudaFree(p);
+      release();
       p = o.p;
       cap = o.cap;
       o.p = nullptr;
@@ -72,18 +78,25 @@ struct DevBuf {
     }
     return *this;
   }
-  ~DevBuf() { if (p) cudaFree(p); }
-  // grow-only; keep=true preserves the old contents
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) {
+      if (g_alloc_stream) cudaFreeAsync(p, g_alloc_stream);
+      else cudaFree(p);
+    }
+    p = nullptr;
+    cap = 0;
+  }
+  // grow-only (x2 headroom); keep=true preserves the old contents (stream-ordered)
   void ensure(size_t bytes, bool keep = false, cudaStream_t s = nullptr) {
     if (bytes <= cap) return;
-    size_t nc = std::max(bytes + bytes / 4, cap + cap / 2);  // headroom: ranks grow by a few per increment
+    if (!s) s = g_alloc_stream;
+    const size_t nc = std::max(bytes + bytes / 4, 2 * cap);
     void* np = nullptr;
-    CK(cudaMalloc(&np, nc));
-    if (keep && p) {
-      CK(cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, s));
-      CK(cudaStreamSynchronize(s));
-    }
-    if (p) cudaFree(p);
+    if (std::getenv("TTG_TRACE")) std::fprintf(stderr, "[ttg-trace] alloc %zu bytes (had %zu)\n", nc, cap);
+    CK(cudaMallocAsync(&np, nc, s));
+    if (keep && p) CK(cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, s));
+    if (p) CK(cudaFreeAsync(p, s));
     p = np;
     cap = nc;
   }
@@ -146,6 +159,24 @@ struct ttg_tt {
 namespace {
 
 using ttg::EigResult;
+
+// TTG_TRACE=1: host-side timeline of the update (wall clock, for stall hunting)
+struct Trace {
+  bool on = std::getenv("TTG_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ttg-trace] %-28s +%8.3f ms (t=%8.3f)\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count(),
+                 std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
+thread_local Trace* g_trace = nullptr;
+void trace(const char* w) {
+  if (g_trace) g_trace->mark(w);
+}
 
 cudaEvent_t get_event(ttg_ctx* c) {
   if (!c->evpool.empty()) {
@@ -453,6 +484,76 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
 }
 
 
+// ---- raw Gram (SYRK) ---------------------------------------------------------
+template <int WBR, int WBC>
+void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) {
+  constexpr int SBD = 8 * 4 * WBR;
+  const bool two = npairs > 1;  // some pairs carry two slices
+  const size_t slice = sizeof(double) * (size_t)args.ldt * ttg::kTC;
+  const size_t stage = (two ? 2 : 1) * slice;
+  // prefer 2 CTAs / SM with >= 2 stages, else 1 CTA with up to 4
+  int nst;
+  if (2 * 3 * stage <= 220 * 1024) nst = 3;
+  else if (2 * 2 * stage <= 220 * 1024) nst = 2;
+  else nst = (int)std::max<size_t>(1, std::min<size_t>(ttg::kMaxStages, (216 * 1024) / stage));
+  args.nst = nst;
+  const size_t smem = nst * stage;
+  auto kern = ttg::k_syrk<WBR, WBC>;
+  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, ttg::kThreads, smem));
+  long long want = std::max<long long>(1, (long long)c->num_sms * occ / npairs);
+  int gx = (int)std::min<long long>(want, std::max<long long>(1, args.n_tiles));
+  c->partials.ensure(sizeof(double) * (size_t)npairs * gx * SBD * SBD);
+  args.partials = c->partials.as<double>();
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
+  const double Ls = (double)args.L * sel_frac;
+  prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
+  kern<<<dim3(gx, npairs), ttg::kThreads, smem, c->stream>>>(args);
+  post_launch(c);
+  const int a = args.a;
+  const long long n = (long long)a * a;
+  prof_begin(c, "k_gram_reduce", 8.0 * npairs * gx * SBD * SBD, (double)gx * a * a);
+  ttg::k_gram_reduce<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, SBD, a,
+                                                                      c->G.as<double>());
+  post_launch(c);
+}
+
+// C = sum over selected columns x x^T -> c->G (a x a); returns whether per-tile
+// sums of squares were produced
+bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
+          double* tsq) {
+  c->G.ensure(sizeof(double) * (size_t)a * a);
+  const int a8 = ttg::round_up(a, 8), nb = a8 / 8;
+  if (a & 1) {  // odd rows: no 16-byte TMA runs -> generic
+    gram_src(c, Src{X, a, L, nullptr, a}, 1, nullptr, 0, sel, cpo, sel_frac, tsq);
+    return tsq != nullptr && ttg::round_up(a, 8) <= kFastMax1;
+  }
+  ttg::SyrkArgs args{};
+  args.X = X;
+  args.a = a;
+  args.a8 = a8;
+  args.L = L;
+  args.sel = sel;
+  args.cpo = cpo;
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  if (nb <= 16) {
+    args.ldt = ttg::smem_ld(a8);
+    args.tsumsq = tsq;
+    if (nb <= 4) launch_syrk_t<1, 2>(c, args, 1, sel_frac);
+    else if (nb <= 8) launch_syrk_t<2, 4>(c, args, 1, sel_frac);
+    else if (nb <= 12) launch_syrk_t<3, 6>(c, args, 1, sel_frac);
+    else launch_syrk_t<4, 8>(c, args, 1, sel_frac);
+  } else {
+    args.ldt = ttg::smem_ld(128);
+    args.tsumsq = nullptr;
+    const int ns = (nb + 15) / 16;
+    launch_syrk_t<4, 8>(c, args, ns * (ns + 1) / 2, sel_frac);
+  }
+  allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+  return tsq != nullptr && nb <= 16;
+}
+
+
 // Residual Gram of a pre-projected unfolding from the RAW Gram of its source:
 // cur_i = K s with K = I_n (x) Psi^T (orthonormal rows), so
 //   G_i = P K C K^T P,   C = sum_{selected s} s s^T,   P = I - U U^T.
@@ -461,23 +562,26 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
 // in c->scal[4] for the accuracy guard (see sweep()).
 bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, const uint8_t* sel,
                   long long cpo, double sel_frac, double* tsq) {
-  const int64_t rows = s.As * n, a = s.r * n;
+  const int64_t rows = s.Psi ? s.As * n : s.r * n, a = s.r * n;
   const long long L = s.Ls / n;
-  const Src plain{s.S, rows, L, nullptr, rows};
-  const bool did = gram_src(c, plain, 1, nullptr, 0, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
+  const bool did = syrk(c, s.S, (int)rows, L, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
   c->Craw.ensure(sizeof(double) * (size_t)(rows * rows));
   CK(cudaMemcpyAsync(c->Craw.p, c->G.p, sizeof(double) * rows * rows, cudaMemcpyDeviceToDevice, c->stream));
-  c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
-  prof_begin(c, "k_kron_eye", 8.0 * rows * a, 0.0);
-  ttg::k_kron_eye<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, (int)s.As, (int)s.r, (int)n,
-                                                                         c->wcomb.as<double>());
-  post_launch(c);
-  c->small[0].ensure(sizeof(double) * (size_t)(rows * a));
   c->small[1].ensure(sizeof(double) * (size_t)(a * a));
-  double* T1 = c->small[0].as<double>();
   double* M = c->small[1].as<double>();
-  gemm<false, false>(c, c->Craw.as<double>(), rows, c->wcomb.as<double>(), rows, T1, rows, rows, a, rows, 1.0, 0.0);
-  gemm<true, false>(c, c->wcomb.as<double>(), rows, T1, rows, M, a, a, a, rows, 1.0, 0.0);  // K C K^T
+  if (s.Psi) {
+    c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
+    prof_begin(c, "k_kron_eye", 8.0 * rows * a, 0.0);
+    ttg::k_kron_eye<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, (int)s.As, (int)s.r, (int)n,
+                                                                           c->wcomb.as<double>());
+    post_launch(c);
+    c->small[0].ensure(sizeof(double) * (size_t)(rows * a));
+    double* T1 = c->small[0].as<double>();
+    gemm<false, false>(c, c->Craw.as<double>(), rows, c->wcomb.as<double>(), rows, T1, rows, rows, a, rows, 1.0, 0.0);
+    gemm<true, false>(c, c->wcomb.as<double>(), rows, T1, rows, M, a, a, a, rows, 1.0, 0.0);  // K C K^T
+  } else {
+    CK(cudaMemcpyAsync(M, c->Craw.p, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
+  }
   c->G.ensure(sizeof(double) * (size_t)(a * a));
   double* G = c->G.as<double>();
   if (r_old > 0) {
@@ -969,7 +1073,9 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       const int64_t rows = src.Psi ? src.As * n_i : a;
       double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
       const double sel_frac = o.star ? (double)o.n_sel_global / (double)(b * c->world) : 1.0;
-      const bool raw = src.Psi != nullptr && !std::getenv("TTG_NO_RAW_GRAM");
+      // raw Gram (SYRK + small-side projector) for every source; the explicit
+      // residual kernel is the accuracy fallback below
+      const bool raw = !std::getenv("TTG_NO_RAW_GRAM") && (src.Psi || ttg::round_up((int)a, 8) > 0);
       const bool did = raw ? gram_raw_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq)
                            : gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq);
       if (tsq) norms_finish(c, nm, rows, did);
@@ -978,8 +1084,10 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         norm_checked = true;
       }
       const long long kmax = o.star ? o.n_sel_global * cpo : L * c->world;
+      trace("sweep:gram launched");
       EigResult er = eig(c, (int)a, kmax, dsrc, dmult);
-      if (raw && er.rank > 0) {
+      trace("sweep:eig done");
+      if (raw && er.rank > 0 && r_old > 0) {  // no projector (empty basis): C is G exactly
         // raw-Gram cancellation costs ~eps*tr(C)/gap in the kept vectors: keep
         // it only for directions carrying >= 1e-3 of the source energy
         const double trC = read_scalar(c, c->scal.as<double>() + 4);
@@ -1101,6 +1209,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     }
     tt->ranks[i + 1] = r_new;
     if (i + 1 == d) out.r_d = (int)r_new;
+    trace("sweep:mode advanced");
   }
   return out;
 }
@@ -1138,9 +1247,11 @@ const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64
       const bool did = project_src(c, src, n_i, Ui, r, dst.as<double>(), tsq);
       if (tsq) norms_finish(c, nm, rows, did);
       if (cache) c->stat_has[i + 1] = true;
+      trace("chain:materialised");
       src = Src{dst.as<double>(), r, L, nullptr, r};
       flip ^= 1;
     } else {
+      trace("chain:last mode");
       DevBuf& dst = cache ? c->scoeffs : c->coeffs;
       dst.ensure(sizeof(double) * (size_t)std::max<long long>(r * L, 1));
       double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
@@ -1295,10 +1406,15 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   rep->n_ranks = d + 2;
   fill_report_ranks(rep->ranks_before, tt);
 
+  Trace tr;
+  g_trace = tr.on ? &tr : nullptr;
+  trace("star:start");
   star_stats(c, tt, Y, b, eps_des);  // norms fused into the stats projection
+  trace("star:stats launched");
   c->d2h += sizeof(ttg::StarStats);
   CK(cudaMemcpyAsync(c->h_stats, c->stats.p, sizeof(ttg::StarStats), cudaMemcpyDeviceToHost, c->stream));
   const double ysq = read_scalar(c, c->scal.as<double>());
+  trace("star:stats synced");
   check_finite_norm(ysq);
   const double y_norm = std::sqrt(ysq);
   const double* s = c->h_stats->sums;
@@ -1362,7 +1478,9 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
     rep->guard_reorthogonalised = so.guards;
     rep->modes_updated = so.modes_updated;
   }
+  trace("star:sweep done");
   append_last_core(c, tt, coeffs, r_d, b);
+  trace("star:append last core");
   fill_report_ranks(rep->ranks_after, tt);
   // estimate: Pythagoras on the appended coefficients (tt_ice_star.cpp:297-300)
   const double* csrc = c->world > 1 ? c->coeffs_all.as<double>() : coeffs;
@@ -1370,6 +1488,8 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   const double lost_sq = std::max(ysq - kept_sq, 0.0);
   rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(lost_sq) / y_norm;
   rep->seconds = tm.stop();
+  trace("star:end");
+  g_trace = nullptr;
 }
 
 ttg_tt* do_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shape, int ndim, double eps,
@@ -1427,6 +1547,13 @@ ttg_tt* do_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shap
 }
 
 int guard(ttg_ctx* c, auto&& fn) {
+  struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(ttg_ctx* cc) : prev(g_alloc_stream) {
+      if (cc && cc->stream) g_alloc_stream = cc->stream;
+    }
+    ~StreamScope() { g_alloc_stream = prev; }
+  } scope(c);
   try {
     fn();
     return TTG_OK;
@@ -1467,6 +1594,12 @@ static int ctx_init(ttg_ctx* c, int device) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
   c->num_sms = prop.multiProcessorCount;
+  {
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
   c->smem_optin = prop.sharedMemPerBlockOptin;
   // eager-load every kernel variant (CUDA lazy loading would otherwise stall
   // the first increment that needs a new shape class, mid-stream)
@@ -1554,8 +1687,13 @@ void ttg_ctx_destroy(ttg_ctx* c) {
   }
   for (auto e : c->evpool) cudaEventDestroy(e);
   cudaStream_t s = c->stream;
-  delete c;  // frees workspaces
-  if (s) cudaStreamDestroy(s);
+  g_alloc_stream = s;
+  delete c;  // frees workspaces (stream-ordered)
+  g_alloc_stream = nullptr;
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
 }
 
 const char* ttg_last_error(const ttg_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -1601,6 +1739,18 @@ int ttg_ctx_kernel_stat(ttg_ctx* c, int idx, char* name, int name_len, int64_t* 
     if (ms) *ms = st.ms;
     if (bytes) *bytes = st.bytes;
     if (flops) *flops = st.flops;
+  });
+}
+
+int ttg_ctx_reserve(ttg_ctx* c, int64_t bytes) {
+  if (!c || bytes < 0) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    // map `bytes` into the stream-ordered pool now (release threshold is
+    // unlimited, so the pages stay cached for later workspace growth)
+    void* p = nullptr;
+    CK(cudaMallocAsync(&p, (size_t)bytes, c->stream));
+    CK(cudaFreeAsync(p, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

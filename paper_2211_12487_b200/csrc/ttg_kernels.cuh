@@ -428,6 +428,144 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// SYRK of the (selected) columns of X (a x L, column-major), any a:
+//   C = sum_q x_q x_q^T      (the raw Gram; the residual projector is applied
+//                             on the a x a side, see gram_raw_src in ttg.cu)
+// blockIdx.y -> super-tile (I, J), I >= J, of SBD = 8*4*WBR rows; each CTA
+// loads only the row slices I (and J) of every column with one TMA bulk copy
+// per (column, slice) into an NST-deep ring of stages (mbarrier per stage),
+// and accumulates the lower-triangle 8x8 blocks in registers (DMMA).
+// ---------------------------------------------------------------------------
+constexpr int kMaxStages = 4;
+
+struct SyrkArgs {
+  const double* X;
+  int a, a8;
+  long long L;
+  const uint8_t* sel;
+  long long cpo;
+  int ldt;            // smem leading dimension of one slice tile
+  int nst;            // ring stages (1..kMaxStages)
+  double* partials;   // [gridDim.y][gridDim.x][SBD*SBD]
+  double* tsumsq;     // per-tile sum of squares (only with a single full-height slice)
+  long long n_tiles;
+};
+
+// warp 0: issue the (1 or 2) row slices of tile q0 into Ti (and Tj), one barrier
+__device__ __forceinline__ void syrk_issue(const SyrkArgs& p, long long q0, int ri0, int nri, double* Ti, int rj0,
+                                           int nrj, double* Tj, uint64_t* bar) {
+  if ((threadIdx.x >> 5) != 0) return;
+  const int lane = threadIdx.x & 31;
+  bool v[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const long long q = q0 + lane + 32 * h;
+    bool ok = q < p.L;
+    if (ok && p.sel) ok = p.sel[q / p.cpo] != 0;
+    v[h] = ok;
+  }
+  const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, v[0])) + __popc(__ballot_sync(0xffffffffu, v[1]));
+  const unsigned bytes = (unsigned)(nri + (Tj ? nrj : 0)) * 8u;
+  fence_proxy_async();
+  if (lane == 0) mbar_expect_tx(bar, nvalid * bytes);
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    const double* col = p.X + (size_t)p.a * (q0 + c);
+    if (v[h]) {
+      bulk_g2s(Ti + (size_t)p.ldt * c, col + ri0, (unsigned)nri * 8u, bar);
+      if (Tj) bulk_g2s(Tj + (size_t)p.ldt * c, col + rj0, (unsigned)nrj * 8u, bar);
+    } else {
+      for (int r = 0; r < nri; ++r) Ti[r + (size_t)p.ldt * c] = 0.0;
+      if (Tj)
+        for (int r = 0; r < nrj; ++r) Tj[r + (size_t)p.ldt * c] = 0.0;
+    }
+  }
+}
+
+template <int WBR, int WBC>
+__global__ void __launch_bounds__(kThreads) k_syrk(SyrkArgs p) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red8[kThreads / 32];
+  __shared__ __align__(8) uint64_t bars[kMaxStages];
+  constexpr int SB = 4 * WBR;
+  constexpr int SBD = 8 * SB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ldt = p.ldt, nst = p.nst;
+  int I = 0, J = blockIdx.y;
+  while (J > I) { J -= I + 1; ++I; }
+  const bool two = I != J;
+  const int ri0 = I * SBD, nri = min(SBD, p.a - ri0);
+  const int rj0 = J * SBD, nrj = min(SBD, p.a - rj0);
+  const int per_stage = (two ? 2 : 1) * ldt * kTC;
+  for (int i = threadIdx.x; i < nst * per_stage; i += kThreads) smem[i] = 0.0;  // padded rows stay zero
+  if (threadIdx.x == 0)
+    for (int s = 0; s < nst; ++s) mbar_init(&bars[s], 1);
+  __syncthreads();
+  auto Ti_of = [&](int s) { return smem + (size_t)s * per_stage; };
+  auto Tj_of = [&](int s) { return two ? smem + (size_t)s * per_stage + (size_t)ldt * kTC : smem + (size_t)s * per_stage; };
+
+  const int nb_i = (nri + 7) >> 3, nb_j = (nrj + 7) >> 3;
+  const int rb0 = (warp >> 1) * WBR, cb0 = (warp & 1) * WBC;  // local 8-blocks
+  double acc[WBR][WBC][2];
+#pragma unroll
+  for (int i = 0; i < WBR; ++i)
+#pragma unroll
+    for (int j = 0; j < WBC; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // prologue: fill nst-1 stages
+  for (int s = 0; s < nst - 1; ++s) {
+    const long long tl = blockIdx.x + (long long)s * gridDim.x;
+    if (tl < p.n_tiles) syrk_issue(p, tl * kTC, ri0, nri, Ti_of(s), rj0, nrj, two ? Tj_of(s) : nullptr, &bars[s]);
+  }
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+    const int st = it % nst;
+    const unsigned ph = (unsigned)((it / nst) & 1);
+    {  // refill the stage consumed in the previous iteration
+      const int sn = (it + nst - 1) % nst;
+      const long long tl = tile + (long long)(nst - 1) * gridDim.x;
+      if (tl < p.n_tiles) syrk_issue(p, tl * kTC, ri0, nri, Ti_of(sn), rj0, nrj, two ? Tj_of(sn) : nullptr, &bars[sn]);
+    }
+    mbar_wait(&bars[st], ph);
+    __syncthreads();
+    const double* Ti = Ti_of(st);
+    const double* Tj = Tj_of(st);
+    if (p.tsumsq) {
+      const double ts = tile_sumsq(Ti, nri, ldt, red8);
+      if (threadIdx.x == 0) p.tsumsq[tile] = ts;
+    }
+#pragma unroll 4
+    for (int k0 = 0; k0 < kTC; k0 += 4) {
+      double af[WBR], bf[WBC];
+#pragma unroll
+      for (int i = 0; i < WBR; ++i) af[i] = (rb0 + i < nb_i) ? Ti[((rb0 + i) * 8 + g) + ldt * (k0 + t)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < WBC; ++j) bf[j] = (cb0 + j < nb_j) ? Tj[((cb0 + j) * 8 + g) + ldt * (k0 + t)] : 0.0;
+#pragma unroll
+      for (int i = 0; i < WBR; ++i)
+#pragma unroll
+        for (int j = 0; j < WBC; ++j)
+          if (two || cb0 + j <= rb0 + i) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  double* out = p.partials + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * SBD * SBD;
+#pragma unroll
+  for (int i = 0; i < WBR; ++i)
+#pragma unroll
+    for (int j = 0; j < WBC; ++j) {
+      const int r = (rb0 + i) * 8 + g;
+      const int c = (cb0 + j) * 8 + 2 * t;
+      out[r + SBD * c] = acc[i][j][0];
+      out[r + SBD * (c + 1)] = acc[i][j][1];
+    }
+}
+
 // Fixed-order reduction of the per-CTA Gram partials into the full symmetric
 // a x a matrix G (column-major).
 __global__ void k_gram_reduce(const double* __restrict__ partials, int nx, int sbd, int a,

@@ -114,6 +114,10 @@ class Context:
             out.append(dict(name=name.value.decode(), launches=la.value, ms=ms.value, bytes=by.value, flops=fl.value))
         return out
 
+    def reserve(self, nbytes: int) -> None:
+        """Pre-map workspace memory (include/ttg.h ttg_ctx_reserve)."""
+        _check(_lib.load().ttg_ctx_reserve(self._h, int(nbytes)), self)
+
     def io_bytes(self):
         h, d = ctypes.c_int64(), ctypes.c_int64()
         _check(_lib.load().ttg_ctx_io_bytes(self._h, ctypes.byref(h), ctypes.byref(d)), self)
