@@ -485,21 +485,20 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
 
 
 // ---- raw Gram (SYRK) ---------------------------------------------------------
-template <int WBR, int WBC>
+template <int MAXT>
 void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) {
-  constexpr int SBD = 8 * 4 * WBR;
+  constexpr int SBD = 128;
   const bool two = npairs > 1;  // some pairs carry two slices
   const size_t slice = sizeof(double) * (size_t)args.ldt * ttg::kTC;
   const size_t stage = (two ? 2 : 1) * slice;
-  // prefer 2 CTAs / SM with >= 2 stages, else 1 CTA with up to 4
-  int nst;
-  if (2 * 3 * stage <= 220 * 1024) nst = 3;
-  else if (2 * 2 * stage <= 220 * 1024) nst = 2;
+  int nst;  // ring depth: prefer 2 CTAs / SM with >= 3 stages
+  if (2 * 4 * stage <= 220 * 1024) nst = 4;
+  else if (2 * 3 * stage <= 220 * 1024) nst = 3;
   else nst = (int)std::max<size_t>(1, std::min<size_t>(ttg::kMaxStages, (216 * 1024) / stage));
   args.nst = nst;
   const size_t smem = nst * stage;
-  auto kern = ttg::k_syrk<WBR, WBC>;
-  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, ttg::kThreads, smem));
+  auto kern = ttg::k_syrk<MAXT>;
+  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, ttg::kSyrkThreads, smem));
   long long want = std::max<long long>(1, (long long)c->num_sms * occ / npairs);
   int gx = (int)std::min<long long>(want, std::max<long long>(1, args.n_tiles));
   c->partials.ensure(sizeof(double) * (size_t)npairs * gx * SBD * SBD);
@@ -508,7 +507,7 @@ void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) 
   std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
   const double Ls = (double)args.L * sel_frac;
   prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
-  kern<<<dim3(gx, npairs), ttg::kThreads, smem, c->stream>>>(args);
+  kern<<<dim3(gx, npairs), ttg::kSyrkThreads, smem, c->stream>>>(args);
   post_launch(c);
   const int a = args.a;
   const long long n = (long long)a * a;
@@ -536,18 +535,20 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
   args.sel = sel;
   args.cpo = cpo;
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  // 2x2-block tiles per super-tile: T(T+1)/2 (diagonal) or T^2 (off-diagonal), T <= 8
   if (nb <= 16) {
     args.ldt = ttg::smem_ld(a8);
     args.tsumsq = tsq;
-    if (nb <= 4) launch_syrk_t<1, 2>(c, args, 1, sel_frac);
-    else if (nb <= 8) launch_syrk_t<2, 4>(c, args, 1, sel_frac);
-    else if (nb <= 12) launch_syrk_t<3, 6>(c, args, 1, sel_frac);
-    else launch_syrk_t<4, 8>(c, args, 1, sel_frac);
+    const int T = (nb + 1) / 2, ntiles = T * (T + 1) / 2;
+    if (ntiles <= 8) launch_syrk_t<1>(c, args, 1, sel_frac);
+    else if (ntiles <= 16) launch_syrk_t<2>(c, args, 1, sel_frac);
+    else if (ntiles <= 24) launch_syrk_t<3>(c, args, 1, sel_frac);
+    else launch_syrk_t<5>(c, args, 1, sel_frac);
   } else {
     args.ldt = ttg::smem_ld(128);
     args.tsumsq = nullptr;
     const int ns = (nb + 15) / 16;
-    launch_syrk_t<4, 8>(c, args, ns * (ns + 1) / 2, sel_frac);
+    launch_syrk_t<8>(c, args, ns * (ns + 1) / 2, sel_frac);
   }
   allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
   return tsq != nullptr && nb <= 16;
@@ -1619,7 +1620,9 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_iface_step1, (const void*)ttg::k_iface_step2, (const void*)ttg::k_coef_stats,
         (const void*)ttg::k_star_local, (const void*)ttg::k_star_mask, (const void*)ttg::k_mask_cols,
         (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
-        (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>};
+        (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
+        (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
+        (const void*)ttg::k_syrk<8>};
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));
   }
   CK(cudaMallocHost((void**)&c->h_eig, sizeof(ttg::EigResult)));

@@ -486,13 +486,20 @@ __device__ __forceinline__ void syrk_issue(const SyrkArgs& p, long long q0, int 
   }
 }
 
-template <int WBR, int WBC>
-__global__ void __launch_bounds__(kThreads) k_syrk(SyrkArgs p) {
+// Warp-specialised SYRK: warps 0..7 consume, warp 8 produces (TMA).  Each
+// consumer warp owns up to MAXT 2x2 tiles of 8x8 blocks from the lower
+// triangle of the super-tile (diagonal tiles also compute their upper block).
+// full[s] / empty[s] mbarriers per ring stage; no block-wide barrier in the
+// main loop.
+constexpr int kConsumerWarps = 8;
+constexpr int kSyrkThreads = (kConsumerWarps + 1) * 32;
+
+template <int MAXT>
+__global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double red8[kThreads / 32];
-  __shared__ __align__(8) uint64_t bars[kMaxStages];
-  constexpr int SB = 4 * WBR;
-  constexpr int SBD = 8 * SB;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ double red8[kConsumerWarps + 1];
+  constexpr int SBD = 128;  // super-tile rows (16 blocks)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int ldt = p.ldt, nst = p.nst;
@@ -502,68 +509,159 @@ __global__ void __launch_bounds__(kThreads) k_syrk(SyrkArgs p) {
   const int ri0 = I * SBD, nri = min(SBD, p.a - ri0);
   const int rj0 = J * SBD, nrj = min(SBD, p.a - rj0);
   const int per_stage = (two ? 2 : 1) * ldt * kTC;
-  for (int i = threadIdx.x; i < nst * per_stage; i += kThreads) smem[i] = 0.0;  // padded rows stay zero
+  for (int i = threadIdx.x; i < nst * per_stage; i += blockDim.x) smem[i] = 0.0;  // padded rows stay zero
   if (threadIdx.x == 0)
-    for (int s = 0; s < nst; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
   __syncthreads();
   auto Ti_of = [&](int s) { return smem + (size_t)s * per_stage; };
   auto Tj_of = [&](int s) { return two ? smem + (size_t)s * per_stage + (size_t)ldt * kTC : smem + (size_t)s * per_stage; };
 
-  const int nb_i = (nri + 7) >> 3, nb_j = (nrj + 7) >> 3;
-  const int rb0 = (warp >> 1) * WBR, cb0 = (warp & 1) * WBC;  // local 8-blocks
-  double acc[WBR][WBC][2];
+  if (warp == kConsumerWarps) {  // ---- producer ----
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+      const int st = it % nst;
+      if (it >= nst) mbar_wait(&empty[st], (unsigned)(((it / nst) - 1) & 1));
+      // syrk_issue is written for warp 0: re-base the warp index
+      const long long q0 = tile * kTC;
+      bool v[2];
 #pragma unroll
-  for (int i = 0; i < WBR; ++i)
+      for (int h = 0; h < 2; ++h) {
+        const long long q = q0 + lane + 32 * h;
+        bool ok = q < p.L;
+        if (ok && p.sel) ok = p.sel[q / p.cpo] != 0;
+        v[h] = ok;
+      }
+      const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, v[0])) + __popc(__ballot_sync(0xffffffffu, v[1]));
+      const unsigned bytes = (unsigned)(nri + (two ? nrj : 0)) * 8u;
+      double* Ti = Ti_of(st);
+      double* Tj = two ? Tj_of(st) : nullptr;
+      // zero-fill first: the arrive below releases these generic writes
 #pragma unroll
-    for (int j = 0; j < WBC; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  // prologue: fill nst-1 stages
-  for (int s = 0; s < nst - 1; ++s) {
-    const long long tl = blockIdx.x + (long long)s * gridDim.x;
-    if (tl < p.n_tiles) syrk_issue(p, tl * kTC, ri0, nri, Ti_of(s), rj0, nrj, two ? Tj_of(s) : nullptr, &bars[s]);
+      for (int h = 0; h < 2; ++h) {
+        const int c = lane + 32 * h;
+        if (!v[h]) {
+          for (int r = 0; r < nri; ++r) Ti[r + (size_t)ldt * c] = 0.0;
+          if (Tj)
+            for (int r = 0; r < nrj; ++r) Tj[r + (size_t)ldt * c] = 0.0;
+        }
+      }
+      __syncwarp();
+      fence_proxy_async();
+      if (lane == 0) mbar_expect_tx(&full[st], nvalid * bytes);
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = lane + 32 * h;
+        const double* col = p.X + (size_t)p.a * (q0 + c);
+        if (v[h]) {
+          bulk_g2s(Ti + (size_t)ldt * c, col + ri0, (unsigned)nri * 8u, &full[st]);
+          if (Tj) bulk_g2s(Tj + (size_t)ldt * c, col + rj0, (unsigned)nrj * 8u, &full[st]);
+        }
+      }
+    }
+    return;
   }
+
+  // ---- consumers: 2x2 tiles of the lower triangle, assigned round-robin ----
+  const int nbi = (nri + 7) >> 3, nbj = (nrj + 7) >> 3;
+  const int tI = (nbi + 1) >> 1, tJ = (nbj + 1) >> 1;  // 2x2-block tiles per side
+  const int ntiles = two ? tI * tJ : tI * (tI + 1) / 2;
+  // tile idx = warp + 8u -> (ta, tb), lower-triangular row-major when !two.
+  // Fully unrolled: the per-tile smem offsets stay in registers.
+  int offA0[MAXT], offA1[MAXT], offB0[MAXT], offB1[MAXT];
+  bool okA1[MAXT], okB1[MAXT], live[MAXT];
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u) {
+    const int idx = warp + kConsumerWarps * u;
+    live[u] = idx < ntiles;
+    int ta = 0, tb = 0;
+    if (two) {
+      ta = idx / max(tJ, 1);
+      tb = idx - ta * max(tJ, 1);
+    } else {
+      ta = (int)((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
+      while ((ta + 1) * (ta + 2) / 2 <= idx) ++ta;
+      while (ta * (ta + 1) / 2 > idx) --ta;
+      tb = idx - ta * (ta + 1) / 2;
+    }
+    const int bi = 2 * ta, bj = 2 * tb;
+    offA0[u] = (bi * 8 + g) + ldt * t;
+    offA1[u] = ((bi + 1) * 8 + g) + ldt * t;
+    offB0[u] = (bj * 8 + g) + ldt * t;
+    offB1[u] = ((bj + 1) * 8 + g) + ldt * t;
+    okA1[u] = bi + 1 < nbi;
+    okB1[u] = bj + 1 < nbj;
+  }
+  double acc[MAXT][2][2][2];
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) acc[u][x][y][0] = acc[u][x][y][1] = 0.0;
+  double tsq_acc = 0.0;
   int it = 0;
   for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const int st = it % nst;
-    const unsigned ph = (unsigned)((it / nst) & 1);
-    {  // refill the stage consumed in the previous iteration
-      const int sn = (it + nst - 1) % nst;
-      const long long tl = tile + (long long)(nst - 1) * gridDim.x;
-      if (tl < p.n_tiles) syrk_issue(p, tl * kTC, ri0, nri, Ti_of(sn), rj0, nrj, two ? Tj_of(sn) : nullptr, &bars[sn]);
-    }
-    mbar_wait(&bars[st], ph);
-    __syncthreads();
+    mbar_wait(&full[st], (unsigned)((it / nst) & 1));
     const double* Ti = Ti_of(st);
     const double* Tj = Tj_of(st);
-    if (p.tsumsq) {
-      const double ts = tile_sumsq(Ti, nri, ldt, red8);
-      if (threadIdx.x == 0) p.tsumsq[tile] = ts;
+    if (p.tsumsq) {  // per-tile sum of squares (single full-height slice only)
+      double sq = 0.0;
+      for (int e = lane + 32 * warp; e < nri * kTC; e += 32 * kConsumerWarps) {
+        const int c = e / nri, r = e - c * nri;
+        const double vv = Ti[r + ldt * c];
+        sq = fma(vv, vv, sq);
+      }
+      tsq_acc = warp_sum(sq);
     }
+#pragma unroll
+    for (int u = 0; u < MAXT; ++u) {
+      if (!live[u]) continue;  // warp-uniform
 #pragma unroll 4
-    for (int k0 = 0; k0 < kTC; k0 += 4) {
-      double af[WBR], bf[WBC];
-#pragma unroll
-      for (int i = 0; i < WBR; ++i) af[i] = (rb0 + i < nb_i) ? Ti[((rb0 + i) * 8 + g) + ldt * (k0 + t)] : 0.0;
-#pragma unroll
-      for (int j = 0; j < WBC; ++j) bf[j] = (cb0 + j < nb_j) ? Tj[((cb0 + j) * 8 + g) + ldt * (k0 + t)] : 0.0;
-#pragma unroll
-      for (int i = 0; i < WBR; ++i)
-#pragma unroll
-        for (int j = 0; j < WBC; ++j)
-          if (two || cb0 + j <= rb0 + i) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      for (int k0 = 0; k0 < kTC; k0 += 4) {
+        const int ko = ldt * k0;
+        const double a0 = Ti[offA0[u] + ko];
+        const double a1 = okA1[u] ? Ti[offA1[u] + ko] : 0.0;
+        const double b0 = Tj[offB0[u] + ko];
+        const double b1 = okB1[u] ? Tj[offB1[u] + ko] : 0.0;
+        dmma(acc[u][0][0][0], acc[u][0][0][1], a0, b0);
+        dmma(acc[u][0][1][0], acc[u][0][1][1], a0, b1);
+        dmma(acc[u][1][0][0], acc[u][1][0][1], a1, b0);
+        dmma(acc[u][1][1][0], acc[u][1][1][1], a1, b1);
+      }
     }
-    __syncthreads();
+    if (p.tsumsq) {  // fixed-order per-tile total: warp partials -> warp 0
+      if (lane == 0) red8[warp] = tsq_acc;
+      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * kConsumerWarps));
+      if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < kConsumerWarps; ++w) tot += red8[w];
+        p.tsumsq[tile] = tot;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * kConsumerWarps));
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
   }
   double* out = p.partials + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * SBD * SBD;
 #pragma unroll
-  for (int i = 0; i < WBR; ++i)
+  for (int u = 0; u < MAXT; ++u) {
+    if (!live[u]) continue;
+    const int rI = offA0[u] - ldt * t - g, rJ = offB0[u] - ldt * t - g;  // first row of the tile
 #pragma unroll
-    for (int j = 0; j < WBC; ++j) {
-      const int r = (rb0 + i) * 8 + g;
-      const int c = (cb0 + j) * 8 + 2 * t;
-      out[r + SBD * c] = acc[i][j][0];
-      out[r + SBD * (c + 1)] = acc[i][j][1];
-    }
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const int r = rI + x * 8 + g;
+        const int c = rJ + y * 8 + 2 * t;
+        out[r + SBD * c] = acc[u][x][y][0];
+        out[r + SBD * (c + 1)] = acc[u][x][y][1];
+      }
+  }
 }
 
 // Fixed-order reduction of the per-CTA Gram partials into the full symmetric
