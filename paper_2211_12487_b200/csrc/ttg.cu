@@ -809,6 +809,27 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   args.out = out;
   args.tsumsq = tsq;
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  if (a & 1) {  // odd rows: no 16-byte bulk runs -> cp.async single-buffered kernel
+    const size_t nfr0 = (size_t)(r8 / 8) * (a8 / 4) * 32;
+    size_t smem0 = sizeof(double) * ((size_t)args.ldt * ttg::kTC + (size_t)2 * r * ttg::kTC);
+    if (smem0 > c->smem_optin - 1024) {
+      gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
+      return false;
+    }
+    if (smem0 + sizeof(double) * nfr0 <= 110 * 1024) {
+      args.frag_smem = 1;
+      smem0 += sizeof(double) * nfr0;
+    }
+    auto k0 = ttg::k_project<false, false>;
+    const int occ0 = std::max(kernel_occupancy((const void*)k0, k0, ttg::kThreads, smem0), 1);
+    const int gx0 = (int)std::min<long long>((long long)c->num_sms * occ0, std::max<long long>(1, args.n_tiles));
+    char nm0[64];
+    std::snprintf(nm0, sizeof nm0, "k_project[a=%d,r=%d]", a, r);
+    prof_begin(c, nm0, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
+    k0<<<gx0, ttg::kThreads, smem0, c->stream>>>(args);
+    post_launch(c);
+    return tsq != nullptr;
+  }
   const bool db = a8 <= kFastMax;
   const size_t nfr = (size_t)(r8 / 8) * (a8 / 4) * 32;
   size_t smem = sizeof(double) * ((size_t)(db ? 2 : 1) * args.ldt * ttg::kTC + (size_t)2 * r * ttg::kTC);
@@ -1006,7 +1027,7 @@ double* norms_tiles_for(ttg_ctx* c, Norms& nm, const double* src, int64_t rows, 
     return nullptr;
   }
   const long long nt = (L + ttg::kTC - 1) / ttg::kTC;
-  c->tsq.ensure(sizeof(double) * (size_t)nt);
+  c->tsq.ensure(sizeof(double) * (size_t)nt * ttg::kConsumerWarps);
   return c->tsq.as<double>();
 }
 
@@ -1017,9 +1038,12 @@ void norms_finish(ttg_ctx* c, Norms& nm, int64_t rows, bool produced) {
     c->on2.ensure(sizeof(double) * nm.b);
     c->scal.ensure(sizeof(double) * 16);
     const long long tpo = nm.S / (rows * ttg::kTC);
-    prof_begin(c, "k_tiles_to_obs", 8.0 * tpo * nm.b, 0.0);
-    ttg::k_tiles_to_obs<<<1, 256, 0, c->stream>>>(c->tsq.as<double>(), tpo, (int)nm.b, c->on2.as<double>(),
-                                                  c->scal.as<double>());
+    prof_begin(c, "k_tiles_to_obs", 8.0 * tpo * ttg::kConsumerWarps * nm.b, 0.0);
+    ttg::k_tiles_to_obs<<<(unsigned)nm.b, 256, 0, c->stream>>>(c->tsq.as<double>(), tpo, (int)nm.b,
+                                                                 c->on2.as<double>(), nullptr);
+    post_launch(c);
+    prof_begin(c, "k_sum_vec", 8.0 * nm.b, 0.0);
+    ttg::k_sum_vec<<<1, 32, 0, c->stream>>>(c->on2.as<double>(), (int)nm.b, c->scal.as<double>());
     post_launch(c);
     allreduce_sum(c, c->scal.as<double>(), 1);
   }
@@ -1622,7 +1646,8 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
         (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
         (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
-        (const void*)ttg::k_syrk<8>};
+        (const void*)ttg::k_syrk<8>, (const void*)ttg::k_project_ws<true>, (const void*)ttg::k_project_ws<false>,
+        (const void*)ttg::k_sum_vec};
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));
   }
   CK(cudaMallocHost((void**)&c->h_eig, sizeof(ttg::EigResult)));

@@ -18,6 +18,8 @@
 namespace ttg {
 
 constexpr int kTC = 64;        // columns of cur per smem tile
+constexpr int kConsumerWarps = 8;                        // warp-specialised kernels: 8 consumers
+constexpr int kSyrkThreads = (kConsumerWarps + 1) * 32;  // + 1 TMA producer warp
 constexpr int kThreads = 256;  // 8 warps; warp w owns tile columns [8w, 8w+8)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
     __syncthreads();
     if (p.tsumsq) {
       const double ts = tile_sumsq(Ssrc, p.src.a, lds, red8);
-      if (threadIdx.x == 0) p.tsumsq[tile] = ts;
+      if (threadIdx.x < kConsumerWarps) p.tsumsq[tile * kConsumerWarps + threadIdx.x] = threadIdx.x == 0 ? ts : 0.0;
     }
     double* T = Ssrc;
     if (PRE) {
@@ -491,8 +493,6 @@ __device__ __forceinline__ void syrk_issue(const SyrkArgs& p, long long q0, int 
 // triangle of the super-tile (diagonal tiles also compute their upper block).
 // full[s] / empty[s] mbarriers per ring stage; no block-wide barrier in the
 // main loop.
-constexpr int kConsumerWarps = 8;
-constexpr int kSyrkThreads = (kConsumerWarps + 1) * 32;
 
 template <int MAXT>
 __global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
@@ -609,14 +609,15 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
     mbar_wait(&full[st], (unsigned)((it / nst) & 1));
     const double* Ti = Ti_of(st);
     const double* Tj = Tj_of(st);
-    if (p.tsumsq) {  // per-tile sum of squares (single full-height slice only)
+    if (p.tsumsq) {  // per-(tile, warp) sum of squares (single full-height slice only)
       double sq = 0.0;
       for (int e = lane + 32 * warp; e < nri * kTC; e += 32 * kConsumerWarps) {
         const int c = e / nri, r = e - c * nri;
         const double vv = Ti[r + ldt * c];
         sq = fma(vv, vv, sq);
       }
-      tsq_acc = warp_sum(sq);
+      sq = warp_sum(sq);
+      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = sq;
     }
 #pragma unroll
     for (int u = 0; u < MAXT; ++u) {
@@ -633,16 +634,6 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
         dmma(acc[u][1][0][0], acc[u][1][0][1], a1, b0);
         dmma(acc[u][1][1][0], acc[u][1][1][1], a1, b1);
       }
-    }
-    if (p.tsumsq) {  // fixed-order per-tile total: warp partials -> warp 0
-      if (lane == 0) red8[warp] = tsq_acc;
-      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * kConsumerWarps));
-      if (threadIdx.x == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < kConsumerWarps; ++w) tot += red8[w];
-        p.tsumsq[tile] = tot;
-      }
-      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * kConsumerWarps));
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
@@ -809,6 +800,7 @@ struct ProjArgs {
   double* tsumsq;     // per-tile sum of squares of the input tile (nullable)
   long long n_tiles;
   int frag_smem;      // stage W^T fragments in shared memory
+  int nst;            // ring stages (k_project_ws)
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
@@ -893,7 +885,7 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
     __syncthreads();
     if (p.tsumsq) {
       const double ts = tile_sumsq(T, p.src.a, ldt, red8);
-      if (threadIdx.x == 0) p.tsumsq[tile] = ts;
+      if (threadIdx.x < kConsumerWarps) p.tsumsq[tile * kConsumerWarps + threadIdx.x] = threadIdx.x == 0 ? ts : 0.0;
     }
     double* O = obuf ? O1 : O0;
     const int c0 = warp * 8;
@@ -972,20 +964,180 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
   if (!tma) cp_async_wait_0();
 }
 
-// per-observation sums from per-tile partials (tiles never straddle observations)
-__global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_per_obs, int nobs,
-                               double* __restrict__ on2, double* __restrict__ total) {
-  for (int o = threadIdx.x; o < nobs; o += blockDim.x) {
-    double s = 0.0;
-    for (long long k = 0; k < tiles_per_obs; ++k) s += ts[(long long)o * tiles_per_obs + k];
-    on2[o] = s;
+// Projection out (r x L) = W^T X, warp-specialised: warp 8 is the TMA
+// producer (one bulk copy per column into an NST-deep ring, full/empty
+// mbarriers), warps 0..7 consume: each owns 8 tile columns, computes its
+// m-blocks (W^T fragments in registers when a8 <= 64 and r8 <= 16, else from
+// shared memory) and stores its outputs straight from the accumulators.  No
+// block-wide barrier in the main loop.  Optional per-(tile, warp) sums of
+// squares of the input (fused norms; reduced in fixed order afterwards).
+template <bool REGW>
+__global__ void __launch_bounds__(kSyrkThreads) k_project_ws(ProjArgs p) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ldt = p.ldt, nst = p.nst;
+  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
+  const int nfr = MR * KA * 32;
+  const int stage = ldt * kTC;
+  double* Wfs = smem + (size_t)nst * stage;
+  for (int i = threadIdx.x; i < nst * stage; i += blockDim.x) smem[i] = 0.0;
+  if (!REGW && p.frag_smem)
+    for (int i = threadIdx.x; i < nfr; i += blockDim.x) Wfs[i] = p.WTf[i];
+  if (threadIdx.x == 0)
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+  __syncthreads();
+  const int a = p.src.a;
+
+  if (warp == kConsumerWarps) {  // ---- producer ----
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+      const int st = it % nst;
+      if (it >= nst) mbar_wait(&empty[st], (unsigned)(((it / nst) - 1) & 1));
+      const long long q0 = tile * kTC;
+      double* T = smem + (size_t)st * stage;
+      bool v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) v[h] = q0 + lane + 32 * h < p.src.L;
+      const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, v[0])) + __popc(__ballot_sync(0xffffffffu, v[1]));
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (!v[h])
+          for (int r = 0; r < a; ++r) T[r + (size_t)ldt * (lane + 32 * h)] = 0.0;
+      __syncwarp();
+      fence_proxy_async();
+      if (lane == 0) mbar_expect_tx(&full[st], nvalid * (unsigned)a * 8u);
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = lane + 32 * h;
+        if (v[h]) bulk_g2s(T + (size_t)ldt * c, p.src.X + (size_t)a * (q0 + c), (unsigned)a * 8u, &full[st]);
+      }
+    }
+    return;
   }
+
+  // ---- consumers ----
+  double wreg[REGW ? 32 : 1];
+  if (REGW) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb)
+        wreg[u * 16 + kb] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
+  }
+  const double* Wf = p.frag_smem ? Wfs : p.WTf;
+  const int c0 = warp * 8;
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+    const int st = it % nst;
+    mbar_wait(&full[st], (unsigned)((it / nst) & 1));
+    const double* T = smem + (size_t)st * stage;
+    const long long q0c = tile * kTC;
+    if (p.tsumsq) {  // this warp's 8 columns
+      double sq = 0.0;
+      for (int e = lane; e < a * 8; e += 32) {
+        const int c = e / a, r = e - c * a;
+        const double vv = T[r + ldt * (c0 + c)];
+        sq = fma(vv, vv, sq);
+      }
+      sq = warp_sum(sq);
+      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = sq;
+    }
+    // my output columns (c0 + 2t, +1): valid?
+    const long long col0 = q0c + c0 + 2 * t;
+    const bool ok0 = col0 < p.src.L, ok1 = col0 + 1 < p.src.L;
+    double* o0 = p.out + col0 * p.r;
+    double* o1 = o0 + p.r;
+    if (REGW) {
+      double q[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb) {
+        if (kb < KA) {
+          const double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (u < MR) dmma(q[u][kb & 1][0], q[u][kb & 1][1], wreg[u * 16 + kb], bv);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int row = u * 8 + g;
+        if (u < MR && row < p.r) {
+          if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
+          if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
+        }
+      }
+    } else {
+      for (int mb0 = 0; mb0 < MR; mb0 += 4) {
+        double q[4][2][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u][0][0] = q[u][0][1] = q[u][1][0] = q[u][1][1] = 0.0;
+        const int nu = min(4, MR - mb0);
+        int kb = 0;
+        for (; kb + 1 < KA; kb += 2) {
+          const double b0 = T[(kb * 4 + t) + ldt * (c0 + g)];
+          const double b1 = T[(kb * 4 + 4 + t) + ldt * (c0 + g)];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < nu) {
+              const double* wf = Wf + ((mb0 + u) * KA + kb) * 32 + lane;
+              dmma(q[u][0][0], q[u][0][1], wf[0], b0);
+              dmma(q[u][1][0], q[u][1][1], wf[32], b1);
+            }
+        }
+        if (kb < KA) {
+          const double b0 = T[(kb * 4 + t) + ldt * (c0 + g)];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < nu) dmma(q[u][0][0], q[u][0][1], Wf[((mb0 + u) * KA + kb) * 32 + lane], b0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int row = (mb0 + u) * 8 + g;
+          if (u < nu && row < p.r) {
+            if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
+            if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+  }
+}
+
+// per-observation sums from per-(tile, warp) partials (tiles never straddle
+// observations): one block per observation, fixed assignment + fixed tree
+__global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_per_obs, int nobs,
+                               double* __restrict__ on2, double* __restrict__ unused) {
+  __shared__ double red[32];
+  const long long per_obs = tiles_per_obs * kConsumerWarps;
+  const int o = blockIdx.x;
+  const double* src = ts + (long long)o * per_obs;
+  double s = 0.0;
+  for (long long k = threadIdx.x; k < per_obs; k += blockDim.x) s += src[k];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int o = 0; o < nobs; ++o) s += on2[o];
-    *total = s;
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    on2[o] = tot;
   }
+}
+
+// total = sum_o v[o] in observation order (one thread: the reference's order)
+__global__ void k_sum_vec(const double* __restrict__ v, int n, double* __restrict__ total) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += v[i];
+  *total = s;
 }
 
 // ---------------------------------------------------------------------------
