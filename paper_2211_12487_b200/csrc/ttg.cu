@@ -15,6 +15,7 @@
 // a handful of scalars are all-reduced and the coefficient columns
 // all-gathered with NCCL; every rank then runs the same deterministic eigen
 // solve on identical bytes.
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -491,8 +492,8 @@ void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) 
   const bool two = npairs > 1;  // some pairs carry two slices
   const size_t slice = sizeof(double) * (size_t)args.ldt * ttg::kTC;
   const size_t stage = (two ? 2 : 1) * slice;
-  int nst;  // ring depth: prefer 2 CTAs / SM with >= 3 stages
-  if (2 * 4 * stage <= 220 * 1024) nst = 4;
+  int nst;  // per-column TMA issue needs >= 3 issuing CTAs / SM to stream (tools/probe/stream_probe.cu)
+  if (3 * 2 * stage <= 220 * 1024) nst = 2;
   else if (2 * 3 * stage <= 220 * 1024) nst = 3;
   else nst = (int)std::max<size_t>(1, std::min<size_t>(ttg::kMaxStages, (216 * 1024) / stage));
   args.nst = nst;
@@ -791,6 +792,33 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
 
 // ---- projection --------------------------------------------------------------
 // out (r x L) = W^T X  (X: a x L, W: a x r with leading dimension ldw)
+// 2-D tensor map of X (a x L, column-major) with 16 x 64 boxes and 128-byte
+// swizzle (ttg_kernels.cuh, "Tensor-map TMA tiles").  The driver entry point
+// is resolved once through the runtime (no -lcuda).  False when the operand
+// does not qualify (odd a, misaligned base, L beyond int32 coordinates).
+bool make_tmap(CUtensorMap* m, const double* X, int a, long long L) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static bool resolved = false;
+  if (!resolved) {
+    resolved = true;
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  }
+  if (!enc || (a & 1) || a <= 0 || L <= 0 || L >= (1LL << 31) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)a, (cuuint64_t)L};
+  cuuint64_t strides[1] = {(cuuint64_t)a * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)ttg::kTC};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
              double* tsq = nullptr) {
   const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
@@ -811,7 +839,7 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
   if (a & 1) {  // odd rows: no 16-byte bulk runs -> cp.async single-buffered kernel
     const size_t nfr0 = (size_t)(r8 / 8) * (a8 / 4) * 32;
-    size_t smem0 = sizeof(double) * ((size_t)args.ldt * ttg::kTC + (size_t)2 * r * ttg::kTC);
+    size_t smem0 = sizeof(double) * (size_t)args.ldt * ttg::kTC;
     if (smem0 > c->smem_optin - 1024) {
       gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
       return false;
@@ -820,6 +848,7 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
       args.frag_smem = 1;
       smem0 += sizeof(double) * nfr0;
     }
+    args.nst = 0;
     auto k0 = ttg::k_project<false, false>;
     const int occ0 = std::max(kernel_occupancy((const void*)k0, k0, ttg::kThreads, smem0), 1);
     const int gx0 = (int)std::min<long long>((long long)c->num_sms * occ0, std::max<long long>(1, args.n_tiles));
@@ -832,7 +861,42 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   }
   const bool db = a8 <= kFastMax;
   const size_t nfr = (size_t)(r8 / 8) * (a8 / 4) * 32;
-  size_t smem = sizeof(double) * ((size_t)(db ? 2 : 1) * args.ldt * ttg::kTC + (size_t)2 * r * ttg::kTC);
+  const size_t stage = sizeof(double) * (size_t)args.ldt * ttg::kTC;
+  CUtensorMap tm;
+  if (db && !std::getenv("TTG_NO_TMAP") && make_tmap(&tm, X, a, L)) {
+    // tensor-map TMA ring: 2 stages at 2 CTAs / SM (the per-tile DMMA work of
+    // one CTA hides behind the other's loads), deeper when only one CTA fits
+    const size_t tstage = sizeof(double) * 1024 * (size_t)((a + 15) / 16);
+    const size_t extra = 1024 + sizeof(double) * (r <= 32 ? (size_t)ttg::kConsumerWarps * 8 * 32 : 0);
+    const bool regw = a8 <= 64 && r8 <= 16;
+    const size_t fr = regw ? 0 : sizeof(double) * nfr;
+    const size_t cap = (size_t)c->smem_optin - 1024;
+    int nst = 2;
+    size_t smem = nst * tstage + extra;
+    if (fr && smem + fr <= std::min<size_t>(cap, 110 * 1024)) {
+      args.frag_smem = 1;
+      smem += fr;
+    }
+    if (2 * smem > 220 * 1024)  // one CTA per SM: deepen the ring instead
+      while (nst < ttg::kMaxStages && smem + tstage <= cap) {
+        ++nst;
+        smem += tstage;
+      }
+    if (smem <= cap) {
+      args.nst = nst;
+      auto kern = regw ? ttg::k_project_tma<true> : ttg::k_project_tma<false>;
+      const int occ = std::max(kernel_occupancy((const void*)kern, kern, ttg::kThreads, smem), 1);
+      const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+      char nm[64];
+      std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
+      prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
+      kern<<<gx, ttg::kThreads, smem, c->stream>>>(tm, args);
+      post_launch(c);
+      return tsq != nullptr;
+    }
+    args.frag_smem = 0;
+  }
+  size_t smem = (db ? 2 : 1) * stage;
   if (smem > c->smem_optin - 1024) {  // does not fit the tile pipeline: generic path
     gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
     return false;
@@ -1646,7 +1710,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
         (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
         (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
-        (const void*)ttg::k_syrk<8>, (const void*)ttg::k_project_ws<true>, (const void*)ttg::k_project_ws<false>,
+        (const void*)ttg::k_syrk<8>, (const void*)ttg::k_project_tma<true>, (const void*)ttg::k_project_tma<false>,
         (const void*)ttg::k_sum_vec};
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));
   }

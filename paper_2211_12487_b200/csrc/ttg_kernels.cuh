@@ -13,6 +13,7 @@
 //   A (8x4):  A[g][t]          B (4x8): B[t][g]          C (8x8): C[g][2t], C[g][2t+1]
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace ttg {
@@ -23,7 +24,7 @@ constexpr int kSyrkThreads = (kConsumerWarps + 1) * 32;  // + 1 TMA producer war
 constexpr int kThreads = 256;  // 8 warps; warp w owns tile columns [8w, 8w+8)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -37,9 +38,23 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+// wait until at most n (runtime, 0..4) cp.async groups of this thread are pending
+__device__ __forceinline__ void cp_async_wait_n(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::); break;
+    case 3: asm volatile("cp.async.wait_group 3;\n" ::); break;
+    default: asm volatile("cp.async.wait_group 4;\n" ::); break;
+  }
+}
 
 // Leading dimension (in doubles) for an smem column-major tile with `rows`
 // rows: >= rows and == 4 (mod 16), which makes both m8n8k4 fragment patterns
@@ -800,7 +815,7 @@ struct ProjArgs {
   double* tsumsq;     // per-tile sum of squares of the input tile (nullable)
   long long n_tiles;
   int frag_smem;      // stage W^T fragments in shared memory
-  int nst;            // ring stages (k_project_ws)
+  int nst;            // ring stages (k_project_ring)
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
@@ -832,8 +847,6 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
   double* T1 = DB ? smem + ldt * kTC : T0;
   double* Wfs = smem + (DB ? 2 : 1) * ldt * kTC;
   const double* Wf = p.frag_smem ? Wfs : p.WTf;
-  double* O0 = Wfs + (p.frag_smem ? nfr : 0);
-  double* O1 = O0 + p.r * kTC;
   const bool tma = (p.src.a & 1) == 0;
   for (int i = threadIdx.x; i < (DB ? 2 : 1) * ldt * kTC; i += kThreads) smem[i] = 0.0;
   if (p.frag_smem)
@@ -880,15 +893,16 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
       mbar_wait(&bars[cb], phase[cb]);
       phase[cb] ^= 1u;
     }
-    // the output staging buffer of two tiles ago must have been read by its bulk store
-    if (threadIdx.x == 0) bulk_wait_read1();
     __syncthreads();
     if (p.tsumsq) {
       const double ts = tile_sumsq(T, p.src.a, ldt, red8);
       if (threadIdx.x < kConsumerWarps) p.tsumsq[tile * kConsumerWarps + threadIdx.x] = threadIdx.x == 0 ? ts : 0.0;
     }
-    double* O = obuf ? O1 : O0;
     const int c0 = warp * 8;
+    const long long col0 = tile * kTC + c0 + 2 * t;  // this thread's output columns col0, col0+1
+    const bool ok0 = col0 < p.src.L, ok1 = col0 + 1 < p.src.L;
+    double* o0 = p.out + col0 * p.r;
+    double* o1 = o0 + p.r;
     if (REGW) {
       // W^T fragments live in registers (MR*KA <= 32): one smem load per DMMA pair
       double q[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
@@ -905,8 +919,8 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
       for (int u = 0; u < 2; ++u) {
         const int row = u * 8 + g;
         if (u < MR && row < p.r) {
-          O[row + p.r * (c0 + 2 * t)] = q[u][0][0] + q[u][1][0];
-          O[row + p.r * (c0 + 2 * t + 1)] = q[u][0][1] + q[u][1][1];
+          if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
+          if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
         }
       }
     } else
@@ -937,26 +951,12 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
       for (int u = 0; u < 4; ++u) {
         const int row = (mb0 + u) * 8 + g;
         if (u < nu && row < p.r) {
-          O[row + p.r * (c0 + 2 * t)] = q[u][0][0] + q[u][1][0];
-          O[row + p.r * (c0 + 2 * t + 1)] = q[u][0][1] + q[u][1][1];
+          if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
+          if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
         }
       }
     }
-    fence_proxy_async();  // generic writes of O -> visible to the bulk store
-    __syncthreads();
-    const long long q0c = tile * kTC;
-    long long ncols = p.src.L - q0c;
-    if (ncols > kTC) ncols = kTC;
-    const long long nout = ncols * p.r;
-    double* dst = p.out + q0c * p.r;
-    if (((nout * 8) & 15) == 0 && (((uintptr_t)dst) & 15) == 0) {
-      if (threadIdx.x == 0) {
-        bulk_s2g(dst, O, (unsigned)(nout * 8));
-        bulk_commit();
-      }
-    } else {
-      for (long long e = threadIdx.x; e < nout; e += kThreads) dst[e] = O[e];
-    }
+    __syncthreads();  // the stage is reused by a later refill
     buf ^= 1;
     obuf ^= 1;
   }
@@ -964,64 +964,54 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
   if (!tma) cp_async_wait_0();
 }
 
-// Projection out (r x L) = W^T X, warp-specialised: warp 8 is the TMA
-// producer (one bulk copy per column into an NST-deep ring, full/empty
-// mbarriers), warps 0..7 consume: each owns 8 tile columns, computes its
-// m-blocks (W^T fragments in registers when a8 <= 64 and r8 <= 16, else from
-// shared memory) and stores its outputs straight from the accumulators.  No
-// block-wide barrier in the main loop.  Optional per-(tile, warp) sums of
-// squares of the input (fused norms; reduced in fixed order afterwards).
+// ---------------------------------------------------------------------------
+// Tensor-map TMA tiles.  X (a x L, column-major) is described by a 2-D tensor
+// map {a, L} with 16 x 64 boxes and 128-byte swizzle: a tile of kTC columns is
+// ceil(a/16) boxes of 8 KB, each 1024-byte aligned in smem, element (k, c) of
+// box b at double offset  b*1024 + c*16 + (((k%16)/2) ^ (c%8))*2 + k%2.
+// Rows >= a and columns >= L are zero-filled by the TMA unit.  One thread
+// issues a whole tile (ceil(a/16) instructions); the swizzle makes the m8n8k4
+// B-fragment pattern (4 consecutive rows x 8 columns) conflict-free without
+// padding, so the smem image is dense and every byte moved is payload.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+
+// Projection out (r x L) = W^T X with tensor-map TMA tiles in an nst-deep
+// ring (full mbarriers; thread 0 refills the stage freed in the previous
+// iteration right after the per-tile block barrier).  Each warp owns 8 tile
+// columns; W^T fragments in registers (REGW: a8 <= 64, r8 <= 16) or shared
+// memory.  Outputs: the warp's 8 x r block is contiguous in `out`, staged per
+// warp (r <= 32) and written with coalesced stores.  Optional per-(tile, warp)
+// input sums of squares from the B fragments already in registers.
 template <bool REGW>
-__global__ void __launch_bounds__(kSyrkThreads) k_project_ws(ProjArgs p) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+__global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxStages + 2];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int ldt = p.ldt, nst = p.nst;
+  const int nst = p.nst;
+  const int nbox = (p.src.a + 15) >> 4;
   const int KA = p.a8 >> 2, MR = p.r8 >> 3;
   const int nfr = MR * KA * 32;
-  const int stage = ldt * kTC;
-  double* Wfs = smem + (size_t)nst * stage;
-  for (int i = threadIdx.x; i < nst * stage; i += blockDim.x) smem[i] = 0.0;
+  const int stage = nbox * 1024;  // doubles
+  double* Wfs = smem + nst * stage;
+  double* stg_all = Wfs + (p.frag_smem ? nfr : 0);
+  const bool staged = p.r <= 32;
+  double* stg = stg_all + warp * 8 * 32;
+  const double* Wf = p.frag_smem ? Wfs : p.WTf;
   if (!REGW && p.frag_smem)
-    for (int i = threadIdx.x; i < nfr; i += blockDim.x) Wfs[i] = p.WTf[i];
-  if (threadIdx.x == 0)
-    for (int s = 0; s < nst; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-  __syncthreads();
-  const int a = p.src.a;
-
-  if (warp == kConsumerWarps) {  // ---- producer ----
-    int it = 0;
-    for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
-      const int st = it % nst;
-      if (it >= nst) mbar_wait(&empty[st], (unsigned)(((it / nst) - 1) & 1));
-      const long long q0 = tile * kTC;
-      double* T = smem + (size_t)st * stage;
-      bool v[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) v[h] = q0 + lane + 32 * h < p.src.L;
-      const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, v[0])) + __popc(__ballot_sync(0xffffffffu, v[1]));
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (!v[h])
-          for (int r = 0; r < a; ++r) T[r + (size_t)ldt * (lane + 32 * h)] = 0.0;
-      __syncwarp();
-      fence_proxy_async();
-      if (lane == 0) mbar_expect_tx(&full[st], nvalid * (unsigned)a * 8u);
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = lane + 32 * h;
-        if (v[h]) bulk_g2s(T + (size_t)ldt * c, p.src.X + (size_t)a * (q0 + c), (unsigned)a * 8u, &full[st]);
-      }
-    }
-    return;
-  }
-
-  // ---- consumers ----
+    for (int i = threadIdx.x; i < nfr; i += kThreads) Wfs[i] = p.WTf[i];
   double wreg[REGW ? 32 : 1];
   if (REGW) {
 #pragma unroll
@@ -1030,46 +1020,70 @@ __global__ void __launch_bounds__(kSyrkThreads) k_project_ws(ProjArgs p) {
       for (int kb = 0; kb < 16; ++kb)
         wreg[u * 16 + kb] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
   }
-  const double* Wf = p.frag_smem ? Wfs : p.WTf;
+  const long long grid = gridDim.x;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm);
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < nst - 1; ++s) {
+      const long long tl = blockIdx.x + s * grid;
+      if (tl < p.n_tiles) {
+        mbar_expect_tx(&full[s], (unsigned)nbox * 8192u);
+        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + s * stage + b * 1024, &tm, 16 * b, (int)(tl * kTC), &full[s]);
+      }
+    }
+  }
+  __syncthreads();
   const int c0 = warp * 8;
+  // lane constants of the swizzled B-fragment address (k = 4kb + t, column c0 + g)
+  const int hsw = (t >> 1) ^ g;
+  const int lbase = (c0 + g) * 16 + (t & 1);
+  int osw[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) osw[m] = lbase + (((m << 1) ^ hsw) << 1);
   int it = 0;
-  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid, ++it) {
     const int st = it % nst;
     mbar_wait(&full[st], (unsigned)((it / nst) & 1));
-    const double* T = smem + (size_t)st * stage;
-    const long long q0c = tile * kTC;
-    if (p.tsumsq) {  // this warp's 8 columns
-      double sq = 0.0;
-      for (int e = lane; e < a * 8; e += 32) {
-        const int c = e / a, r = e - c * a;
-        const double vv = T[r + ldt * (c0 + c)];
-        sq = fma(vv, vv, sq);
+    __syncthreads();  // every warp is done with the stage consumed in iteration it-1
+    if (threadIdx.x == 0) {
+      const long long tl = tile + (nst - 1) * grid;
+      if (tl < p.n_tiles) {
+        const int sn = (it + nst - 1) % nst;
+        mbar_expect_tx(&full[sn], (unsigned)nbox * 8192u);
+        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + sn * stage + b * 1024, &tm, 16 * b, (int)(tl * kTC), &full[sn]);
       }
-      sq = warp_sum(sq);
-      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = sq;
     }
-    // my output columns (c0 + 2t, +1): valid?
-    const long long col0 = q0c + c0 + 2 * t;
-    const bool ok0 = col0 < p.src.L, ok1 = col0 + 1 < p.src.L;
+    const double* T = smem + st * stage;
+    const long long colw = tile * kTC + c0;
+    const int nval = (int)max(0LL, min(8LL, p.src.L - colw));
+    const long long col0 = colw + 2 * t;
+    const bool ok0 = 2 * t < nval, ok1 = 2 * t + 1 < nval;
     double* o0 = p.out + col0 * p.r;
     double* o1 = o0 + p.r;
+    double ss = 0.0;
     if (REGW) {
       double q[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+      double bv[16];
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb) bv[kb] = kb < KA ? T[(kb >> 2) * 1024 + osw[kb & 3]] : 0.0;
 #pragma unroll
       for (int kb = 0; kb < 16; ++kb) {
-        if (kb < KA) {
-          const double bv = T[(kb * 4 + t) + ldt * (c0 + g)];
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            if (u < MR) dmma(q[u][kb & 1][0], q[u][kb & 1][1], wreg[u * 16 + kb], bv);
-        }
+        ss = fma(bv[kb], bv[kb], ss);
+        dmma(q[0][kb & 1][0], q[0][kb & 1][1], wreg[kb], bv[kb]);
+        if (MR > 1) dmma(q[1][kb & 1][0], q[1][kb & 1][1], wreg[16 + kb], bv[kb]);
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int row = u * 8 + g;
         if (u < MR && row < p.r) {
-          if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
-          if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
+          if (staged) {
+            stg[row + p.r * (2 * t)] = q[u][0][0] + q[u][1][0];
+            stg[row + p.r * (2 * t + 1)] = q[u][0][1] + q[u][1][1];
+          } else {
+            if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
+            if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
+          }
         }
       }
     } else {
@@ -1080,8 +1094,9 @@ __global__ void __launch_bounds__(kSyrkThreads) k_project_ws(ProjArgs p) {
         const int nu = min(4, MR - mb0);
         int kb = 0;
         for (; kb + 1 < KA; kb += 2) {
-          const double b0 = T[(kb * 4 + t) + ldt * (c0 + g)];
-          const double b1 = T[(kb * 4 + 4 + t) + ldt * (c0 + g)];
+          const double b0 = T[(kb >> 2) * 1024 + osw[kb & 3]];
+          const double b1 = T[((kb + 1) >> 2) * 1024 + osw[(kb + 1) & 3]];
+          if (mb0 == 0) ss = fma(b1, b1, fma(b0, b0, ss));
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (u < nu) {
@@ -1091,7 +1106,8 @@ __global__ void __launch_bounds__(kSyrkThreads) k_project_ws(ProjArgs p) {
             }
         }
         if (kb < KA) {
-          const double b0 = T[(kb * 4 + t) + ldt * (c0 + g)];
+          const double b0 = T[(kb >> 2) * 1024 + osw[kb & 3]];
+          if (mb0 == 0) ss = fma(b0, b0, ss);
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (u < nu) dmma(q[u][0][0], q[u][0][1], Wf[((mb0 + u) * KA + kb) * 32 + lane], b0);
@@ -1100,14 +1116,29 @@ __global__ void __launch_bounds__(kSyrkThreads) k_project_ws(ProjArgs p) {
         for (int u = 0; u < 4; ++u) {
           const int row = (mb0 + u) * 8 + g;
           if (u < nu && row < p.r) {
-            if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
-            if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
+            if (staged) {
+              stg[row + p.r * (2 * t)] = q[u][0][0] + q[u][1][0];
+              stg[row + p.r * (2 * t + 1)] = q[u][0][1] + q[u][1][1];
+            } else {
+              if (ok0) o0[row] = q[u][0][0] + q[u][1][0];
+              if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
+            }
           }
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+    if (staged) {
+      __syncwarp();
+      double* dst = p.out + colw * p.r;
+      const int n = nval * p.r;
+      for (int e = lane; e < n; e += 32) dst[e] = stg[e];
+      __syncwarp();
+    }
+    if (p.tsumsq) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = ss;
+    }
   }
 }
 

@@ -1,0 +1,120 @@
+// Isolated timing of the projection kernels (out = W^T X, a = 64) on a 4.29 GB
+// operand: ring vs. double-buffered TMA, r = 1 / 16, with/without norms.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -I paper_2211_12487_b200/csrc tools/probe/proj_probe.cu
+#include <cstdio>
+#include "ttg_eig.cuh"
+#include "ttg_kernels.cuh"
+
+__global__ void fill(double* x, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = (double)((i * 2654435761ull) % 1000) * 1e-3 - 0.5;
+}
+
+#include <cudaTypedefs.h>
+CUtensorMap make_map(const double* X, int a, long long L) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)a, (cuuint64_t)L};
+  cuuint64_t strides[1] = {(cuuint64_t)a * 8};
+  cuuint32_t box[2] = {16, 64};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)X, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) printf("encode failed %d\n", (int)r);
+  return m;
+}
+template <class K>
+void timetma(const char* name, K kern, const CUtensorMap& tm, ttg::ProjArgs p, size_t smem, double bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem);
+  const int gx = 148 * (occ > 0 ? occ : 1);
+  kern<<<gx, ttg::kThreads, smem>>>(tm, p);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) kern<<<gx, ttg::kThreads, smem>>>(tm, p);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= 5;
+  printf("%-44s smem=%6zu occ=%d nst=%d  %.3f ms  %.0f GB/s  (%s)\n", name, smem, occ, p.nst, ms, bytes / (ms * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
+// correctness: out (r x L) vs a plain reference on the first columns
+__global__ void ref_proj(const double* X, int a, const double* W, int r, double* out, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n * r) return;
+  long long c = i / r;
+  int j = (int)(i % r);
+  double s = 0;
+  for (int k = 0; k < a; ++k) s += W[k + (long long)a * j] * X[k + (long long)a * c];
+  out[i] = s;
+}
+template <class K>
+void timeit(const char* name, K kern, ttg::ProjArgs p, size_t smem, double bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem);
+  const int gx = 148 * (occ > 0 ? occ : 1);
+  kern<<<gx, ttg::kThreads, smem>>>(p);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) kern<<<gx, ttg::kThreads, smem>>>(p);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= 5;
+  printf("%-44s smem=%6zu occ=%d nst=%d  %.3f ms  %.0f GB/s  (%s)\n", name, smem, occ, p.nst, ms, bytes / (ms * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  const int a = 64;
+  const long long L = 1ll << 23;
+  double* X;
+  cudaMalloc(&X, sizeof(double) * a * L);
+  fill<<<4096, 256>>>(X, a * L);
+  double *W, *out, *tsq;
+  cudaMalloc(&W, sizeof(double) * 128 * 64);
+  fill<<<16, 256>>>(W, 128 * 64);
+  cudaMalloc(&out, sizeof(double) * 32 * L);
+  cudaMalloc(&tsq, sizeof(double) * 8 * (L / 64));
+  for (int r : {1, 16}) {
+    for (int norms = 0; norms < 2; ++norms) {
+      ttg::ProjArgs p{};
+      p.src = ttg::TileSrc{X, a, L, nullptr, 1};
+      p.a8 = 64;
+      p.ldt = ttg::smem_ld(64);
+      p.WTf = W;
+      p.r = r;
+      p.r8 = ttg::round_up(r, 8);
+      p.out = out;
+      p.tsumsq = norms ? tsq : nullptr;
+      p.n_tiles = L / 64;
+      const double bytes = 8.0 * (a + r) * L;
+      const size_t stage = sizeof(double) * p.ldt * 64;
+      const size_t stg = sizeof(double) * 8 * 8 * 32;
+      char nm[128];
+      const CUtensorMap tm = make_map(X, a, L);
+      for (int nst : {2, 3, 4, 6}) {
+        p.nst = nst;
+        std::snprintf(nm, sizeof nm, "tmap r=%d norms=%d", r, norms);
+        timetma(nm, ttg::k_project_tma<true>, tm, p, 1024 + nst * 8192 * 4 + stg, bytes);
+      }
+      p.nst = 0;
+      std::snprintf(nm, sizeof nm, "tma-db r=%d norms=%d", r, norms);
+      timeit(nm, ttg::k_project<true, true>, p, 2 * stage, bytes);
+    }
+  }
+  return 0;
+}
