@@ -603,10 +603,11 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
   // trace(C) for the guard, then symmetrise G
   c->scal.ensure(sizeof(double) * 16);
   prof_begin(c, "k_symmetrize_trace", 16.0 * rows * rows, 0.0);
-  ttg::k_symmetrize_trace<<<1, 256, 0, c->stream>>>(c->Craw.as<double>(), (int)rows, c->scal.as<double>() + 4);
+  ttg::k_symmetrize_trace<<<grid_for(rows * rows, 256, 64), 256, 0, c->stream>>>(c->Craw.as<double>(), (int)rows,
+                                                                                 c->scal.as<double>() + 4);
   post_launch(c);
   prof_begin(c, "k_symmetrize_trace", 16.0 * a * a, 0.0);
-  ttg::k_symmetrize_trace<<<1, 256, 0, c->stream>>>(G, (int)a, nullptr);
+  ttg::k_symmetrize_trace<<<grid_for(a * a, 256, 64), 256, 0, c->stream>>>(G, (int)a, nullptr);
   post_launch(c);
   return did;
 }
@@ -633,28 +634,37 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     // fast path: block subspace iteration for the few kept directions
     bool done = false;
     if (!std::getenv("TTG_FULL_EIG")) {
-      const size_t sub_vec = sizeof(double) * (size_t)2 * a * ttg::kSubK;
-      size_t smem_s = sizeof(double) * (size_t)a * a + sub_vec;
-      ttg::SyevArgs sa = args;
-      if (smem_s <= c->smem_optin) {
-        sa.in_smem = 1;
-      } else {
-        sa.in_smem = 0;
-        smem_s = sub_vec;
+      // block of 4 first (the common case keeps 1-2 directions), then 8
+      for (int K : {4, 8}) {
+        if (done) break;
+        const size_t sub_vec = sizeof(double) * (size_t)2 * a * K;
+        size_t smem_s = sizeof(double) * (size_t)a * a + sub_vec;
+        ttg::SyevArgs sa = args;
+        if (smem_s <= c->smem_optin) {
+          sa.in_smem = 1;
+        } else {
+          sa.in_smem = 0;
+          smem_s = sub_vec;
+        }
+        auto kern = K == 4 ? ttg::k_syev_top<4> : ttg::k_syev_top<8>;
+        kernel_occupancy((const void*)kern, kern, ttg::kSubThreads, smem_s);
+        char nm[64];
+        std::snprintf(nm, sizeof nm, "k_syev_top[a=%d]", a);
+        prof_begin(c, nm, 16.0 * a * a, 2.0 * a * a * K);
+        kern<<<1, ttg::kSubThreads, smem_s, c->stream>>>(sa);
+        post_launch(c);
+        c->d2h += sizeof(EigResult);
+        CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        done = c->h_eig->converged != 0;
+        if (std::getenv("TTG_DEBUG"))
+          std::fprintf(stderr, "[ttg] eig_top K=%d a=%d conv=%d iters=%d rank=%d jac=%lld cycles copy=%lld init=%lld qr=%lld iter=%lld gx=%lld h=%lld eig=%lld res=%lld\n",
+                       K, a, c->h_eig->converged, c->h_eig->sweeps, c->h_eig->rank, c->h_eig->t_phase[1] >> 40,
+                       c->h_eig->t_phase[0] & 0xfffff, (c->h_eig->t_phase[0] >> 20) & 0xfffff,
+                       c->h_eig->t_phase[0] >> 40, c->h_eig->t_phase[1] & 0xffffffffffll,
+                       c->h_eig->t_phase[2] & 0xffffffffll, c->h_eig->t_phase[2] >> 32,
+                       c->h_eig->t_phase[3] & 0xffffffffll, c->h_eig->t_phase[3] >> 32);
       }
-      kernel_occupancy((const void*)ttg::k_syev_top, ttg::k_syev_top, ttg::kSubThreads, smem_s);
-      char nm[64];
-      std::snprintf(nm, sizeof nm, "k_syev_top[a=%d]", a);
-      prof_begin(c, nm, 16.0 * a * a, 2.0 * a * a * ttg::kSubK);
-      ttg::k_syev_top<<<1, ttg::kSubThreads, smem_s, c->stream>>>(sa);
-      post_launch(c);
-      c->d2h += sizeof(EigResult);
-      CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      done = c->h_eig->converged != 0;
-      if (std::getenv("TTG_DEBUG"))
-        std::fprintf(stderr, "[ttg] eig_top a=%d conv=%d iters=%d rank=%d\n", a, c->h_eig->converged,
-                     c->h_eig->sweeps, c->h_eig->rank);
     }
     if (!done) {
       size_t vec = sizeof(double) * (size_t)7 * a;
@@ -796,7 +806,7 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
 // swizzle (ttg_kernels.cuh, "Tensor-map TMA tiles").  The driver entry point
 // is resolved once through the runtime (no -lcuda).  False when the operand
 // does not qualify (odd a, misaligned base, L beyond int32 coordinates).
-bool make_tmap(CUtensorMap* m, const double* X, int a, long long L) {
+bool make_tmap(CUtensorMap* m, const double* X, int a, long long L, int box_cols = ttg::kTC) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   static bool resolved = false;
   if (!resolved) {
@@ -812,7 +822,7 @@ bool make_tmap(CUtensorMap* m, const double* X, int a, long long L) {
   if (!enc || (a & 1) || a <= 0 || L <= 0 || L >= (1LL << 31) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
   cuuint64_t dims[2] = {(cuuint64_t)a, (cuuint64_t)L};
   cuuint64_t strides[1] = {(cuuint64_t)a * sizeof(double)};
-  cuuint32_t box[2] = {16, (cuuint32_t)ttg::kTC};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_cols};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -863,10 +873,12 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   const size_t nfr = (size_t)(r8 / 8) * (a8 / 4) * 32;
   const size_t stage = sizeof(double) * (size_t)args.ldt * ttg::kTC;
   CUtensorMap tm;
-  if (db && !std::getenv("TTG_NO_TMAP") && make_tmap(&tm, X, a, L)) {
+  const bool narrow = a8 > 64 && r <= 32;  // 32-column tiles keep 2 CTAs x 2 stages per SM
+  const int tc = narrow ? 32 : ttg::kTC;
+  if (a8 <= 256 && !std::getenv("TTG_NO_TMAP") && make_tmap(&tm, X, a, L, tc)) {
     // tensor-map TMA ring: 2 stages at 2 CTAs / SM (the per-tile DMMA work of
     // one CTA hides behind the other's loads), deeper when only one CTA fits
-    const size_t tstage = sizeof(double) * 1024 * (size_t)((a + 15) / 16);
+    const size_t tstage = sizeof(double) * 16 * tc * (size_t)((a + 15) / 16);
     const size_t extra = 1024 + sizeof(double) * (r <= 32 ? (size_t)ttg::kConsumerWarps * 8 * 32 : 0);
     const bool regw = a8 <= 64 && r8 <= 16;
     const size_t fr = regw ? 0 : sizeof(double) * nfr;
@@ -884,7 +896,9 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
       }
     if (smem <= cap) {
       args.nst = nst;
-      auto kern = regw ? ttg::k_project_tma<true> : ttg::k_project_tma<false>;
+      args.n_tiles = (L + tc - 1) / tc;
+      auto kern = narrow ? (regw ? ttg::k_project_tma<true, 32> : ttg::k_project_tma<false, 32>)
+                         : (regw ? ttg::k_project_tma<true, 64> : ttg::k_project_tma<false, 64>);
       const int occ = std::max(kernel_occupancy((const void*)kern, kern, ttg::kThreads, smem), 1);
       const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
       char nm[64];
@@ -895,6 +909,7 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
       return tsq != nullptr;
     }
     args.frag_smem = 0;
+    args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
   }
   size_t smem = (db ? 2 : 1) * stage;
   if (smem > c->smem_optin - 1024) {  // does not fit the tile pipeline: generic path
@@ -1701,7 +1716,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
         (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
         (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
-        (const void*)ttg::k_gram_reduce, (const void*)ttg::k_syev, (const void*)ttg::k_syev_top,
+        (const void*)ttg::k_gram_reduce, (const void*)ttg::k_syev, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,
@@ -1710,7 +1725,8 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
         (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
         (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
-        (const void*)ttg::k_syrk<8>, (const void*)ttg::k_project_tma<true>, (const void*)ttg::k_project_tma<false>,
+        (const void*)ttg::k_syrk<8>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
+        (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec};
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));
   }

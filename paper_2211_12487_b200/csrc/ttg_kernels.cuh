@@ -124,6 +124,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#ifdef TTG_MBAR_TEST
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -133,6 +144,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
@@ -986,15 +998,23 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
-// Projection out (r x L) = W^T X with tensor-map TMA tiles in an nst-deep
-// ring (full mbarriers; thread 0 refills the stage freed in the previous
-// iteration right after the per-tile block barrier).  Each warp owns 8 tile
-// columns; W^T fragments in registers (REGW: a8 <= 64, r8 <= 16) or shared
-// memory.  Outputs: the warp's 8 x r block is contiguous in `out`, staged per
-// warp (r <= 32) and written with coalesced stores.  Optional per-(tile, warp)
-// input sums of squares from the B fragments already in registers.
-template <bool REGW>
+// Projection out (r x L) = W^T X with tensor-map TMA tiles of TC columns
+// (TC = 64, or 32 for tall operands so that two CTAs with two stages each fit
+// one SM) in an nst-deep ring (full mbarriers; thread 0 refills the stage
+// freed in the previous iteration right after the per-tile block barrier).
+// Warp w owns the 8 columns 8*(w % (TC/8)) of the tile; with TC = 32 the
+// warps w and w+4 split the boxes (k range) by parity and the upper half adds
+// its partial sums through shared memory.  W^T fragments in registers (REGW:
+// a8 <= 64, r8 <= 16) or shared memory.  Outputs: a warp's 8 x r block is
+// contiguous in `out`, staged per warp (r <= 32) and written with coalesced
+// stores.  Optional per-(tile, warp) input sums of squares.
+template <bool REGW, int TC>
 __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  static_assert(TC == 64 || TC == 32, "tile width");
+  __shared__ double red_ss[4];
+  constexpr int CW = TC / 8;   // column warps
+  constexpr int KS = 8 / CW;   // k-split ways (1 or 2)
+  constexpr int BOX = 16 * TC; // doubles per box
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxStages + 2];
   double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1004,12 +1024,13 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
   const int nbox = (p.src.a + 15) >> 4;
   const int KA = p.a8 >> 2, MR = p.r8 >> 3;
   const int nfr = MR * KA * 32;
-  const int stage = nbox * 1024;  // doubles
+  const int stage = nbox * BOX;  // doubles
   double* Wfs = smem + nst * stage;
   double* stg_all = Wfs + (p.frag_smem ? nfr : 0);
-  const bool staged = p.r <= 32;
+  const bool staged = p.r <= 32;  // (always true when KS > 1)
   double* stg = stg_all + warp * 8 * 32;
   const double* Wf = p.frag_smem ? Wfs : p.WTf;
+  const int cw = warp % CW, kh = warp / CW;
   if (!REGW && p.frag_smem)
     for (int i = threadIdx.x; i < nfr; i += kThreads) Wfs[i] = p.WTf[i];
   double wreg[REGW ? 32 : 1];
@@ -1028,13 +1049,13 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
     for (int s = 0; s < nst - 1; ++s) {
       const long long tl = blockIdx.x + s * grid;
       if (tl < p.n_tiles) {
-        mbar_expect_tx(&full[s], (unsigned)nbox * 8192u);
-        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + s * stage + b * 1024, &tm, 16 * b, (int)(tl * kTC), &full[s]);
+        mbar_expect_tx(&full[s], (unsigned)nbox * BOX * 8u);
+        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + s * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[s]);
       }
     }
   }
   __syncthreads();
-  const int c0 = warp * 8;
+  const int c0 = cw * 8;
   // lane constants of the swizzled B-fragment address (k = 4kb + t, column c0 + g)
   const int hsw = (t >> 1) ^ g;
   const int lbase = (c0 + g) * 16 + (t & 1);
@@ -1050,12 +1071,12 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
       const long long tl = tile + (nst - 1) * grid;
       if (tl < p.n_tiles) {
         const int sn = (it + nst - 1) % nst;
-        mbar_expect_tx(&full[sn], (unsigned)nbox * 8192u);
-        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + sn * stage + b * 1024, &tm, 16 * b, (int)(tl * kTC), &full[sn]);
+        mbar_expect_tx(&full[sn], (unsigned)nbox * BOX * 8u);
+        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + sn * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[sn]);
       }
     }
     const double* T = smem + st * stage;
-    const long long colw = tile * kTC + c0;
+    const long long colw = tile * TC + c0;
     const int nval = (int)max(0LL, min(8LL, p.src.L - colw));
     const long long col0 = colw + 2 * t;
     const bool ok0 = 2 * t < nval, ok1 = 2 * t + 1 < nval;
@@ -1066,7 +1087,8 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
       double q[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
       double bv[16];
 #pragma unroll
-      for (int kb = 0; kb < 16; ++kb) bv[kb] = kb < KA ? T[(kb >> 2) * 1024 + osw[kb & 3]] : 0.0;
+      for (int kb = 0; kb < 16; ++kb)
+        bv[kb] = (kb < KA && ((kb >> 2) % KS) == kh) ? T[(kb >> 2) * BOX + osw[kb & 3]] : 0.0;
 #pragma unroll
       for (int kb = 0; kb < 16; ++kb) {
         ss = fma(bv[kb], bv[kb], ss);
@@ -1092,25 +1114,25 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
 #pragma unroll
         for (int u = 0; u < 4; ++u) q[u][0][0] = q[u][0][1] = q[u][1][0] = q[u][1][1] = 0.0;
         const int nu = min(4, MR - mb0);
-        int kb = 0;
-        for (; kb + 1 < KA; kb += 2) {
-          const double b0 = T[(kb >> 2) * 1024 + osw[kb & 3]];
-          const double b1 = T[((kb + 1) >> 2) * 1024 + osw[(kb + 1) & 3]];
-          if (mb0 == 0) ss = fma(b1, b1, fma(b0, b0, ss));
+        for (int b = kh; b < nbox; b += KS) {
+          // issue every load of the box first (clamped, always in range), then the DMMAs
+          double bv[4], wv[4][4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (u < nu) {
-              const double* wf = Wf + ((mb0 + u) * KA + kb) * 32 + lane;
-              dmma(q[u][0][0], q[u][0][1], wf[0], b0);
-              dmma(q[u][1][0], q[u][1][1], wf[32], b1);
+          for (int j = 0; j < 4; ++j) {
+            const int kbc = min(4 * b + j, KA - 1);
+            bv[j] = T[b * BOX + osw[j]];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) wv[u][j] = Wf[((mb0 + min(u, nu - 1)) * KA + kbc) * 32 + lane];
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (4 * b + j < KA) {
+              if (mb0 == 0) ss = fma(bv[j], bv[j], ss);
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < nu) dmma(q[u][j & 1][0], q[u][j & 1][1], wv[u][j], bv[j]);
             }
-        }
-        if (kb < KA) {
-          const double b0 = T[(kb >> 2) * 1024 + osw[kb & 3]];
-          if (mb0 == 0) ss = fma(b0, b0, ss);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (u < nu) dmma(q[u][0][0], q[u][0][1], Wf[((mb0 + u) * KA + kb) * 32 + lane], b0);
+          }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1124,6 +1146,171 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
               if (ok1) o1[row] = q[u][0][1] + q[u][1][1];
             }
           }
+        }
+      }
+    }
+    if (p.tsumsq) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (KS > 1 && kh == 1 && lane == 0) red_ss[cw] = ss;
+    }
+    if (KS > 1) {  // upper warps hand their partial 8 x r blocks (and sums) to warp w - 4
+      asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
+      if (kh == 0) {
+        const double* oth = stg_all + (warp + CW) * 8 * 32;
+        for (int e = lane; e < 8 * p.r; e += 32) stg[e] += oth[e];
+      }
+    }
+    if (staged && kh == 0) {
+      __syncwarp();
+      double* dst = p.out + colw * p.r;
+      const int n = nval * p.r;
+      for (int e = lane; e < n; e += 32) dst[e] = stg[e];
+      __syncwarp();
+    }
+    // per-(64-column tile, 8-column group) sums: the layout of the TC = 64 kernels
+    if (p.tsumsq && kh == 0 && lane == 0)
+      p.tsumsq[((tile * TC) >> 6) * kConsumerWarps + (((tile * TC) & 63) >> 3) + cw] = KS > 1 ? ss + red_ss[cw] : ss;
+  }
+}
+
+// Projection out (r x L) = W^T X over a ring of single TMA boxes (16 rows x
+// 64 columns = 8 KB, 128-byte swizzle): warp 8 lane 0 is the producer (full /
+// empty mbarriers per stage), warps 0..7 consume.  A column tile of any height
+// streams through the ring box by box while the warp's accumulators (all MR
+// m-blocks of its 8 columns) stay in registers, so the pipeline depth does not
+// shrink with a.  W^T fragments in registers (REGW: a8 <= 64, MR <= 2),
+// shared memory (frag_smem) or global (L1).  Outputs staged per warp (r <= 32)
+// and written coalesced; optional per-(tile, warp) input sums of squares.
+constexpr int kBoxStages = 16;
+template <int MRMAX, bool REGW>
+__global__ void __launch_bounds__(kSyrkThreads) k_project_box(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kBoxStages], empty[kBoxStages];
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nst = p.nst;
+  const int nbox = (p.src.a + 15) >> 4;
+  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
+  const int nfr = MR * KA * 32;
+  double* Wfs = ring + nst * 1024;
+  double* stg_all = Wfs + (p.frag_smem ? nfr : 0);
+  const bool staged = p.r <= 32;
+  if (!REGW && p.frag_smem)
+    for (int i = threadIdx.x; i < nfr; i += blockDim.x) Wfs[i] = p.WTf[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long grid = gridDim.x;
+  if (warp == kConsumerWarps) {  // ---- producer ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      int it = 0;
+      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid)
+        for (int b = 0; b < nbox; ++b, ++it) {
+          const int s = it % nst;
+          if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
+          mbar_expect_tx(&full[s], 8192u);
+          tma_load_2d(ring + s * 1024, &tm, 16 * b, (int)(tile * kTC), &full[s]);
+        }
+    }
+    return;
+  }
+  // ---- consumers ----
+  constexpr int NS = MRMAX <= 4 ? 2 : 1;  // independent accumulator sets (k split)
+  double wreg[REGW ? 32 : 1];
+  if (REGW) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb)
+        wreg[u * 16 + kb] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
+  }
+  const double* Wf = p.frag_smem ? Wfs : p.WTf;
+  double* stg = stg_all + warp * 8 * 32;
+  const int c0 = warp * 8;
+  const int hsw = (t >> 1) ^ g;
+  const int lbase = (c0 + g) * 16 + (t & 1);
+  int osw[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) osw[m] = lbase + (((m << 1) ^ hsw) << 1);
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+    double q[MRMAX][NS][2];
+#pragma unroll
+    for (int u = 0; u < MRMAX; ++u)
+#pragma unroll
+      for (int x = 0; x < NS; ++x) q[u][x][0] = q[u][x][1] = 0.0;
+    double ss = 0.0;
+    if (REGW) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (b < nbox) {
+          const int s = it % nst;
+          mbar_wait(&full[s], (unsigned)((it / nst) & 1));
+          const double* T = ring + s * 1024;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int kb = 4 * b + j;
+            if (kb < KA) {
+              const double bv = T[osw[j]];
+              ss = fma(bv, bv, ss);
+              dmma(q[0][j & (NS - 1)][0], q[0][j & (NS - 1)][1], wreg[kb], bv);
+              if (MRMAX > 1 && MR > 1) dmma(q[1][j & (NS - 1)][0], q[1][j & (NS - 1)][1], wreg[16 + kb], bv);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[s])) : "memory");
+          ++it;
+        }
+      }
+    } else {
+      for (int b = 0; b < nbox; ++b, ++it) {
+        const int s = it % nst;
+        mbar_wait(&full[s], (unsigned)((it / nst) & 1));
+        const double* T = ring + s * 1024;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int kb = 4 * b + j;
+          if (kb < KA) {
+            const double bv = T[osw[j]];
+            ss = fma(bv, bv, ss);
+#pragma unroll
+            for (int u = 0; u < MRMAX; ++u)
+              if (u < MR) dmma(q[u][j & (NS - 1)][0], q[u][j & (NS - 1)][1], Wf[(u * KA + kb) * 32 + lane], bv);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[s])) : "memory");
+      }
+    }
+    const long long colw = tile * kTC + c0;
+    const int nval = (int)max(0LL, min(8LL, p.src.L - colw));
+    const long long col0 = colw + 2 * t;
+    const bool ok0 = 2 * t < nval, ok1 = 2 * t + 1 < nval;
+    double* o0 = p.out + col0 * p.r;
+    double* o1 = o0 + p.r;
+#pragma unroll
+    for (int u = 0; u < MRMAX; ++u) {
+      const int row = u * 8 + g;
+      if (u < MR && row < p.r) {
+        double v0 = q[u][0][0], v1 = q[u][0][1];
+        if (NS > 1) {
+          v0 += q[u][NS - 1][0];
+          v1 += q[u][NS - 1][1];
+        }
+        if (staged) {
+          stg[row + p.r * (2 * t)] = v0;
+          stg[row + p.r * (2 * t + 1)] = v1;
+        } else {
+          if (ok0) o0[row] = v0;
+          if (ok1) o1[row] = v1;
         }
       }
     }

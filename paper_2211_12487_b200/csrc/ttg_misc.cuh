@@ -196,21 +196,25 @@ __global__ void k_merge_rows(const double* __restrict__ old, int ro, const doubl
   }
 }
 
-// G <- (G + G^T) / 2 and trace -> *tr (fixed order, one block)
+// G <- (G + G^T) / 2 over a grid (one thread per strictly-lower element);
+// block 0 also writes trace(G) -> *tr (the diagonal is not modified; fixed
+// warp-tree order, deterministic).
 __global__ void k_symmetrize_trace(double* __restrict__ G, int a, double* __restrict__ tr) {
-  for (long long e = threadIdx.x; e < (long long)a * a; e += blockDim.x) {
+  const long long n = (long long)a * a;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(e % a), j = (int)(e / a);
-    if (i < j) {
+    if (i > j) {
       const double m = 0.5 * (G[i + (long long)a * j] + G[j + (long long)a * i]);
       G[i + (long long)a * j] = m;
       G[j + (long long)a * i] = m;
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && tr) {
+  if (blockIdx.x == 0 && tr && threadIdx.x < 32) {
     double s = 0.0;
-    for (int i = 0; i < a; ++i) s += G[i + (long long)a * i];
-    *tr = s;
+    for (int i = threadIdx.x; i < a; i += 32) s += G[i + (long long)a * i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *tr = s;
   }
 }
 

@@ -403,114 +403,218 @@ constexpr int kSubK = 8;
 constexpr int kSubIters = 40;
 constexpr int kSubThreads = 256;
 
-// one warp: parallel cyclic Jacobi on the symmetric k x k H (k <= 8, ld k),
-// eigenvectors into W.  Round-robin pairs, one lane per pair; all row
-// rotations of a round, then all column rotations (disjoint supports commute).
-// A rotation is skipped when |h_pq| <= 1e-18 sqrt(|h_pp h_qq|); stops after a
-// sweep without rotations.
-__device__ void small_sym_eig(double* H, double* W, int k) {
-  const int lane = threadIdx.x & 31;
-  for (int i = lane; i < k * k; i += 32) W[i] = ((i % k) == (i / k)) ? 1.0 : 0.0;
+// One warp: cyclic Jacobi on the symmetric k x k (k <= N, N = 4 or 8) H held
+// in registers (lane (N/2) i + m owns H[i][2m..2m+1] and W[i][2m..2m+1]); the
+// N/2 disjoint round-robin pairs of a round are rotated together (rows, then
+// columns of H, then columns of W) with shuffles only.  A rotation is skipped
+// when |h_pq| <= 1e-15 sqrt(|h_pp h_qq|) or |h_pq| <= 4 eps max_i |h_ii| (at
+// that size a rotation only reshuffles rounding noise: eigenvalues move by
+// O(h_pq^2 / gap)); stops after a sweep without rotations.  Output: eigenvalues descending in
+// theta[0..k), eigenvectors as the matching columns of Wv (k x k, ld k);
+// Wt is an 8 x 8 shared scratch.
+template <int N>
+__device__ int warp_sym_eig(const double* Hs, int k, double* theta, double* Wv, double* Wt) {
+  constexpr int NH = N / 2, NR = N - 1;
+  const int lane = threadIdx.x & 31, i = lane / NH, m = lane % NH;
+  const bool valid = i < N;
+  const int j0 = 2 * m, j1 = 2 * m + 1;
+  auto hsym = [&](int r, int c) { return (r < k && c < k) ? 0.5 * (Hs[r + k * c] + Hs[c + k * r]) : 0.0; };
+  double h0 = hsym(i, j0), h1 = hsym(i, j1);
+  double w0 = (i == j0) ? 1.0 : 0.0, w1 = (i == j1) ? 1.0 : 0.0;
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    double dg = ((i >> 1) == m) ? ((i & 1) ? h1 : h0) : 0.0;
+    double hmax = fabs(dg);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hmax = fmax(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    const double floor_abs = 8.881784197001252e-16 * hmax;
+    bool rotated = false;
+    for (int rnd = 0; rnd < NR; ++rnd) {
+      // round-robin positions: index 0 fixed at position 0, 1..7 rotate;
+      // pairs are positions (u, 7-u), slot = min(u, 7-u)
+      auto idx_at = [&](int u) { return u == 0 ? 0 : ((u - 1 + rnd) % NR) + 1; };
+      auto pos_of = [&](int x) { return x == 0 ? 0 : ((x - 1 - rnd + NR) % NR) + 1; };
+      auto partner = [&](int x) { return idx_at(NR - pos_of(x)); };
+      auto slot_of = [&](int x) { const int u = pos_of(x); return u < NR - u ? u : NR - u; };
+      const int pi = partner(i);
+      dg = ((i >> 1) == m) ? ((i & 1) ? h1 : h0) : 0.0;
+      const double mypq = ((pi >> 1) == m) ? ((pi & 1) ? h1 : h0) : 0.0;
+      // lane evaluates the rotation of slot (lane & 3); lanes 0..3 publish it
+      double cme = 1.0, sme = 0.0;
+      int ame = 0;
+      {
+        int p = idx_at(m), q = idx_at(NR - m);
+        if (p > q) { const int t = p; p = q; q = t; }
+        const double hpp = __shfl_sync(0xffffffffu, dg, p * NH + (p >> 1));
+        const double hqq = __shfl_sync(0xffffffffu, dg, q * NH + (q >> 1));
+        const double hpq = __shfl_sync(0xffffffffu, mypq, p * NH + (q >> 1));
+        if (q < k && fabs(hpq) > floor_abs && fabs(hpq) > 1e-15 * sqrt(fabs(hpp * hqq))) {
+          const double zeta = (hqq - hpp) / (2.0 * hpq);
+          const double az = fabs(zeta);
+          const double t = az > 1e150 ? 0.5 / zeta : copysign(1.0, zeta) / (az + sqrt(fma(zeta, zeta, 1.0)));
+          cme = rsqrt(fma(t, t, 1.0));
+          sme = cme * t;
+          ame = 1;
+        }
+      }
+      rotated |= __any_sync(0xffffffffu, ame != 0);
+      // rows p, q of H
+      {
+        const int sl = slot_of(i);
+        const double c = __shfl_sync(0xffffffffu, cme, sl), sn = __shfl_sync(0xffffffffu, sme, sl);
+        const bool act = __shfl_sync(0xffffffffu, ame, sl) != 0;
+        const double o0 = __shfl_sync(0xffffffffu, h0, pi * NH + m);
+        const double o1 = __shfl_sync(0xffffffffu, h1, pi * NH + m);
+        if (act) {
+          const bool isp = i < pi;
+          h0 = isp ? c * h0 - sn * o0 : sn * o0 + c * h0;
+          h1 = isp ? c * h1 - sn * o1 : sn * o1 + c * h1;
+        }
+      }
+      // columns p, q of H and W
+      {
+        const int pj0 = partner(j0), pj1 = partner(j1);
+        const int s0 = slot_of(j0), s1 = slot_of(j1);
+        const double c0s = __shfl_sync(0xffffffffu, cme, s0), s0s = __shfl_sync(0xffffffffu, sme, s0);
+        const double c1s = __shfl_sync(0xffffffffu, cme, s1), s1s = __shfl_sync(0xffffffffu, sme, s1);
+        const bool a0s = __shfl_sync(0xffffffffu, ame, s0) != 0, a1s = __shfl_sync(0xffffffffu, ame, s1) != 0;
+        const double a0 = __shfl_sync(0xffffffffu, h0, i * NH + (pj0 >> 1));
+        const double a1 = __shfl_sync(0xffffffffu, h1, i * NH + (pj0 >> 1));
+        const double b0 = __shfl_sync(0xffffffffu, h0, i * NH + (pj1 >> 1));
+        const double b1 = __shfl_sync(0xffffffffu, h1, i * NH + (pj1 >> 1));
+        const double c0 = __shfl_sync(0xffffffffu, w0, i * NH + (pj0 >> 1));
+        const double c1 = __shfl_sync(0xffffffffu, w1, i * NH + (pj0 >> 1));
+        const double d0 = __shfl_sync(0xffffffffu, w0, i * NH + (pj1 >> 1));
+        const double d1 = __shfl_sync(0xffffffffu, w1, i * NH + (pj1 >> 1));
+        const double hx0 = (pj0 & 1) ? a1 : a0, hx1 = (pj1 & 1) ? b1 : b0;
+        const double wx0 = (pj0 & 1) ? c1 : c0, wx1 = (pj1 & 1) ? d1 : d0;
+        if (a0s) {
+          const bool isp = j0 < pj0;
+          h0 = isp ? c0s * h0 - s0s * hx0 : s0s * hx0 + c0s * h0;
+          w0 = isp ? c0s * w0 - s0s * wx0 : s0s * wx0 + c0s * w0;
+        }
+        if (a1s) {
+          const bool isp = j1 < pj1;
+          h1 = isp ? c1s * h1 - s1s * hx1 : s1s * hx1 + c1s * h1;
+          w1 = isp ? c1s * w1 - s1s * wx1 : s1s * wx1 + c1s * w1;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
+  }
+  // eigenvalues (diagonal) and W into scratch, then a stable descending sort
+  if (valid) {
+    Wt[i + 8 * j0] = w0;
+    Wt[i + 8 * j1] = w1;
+    if ((i >> 1) == m) Wt[64 + i] = (i & 1) ? h1 : h0;
+  }
   __syncwarp();
-  const int n = k + (k & 1);
-  for (int sweep = 0; sweep < 20; ++sweep) {
-    int rotated = 0;
-    for (int rnd = 0; rnd < n - 1; ++rnd) {
-      int pp = -1, qq = -1;
-      double c = 1.0, sn = 0.0;
-      bool act = false;
-      if (lane < n / 2) {
-        pp = (lane == 0) ? 0 : ((lane - 1 + rnd) % (n - 1)) + 1;
-        qq = ((n - 2 - lane + rnd) % (n - 1)) + 1;
-        if (pp > qq) { const int tq = pp; pp = qq; qq = tq; }
-        if (qq < k) {
-          const double hpq = H[pp + k * qq], hpp = H[pp + k * pp], hqq = H[qq + k * qq];
-          if (hpq != 0.0 && fabs(hpq) > 1e-18 * sqrt(fabs(hpp * hqq))) {
-            const double zeta = (hqq - hpp) / (2.0 * hpq);
-            const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-            c = 1.0 / sqrt(1.0 + t * t);
-            sn = c * t;
-            act = true;
-          }
-        }
-      }
-      rotated |= __any_sync(0xffffffffu, act);
-      __syncwarp();
-      if (act)
-        for (int r = 0; r < k; ++r) {  // rows p, q
-          const double hp = H[pp + k * r], hq = H[qq + k * r];
-          H[pp + k * r] = c * hp - sn * hq;
-          H[qq + k * r] = sn * hp + c * hq;
-        }
-      __syncwarp();
-      if (act) {
-        for (int r = 0; r < k; ++r) {  // columns p, q
-          const double hp = H[r + k * pp], hq = H[r + k * qq];
-          H[r + k * pp] = c * hp - sn * hq;
-          H[r + k * qq] = sn * hp + c * hq;
-        }
-        for (int r = 0; r < k; ++r) {
-          const double wp = W[r + k * pp], wq = W[r + k * qq];
-          W[r + k * pp] = c * wp - sn * wq;
-          W[r + k * qq] = sn * wp + c * wq;
-        }
-      }
-      __syncwarp();
+  if (lane < k) {
+    const double tx = Wt[64 + lane];
+    int pos = 0;
+    for (int y = 0; y < k; ++y) {
+      const double ty = Wt[64 + y];
+      pos += (ty > tx || (ty == tx && y < lane)) ? 1 : 0;
     }
-    if (!rotated) break;
+    theta[pos] = tx;
+    for (int r = 0; r < k; ++r) Wv[r + k * pos] = Wt[r + 8 * lane];
   }
+  __syncwarp();
+  return sweep;
 }
 
-// block MGS (twice) of the k columns of X (a x k, ld a); warp-per-column dots,
-// sequential over columns; all threads participate, returns after a barrier.
-__device__ void block_mgs2(double* X, int a, int k, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// Orthonormalise the k (<= kSubK) columns of X (a x k, ld a) in place:
+// column-scaled Cholesky QR, twice (X D R^-1 with D = diag(X^T X)^-1/2, so the
+// Gram matrix factored is unit-diagonal and CholQR2 is stable up to
+// cond ~ 1e8).  Exactly dependent / zero columns come out as zero columns.
+// Y is an a x k scratch; S, Ri are k x k shared scratch.  Ends after a barrier.
+template <int K>
+__device__ void block_cholqr2(double* X, double* Y, int a, int k, double* S, double* Ri) {
+  (void)Y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int pass = 0; pass < 2; ++pass) {
-    for (int j = 0; j < k; ++j) {
-      double* xj = X + (size_t)a * j;
-      // dots with earlier columns: warp i computes <x_i, x_j>
-      for (int i = warp; i < j; i += nw) {
-        const double* xi = X + (size_t)a * i;
-        double s = 0.0;
-        for (int r = lane; r < a; r += 32) s = fma(xi[r], xj[r], s);
-        s = warp_sum(s);
-        if (lane == 0) red[i] = s;
-      }
-      __syncthreads();
-      for (int r = threadIdx.x; r < a; r += blockDim.x) {
-        double v = xj[r];
-        for (int i = 0; i < j; ++i) v -= red[i] * X[r + (size_t)a * i];
-        xj[r] = v;
-      }
-      __syncthreads();
-      double s = 0.0;
-      for (int r = threadIdx.x; r < a; r += blockDim.x) s = fma(xj[r], xj[r], s);
-      s = warp_sum(s);
-      if (lane == 0) red[32 + warp] = s;
-      __syncthreads();
-      double nn = 0.0;
-      for (int w = 0; w < nw; ++w) nn += red[32 + w];
-      const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-      for (int r = threadIdx.x; r < a; r += blockDim.x) xj[r] *= inv;
-      __syncthreads();
+    for (int e = warp; e < k * k; e += nw) {
+      const int i = e % k, j = e / k;
+      if (i > j) continue;
+      double sacc = 0.0;
+      for (int r = lane; r < a; r += 32) sacc = fma(X[r + (size_t)a * i], X[r + (size_t)a * j], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) S[i + k * j] = sacc;
     }
+    __syncthreads();
+    if (warp == 0) {
+      // Ri[0..k) = D = diag(S)^-1/2; S <- D S D (upper); right-looking Cholesky
+      // in place: R (upper) overwrites S.  Lane e owns upper entries e, e+32.
+      if (lane < k) Ri[lane] = S[lane + k * lane] > 0.0 ? 1.0 / sqrt(S[lane + k * lane]) : 0.0;
+      __syncwarp();
+      for (int e = lane; e < k * k; e += 32) {
+        const int i = e % k, j = e / k;
+        if (i <= j) S[e] *= Ri[i] * Ri[j];
+      }
+      __syncwarp();
+      for (int jj = 0; jj < k; ++jj) {
+        const double piv = S[jj + k * jj];
+        const double rjj = piv > 1e-28 ? sqrt(piv) : 0.0;
+        const double inv = rjj > 0.0 ? 1.0 / rjj : 0.0;
+        __syncwarp();
+        if (lane == 0) Ri[K + jj] = inv;
+        // row jj of R
+        for (int l = jj + lane; l < k; l += 32) S[jj + k * l] = (l == jj) ? rjj : S[jj + k * l] * inv;
+        __syncwarp();
+        // trailing update S[i][l] -= R[jj][i] R[jj][l], jj < i <= l
+        for (int e = lane; e < k * k; e += 32) {
+          const int i = e % k, l = e / k;
+          if (i > jj && i <= l) S[e] -= S[jj + k * i] * S[jj + k * l];
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // X <- X D R^-1, row by row (forward substitution on the row vector)
+    for (int r = tid; r < a; r += blockDim.x) {
+      double v[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < k) {
+          double t = X[r + (size_t)a * j] * Ri[j];
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            if (m < j) t -= v[m] * S[m + k * j];
+          v[j] = t * Ri[K + j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (j < k) X[r + (size_t)a * j] = v[j];
+    }
+    __syncthreads();
   }
 }
 
+template <int K>
 __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[64];
-  __shared__ double H[kSubK * kSubK], Wv[kSubK * kSubK], theta[kSubK], resn[kSubK];
+  __shared__ double H[K * K], Wv[K * K], theta[K], resn[K];
+  __shared__ double Sq[K * K], Rq[2 * K], Wt[72];
   __shared__ int s_state, s_rank;
   __shared__ double s_tail;
+  const long long t0 = clock64();
   const int a = p.a;
-  const int k = a < kSubK ? a : kSubK;
+  const int k = a < K ? a : K;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double* G = p.in_smem ? sm : const_cast<double*>(p.G);
   double* X = p.in_smem ? sm + (size_t)a * a : sm;
-  double* Z = X + (size_t)a * kSubK;
-  if (p.in_smem)
-    for (long long i = tid; i < (long long)a * a; i += blockDim.x) G[i] = p.G[i];
+  double* Z = X + (size_t)a * K;
+  if (p.in_smem) {  // a*a is even or odd: copy pairs, then the odd tail
+    const long long n = (long long)a * a, n2 = n >> 1;
+    const double2* src = reinterpret_cast<const double2*>(p.G);
+    double2* dst = reinterpret_cast<double2*>(G);
+#pragma unroll 8
+    for (long long i = tid; i < n2; i += blockDim.x) dst[i] = __ldg(src + i);
+    if ((n & 1) && tid == 0) G[n - 1] = p.G[n - 1];
+  }
+  const long long ts1 = clock64();
   // deterministic pseudo-random start block
   for (int e = tid; e < a * k; e += blockDim.x) {
     unsigned long long h = 0x9E3779B97F4A7C15ull * (unsigned long long)(e + 1);
@@ -530,24 +634,33 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
     }
     return;
   }
-  block_mgs2(X, a, k, red);
+  const long long ts2 = clock64();
+  block_cholqr2<K>(X, Z, a, k, Sq, Rq);
+  const long long t1 = clock64();
   double prev_res = 1e300;
+  long long ph[4] = {0, 0, 0, 0};
+  int jac_sweeps = 0;
   int it = 0;
   for (; it < kSubIters; ++it) {
-    // Z = G X  (thread-consecutive rows i: G[i + a*j] is bank-conflict free)
-    for (int e = tid; e < a * k; e += blockDim.x) {
-      const int i = e % a, c = e / a;
-      const double* xc = X + (size_t)a * c;
-      double s0 = 0.0, s1 = 0.0;
-      int j = 0;
-      for (; j + 1 < a; j += 2) {
-        s0 = fma(G[i + (size_t)a * j], xc[j], s0);
-        s1 = fma(G[i + (size_t)a * (j + 1)], xc[j + 1], s1);
+    long long tq0 = clock64();
+    // Z = G X: one thread per row i (G[i + a*j] over consecutive i is
+    // conflict-free, X[j + a*c] is a broadcast), K independent chains
+    for (int i = tid; i < a; i += blockDim.x) {
+      double acc[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) acc[c] = 0.0;
+      for (int j = 0; j < a; ++j) {
+        const double gij = G[i + (size_t)a * j];
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+          if (c < k) acc[c] = fma(gij, X[j + (size_t)a * c], acc[c]);
       }
-      if (j < a) s0 = fma(G[i + (size_t)a * j], xc[j], s0);
-      Z[e] = s0 + s1;
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        if (c < k) Z[i + (size_t)a * c] = acc[c];
     }
     __syncthreads();
+    long long tq1 = clock64();
     // H = X^T Z (k x k), symmetrised
     for (int e = warp; e < k * k; e += nw) {
       const int i = e % k, j = e / k;
@@ -557,31 +670,13 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
       if (lane == 0) H[e] = s;
     }
     __syncthreads();
+    long long tq2 = clock64();
     if (warp == 0) {
-      for (int e = lane; e < k * k; e += 32) {
-        const int i = e % k, j = e / k;
-        if (i < j) {
-          const double m = 0.5 * (H[i + k * j] + H[j + k * i]);
-          H[i + k * j] = m;
-          H[j + k * i] = m;
-        }
-      }
-      __syncwarp();
-      small_sym_eig(H, Wv, k);
-      if (lane == 0) {  // sort descending (selection sort on k <= 8), permute W
-        for (int i = 0; i < k; ++i) theta[i] = H[i + k * i];
-        for (int i = 0; i < k; ++i) {
-          int m = i;
-          for (int j = i + 1; j < k; ++j)
-            if (theta[j] > theta[m]) m = j;
-          if (m != i) {
-            const double tv = theta[i]; theta[i] = theta[m]; theta[m] = tv;
-            for (int r = 0; r < k; ++r) { const double w = Wv[r + k * i]; Wv[r + k * i] = Wv[r + k * m]; Wv[r + k * m] = w; }
-          }
-        }
-      }
+      const int nsw = warp_sym_eig<K>(H, k, theta, Wv, Wt);
+      if (lane == 0) jac_sweeps += nsw;
     }
     __syncthreads();
+    long long tq3 = clock64();
     // residuals |Z w_j - theta_j X w_j|
     for (int j = warp; j < k; j += nw) {
       double s = 0.0;
@@ -620,12 +715,17 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
         }
       } else {
         worst = resn[0];
-        if (it >= 5) s_state = 2;  // more kept directions than the block holds: full solver
+        if (it >= 3) s_state = 2;  // more kept directions than the block holds: larger block / full solver
       }
       prev_res = worst;
       red[63] = worst;
     }
     __syncthreads();
+    if (tid == 0) {
+      const long long tq4 = clock64();
+      p.res->t_phase[2] += 0;  // keep
+      ph[0] += tq1 - tq0; ph[1] += tq2 - tq1; ph[2] += tq3 - tq2; ph[3] += tq4 - tq3;
+    }
     if (s_state) break;
     prev_res = red[63];
     // next block: X = orth(Z W)   (Ritz-rotated power step)
@@ -636,10 +736,14 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
       X[e] = s;
     }
     __syncthreads();
-    block_mgs2(X, a, k, red);
+    block_cholqr2<K>(X, Z, a, k, Sq, Rq);
   }
   const int rank = s_rank;
   if (tid == 0) {
+    p.res->t_phase[0] = (ts1 - t0) | ((ts2 - ts1) << 20) | ((t1 - ts2) << 40);
+    p.res->t_phase[1] = (clock64() - t1) | ((long long)jac_sweeps << 40);
+    p.res->t_phase[2] = ph[0] | (ph[1] << 32);
+    p.res->t_phase[3] = ph[2] | (ph[3] << 32);
     p.res->converged = (s_state == 1) ? 1 : 0;
     p.res->sweeps = it;
     p.res->rank = rank;

@@ -11,7 +11,7 @@ __global__ void fill(double* x, long long n) {
 }
 
 #include <cudaTypedefs.h>
-CUtensorMap make_map(const double* X, int a, long long L) {
+CUtensorMap make_map(const double* X, int a, long long L, int bc = 64) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -20,7 +20,7 @@ CUtensorMap make_map(const double* X, int a, long long L) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)a, (cuuint64_t)L};
   cuuint64_t strides[1] = {(cuuint64_t)a * 8};
-  cuuint32_t box[2] = {16, 64};
+  cuuint32_t box[2] = {16, (cuuint32_t)bc};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)X, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -28,17 +28,18 @@ CUtensorMap make_map(const double* X, int a, long long L) {
   return m;
 }
 template <class K>
-void timetma(const char* name, K kern, const CUtensorMap& tm, ttg::ProjArgs p, size_t smem, double bytes) {
+void timetma(const char* name, K kern, const CUtensorMap& tm, ttg::ProjArgs p, size_t smem, double bytes,
+             int threads = ttg::kThreads) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ttg::kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   const int gx = 148 * (occ > 0 ? occ : 1);
-  kern<<<gx, ttg::kThreads, smem>>>(tm, p);
+  kern<<<gx, threads, smem>>>(tm, p);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  for (int i = 0; i < 5; ++i) kern<<<gx, ttg::kThreads, smem>>>(tm, p);
+  for (int i = 0; i < 5; ++i) kern<<<gx, threads, smem>>>(tm, p);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -109,12 +110,62 @@ int main() {
       for (int nst : {2, 3, 4, 6}) {
         p.nst = nst;
         std::snprintf(nm, sizeof nm, "tmap r=%d norms=%d", r, norms);
-        timetma(nm, ttg::k_project_tma<true>, tm, p, 1024 + nst * 8192 * 4 + stg, bytes);
+        timetma(nm, ttg::k_project_tma<true, 64>, tm, p, 1024 + nst * 8192 * 4 + stg, bytes);
+      }
+      for (int nst : {6, 8, 11, 16}) {
+        p.nst = nst;
+        std::snprintf(nm, sizeof nm, "box r=%d norms=%d", r, norms);
+        if (r <= 16)
+          timetma(nm, ttg::k_project_box<2, true>, tm, p, 1024 + nst * 8192 + stg, bytes, ttg::kSyrkThreads);
+        std::snprintf(nm, sizeof nm, "box-smemW r=%d norms=%d", r, norms);
+        p.frag_smem = 1;
+        timetma(nm, ttg::k_project_box<4, false>, tm, p, 1024 + nst * 8192 + stg + 8 * 4 * 16 * 32, bytes, ttg::kSyrkThreads);
+        p.frag_smem = 0;
       }
       p.nst = 0;
       std::snprintf(nm, sizeof nm, "tma-db r=%d norms=%d", r, norms);
       timeit(nm, ttg::k_project<true, true>, p, 2 * stage, bytes);
     }
+  }
+  {  // a = 144 (cur_2-like), r = 18
+    const int a2 = 144, r2 = 18;
+    const long long L2 = (1ll << 32) / (8 * a2) / 64 * 64;
+    ttg::ProjArgs p{};
+    p.src = ttg::TileSrc{X, a2, L2, nullptr, 1};
+    p.a8 = a2;
+    p.ldt = ttg::smem_ld(a2);
+    p.WTf = W;
+    p.r = r2;
+    p.r8 = 24;
+    p.out = out;
+    p.n_tiles = L2 / 64;
+    const double bytes = 8.0 * (a2 + r2) * L2;
+    const CUtensorMap tm = make_map(X, a2, L2);
+    char nm[128];
+    for (int nst : {6, 8, 11, 16}) {
+      p.nst = nst;
+      std::snprintf(nm, sizeof nm, "box a=144 r=18 (W global)");
+      timetma(nm, ttg::k_project_box<4, false>, tm, p, 1024 + nst * 8192 + 8 * 8 * 32 * 8, bytes, ttg::kSyrkThreads);
+    }
+    {
+      const CUtensorMap tm32 = make_map(X, a2, L2, 32);
+      ttg::ProjArgs q = p;
+      q.n_tiles = L2 / 32;
+      for (int nst : {2, 3}) {
+        q.nst = nst;
+        timetma("tmap32 a=144 r=18 (W global)", ttg::k_project_tma<false, 32>, tm32, q, 1024 + nst * 9 * 4096 + 8 * 8 * 32 * 8, bytes);
+      }
+      const CUtensorMap tm32b = make_map(X, 128, (1ll << 32) / (8 * 128));
+      q.src = ttg::TileSrc{X, 128, (1ll << 32) / (8 * 128), nullptr, 1};
+      q.a8 = 128; q.r = 16; q.r8 = 16; q.n_tiles = q.src.L / 32;
+      const CUtensorMap tm128 = make_map(X, 128, q.src.L, 32);
+      for (int nst : {2, 3}) {
+        q.nst = nst;
+        timetma("tmap32 a=128 r=16 (W global)", ttg::k_project_tma<false, 32>, tm128, q, 1024 + nst * 8 * 4096 + 8 * 8 * 32 * 8, 8.0 * 144 * q.src.L);
+      }
+    }
+    p.nst = 0;
+    timeit("old single-buffer a=144 r=18", ttg::k_project<false, false>, p, sizeof(double) * p.ldt * 64, bytes);
   }
   return 0;
 }
