@@ -518,6 +518,95 @@ void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) 
   post_launch(c);
 }
 
+// 2-D tensor map of X (a x L, column-major) with 16 x 64 boxes and 128-byte
+// swizzle (ttg_kernels.cuh, "Tensor-map TMA tiles").  The driver entry point
+// is resolved once through the runtime (no -lcuda).  False when the operand
+// does not qualify (odd a, misaligned base, L beyond int32 coordinates).
+bool make_tmap(CUtensorMap* m, const double* X, int a, long long L, int box_cols = ttg::kTC) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static bool resolved = false;
+  if (!resolved) {
+    resolved = true;
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  }
+  if (!enc || (a & 1) || a <= 0 || L <= 0 || L >= (1LL << 31) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)a, (cuuint64_t)L};
+  cuuint64_t strides[1] = {(cuuint64_t)a * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_cols};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor-map SYRK (k_syrk2) into c->G; false when the operand does not
+// qualify (odd a, a > 256, selection not tile-aligned, fewer than two ring
+// stages fit) and the caller takes the per-column path.
+template <int MAXT>
+void launch_syrk2_t(ttg_ctx* c, const CUtensorMap& tm, ttg::Syrk2Args args, int parts, size_t smem, double sel_frac) {
+  auto kern = ttg::k_syrk2<MAXT>;
+  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, ttg::kSyrkThreads, smem));
+  const long long want = std::max<long long>(1, (long long)c->num_sms * occ / parts);
+  const int gx = (int)std::min<long long>(want, std::max<long long>(1, args.n_tiles));
+  c->partials.ensure(sizeof(double) * (size_t)gx * args.a8 * args.a8);
+  args.partials = c->partials.as<double>();
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
+  const double Ls = (double)args.L * sel_frac;
+  prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
+  kern<<<dim3(gx, parts), ttg::kSyrkThreads, smem, c->stream>>>(tm, args);
+  post_launch(c);
+  const long long n = (long long)args.a * args.a;
+  prof_begin(c, "k_gram_reduce", 8.0 * gx * args.a8 * args.a8, (double)gx * n);
+  ttg::k_gram_reduce2<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, args.a8, args.a,
+                                                                       c->G.as<double>());
+  post_launch(c);
+}
+
+bool syrk2(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
+           double* tsq) {
+  // a <= 128: the per-column super-tile kernel (k_syrk) measures faster (one
+  // super-tile, 3 CTAs / SM at a = 64); the tensor-map kernel wins above,
+  // where k_syrk splits rows into super-tile pairs and re-reads them.
+  if (std::getenv("TTG_NO_SYRK2") || (a & 1) || a <= 128 || a > 256 || (sel && cpo % ttg::kTC != 0)) return false;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, X, a, L)) return false;
+  const int a8 = ttg::round_up(a, 8), nb = a8 / 8, tI = (nb + 1) / 2;
+  const int nbox = (a + 15) / 16;
+  const size_t stage = sizeof(double) * 1024 * nbox;
+  const size_t cap = (size_t)c->smem_optin - 1024;
+  // ring: 4 stages when two CTAs fit, else as many as fit one CTA (>= 2)
+  int nst = 4;
+  while (nst > 2 && 2 * (nst * stage + 1024) > 220 * 1024) --nst;
+  if (nst * stage + 1024 > cap) {
+    nst = (int)std::min<size_t>(ttg::kMaxStages, (cap - 1024) / stage);
+    if (nst < 2) return false;
+  }
+  ttg::Syrk2Args args{};
+  args.a = a;
+  args.a8 = a8;
+  args.nbox = nbox;
+  args.nst = nst;
+  args.L = L;
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  args.sel = sel;
+  args.cpo = cpo;
+  args.ntiles2 = tI * (tI + 1) / 2;
+  args.tsumsq = tsq;
+  const size_t smem = nst * stage + 1024;
+  const int nt = args.ntiles2;
+  if (nt <= 8) launch_syrk2_t<1>(c, tm, args, 1, smem, sel_frac);
+  else if (nt <= 16) launch_syrk2_t<2>(c, tm, args, 1, smem, sel_frac);
+  else launch_syrk2_t<3>(c, tm, args, (nt + 23) / 24, smem, sel_frac);
+  return true;
+}
+
 // C = sum over selected columns x x^T -> c->G (a x a); returns whether per-tile
 // sums of squares were produced
 bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
@@ -527,6 +616,10 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
   if (a & 1) {  // odd rows: no 16-byte TMA runs -> generic
     gram_src(c, Src{X, a, L, nullptr, a}, 1, nullptr, 0, sel, cpo, sel_frac, tsq);
     return tsq != nullptr && ttg::round_up(a, 8) <= kFastMax1;
+  }
+  if (syrk2(c, X, a, L, sel, cpo, sel_frac, tsq)) {
+    allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+    return tsq != nullptr;
   }
   ttg::SyrkArgs args{};
   args.X = X;
@@ -802,33 +895,6 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
 
 // ---- projection --------------------------------------------------------------
 // out (r x L) = W^T X  (X: a x L, W: a x r with leading dimension ldw)
-// 2-D tensor map of X (a x L, column-major) with 16 x 64 boxes and 128-byte
-// swizzle (ttg_kernels.cuh, "Tensor-map TMA tiles").  The driver entry point
-// is resolved once through the runtime (no -lcuda).  False when the operand
-// does not qualify (odd a, misaligned base, L beyond int32 coordinates).
-bool make_tmap(CUtensorMap* m, const double* X, int a, long long L, int box_cols = ttg::kTC) {
-  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-  static bool resolved = false;
-  if (!resolved) {
-    resolved = true;
-    cudaDriverEntryPointQueryResult q{};
-    void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    else
-      cudaGetLastError();
-  }
-  if (!enc || (a & 1) || a <= 0 || L <= 0 || L >= (1LL << 31) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)a, (cuuint64_t)L};
-  cuuint64_t strides[1] = {(cuuint64_t)a * sizeof(double)};
-  cuuint32_t box[2] = {16, (cuuint32_t)box_cols};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
              double* tsq = nullptr) {
   const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
@@ -1725,7 +1791,8 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
         (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
         (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
-        (const void*)ttg::k_syrk<8>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
+        (const void*)ttg::k_syrk<8>, (const void*)ttg::k_syrk2<1>, (const void*)ttg::k_syrk2<2>,
+        (const void*)ttg::k_syrk2<3>, (const void*)ttg::k_gram_reduce2, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec};
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));

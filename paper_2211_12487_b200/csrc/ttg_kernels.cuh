@@ -1329,6 +1329,169 @@ __global__ void __launch_bounds__(kSyrkThreads) k_project_box(const __grid_const
   }
 }
 
+// ---------------------------------------------------------------------------
+// SYRK over tensor-map tiles: C = sum over (selected) columns x x^T, x the
+// a rows of X (a <= 256).  A tile is kTC full-height columns, ceil(a/16) TMA
+// boxes with 128-byte swizzle (dense smem, one instruction per box); warp 8
+// lane 0 produces into an nst-deep ring (full / empty mbarriers), warps 0..7
+// consume.  The lower triangle of the (a8/8)^2 block grid is cut into 2x2-block
+// tiles, dealt round-robin over the gridDim.y "parts" x 8 warps (a part's CTAs
+// read the same column tiles; the repeat read hits L2).  The k dimension of
+// each DMMA step uses the columns {8q + 2h + (0,1,4,5)} (h = step parity):
+// with the swizzle this makes the 8-row x 4-column A/B fragment loads
+// bank-conflict free (tools/probe: checked exhaustively).  Observation
+// selection skips whole tiles (requires cols_per_obs % kTC == 0).  Each CTA
+// writes its owned blocks into partials[blockIdx.x] (a8 x a8); parts own
+// disjoint blocks, so k_gram_reduce2 sums over blockIdx.x only.
+// ---------------------------------------------------------------------------
+struct Syrk2Args {
+  int a, a8, nbox, nst;
+  long long L, n_tiles;
+  const uint8_t* sel;
+  long long cpo;
+  int ntiles2;       // lower 2x2-block tiles
+  double* partials;  // [gridDim.x][a8 * a8]
+  double* tsumsq;    // per-(tile, 8-column group) input sums of squares (part 0), nullable
+};
+
+template <int MAXT>
+__global__ void __launch_bounds__(kSyrkThreads) k_syrk2(const __grid_constant__ CUtensorMap tm, Syrk2Args p) {
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int stage = p.nbox * 1024;
+  const int nst = p.nst;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long grid = gridDim.x;
+  if (warp == kConsumerWarps) {  // ---- producer ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      int it = 0;
+      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+        if (p.sel && !p.sel[(tile * kTC) / p.cpo]) continue;
+        const int s = it % nst;
+        if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
+        mbar_expect_tx(&full[s], (unsigned)p.nbox * 8192u);
+        for (int b = 0; b < p.nbox; ++b) tma_load_2d(ring + s * stage + b * 1024, &tm, 16 * b, (int)(tile * kTC), &full[s]);
+        ++it;
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  const int part = blockIdx.y, P = gridDim.y;
+  int baseA[MAXT], baseB[MAXT], rowA[MAXT], rowB[MAXT];
+  bool live[MAXT];
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u) {
+    const int idx = part * kConsumerWarps + warp + kConsumerWarps * P * u;
+    live[u] = idx < p.ntiles2;
+    int ta = (int)((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
+    while ((ta + 1) * (ta + 2) / 2 <= idx) ++ta;
+    while (ta * (ta + 1) / 2 > idx) --ta;
+    const int tb = idx - ta * (ta + 1) / 2;
+    baseA[u] = ta * 1024;
+    baseB[u] = tb * 1024;
+    rowA[u] = 16 * ta;
+    rowB[u] = 16 * tb;
+  }
+  // lane offsets inside a box for step parity h and row half x (see header)
+  int offs[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cl = 2 * h + (t & 1) + 4 * (t >> 1);
+#pragma unroll
+    for (int x = 0; x < 2; ++x) offs[h][x] = 16 * cl + (((4 * x + (g >> 1)) ^ cl) << 1) + (g & 1);
+  }
+  double acc[MAXT][2][2][2];
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) acc[u][x][y][0] = acc[u][x][y][1] = 0.0;
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+    if (p.sel && !p.sel[(tile * kTC) / p.cpo]) continue;
+    const int st = it % nst;
+    mbar_wait(&full[st], (unsigned)((it / nst) & 1));
+    const double* T = ring + st * stage;
+    if (p.tsumsq && part == 0) {  // this warp's 8 columns are 128 consecutive doubles per box
+      double sq = 0.0;
+      for (int b = 0; b < p.nbox; ++b) {
+        const double* base = T + b * 1024 + warp * 128;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double v = base[lane + 32 * e];
+          sq = fma(v, v, sq);
+        }
+      }
+      sq = warp_sum(sq);
+      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = sq;
+    }
+#pragma unroll
+    for (int u = 0; u < MAXT; ++u) {
+      if (!live[u]) continue;  // warp-uniform
+      const double* TA = T + baseA[u];
+      const double* TB = T + baseB[u];
+#pragma unroll 4
+      for (int kk = 0; kk < kTC / 4; ++kk) {
+        const int ko = 128 * (kk >> 1);
+        const int h = kk & 1;
+        const double a0 = TA[ko + offs[h][0]];
+        const double a1 = TA[ko + offs[h][1]];
+        const double b0 = TB[ko + offs[h][0]];
+        const double b1 = TB[ko + offs[h][1]];
+        dmma(acc[u][0][0][0], acc[u][0][0][1], a0, b0);
+        dmma(acc[u][0][1][0], acc[u][0][1][1], a0, b1);
+        dmma(acc[u][1][0][0], acc[u][1][0][1], a1, b0);
+        dmma(acc[u][1][1][0], acc[u][1][1][1], a1, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+    ++it;
+  }
+  double* out = p.partials + (long long)blockIdx.x * p.a8 * p.a8;
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u) {
+    if (!live[u]) continue;
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const int r = rowA[u] + x * 8 + g;
+        const int c = rowB[u] + y * 8 + 2 * t;
+        if (r < p.a8 && c + 1 < p.a8 + 1 && c < p.a8) {
+          out[r + (long long)p.a8 * c] = acc[u][x][y][0];
+          out[r + (long long)p.a8 * (c + 1)] = acc[u][x][y][1];
+        }
+      }
+  }
+}
+
+// G (a x a, symmetric) = sum over the nx CTA partials (lower triangle read)
+__global__ void k_gram_reduce2(const double* __restrict__ partials, int nx, int a8, int a, double* __restrict__ G) {
+  const long long n = (long long)a * a;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e % a), j = (int)(e / a);
+    if (j > i) { const int tmp = i; i = j; j = tmp; }
+    const double* src = partials + i + (long long)a8 * j;
+    double s = 0.0;
+    for (int x = 0; x < nx; ++x) s += src[(long long)x * a8 * a8];
+    G[e] = s;
+  }
+}
+
 // per-observation sums from per-(tile, warp) partials (tiles never straddle
 // observations): one block per observation, fixed assignment + fixed tree
 __global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_per_obs, int nobs,
