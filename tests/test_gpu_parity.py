@@ -69,6 +69,14 @@ def test_cfg3_shape_star_midsize(ctx):
     run_stream(ctx, s, 5, "star")
 
 
+@pytest.mark.parametrize("algo", ["ice", "star"])
+def test_wide_unfoldings(ctx, algo):
+    """Unfoldings with 128 < r*n <= 256 rows (tensor-map SYRK, 32-column
+    projection tiles) and odd/even row counts: modes 16^3 x 6, batch 16."""
+    s = Stream(3, seed=4, modes=(16, 16, 16, 6), batch=16, true_rank=11)
+    run_stream(ctx, s, 6, algo)
+
+
 def test_cfg1_video_small_batch(ctx):
     """BASELINE configs[1] shape (14,15,16,10,3) at batch 10, 6 increments."""
     s = Stream(1, seed=0, batch=10)
