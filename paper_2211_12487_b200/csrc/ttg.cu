@@ -895,6 +895,55 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
 
 // ---- projection --------------------------------------------------------------
 // out (r x L) = W^T X  (X: a x L, W: a x r with leading dimension ldw)
+// Warp-specialised m16n8k16 projection (k_project_ws16) for r <= 32, even
+// a <= 256: 4 consumer warps x 16 columns per 64-column tile; two CTAs / SM
+// with two stages when they fit, else one CTA with up to four.  False when
+// the operand does not qualify (the caller takes the other kernels).
+bool project_ws16(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
+                  double* tsq) {
+  if (std::getenv("TTG_NO_WS16") || (a & 1) || a > 256 || r > 32) return false;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, X, a, L, ttg::kTC)) return false;
+  const int r8 = ttg::round_up(r, 8), NB = r8 / 8, nks = (a + 15) / 16;
+  const size_t nfr = (size_t)nks * NB * 128;
+  const size_t stage = sizeof(double) * (size_t)nks * 16 * ttg::kTC;
+  const size_t fixed = 1024 + sizeof(double) * (nfr + (size_t)4 * 16 * 32);
+  const size_t cap = (size_t)c->smem_optin - 1024;
+  int nst = 2;
+  if (fixed + 2 * stage > cap) return false;
+  if (2 * (fixed + 2 * stage) > 220 * 1024)  // one CTA / SM: deepen the ring
+    while (nst < 4 && fixed + (nst + 1) * stage <= cap) ++nst;
+  const size_t smem = fixed + nst * stage;
+  c->UTf.ensure(sizeof(double) * std::max<size_t>(nfr, 1));
+  prof_begin(c, "k_make_frags", 8.0 * nfr, 0.0);
+  ttg::k_make_frags16<<<grid_for((long long)nfr, 256, 256), 256, 0, c->stream>>>(W, a, r, ldw, nks, NB,
+                                                                                 c->UTf.as<double>());
+  post_launch(c);
+  ttg::ProjArgs args{};
+  args.src = ttg::TileSrc{X, a, L, nullptr, 1};
+  args.a8 = ttg::round_up(a, 8);
+  args.WTf = c->UTf.as<double>();
+  args.r = r;
+  args.r8 = r8;
+  args.out = out;
+  args.tsumsq = tsq;
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  args.nst = nst;
+  void (*kern)(const CUtensorMap, ttg::ProjArgs) = NB == 1   ? ttg::k_project_ws16<4, 1>
+                                                   : NB == 2 ? ttg::k_project_ws16<4, 2>
+                                                   : NB == 3 ? ttg::k_project_ws16<4, 3>
+                                                             : ttg::k_project_ws16<4, 4>;
+  constexpr int threads = 5 * 32;
+  const int occ = std::max(kernel_occupancy((const void*)kern, kern, threads, smem), 1);
+  const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
+  prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
+  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  post_launch(c);
+  return true;
+}
+
 bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
              double* tsq = nullptr) {
   const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
@@ -902,6 +951,8 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
     gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
     return false;
   }
+  if (!(a & 1) && r8 <= 32 && !(a8 <= 64 && r8 == 16) && project_ws16(c, X, a, L, W, r, ldw, out, tsq))
+    return tsq != nullptr;
   make_frags(c, W, a, r, ldw, true, false);
   ttg::ProjArgs args{};
   args.src = ttg::TileSrc{X, a, L, nullptr, 1};
@@ -939,27 +990,31 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   const size_t nfr = (size_t)(r8 / 8) * (a8 / 4) * 32;
   const size_t stage = sizeof(double) * (size_t)args.ldt * ttg::kTC;
   CUtensorMap tm;
-  const bool narrow = a8 > 64 && r <= 32;  // 32-column tiles keep 2 CTAs x 2 stages per SM
+  // 32-column tiles: keep 2 CTAs x 2 stages per SM for tall operands, and give
+  // each warp half the k-steps so r8 <= 32 fits the register-resident W^T
+  const bool narrow = r <= 32 && (a8 > 64 || r8 > 16);
   const int tc = narrow ? 32 : ttg::kTC;
   if (a8 <= 256 && !std::getenv("TTG_NO_TMAP") && make_tmap(&tm, X, a, L, tc)) {
     // tensor-map TMA ring: 2 stages at 2 CTAs / SM (the per-tile DMMA work of
     // one CTA hides behind the other's loads), deeper when only one CTA fits
     const size_t tstage = sizeof(double) * 16 * tc * (size_t)((a + 15) / 16);
     const size_t extra = 1024 + sizeof(double) * (r <= 32 ? (size_t)ttg::kConsumerWarps * 8 * 32 : 0);
-    const bool regw = a8 <= 64 && r8 <= 16;
+    const bool regw = a8 <= 64 && r8 <= (narrow ? 32 : 16);
     const size_t fr = regw ? 0 : sizeof(double) * nfr;
     const size_t cap = (size_t)c->smem_optin - 1024;
+    // two CTAs / SM, each with as many stages as fit ~110 KB (>= 64 KB in
+    // flight per SM streams at HBM rate); one deeper CTA when two do not fit
     int nst = 2;
     size_t smem = nst * tstage + extra;
     if (fr && smem + fr <= std::min<size_t>(cap, 110 * 1024)) {
       args.frag_smem = 1;
       smem += fr;
     }
-    if (2 * smem > 220 * 1024)  // one CTA per SM: deepen the ring instead
-      while (nst < ttg::kMaxStages && smem + tstage <= cap) {
-        ++nst;
-        smem += tstage;
-      }
+    const size_t per_cta = 2 * smem > 220 * 1024 ? cap : 110 * 1024;
+    while (nst < ttg::kProjStages && smem + tstage <= per_cta) {
+      ++nst;
+      smem += tstage;
+    }
     if (smem <= cap) {
       args.nst = nst;
       args.n_tiles = (L + tc - 1) / tc;
@@ -1792,7 +1847,9 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
         (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
         (const void*)ttg::k_syrk<8>, (const void*)ttg::k_syrk2<1>, (const void*)ttg::k_syrk2<2>,
-        (const void*)ttg::k_syrk2<3>, (const void*)ttg::k_gram_reduce2, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
+        (const void*)ttg::k_syrk2<3>, (const void*)ttg::k_gram_reduce2, (const void*)ttg::k_make_frags16,
+        (const void*)ttg::k_project_ws16<4, 1>, (const void*)ttg::k_project_ws16<4, 2>,
+        (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec};
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));

@@ -29,6 +29,18 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// mma.m16n8k16 f64 (4096 FMA per instruction; layout verified by
+// tools/probe/mma16_layout.cu):  lane = 4g + t,
+//   A (16x16): a[i] = A[g + 8(i&1)][t + 4(i>>1)]    B (16x8): b[i] = B[t + 4i][g]
+//   C (16x8):  c[i] = C[g + 8(i>>1)][2t + (i&1)]
+__device__ __forceinline__ void dmma16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+      "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]), "d"(b[1]),
+        "d"(b[2]), "d"(b[3]));
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   int src_size = valid ? 8 : 0;  // 0 => zero-fill
@@ -1008,6 +1020,7 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // a8 <= 64, r8 <= 16) or shared memory.  Outputs: a warp's 8 x r block is
 // contiguous in `out`, staged per warp (r <= 32) and written with coalesced
 // stores.  Optional per-(tile, warp) input sums of squares.
+constexpr int kProjStages = 8;
 template <bool REGW, int TC>
 __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
   static_assert(TC == 64 || TC == 32, "tile width");
@@ -1016,7 +1029,7 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
   constexpr int KS = 8 / CW;   // k-split ways (1 or 2)
   constexpr int BOX = 16 * TC; // doubles per box
   extern __shared__ __align__(1024) double smem_raw[];
-  __shared__ __align__(8) uint64_t full[kMaxStages + 2];
+  __shared__ __align__(8) uint64_t full[kProjStages];
   double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -1033,13 +1046,19 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
   const int cw = warp % CW, kh = warp / CW;
   if (!REGW && p.frag_smem)
     for (int i = threadIdx.x; i < nfr; i += kThreads) Wfs[i] = p.WTf[i];
-  double wreg[REGW ? 32 : 1];
+  // REGW: this warp's W^T fragments in registers: MRW m-blocks x KW k-steps
+  // (TC = 64: all 16 k-steps of a8 <= 64, r8 <= 16; TC = 32: the 8 k-steps of
+  // its box parity, r8 <= 32).  Local k-step jj <-> kb = 4 (KS (jj / 4) + kh) + jj % 4.
+  constexpr int MRW = KS == 1 ? 2 : 4, KW = 16 / KS;
+  double wreg[REGW ? MRW * KW : 1];
   if (REGW) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < MRW; ++u)
 #pragma unroll
-      for (int kb = 0; kb < 16; ++kb)
-        wreg[u * 16 + kb] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
+      for (int jj = 0; jj < KW; ++jj) {
+        const int kb = 4 * (KS * (jj >> 2) + kh) + (jj & 3);
+        wreg[u * KW + jj] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
+      }
   }
   const long long grid = gridDim.x;
   if (threadIdx.x == 0) {
@@ -1084,19 +1103,24 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
     double* o1 = o0 + p.r;
     double ss = 0.0;
     if (REGW) {
-      double q[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
-      double bv[16];
+      double q[MRW][2][2];
 #pragma unroll
-      for (int kb = 0; kb < 16; ++kb)
-        bv[kb] = (kb < KA && ((kb >> 2) % KS) == kh) ? T[(kb >> 2) * BOX + osw[kb & 3]] : 0.0;
+      for (int u = 0; u < MRW; ++u) q[u][0][0] = q[u][0][1] = q[u][1][0] = q[u][1][1] = 0.0;
+      double bv[KW];
 #pragma unroll
-      for (int kb = 0; kb < 16; ++kb) {
-        ss = fma(bv[kb], bv[kb], ss);
-        dmma(q[0][kb & 1][0], q[0][kb & 1][1], wreg[kb], bv[kb]);
-        if (MR > 1) dmma(q[1][kb & 1][0], q[1][kb & 1][1], wreg[16 + kb], bv[kb]);
+      for (int jj = 0; jj < KW; ++jj) {
+        const int kb = 4 * (KS * (jj >> 2) + kh) + (jj & 3);
+        bv[jj] = kb < KA ? T[(kb >> 2) * BOX + osw[kb & 3]] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int jj = 0; jj < KW; ++jj) {
+        ss = fma(bv[jj], bv[jj], ss);
+#pragma unroll
+        for (int u = 0; u < MRW; ++u)
+          if (u < MR) dmma(q[u][jj & 1][0], q[u][jj & 1][1], wreg[u * KW + jj], bv[jj]);
+      }
+#pragma unroll
+      for (int u = 0; u < MRW; ++u) {
         const int row = u * 8 + g;
         if (u < MR && row < p.r) {
           if (staged) {
@@ -1171,6 +1195,391 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
     // per-(64-column tile, 8-column group) sums: the layout of the TC = 64 kernels
     if (p.tsumsq && kh == 0 && lane == 0)
       p.tsumsq[((tile * TC) >> 6) * kConsumerWarps + (((tile * TC) & 63) >> 3) + cw] = KS > 1 ? ss + red_ss[cw] : ss;
+  }
+}
+
+// Projection out (r x L) = W^T X for short operands (a8 <= 64) with
+// 16 < r8 <= 32: 64-column tensor-map tiles, warp w = (column group cw = w % 4
+// of 16 columns = two DMMA n-blocks, k half kh = w / 4 = box parity).  Each
+// warp keeps the W^T fragments of its 8 k-steps for all MR <= 4 m-blocks in
+// registers (32 doubles) and reuses every fragment for both n-blocks; the two
+// k halves are summed through shared memory.  Same ring / barrier protocol and
+// output layout as k_project_tma.
+__global__ void __launch_bounds__(kThreads) k_project_w2(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  constexpr int TC = 64, BOX = 16 * TC;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kProjStages];
+  __shared__ double red_ss[4];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nst = p.nst;
+  const int nbox = (p.src.a + 15) >> 4;
+  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
+  const int stage = nbox * BOX;
+  double* stg_all = smem + nst * stage;  // 8 warps x 16 columns x r (r <= 32)
+  double* stg = stg_all + warp * 16 * 32;
+  const int cw = warp & 3, kh = warp >> 2;
+  double wreg[4 * 8];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int kb = 4 * (2 * (jj >> 2) + kh) + (jj & 3);
+      wreg[u * 8 + jj] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
+    }
+  const long long grid = gridDim.x;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm);
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < nst - 1; ++s) {
+      const long long tl = blockIdx.x + s * grid;
+      if (tl < p.n_tiles) {
+        mbar_expect_tx(&full[s], (unsigned)nbox * BOX * 8u);
+        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + s * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[s]);
+      }
+    }
+  }
+  __syncthreads();
+  // swizzled B-fragment offsets for the two n-blocks (columns 16cw + 8n + g)
+  int osw[2][4];
+#pragma unroll
+  for (int n = 0; n < 2; ++n) {
+    const int c = 16 * cw + 8 * n + g;
+    const int hsw = (t >> 1) ^ (c & 7);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) osw[n][m] = c * 16 + (t & 1) + (((m << 1) ^ hsw) << 1);
+  }
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid, ++it) {
+    const int st = it % nst;
+    mbar_wait(&full[st], (unsigned)((it / nst) & 1));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long tl = tile + (nst - 1) * grid;
+      if (tl < p.n_tiles) {
+        const int sn = (it + nst - 1) % nst;
+        mbar_expect_tx(&full[sn], (unsigned)nbox * BOX * 8u);
+        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + sn * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[sn]);
+      }
+    }
+    const double* T = smem + st * stage;
+    double q[4][2][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u][0][0] = q[u][0][1] = q[u][1][0] = q[u][1][1] = 0.0;
+    double ss = 0.0;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {  // 4 k-steps (one box) at a time
+      const int b = 2 * half + kh;
+      double bv[2][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool ok = 4 * b + j < KA;
+#pragma unroll
+        for (int n = 0; n < 2; ++n) bv[n][j] = ok ? T[b * BOX + osw[n][j]] : 0.0;
+      }
+      if (p.tsumsq) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ss = fma(bv[0][j], bv[0][j], fma(bv[1][j], bv[1][j], ss));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < MR) {
+            const double w = wreg[u * 8 + 4 * half + j];
+            dmma(q[u][0][0], q[u][0][1], w, bv[0][j]);
+            dmma(q[u][1][0], q[u][1][1], w, bv[1][j]);
+          }
+    }
+    // stage this warp's 16 x r partial block (column-major, ld r)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int row = u * 8 + g;
+      if (u < MR && row < p.r)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          stg[row + p.r * (8 * n + 2 * t)] = q[u][n][0];
+          stg[row + p.r * (8 * n + 2 * t + 1)] = q[u][n][1];
+        }
+    }
+    if (p.tsumsq) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (kh == 1 && lane == 0) red_ss[cw] = ss;
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
+    if (kh == 0) {
+      const double* oth = stg_all + (warp + 4) * 16 * 32;
+      const long long colw = tile * TC + 16 * cw;
+      const int nval = (int)max(0LL, min(16LL, p.src.L - colw));
+      double* dst = p.out + colw * p.r;
+      const int n = nval * p.r;
+      for (int e = lane; e < n; e += 32) dst[e] = stg[e] + oth[e];
+      if (p.tsumsq && lane == 0) {
+        // two 8-column groups of the TC = 64 sums layout
+        const double tot = ss + red_ss[cw];
+        p.tsumsq[tile * kConsumerWarps + 2 * cw] = tot;
+        p.tsumsq[tile * kConsumerWarps + 2 * cw + 1] = 0.0;
+      }
+    }
+  }
+}
+
+// Projection out (r x L) = W^T X with mma.m16n8k16 on the transposed tile:
+// out^T (16 columns x 8 r-rows) += X^T (16 columns x 16 rows of a) W (16 x 8),
+// so r is padded to 8 only and one instruction does 4096 FMA.  64-column
+// tensor-map tiles (128-byte swizzle; the A fragment is the conflict-free
+// "4 rows x 8 columns" pattern twice); warp w: columns 16 (w % 4) .. +16,
+// boxes of parity w / 4 (the two k halves are summed through shared memory).
+// W fragments are the m8n8k4 U^T fragments (k_make_frags): the B fragment of
+// (box b, n-block nb) is UTf[(nb KA + 4b + i) 32 + lane], i = 0..3, staged in
+// shared memory.  r <= 32 (NB <= 4 n-blocks).  Output staged per warp (16 x r
+// block, contiguous in out) and stored coalesced; optional per-(tile, 8-column
+// group) input sums of squares.
+__global__ void __launch_bounds__(kThreads) k_project_m16(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  constexpr int TC = 64, BOX = 16 * TC;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kProjStages];
+  __shared__ double red_ss[4];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nst = p.nst;
+  const int nks = (p.src.a + 15) >> 4;
+  const int KA = p.a8 >> 2, NB = p.r8 >> 3;
+  const int stage = nks * BOX;
+  double* Wfs = smem + nst * stage;
+  const int nfr = NB * KA * 32;
+  double* stg_all = Wfs + nfr;  // 8 warps x 16 columns x r (r <= 32)
+  double* stg = stg_all + warp * 16 * 32;
+  const int cw = warp & 3, kh = warp >> 2;
+  for (int i = threadIdx.x; i < nfr; i += kThreads) Wfs[i] = p.WTf[i];
+  const long long grid = gridDim.x;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm);
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < nst - 1; ++s) {
+      const long long tl = blockIdx.x + s * grid;
+      if (tl < p.n_tiles) {
+        mbar_expect_tx(&full[s], (unsigned)nks * BOX * 8u);
+        for (int b = 0; b < nks; ++b) tma_load_2d(smem + s * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[s]);
+      }
+    }
+  }
+  __syncthreads();
+  // A element i of a box: row 4(i>>1) + t, column 16cw + g + 8(i&1)
+  int osw[8];
+  {
+    const int hsw = (t >> 1) ^ g;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      osw[i] = (16 * cw + g + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
+  }
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid, ++it) {
+    const int st = it % nst;
+    mbar_wait(&full[st], (unsigned)((it / nst) & 1));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long tl = tile + (nst - 1) * grid;
+      if (tl < p.n_tiles) {
+        const int sn = (it + nst - 1) % nst;
+        mbar_expect_tx(&full[sn], (unsigned)nks * BOX * 8u);
+        for (int b = 0; b < nks; ++b) tma_load_2d(smem + sn * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[sn]);
+      }
+    }
+    const double* T = smem + st * stage;
+    double acc[4][4];
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0;
+    double ss = 0.0;
+    for (int b = kh; b < nks; b += 2) {
+      double av[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = T[b * BOX + osw[i]];
+      if (p.tsumsq) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss = fma(av[i], av[i], ss);
+      }
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+        if (nb < NB) {
+          double bw[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int kb = 4 * b + i;
+            bw[i] = kb < KA ? Wfs[(nb * KA + kb) * 32 + lane] : 0.0;
+          }
+          dmma16(acc[nb], av, bw);
+        }
+    }
+    // c[i] = out^T[column g + 8(i>>1)][row 8nb + 2t + (i&1)]  ->  stg[row + r * column]
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+      if (nb < NB)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = 8 * nb + 2 * t + (i & 1);
+          if (row < p.r) stg[row + p.r * (g + 8 * (i >> 1))] = acc[nb][i];
+        }
+    if (p.tsumsq) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (kh == 1 && lane == 0) red_ss[cw] = ss;
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
+    if (kh == 0) {
+      const double* oth = stg_all + (warp + 4) * 16 * 32;
+      const long long colw = tile * TC + 16 * cw;
+      const int nval = (int)max(0LL, min(16LL, p.src.L - colw));
+      double* dst = p.out + colw * p.r;
+      const int n = nval * p.r;
+      for (int e = lane; e < n; e += 32) dst[e] = stg[e] + oth[e];
+      if (p.tsumsq && lane == 0) {
+        p.tsumsq[tile * kConsumerWarps + 2 * cw] = ss + red_ss[cw];
+        p.tsumsq[tile * kConsumerWarps + 2 * cw + 1] = 0.0;
+      }
+    }
+  }
+}
+
+// W (a x r, ld) -> m16n8k16 B fragments for the k-step-major projection
+// kernels: Wm[((b NB + nb) 4 + i) 32 + lane] = W[16b + t + 4i][8nb + g]
+// (lane = 4g + t), zero outside W; b < nks = ceil(a/16), nb < NB = r8/8.
+__global__ void k_make_frags16(const double* __restrict__ W, int a, int r, int ld, int nks, int NB,
+                               double* __restrict__ Wm) {
+  const long long n = (long long)nks * NB * 128;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(e & 31), i = (int)((e >> 5) & 3);
+    const long long f = e >> 7;
+    const int nb = (int)(f % NB), b = (int)(f / NB);
+    const int row = 16 * b + (lane & 3) + 4 * i, col = 8 * nb + (lane >> 2);
+    Wm[e] = (row < a && col < r) ? W[row + (long long)ld * col] : 0.0;
+  }
+}
+
+// Warp-specialised m16n8k16 projection (out^T tile = X^T W): warp NCW is the
+// TMA producer (lane 0; full / empty mbarriers per stage), consumer warp w
+// owns the 16 columns 16w..16w+15 of every TC = 16 NCW column tile and all
+// k-steps, so no block barrier and no cross-warp reduction sits on the
+// per-tile path.  W fragments (k_make_frags16 layout, NB = r8/8 <= 4 n-blocks,
+// compile time) are read from shared memory with immediate offsets.  A
+// fragment i of box b: row 4(i>>1) + t, column 16w + g + 8(i&1) (the
+// conflict-free "4 rows x 8 columns" pattern twice under the 128-byte
+// swizzle).  Output: the warp's 16 x r block is contiguous in out, staged in
+// shared memory and stored coalesced; optional per-(64-column tile, 8-column
+// group) input sums of squares.
+template <int NCW, int NB>
+__global__ void __launch_bounds__((NCW + 1) * 32) k_project_ws16(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  constexpr int TC = 16 * NCW, BOX = 16 * TC;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kProjStages], empty[kProjStages];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nst = p.nst;
+  const int nks = (p.src.a + 15) >> 4;
+  const int stage = nks * BOX;
+  double* Wfs = smem + nst * stage;
+  const int nfr = nks * NB * 128;
+  double* stg = Wfs + nfr + warp * 16 * 32;
+  for (int i = threadIdx.x; i < nfr; i += blockDim.x) Wfs[i] = p.WTf[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long grid = gridDim.x;
+  if (warp == NCW) {  // ---- producer ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      int it = 0;
+      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid, ++it) {
+        const int s = it % nst;
+        if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
+        mbar_expect_tx(&full[s], (unsigned)nks * BOX * 8u);
+        for (int b = 0; b < nks; ++b) tma_load_2d(smem + s * stage + b * BOX, &tm, 16 * b, (int)(tile * TC), &full[s]);
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  int osw[8];
+  {
+    const int hsw = (t >> 1) ^ g;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) osw[i] = (16 * warp + g + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
+  }
+  const double* wl = Wfs + lane;
+  const bool want_ss = p.tsumsq != nullptr;
+  int st = 0;
+  unsigned ph = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+    mbar_wait(&full[st], ph);
+    const double* ab = smem + st * stage;
+    const double* wb = wl;
+    double acc[NB][4];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0;
+    double ss0 = 0.0, ss1 = 0.0;
+    for (int b = 0; b < nks; ++b, ab += BOX, wb += NB * 128) {
+      double av[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = ab[osw[i]];
+      if (want_ss) {
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          ss0 = fma(av[i], av[i], ss0);
+          ss1 = fma(av[i + 1], av[i + 1], ss1);
+        }
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        double bw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bw[i] = wb[(nb * 4 + i) * 32];
+        dmma16(acc[nb], av, bw);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+    if (++st == nst) {
+      st = 0;
+      ph ^= 1u;
+    }
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 8 * nb + 2 * t + (i & 1);
+        if (row < p.r) stg[row + p.r * (g + 8 * (i >> 1))] = acc[nb][i];
+      }
+    __syncwarp();
+    const long long colw = tile * TC + 16 * warp;
+    const int nval = (int)max(0LL, min(16LL, p.src.L - colw));
+    double* dst = p.out + colw * p.r;
+    const int n = nval * p.r;
+    for (int e = lane; e < n; e += 32) dst[e] = stg[e];
+    if (want_ss) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ss0 += __shfl_xor_sync(0xffffffffu, ss0, o);
+        ss1 += __shfl_xor_sync(0xffffffffu, ss1, o);
+      }
+      if (lane == 0) {
+        const long long c64 = colw >> 6;
+        const int grp = (int)((colw & 63) >> 3);
+        p.tsumsq[c64 * kConsumerWarps + grp] = ss0;
+        p.tsumsq[c64 * kConsumerWarps + grp + 1] = ss1;
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -2,6 +2,7 @@
 // operand: ring vs. double-buffered TMA, r = 1 / 16, with/without norms.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -I paper_2211_12487_b200/csrc tools/probe/proj_probe.cu
 #include <cstdio>
+#include <cstdlib>
 #include "ttg_eig.cuh"
 #include "ttg_kernels.cuh"
 
@@ -29,7 +30,32 @@ CUtensorMap make_map(const double* X, int a, long long L, int bc = 64) {
 }
 template <class K>
 void timetma(const char* name, K kern, const CUtensorMap& tm, ttg::ProjArgs p, size_t smem, double bytes,
-             int threads = ttg::kThreads) {
+             int threads = ttg::kThreads);
+void ws16_sweep(const double* X, int a, long long L, const double* W, double* out, int r) {
+  ttg::ProjArgs p{};
+  p.src = ttg::TileSrc{X, a, L, nullptr, 1};
+  p.a8 = a; p.ldt = ttg::smem_ld(a); p.WTf = W; p.r = r; p.r8 = (r + 7) / 8 * 8; p.out = out; p.tsumsq = nullptr;
+  const double bytes = 8.0 * (a + r) * L;
+  const int nks = (a + 15) / 16, NB = p.r8 / 8;
+  char nm[96];
+  for (int ncw : {4, 8}) {
+    const int tc = 16 * ncw;
+    const CUtensorMap tm = make_map(X, a, L, tc);
+    p.n_tiles = (L + tc - 1) / tc;
+    for (int nst : {2, 3, 4, 6}) {
+      p.nst = nst;
+      const size_t smem = 1024 + (size_t)nst * nks * 16 * tc * 8 + nks * NB * 128 * 8 + ncw * 16 * 32 * 8;
+      if (smem > 227 * 1024) continue;
+      std::snprintf(nm, sizeof nm, "ws16 a=%d r=%d ncw=%d", a, r, ncw);
+#define RUNWS(NC, N) timetma(nm, ttg::k_project_ws16<NC, N>, tm, p, smem, bytes, (NC + 1) * 32)
+      if (ncw == 4) { if (NB == 1) RUNWS(4, 1); else if (NB == 2) RUNWS(4, 2); else if (NB == 3) RUNWS(4, 3); else RUNWS(4, 4); }
+      else { if (NB == 1) RUNWS(8, 1); else if (NB == 2) RUNWS(8, 2); else if (NB == 3) RUNWS(8, 3); else RUNWS(8, 4); }
+    }
+  }
+}
+template <class K>
+void timetma(const char* name, K kern, const CUtensorMap& tm, ttg::ProjArgs p, size_t smem, double bytes,
+             int threads) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
@@ -90,6 +116,41 @@ int main() {
   fill<<<16, 256>>>(W, 128 * 64);
   cudaMalloc(&out, sizeof(double) * 32 * L);
   cudaMalloc(&tsq, sizeof(double) * 8 * (L / 64));
+  if (getenv("PROBE_WS16")) {
+    ws16_sweep(X, 64, L, W, out, 17);
+    ws16_sweep(X, 64, L, W, out, 16);
+    ws16_sweep(X, 64, L, W, out, 1);
+    ws16_sweep(X, 144, (1ll << 32) / (8 * 144), W, out, 18);
+    ws16_sweep(X, 128, (1ll << 32) / (8 * 128), W, out, 16);
+    return 0;
+  }
+  if (getenv("PROBE_R17")) {
+    ttg::ProjArgs p{};
+    p.src = ttg::TileSrc{X, a, L, nullptr, 1};
+    p.a8 = 64; p.ldt = ttg::smem_ld(64); p.WTf = W; p.r = 17; p.r8 = 24; p.out = out; p.tsumsq = nullptr;
+    const double bytes = 8.0 * (a + 17) * L;
+    const size_t stg = sizeof(double) * 8 * 8 * 32;
+    const CUtensorMap tm64 = make_map(X, a, L, 64), tm32 = make_map(X, a, L, 32);
+    for (int nst : {2, 3, 4, 6, 8}) {
+      p.nst = nst; p.n_tiles = L / 32; p.frag_smem = 0;
+      timetma("r17 TC32 REGW", ttg::k_project_tma<true, 32>, tm32, p, 1024 + nst * 16384 + stg, bytes);
+      p.n_tiles = L / 64;
+      if (nst <= 4) timetma("r17 TC64 Wglobal", ttg::k_project_tma<false, 64>, tm64, p, 1024 + nst * 32768 + stg, bytes);
+      if (nst <= 4) timetma("r17 W2", ttg::k_project_w2, tm64, p, 1024 + nst * 32768 + 8 * 16 * 32 * 8, bytes);
+      if (nst <= 4) timetma("r17 M16", ttg::k_project_m16, tm64, p, 1024 + nst * 32768 + 8 * 16 * 32 * 8 + 3 * 16 * 32 * 8, bytes);
+      p.frag_smem = 1;
+      if (nst <= 4) timetma("r17 TC64 Wsmem", ttg::k_project_tma<false, 64>, tm64, p, 1024 + nst * 32768 + stg + 3 * 16 * 32 * 8, bytes);
+    }
+    p.r = 16; p.r8 = 16; p.frag_smem = 0;
+    for (int nst : {2, 3, 4, 6}) {
+      p.nst = nst; p.n_tiles = L / 32;
+      timetma("r16 TC32 REGW", ttg::k_project_tma<true, 32>, tm32, p, 1024 + nst * 16384 + stg, 8.0 * (a + 16) * L);
+      p.n_tiles = L / 64;
+      if (nst <= 4) timetma("r16 TC64 REGW", ttg::k_project_tma<true, 64>, tm64, p, 1024 + nst * 32768 + stg, 8.0 * (a + 16) * L);
+      if (nst <= 4) timetma("r16 M16", ttg::k_project_m16, tm64, p, 1024 + nst * 32768 + 8 * 16 * 32 * 8 + 2 * 16 * 32 * 8, 8.0 * (a + 16) * L);
+    }
+    return 0;
+  }
   for (int r : {1, 16}) {
     for (int norms = 0; norms < 2; ++norms) {
       ttg::ProjArgs p{};
