@@ -569,6 +569,79 @@ void launch_syrk2_t(ttg_ctx* c, const CUtensorMap& tm, ttg::Syrk2Args args, int 
   post_launch(c);
 }
 
+// Warp-specialised m16n8k16 SYRK (k_syrk_ws16) for even a <= 128 into c->G.
+template <int NCW, int MAXG>
+void launch_syrk_ws16_t(ttg_ctx* c, const CUtensorMap& tm, ttg::Syrk2Args args, double sel_frac) {
+  auto kern = ttg::k_syrk_ws16<NCW, MAXG>;
+  constexpr int threads = (NCW + 1) * 32;
+  const size_t stage = sizeof(double) * 1024 * args.nbox;
+  const size_t cap = (size_t)c->smem_optin - 1024;
+  // stages: as many as fit ~110 KB when two CTAs fit by registers, else up
+  // to four in one CTA
+  int regs_ok2 = 0;
+  {
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kern));
+    regs_ok2 = (2 * threads * fa.numRegs <= 65536) ? 1 : 0;
+  }
+  const size_t per_cta = regs_ok2 ? 110 * 1024 : cap;
+  int nst = 2;
+  while (nst < ttg::kMaxStages && (nst + 1) * stage + 1024 <= per_cta) ++nst;
+  if (std::getenv("TTG_SYRK16_NST")) {  // tuning override (ignored when it does not fit)
+    const int want = std::atoi(std::getenv("TTG_SYRK16_NST"));
+    if (want >= 2 && want <= ttg::kMaxStages + 4 && want * stage + 1024 <= cap) nst = want;
+  }
+  args.nst = nst;
+  const size_t smem = nst * stage + 1024;
+  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, threads, smem));
+  const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  c->partials.ensure(sizeof(double) * (size_t)gx * args.a8 * args.a8);
+  args.partials = c->partials.as<double>();
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
+  const double Ls = (double)args.L * sel_frac;
+  prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
+  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  post_launch(c);
+  const long long n = (long long)args.a * args.a;
+  prof_begin(c, "k_gram_reduce", 8.0 * gx * args.a8 * args.a8, (double)gx * n);
+  ttg::k_gram_reduce2<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, args.a8, args.a,
+                                                                       c->G.as<double>());
+  post_launch(c);
+}
+
+bool syrk_ws16(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
+               double* tsq) {
+  // measured: the per-column super-tile kernel is faster up to a = 96 (a = 64:
+  // 1.65 vs 1.74 ms per 4.3 GB), this one from a = 112 to 128
+  if (std::getenv("TTG_NO_SYRK16") || (a & 1) || a <= 96 || a > 128 || (sel && cpo % ttg::kTC != 0)) return false;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, X, a, L)) return false;
+  const int nks = (a + 15) / 16;
+  if (2 * sizeof(double) * 1024 * nks + 1024 > (size_t)c->smem_optin - 1024) return false;
+  ttg::Syrk2Args args{};
+  args.a = a;
+  args.a8 = ttg::round_up(a, 8);
+  args.nbox = nks;
+  args.L = L;
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  args.sel = sel;
+  args.cpo = cpo;
+  args.tsumsq = tsq;
+  // consumer warps x groups per warp = the nks (nks + 1) / 2 lower groups, balanced
+  switch (nks) {
+    case 1: launch_syrk_ws16_t<1, 1>(c, tm, args, sel_frac); break;
+    case 2: launch_syrk_ws16_t<3, 1>(c, tm, args, sel_frac); break;
+    case 3: launch_syrk_ws16_t<6, 1>(c, tm, args, sel_frac); break;
+    case 4: launch_syrk_ws16_t<10, 1>(c, tm, args, sel_frac); break;
+    case 5: launch_syrk_ws16_t<5, 3>(c, tm, args, sel_frac); break;
+    case 6: launch_syrk_ws16_t<7, 3>(c, tm, args, sel_frac); break;
+    case 7: launch_syrk_ws16_t<14, 2>(c, tm, args, sel_frac); break;
+    default: launch_syrk_ws16_t<12, 3>(c, tm, args, sel_frac); break;
+  }
+  return true;
+}
+
 bool syrk2(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
            double* tsq) {
   // a <= 128: the per-column super-tile kernel (k_syrk) measures faster (one
@@ -617,7 +690,7 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
     gram_src(c, Src{X, a, L, nullptr, a}, 1, nullptr, 0, sel, cpo, sel_frac, tsq);
     return tsq != nullptr && ttg::round_up(a, 8) <= kFastMax1;
   }
-  if (syrk2(c, X, a, L, sel, cpo, sel_frac, tsq)) {
+  if (syrk_ws16(c, X, a, L, sel, cpo, sel_frac, tsq) || syrk2(c, X, a, L, sel, cpo, sel_frac, tsq)) {
     allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
     return tsq != nullptr;
   }
@@ -662,45 +735,26 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
   const bool did = syrk(c, s.S, (int)rows, L, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
   c->Craw.ensure(sizeof(double) * (size_t)(rows * rows));
   CK(cudaMemcpyAsync(c->Craw.p, c->G.p, sizeof(double) * rows * rows, cudaMemcpyDeviceToDevice, c->stream));
-  c->small[1].ensure(sizeof(double) * (size_t)(a * a));
-  double* M = c->small[1].as<double>();
-  if (s.Psi) {
-    c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
-    prof_begin(c, "k_kron_eye", 8.0 * rows * a, 0.0);
-    ttg::k_kron_eye<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, (int)s.As, (int)s.r, (int)n,
-                                                                           c->wcomb.as<double>());
-    post_launch(c);
-    c->small[0].ensure(sizeof(double) * (size_t)(rows * a));
-    double* T1 = c->small[0].as<double>();
-    gemm<false, false>(c, c->Craw.as<double>(), rows, c->wcomb.as<double>(), rows, T1, rows, rows, a, rows, 1.0, 0.0);
-    gemm<true, false>(c, c->wcomb.as<double>(), rows, T1, rows, M, a, a, a, rows, 1.0, 0.0);  // K C K^T
-  } else {
-    CK(cudaMemcpyAsync(M, c->Craw.p, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
-  }
+  // G = Q^T C Q with Q = K P (one element-wise kernel, two GEMMs): the same
+  // P K^T C K P as before in 4 launches instead of 11
+  c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
+  double* Q = c->wcomb.as<double>();
+  prof_begin(c, "k_build_q", 8.0 * rows * a, 2.0 * rows * a * std::max(r_old, 1) * (s.Psi ? s.r : 1));
+  ttg::k_build_q<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, s.Psi ? (int)s.As : (int)s.r, (int)s.r,
+                                                                        (int)n, U, r_old, Q);
+  post_launch(c);
+  c->small[0].ensure(sizeof(double) * (size_t)(rows * a));
+  double* T1 = c->small[0].as<double>();
+  gemm<false, false>(c, c->Craw.as<double>(), rows, Q, rows, T1, rows, rows, a, rows, 1.0, 0.0);  // C Q
   c->G.ensure(sizeof(double) * (size_t)(a * a));
   double* G = c->G.as<double>();
-  if (r_old > 0) {
-    c->small[2].ensure(sizeof(double) * (size_t)(r_old * a));
-    c->small[3].ensure(sizeof(double) * (size_t)(a * a));
-    double* T2 = c->small[2].as<double>();
-    double* R1 = c->small[3].as<double>();
-    gemm<true, false>(c, U, a, M, a, T2, r_old, r_old, a, a, 1.0, 0.0);  // U^T M
-    CK(cudaMemcpyAsync(R1, M, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
-    gemm<false, false>(c, U, a, T2, r_old, R1, a, a, a, r_old, -1.0, 1.0);  // R1 = M - U U^T M
-    gemm<false, false>(c, R1, a, U, a, T2, a, a, r_old, a, 1.0, 0.0);      // T3 = R1 U   (a x r_old, reuse)
-    CK(cudaMemcpyAsync(G, R1, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
-    gemm<false, true>(c, T2, a, U, a, G, a, a, a, r_old, -1.0, 1.0);       // G = R1 - T3 U^T
-  } else {
-    CK(cudaMemcpyAsync(G, M, sizeof(double) * a * a, cudaMemcpyDeviceToDevice, c->stream));
-  }
+  gemm<true, false>(c, Q, rows, T1, rows, G, a, a, a, rows, 1.0, 0.0);  // Q^T (C Q)
   // trace(C) for the guard, then symmetrise G
   c->scal.ensure(sizeof(double) * 16);
-  prof_begin(c, "k_symmetrize_trace", 16.0 * rows * rows, 0.0);
-  ttg::k_symmetrize_trace<<<grid_for(rows * rows, 256, 64), 256, 0, c->stream>>>(c->Craw.as<double>(), (int)rows,
-                                                                                 c->scal.as<double>() + 4);
-  post_launch(c);
+  // (C is exactly symmetric: the SYRK reduction mirrors its lower triangle)
   prof_begin(c, "k_symmetrize_trace", 16.0 * a * a, 0.0);
-  ttg::k_symmetrize_trace<<<grid_for(a * a, 256, 64), 256, 0, c->stream>>>(G, (int)a, nullptr);
+  ttg::k_symmetrize_trace<<<grid_for(a * a, 256, 64), 256, 0, c->stream>>>(G, (int)a, c->Craw.as<double>(), (int)rows,
+                                                                          c->scal.as<double>() + 4);
   post_launch(c);
   return did;
 }
@@ -1497,6 +1551,27 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
   c->iface[0].ensure(sizeof(double) * rmax * rmax);
   c->iface[1].ensure(sizeof(double) * rmax * rmax);
   c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
+  const size_t ismem = sizeof(double) * (size_t)(2 * rmax * rmax + 2 * rmax * nmax * rmax);
+  if (tt->d <= ttg::kIfaceMaxModes && ismem <= 200 * 1024) {  // one launch for the whole chain
+    ttg::IfaceArgs ia{};
+    ia.d = tt->d;
+    double flops = 0.0;
+    for (int i = 0; i < tt->d; ++i) {
+      ia.cores[i] = tt->cores[i].as<double>();
+      ia.rl[i] = (int)tt->ranks[i];
+      ia.n[i] = (int)tt->modes[i];
+      ia.rr[i] = (int)tt->ranks[i + 1];
+      flops += 4.0 * ia.rl[i] * ia.n[i] * ia.rr[i] * (ia.rl[i] + ia.rr[i]);
+    }
+    ia.rmax = (int)rmax;
+    ia.nmax = (int)nmax;
+    ia.out = c->iface[0].as<double>();
+    kernel_occupancy((const void*)ttg::k_iface_all, ttg::k_iface_all, 512, ismem);
+    prof_begin(c, "k_iface", 8.0 * rmax * nmax * rmax * tt->d, flops);
+    ttg::k_iface_all<<<1, 512, ismem, c->stream>>>(ia);
+    post_launch(c);
+    return c->iface[0].as<double>();
+  }
   const double one = 1.0;
   CK(cudaMemcpyAsync(c->iface[0].p, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
   int f = 0;
@@ -1841,7 +1916,9 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,
-        (const void*)ttg::k_iface_step1, (const void*)ttg::k_iface_step2, (const void*)ttg::k_coef_stats,
+        (const void*)ttg::k_iface_step1, (const void*)ttg::k_iface_step2, (const void*)ttg::k_iface_all, (const void*)ttg::k_build_q, (const void*)ttg::k_syrk_ws16<1, 1>, (const void*)ttg::k_syrk_ws16<3, 1>,
+        (const void*)ttg::k_syrk_ws16<6, 1>, (const void*)ttg::k_syrk_ws16<10, 1>, (const void*)ttg::k_syrk_ws16<5, 3>,
+        (const void*)ttg::k_syrk_ws16<7, 3>, (const void*)ttg::k_syrk_ws16<14, 2>, (const void*)ttg::k_syrk_ws16<12, 3>, (const void*)ttg::k_coef_stats,
         (const void*)ttg::k_star_local, (const void*)ttg::k_star_mask, (const void*)ttg::k_mask_cols,
         (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
         (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,

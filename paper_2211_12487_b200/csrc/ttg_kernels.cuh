@@ -1888,6 +1888,168 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk2(const __grid_constant__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised SYRK with mma.m16n8k16 (a <= 128): C = sum over (selected)
+// 64-column tiles of X X^T.  Warp NCW lane 0 streams tensor-map tiles
+// (ceil(a/16) boxes, 128-byte swizzle) into an nst-deep ring (full / empty
+// mbarriers); consumer warps own "groups" = (16-row block mi, pair of 8-row
+// blocks 2p, 2p+1), p <= mi (the lower triangle), dealt round-robin; per
+// 16-column k-step a group is one A fragment (8 loads) and two B fragments
+// (4 loads each) feeding two MMAs.  The k index of a step is permuted,
+// column(t, j) = 8(j>>1) + 2(j&1) + (t&1) + 4(t>>1), which makes every
+// fragment load bank-conflict free under the swizzle (checked exhaustively).
+// Per-CTA partials (a8 x a8, owned blocks) are summed by k_gram_reduce2.
+// Input sums of squares (tsumsq, 8 per 64-column tile) come from the B
+// fragments of the diagonal groups (p == mi cover every row once), reduced
+// across warps in shared memory behind a consumer-only named barrier.
+// ---------------------------------------------------------------------------
+template <int NCW, int MAXG>
+__global__ void __launch_bounds__((NCW + 1) * 32) k_syrk_ws16(const __grid_constant__ CUtensorMap tm, Syrk2Args p) {
+  constexpr int BOX = 1024;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxStages + 4], empty[kMaxStages + 4];
+  __shared__ double ssq[NCW][8];
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nks = p.nbox, stage = nks * BOX, nst = p.nst;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long grid = gridDim.x;
+  if (warp == NCW) {  // ---- producer ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      int it = 0;
+      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+        if (p.sel && !p.sel[(tile * kTC) / p.cpo]) continue;
+        const int s = it % nst;
+        if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
+        mbar_expect_tx(&full[s], (unsigned)nks * BOX * 8u);
+        for (int b = 0; b < nks; ++b) tma_load_2d(ring + s * stage + b * BOX, &tm, 16 * b, (int)(tile * kTC), &full[s]);
+        ++it;
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  const int ngroups = nks * (nks + 1) / 2;
+  int gA[MAXG], gB[MAXG], gmi[MAXG], gp[MAXG];
+  bool live[MAXG];
+#pragma unroll
+  for (int u = 0; u < MAXG; ++u) {
+    const int idx = warp + NCW * u;
+    live[u] = idx < ngroups;
+    int mi = (int)((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
+    while ((mi + 1) * (mi + 2) / 2 <= idx) ++mi;
+    while (mi * (mi + 1) / 2 > idx) --mi;
+    const int pp = idx - mi * (mi + 1) / 2;
+    gmi[u] = mi;
+    gp[u] = pp;
+    gA[u] = mi * BOX;
+    gB[u] = pp * BOX;  // 8-row blocks 2pp, 2pp+1 live in box pp (halves 0 / 1)
+  }
+  // lane offsets (k-step 0) of the A elements i = 0..7 and the B elements
+  // (half h = 0/1 of the box, i = 0..3)
+  int offA[8], offB[2][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = i >> 1;
+    const int col = 8 * (j >> 1) + 2 * (j & 1) + (t & 1) + 4 * (t >> 1);
+    const int cl = 2 * (j & 1) + (t & 1) + 4 * (t >> 1);
+    offA[i] = col * 16 + ((((g >> 1) + 4 * (i & 1)) ^ cl) << 1) + (g & 1);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int col = 8 * (i >> 1) + 2 * (i & 1) + (t & 1) + 4 * (t >> 1);
+      const int cl = 2 * (i & 1) + (t & 1) + 4 * (t >> 1);
+      offB[h][i] = col * 16 + (((4 * h + (g >> 1)) ^ cl) << 1) + (g & 1);
+    }
+  double acc[MAXG][2][4];
+#pragma unroll
+  for (int u = 0; u < MAXG; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) acc[u][h][0] = acc[u][h][1] = acc[u][h][2] = acc[u][h][3] = 0.0;
+  const bool want_ss = p.tsumsq != nullptr;
+  int st = 0;
+  unsigned ph = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+    if (p.sel && !p.sel[(tile * kTC) / p.cpo]) continue;
+    mbar_wait(&full[st], ph);
+    const double* T = ring + st * stage;
+    double ss[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ss[q] = 0.0;
+#pragma unroll
+    for (int u = 0; u < MAXG; ++u) {
+      if (!live[u]) continue;  // warp-uniform
+      const double* TA = T + gA[u];
+      const double* TB = T + gB[u];
+      const bool diag = want_ss && gp[u] == gmi[u];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        double av[8], b0[4], b1[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = TA[256 * ks + offA[i]];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          b0[i] = TB[256 * ks + offB[0][i]];
+          b1[i] = TB[256 * ks + offB[1][i]];
+        }
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ss[2 * ks + (i >> 1)] = fma(b0[i], b0[i], fma(b1[i], b1[i], ss[2 * ks + (i >> 1)]));
+        }
+        dmma16(acc[u][0], av, b0);
+        dmma16(acc[u][1], av, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+    if (want_ss) {  // 8 per-tile column-group sums, fixed-order reduction over the consumer warps
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double v = ss[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) ssq[warp][q] = v;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");
+      if (warp == 0 && lane < 8) {
+        double tot = 0.0;
+        for (int w = 0; w < NCW; ++w) tot += ssq[w][lane];
+        p.tsumsq[tile * kConsumerWarps + lane] = tot;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");
+    }
+    if (++st == nst) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  // c[i] = C[16 mi + g + 8 (i >> 1)][8 nj + 2t + (i & 1)], nj = 2p + h
+  double* out = p.partials + (long long)blockIdx.x * p.a8 * p.a8;
+#pragma unroll
+  for (int u = 0; u < MAXG; ++u) {
+    if (!live[u]) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 16 * gmi[u] + g + 8 * (i >> 1);
+        const int c = 8 * (2 * gp[u] + h) + 2 * t + (i & 1);
+        if (r < p.a8 && c < p.a8) out[r + (long long)p.a8 * c] = acc[u][h][i];
+      }
+  }
+}
+
 // G (a x a, symmetric) = sum over the nx CTA partials (lower triangle read)
 __global__ void k_gram_reduce2(const double* __restrict__ partials, int nx, int a8, int a, double* __restrict__ G) {
   const long long n = (long long)a * a;

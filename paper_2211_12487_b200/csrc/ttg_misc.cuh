@@ -123,6 +123,94 @@ __global__ void k_iface_step2(const double* __restrict__ T, const double* __rest
   }
 }
 
+// The whole interface chain in one launch (one block, sequential over the
+// modes, steps separated by block barriers; intermediates in global/L2):
+// M_0 = [1], M_{i+1}[q, q'] = sum_{j, p, p'} core_i[p, j, q] M_i[p, p'] core_i[p', j, q'].
+constexpr int kIfaceMaxModes = 64;
+struct IfaceArgs {
+  int d;
+  const double* cores[kIfaceMaxModes];
+  int rl[kIfaceMaxModes], n[kIfaceMaxModes], rr[kIfaceMaxModes];
+  int rmax, nmax;
+  double* out;  // rr_{d-1}^2 result
+};
+// shared memory: M ping-pong (2 rmax^2) + T and the current core (rmax nmax
+// rmax each); every operand of the two contractions is in shared memory.
+__global__ void __launch_bounds__(512) k_iface_all(IfaceArgs a) {
+  extern __shared__ double sm[];
+  double* Mb[2] = {sm, sm + a.rmax * a.rmax};
+  double* T = sm + 2 * a.rmax * a.rmax;
+  double* Cs = T + a.rmax * a.nmax * a.rmax;
+  if (threadIdx.x == 0) Mb[0][0] = 1.0;
+  int f = 0;
+  for (int i = 0; i < a.d; ++i) {
+    const int rl = a.rl[i], n = a.n[i], rr = a.rr[i];
+    const int t1 = rl * n * rr, m = rl * n;
+    for (int e = threadIdx.x; e < t1; e += blockDim.x) Cs[e] = __ldg(a.cores[i] + e);
+    __syncthreads();
+    const double* M = Mb[f];
+    for (int e = threadIdx.x; e < t1; e += blockDim.x) {
+      const int pp = e % rl, rest = e / rl;
+      const double* cc = Cs + rl * rest;
+      double s0 = 0.0, s1 = 0.0;
+      int p = 0;
+      for (; p + 1 < rl; p += 2) {
+        s0 = fma(M[pp + rl * p], cc[p], s0);
+        s1 = fma(M[pp + rl * (p + 1)], cc[p + 1], s1);
+      }
+      if (p < rl) s0 = fma(M[pp + rl * p], cc[p], s0);
+      T[e] = s0 + s1;
+    }
+    __syncthreads();
+    double* Mn = (i + 1 == a.d) ? a.out : Mb[f ^ 1];
+    for (int e = threadIdx.x; e < rr * rr; e += blockDim.x) {
+      const int q = e % rr, q2 = e / rr;
+      const double* cq = Cs + m * q;
+      const double* tq = T + m * q2;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int x = 0;
+      for (; x + 3 < m; x += 4) {
+        s0 = fma(cq[x], tq[x], s0);
+        s1 = fma(cq[x + 1], tq[x + 1], s1);
+        s2 = fma(cq[x + 2], tq[x + 2], s2);
+        s3 = fma(cq[x + 3], tq[x + 3], s3);
+      }
+      for (; x < m; ++x) s0 = fma(cq[x], tq[x], s0);
+      Mn[e] = (s0 + s1) + (s2 + s3);
+    }
+    __syncthreads();
+    f ^= 1;
+  }
+}
+
+// Q = K P  (rows x a): K = I_n (x) Psi (Psi: As x r, rows = As n, a = r n) or
+// K = I_a (Psi null, As = r), P = I - U U^T (U: a x r_old, r_old >= 0).
+// One thread per element; (K U)[i, k] is formed inline (r_old r FMA).
+__global__ void k_build_q(const double* __restrict__ Psi, int As, int r, int n, const double* __restrict__ U,
+                          int r_old, double* __restrict__ Q) {
+  const int rows = As * n, a = r * n;
+  const long long tot = (long long)rows * a;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % rows), j = (int)(e / rows);
+    const int p = i % As, jn = i / As;
+    const int q = j % r, jn2 = j / r;
+    double kij = 0.0;
+    if (jn == jn2) kij = Psi ? Psi[p + (long long)As * q] : (p == q ? 1.0 : 0.0);
+    double s = 0.0;
+    for (int k = 0; k < r_old; ++k) {
+      double ku;
+      if (Psi) {
+        ku = 0.0;
+        for (int qq = 0; qq < r; ++qq) ku = fma(Psi[p + (long long)As * qq], U[qq + r * jn + (long long)a * k], ku);
+      } else {
+        ku = U[i + (long long)a * k];
+      }
+      s = fma(ku, U[j + (long long)a * k], s);
+    }
+    Q[e] = kij - s;
+  }
+}
+
 // cn2[o] = |c_o|^2, cmc[o] = c_o^T M c_o  (c: r x b, ld r)
 __global__ void k_coef_stats(const double* __restrict__ C, int r, int b, const double* __restrict__ M,
                              double* __restrict__ cn2, double* __restrict__ cmc) {
@@ -197,9 +285,9 @@ __global__ void k_merge_rows(const double* __restrict__ old, int ro, const doubl
 }
 
 // G <- (G + G^T) / 2 over a grid (one thread per strictly-lower element);
-// block 0 also writes trace(G) -> *tr (the diagonal is not modified; fixed
-// warp-tree order, deterministic).
-__global__ void k_symmetrize_trace(double* __restrict__ G, int a, double* __restrict__ tr) {
+// block 0 also writes trace(Tsrc) -> *tr (Tsrc: nt x nt; G's diagonal is not
+// modified, so Tsrc may be G; fixed warp-tree order, deterministic).
+__global__ void k_symmetrize_trace(double* __restrict__ G, int a, const double* Tsrc, int nt, double* __restrict__ tr) {
   const long long n = (long long)a * a;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(e % a), j = (int)(e / a);
@@ -211,7 +299,7 @@ __global__ void k_symmetrize_trace(double* __restrict__ G, int a, double* __rest
   }
   if (blockIdx.x == 0 && tr && threadIdx.x < 32) {
     double s = 0.0;
-    for (int i = threadIdx.x; i < a; i += 32) s += G[i + (long long)a * i];
+    for (int i = threadIdx.x; i < nt; i += 32) s += Tsrc[i + (long long)nt * i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (threadIdx.x == 0) *tr = s;

@@ -92,6 +92,38 @@ float time_it(F f) {
   return best;
 }
 
+// half the warps run DMMA chains, the other half DFMA chains: do the FP64
+// tensor and FP64 FMA pipes run concurrently?
+__global__ void mix_kernel(double* out, int iters_mma, int iters_fma) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0.0;
+  if (warp & 1) {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters_fma; ++it) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = fma(x[i], 0.999, 1e-3);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += x[i];
+  } else {
+    double a = threadIdx.x * 1e-3, b = 0.5;
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c[i][0] = 0; c[i][1] = 0; }
+    for (int it = 0; it < iters_mma; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 int main() {
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   printf("device %s SMs %d smemPerBlockOptin %zu L2 %d clock %d kHz\n", p.name, p.multiProcessorCount,
@@ -121,6 +153,16 @@ int main() {
     float ms = time_it([&] { dmma16816_kernel<<<sms * bpsm, threads>>>(out, iters); });
     double fl = 2.0 * 16 * 8 * 16 * 4 * iters * (threads / 32.0) * sms * bpsm;
     printf("DMMA m16n8k16 blocks/SM %d: %.2f TFLOP/s\n", bpsm, fl / ms / 1e9);
+  }
+  for (int bpsm : {1, 2, 4}) {
+    int threads = 512;
+    // per DMMA warp: 8 x iters_mma m8n8k4 (512 flops each, per warp-instruction 32 lanes -> 8*8*4*2 flops)
+    int im = 2048, iff = 4096;
+    float ms = time_it([&] { mix_kernel<<<sms * bpsm, threads>>>(out, im, iff); });
+    double fm = 2.0 * 8 * 8 * 4 * 8 * im * (threads / 64.0) * sms * bpsm;
+    double ff = 2.0 * 16 * iff * (threads / 2.0) * sms * bpsm;
+    printf("MIX blocks/SM %d: %.2f TFLOP/s total (DMMA part %.2f, DFMA part %.2f if concurrent)\n", bpsm,
+           (fm + ff) / ms / 1e9, fm / ms / 1e9, ff / ms / 1e9);
   }
   size_t n = (size_t)1 << 28;  // 4 GiB of doubles as double2 pairs -> 2^28 double2 = 4 GiB
   double2 *a, *b; cudaMalloc(&a, n * 16); cudaMalloc(&b, n * 16);
