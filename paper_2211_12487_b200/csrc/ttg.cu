@@ -1551,7 +1551,9 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
   c->iface[0].ensure(sizeof(double) * rmax * rmax);
   c->iface[1].ensure(sizeof(double) * rmax * rmax);
   c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
-  const size_t ismem = sizeof(double) * (size_t)(2 * rmax * rmax + 2 * rmax * nmax * rmax);
+  size_t core_tot = 0;
+  for (int i = 0; i < tt->d; ++i) core_tot += (size_t)((tt->ranks[i] * tt->modes[i] + 1) * tt->ranks[i + 1]);
+  const size_t ismem = sizeof(double) * ((size_t)(2 * rmax * rmax + (rmax * nmax + 1) * rmax) + core_tot);
   if (tt->d <= ttg::kIfaceMaxModes && ismem <= 200 * 1024) {  // one launch for the whole chain
     ttg::IfaceArgs ia{};
     ia.d = tt->d;
@@ -1566,9 +1568,9 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
     ia.rmax = (int)rmax;
     ia.nmax = (int)nmax;
     ia.out = c->iface[0].as<double>();
-    kernel_occupancy((const void*)ttg::k_iface_all, ttg::k_iface_all, 512, ismem);
-    prof_begin(c, "k_iface", 8.0 * rmax * nmax * rmax * tt->d, flops);
-    ttg::k_iface_all<<<1, 512, ismem, c->stream>>>(ia);
+    kernel_occupancy((const void*)ttg::k_iface_all, ttg::k_iface_all, 1024, ismem);
+    prof_begin(c, "k_iface", 8.0 * core_tot, flops);
+    ttg::k_iface_all<<<1, 1024, ismem, c->stream>>>(ia);
     post_launch(c);
     return c->iface[0].as<double>();
   }
@@ -1610,7 +1612,7 @@ void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double
                                                                    c->cmc.as<double>());
   post_launch(c);
   prof_begin(c, "k_star_local", 32.0 * b, 10.0 * b);
-  ttg::k_star_local<<<1, 32, 0, c->stream>>>(c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
+  ttg::k_star_local<<<1, 256, 0, c->stream>>>(c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
                                              (int)b, eps, c->errs.as<double>(), c->rn2.as<double>(),
                                              c->stats.as<ttg::StarStats>());
   post_launch(c);

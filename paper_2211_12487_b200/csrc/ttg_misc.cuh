@@ -134,24 +134,41 @@ struct IfaceArgs {
   int rmax, nmax;
   double* out;  // rr_{d-1}^2 result
 };
-// shared memory: M ping-pong (2 rmax^2) + T and the current core (rmax nmax
-// rmax each); every operand of the two contractions is in shared memory.
-__global__ void __launch_bounds__(512) k_iface_all(IfaceArgs a) {
+// shared memory: M ping-pong (2 rmax^2) + T + every core, prefetched up
+// front (all loads in flight).  A core (rl x n x rr) and T are stored as rr
+// columns of m = rl n entries with a padded stride m + 1, so the per-thread
+// column walks of the second contraction hit distinct banks (m is often a
+// multiple of 16).
+__global__ void __launch_bounds__(1024) k_iface_all(IfaceArgs a) {
   extern __shared__ double sm[];
   double* Mb[2] = {sm, sm + a.rmax * a.rmax};
   double* T = sm + 2 * a.rmax * a.rmax;
-  double* Cs = T + a.rmax * a.nmax * a.rmax;
+  double* Cs0 = T + (a.rmax * a.nmax + 1) * a.rmax;
+  {
+    double* dst = Cs0;
+    for (int i = 0; i < a.d; ++i) {
+      const int m = a.rl[i] * a.n[i], t1 = m * a.rr[i];
+      const double* __restrict__ src = a.cores[i];
+      for (int e = threadIdx.x; e < t1; e += blockDim.x) {
+        const int q = e / m, x = e - q * m;
+        dst[x + (m + 1) * q] = __ldg(src + e);
+      }
+      dst += (m + 1) * a.rr[i];
+    }
+  }
   if (threadIdx.x == 0) Mb[0][0] = 1.0;
+  __syncthreads();
   int f = 0;
+  const double* Cs = Cs0;
   for (int i = 0; i < a.d; ++i) {
     const int rl = a.rl[i], n = a.n[i], rr = a.rr[i];
-    const int t1 = rl * n * rr, m = rl * n;
-    for (int e = threadIdx.x; e < t1; e += blockDim.x) Cs[e] = __ldg(a.cores[i] + e);
-    __syncthreads();
+    const int m = rl * n, t1 = m * rr, ms = m + 1;
     const double* M = Mb[f];
+    // T[p', j, q] = sum_p M[p', p] core[p, j, q]
     for (int e = threadIdx.x; e < t1; e += blockDim.x) {
-      const int pp = e % rl, rest = e / rl;
-      const double* cc = Cs + rl * rest;
+      const int q = e / m, x = e - q * m;  // x = p' + rl j
+      const int pp = x % rl, jj = x / rl;
+      const double* cc = Cs + ms * q + rl * jj;
       double s0 = 0.0, s1 = 0.0;
       int p = 0;
       for (; p + 1 < rl; p += 2) {
@@ -159,14 +176,15 @@ __global__ void __launch_bounds__(512) k_iface_all(IfaceArgs a) {
         s1 = fma(M[pp + rl * (p + 1)], cc[p + 1], s1);
       }
       if (p < rl) s0 = fma(M[pp + rl * p], cc[p], s0);
-      T[e] = s0 + s1;
+      T[x + ms * q] = s0 + s1;
     }
     __syncthreads();
+    // M'[q, q2] = sum_x core[x, q] T[x, q2]
     double* Mn = (i + 1 == a.d) ? a.out : Mb[f ^ 1];
     for (int e = threadIdx.x; e < rr * rr; e += blockDim.x) {
       const int q = e % rr, q2 = e / rr;
-      const double* cq = Cs + m * q;
-      const double* tq = T + m * q2;
+      const double* cq = Cs + ms * q;
+      const double* tq = T + ms * q2;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int x = 0;
       for (; x + 3 < m; x += 4) {
@@ -179,6 +197,7 @@ __global__ void __launch_bounds__(512) k_iface_all(IfaceArgs a) {
       Mn[e] = (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
+    Cs += ms * rr;
     f ^= 1;
   }
 }
@@ -236,27 +255,47 @@ __global__ void k_coef_stats(const double* __restrict__ C, int r, int b, const d
 struct StarStats {
   double sums[9];
 };
-__global__ void k_star_local(const double* __restrict__ on2, const double* __restrict__ cn2,
-                             const double* __restrict__ cmc, int b, double eps, double* __restrict__ errs,
-                             double* __restrict__ rn2_out, StarStats* st) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(256) k_star_local(const double* __restrict__ on2, const double* __restrict__ cn2,
+                                                    const double* __restrict__ cmc, int b, double eps,
+                                                    double* __restrict__ errs, double* __restrict__ rn2_out,
+                                                    StarStats* st) {
+  // per-observation values in parallel (256 at a time, staged in shared
+  // memory), the nine decision sums by one thread in observation order (the
+  // reference's loop order, so the sums are bit-identical to a serial pass)
+  __shared__ double s_err[256], s_on2[256], s_rn2[256];
   double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (int o = 0; o < b; ++o) {
-    double on = sqrt(on2[o]);
-    // |y - Phi c|^2 = |y|^2 - 2|c|^2 + c^T (Phi^T Phi) c   (c = Phi^T y)
-    double rsq = on2[o] - 2.0 * cn2[o] + cmc[o];
-    if (rsq < 0.0) rsq = 0.0;
-    double rn = sqrt(rsq);
-    double err = (on == 0.0) ? 0.0 : rn / on;
-    errs[o] = err;
-    rn2_out[o] = rn * rn;
-    if (on > 0.0) { s[0] += err; s[1] += 1.0; }
-    s[2] += rn * rn;
-    s[3] += on * on;
-    if (err > eps) { s[5] += on2[o]; s[6] += 1.0; }
-    else { double r = err * on; s[4] += r * r; s[7] += 1.0; s[8] += err; }
+  for (int base = 0; base < b; base += 256) {
+    const int o = base + threadIdx.x;
+    if (o < b) {
+      const double on = sqrt(on2[o]);
+      // |y - Phi c|^2 = |y|^2 - 2|c|^2 + c^T (Phi^T Phi) c   (c = Phi^T y)
+      double rsq = on2[o] - 2.0 * cn2[o] + cmc[o];
+      if (rsq < 0.0) rsq = 0.0;
+      const double rn = sqrt(rsq);
+      const double err = (on == 0.0) ? 0.0 : rn / on;
+      errs[o] = err;
+      rn2_out[o] = rn * rn;
+      s_err[threadIdx.x] = err;
+      s_on2[threadIdx.x] = on2[o];
+      s_rn2[threadIdx.x] = rn * rn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int m = min(256, b - base);
+      for (int q = 0; q < m; ++q) {
+        const double err = s_err[q], o2 = s_on2[q], r2 = s_rn2[q];
+        const double on = sqrt(o2);
+        if (on > 0.0) { s[0] += err; s[1] += 1.0; }
+        s[2] += r2;
+        s[3] += on * on;
+        if (err > eps) { s[5] += o2; s[6] += 1.0; }
+        else { const double r = err * on; s[4] += r * r; s[7] += 1.0; s[8] += err; }
+      }
+    }
+    __syncthreads();
   }
-  for (int i = 0; i < 9; ++i) st->sums[i] = s[i];
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 9; ++i) st->sums[i] = s[i];
 }
 
 // W = I_n (x) Psi  ((As*n) x (r*n), block diagonal)
