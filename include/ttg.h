@@ -158,6 +158,46 @@ int ttg_project(ttg_ctx* ctx, const ttg_tt* tt, const double* y, int where,
 int ttg_reconstruct(ttg_ctx* ctx, const ttg_tt* tt, int64_t obs_begin, int64_t obs_end,
                     double* out, int where);
 
+/* ---- metrics (reference proj/include/ttstream/metrics.hpp) ---- */
+/* compression_ratio, metrics.hpp:11 / metrics.cpp:7-11: (prod n_i * n_obs) / param_count. */
+int ttg_compression_ratio(const ttg_tt* tt, double* cr);
+/* rre, metrics.hpp:15-18 / metrics.cpp:34-38: ||x_ref - reconstruct(obs_begin, obs_end)|| / ||x_ref||,
+ * computed on the device without materialising the reconstruction.  Zero-norm reference -> 0 and
+ * *zero_reference = 1 (nullable).  x_ref shape: (n_1..n_d, obs_end - obs_begin). */
+int ttg_rre(ttg_ctx* ctx, const ttg_tt* tt, const double* x_ref, int where, const int64_t* shape, int ndim,
+            int64_t obs_begin, int64_t obs_end, double* rre, int* zero_reference);
+/* rpe, metrics.hpp:24 / metrics.cpp:44-47: relative error of tt_expand(tt_project(unseen)). */
+int ttg_rpe(ttg_ctx* ctx, const ttg_tt* tt, const double* unseen, int where, const int64_t* shape,
+            int ndim, double* rpe, int* zero_reference);
+/* TensorTrain::measure_ortho_count, tensor_train.cpp:135-146 (device Gram of each left unfolding). */
+int ttg_tt_measure_ortho_count(ttg_ctx* ctx, const ttg_tt* tt, double tol, int64_t* count);
+
+/* ---- TTC1 checkpoint (reference serialization.hpp:12-22) ---- */
+/* serialize, serialization.cpp:68-87: strided D2H of the device train into the TTC1 image.
+ * Call with buf = NULL to get *len; then with a buffer of cap >= *len. */
+int ttg_tt_serialize(ttg_ctx* ctx, const ttg_tt* tt, uint8_t* buf, int64_t cap, int64_t* len);
+/* deserialize, serialization.cpp:89-129: same validation and FormatError messages; the
+ * orthonormality is re-measured on the device (tol 1e-10), not trusted from the file. */
+int ttg_tt_deserialize(ttg_ctx* ctx, const uint8_t* buf, int64_t len, ttg_tt** out);
+/* save_ttc / load_ttc, serialization.cpp:131-152. */
+int ttg_tt_save_ttc(ttg_ctx* ctx, const ttg_tt* tt, const char* path);
+int ttg_tt_load_ttc(ttg_ctx* ctx, const char* path, ttg_tt** out);
+
+/* ---- TTB1 ingest (reference stream_io.hpp:57-65) ---- */
+/* write_batch / read_batch, stream_io.cpp:123-187.  read: call with data = NULL to get ndim,
+ * shape (int64_t[255] or NULL) and *count, then with a buffer of cap >= *count doubles. */
+int ttg_write_batch(const char* path, const int64_t* shape, int ndim, const double* data);
+int ttg_read_batch(const char* path, int64_t* shape, int* ndim, double* data, int64_t cap, int64_t* count);
+/* A directory of .ttb increments in lexicographic order (list_stream, stream_io.cpp:189-204),
+ * read by a host thread into pinned buffers and copied H2D on a side stream while the caller
+ * updates on the previous increment.  ttg_stream_next returns a DEVICE pointer (pass it with
+ * TTG_DEVICE) valid until the next call; the library stream already waits for its copy. */
+typedef struct ttg_stream ttg_stream;
+int ttg_stream_open(ttg_ctx* ctx, const char* dir, ttg_stream** out);
+int64_t ttg_stream_count(const ttg_stream* s);
+int ttg_stream_next(ttg_stream* s, const double** y, int64_t* shape, int* ndim);
+int ttg_stream_close(ttg_stream* s);
+
 #ifdef __cplusplus
 }
 #endif

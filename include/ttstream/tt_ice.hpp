@@ -28,4 +28,11 @@ std::pair<TensorTrain, UpdateReport> tt_ice_update_with_tolerances(const TensorT
                                                                    std::span<const double> deltas);
 std::pair<TensorTrain, UpdateReport> tt_ice_bootstrap(const DenseTensor& y, double eps_des);
 
+/// Device-pointer overloads (drop-in extension): y_device is a
+/// first-index-fastest float64 increment already in GPU memory (no PCIe copy).
+std::pair<TensorTrain, UpdateReport> tt_ice_update(const TensorTrain& tt, const double* y_device,
+                                                   std::span<const Index> shape, double eps_des);
+std::pair<TensorTrain, UpdateReport> tt_ice_bootstrap(const double* y_device, std::span<const Index> shape,
+                                                      double eps_des);
+
 }  // namespace ttstream

@@ -33,5 +33,9 @@ double relaxed_tolerance_approx(Index n_batch, Index n_rejected, double mean_rej
 
 std::pair<TensorTrain, UpdateReport> tt_ice_star_update(const TensorTrain& tt, const DenseTensor& y, double eps_des,
                                                         const HeuristicConfig& cfg = {});
+/// Device-pointer overload (drop-in extension): y_device already in GPU memory.
+std::pair<TensorTrain, UpdateReport> tt_ice_star_update(const TensorTrain& tt, const double* y_device,
+                                                        std::span<const Index> shape, double eps_des,
+                                                        const HeuristicConfig& cfg = {});
 
 }  // namespace ttstream

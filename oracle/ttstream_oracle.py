@@ -22,6 +22,11 @@ What it restates (reference = /root/reference/proj, C++20 + Eigen):
 * ``tt_project`` / ``tt_expand`` / ``tt_reconstruct`` / ``spatial_chain`` /
   ``occupancy`` / ``tt_norm`` / ``measure_ortho_count``
                                 src/tensor_train.cpp:135-226, 377-390
+* ``compression_ratio`` / ``rre`` / ``rpe`` / ``mean_rre_per_increment``
+                                src/metrics.cpp:7-68
+* ``serialize`` / ``deserialize`` (TTC1)  src/serialization.cpp:68-129
+* ``write_batch`` / ``read_batch`` (TTB1) / ``list_stream``
+                                src/stream_io.cpp:123-204
 
 Parity status: the reference ships NO golden vectors and cannot be compiled
 here (Eigen3 is absent).  This oracle is therefore pinned
@@ -811,3 +816,182 @@ def rel_diff(a: np.ndarray, b: np.ndarray) -> float:
     den = float(np.linalg.norm(np.ravel(a)))
     num = float(np.linalg.norm(np.ravel(a) - np.ravel(b)))
     return float(np.linalg.norm(np.ravel(b))) if den == 0.0 else num / den
+
+
+# --------------------------------------------------------------------------
+# metrics (src/metrics.cpp:7-68)
+# --------------------------------------------------------------------------
+
+
+def compression_ratio(tt: TensorTrain) -> float:
+    """metrics.cpp:7-11: elements of the represented tensor / stored parameters."""
+    elements = 1.0
+    for n in tt.mode_sizes():
+        elements *= float(n)
+    return elements / float(tt.param_count())
+
+
+def _relative_error(ref: np.ndarray, approx: np.ndarray):
+    """metrics.cpp:15-29; returns (error, zero_reference)."""
+    if ref.shape != approx.shape:
+        raise DimensionError("reference shape does not match reconstruction")
+    ref_norm = float(np.linalg.norm(np.ravel(ref, order="F")))
+    if ref_norm == 0.0:
+        return 0.0, True
+    return float(np.linalg.norm(np.ravel(ref, order="F") - np.ravel(approx, order="F"))) / ref_norm, False
+
+
+def rre(tt: TensorTrain, x_ref: np.ndarray, obs_begin: int = 0, obs_end: Optional[int] = None):
+    """metrics.cpp:34-42 -> (rre, zero_reference)."""
+    if obs_end is None:
+        obs_end = tt.obs_count()
+    return _relative_error(x_ref, tt_reconstruct(tt, obs_begin, obs_end))
+
+
+def rpe(tt: TensorTrain, unseen: np.ndarray):
+    """metrics.cpp:44-47 -> (rpe, zero_reference)."""
+    coeffs = tt_project(tt, unseen)
+    return _relative_error(unseen, tt_expand(tt, coeffs))
+
+
+def mean_rre_per_increment(tt: TensorTrain, refs: Sequence[np.ndarray]):
+    """metrics.cpp:49-66 -> (per-increment list, mean)."""
+    if len(refs) != tt.num_increments():
+        raise DimensionError("need one reference per stored increment")
+    per = []
+    for k in range(tt.num_increments()):
+        begin, end = tt.increment_range(k)
+        if refs[k].shape[-1] != end - begin:
+            raise DimensionError("reference observation count does not match increment")
+        per.append(rre(tt, refs[k], begin, end)[0])
+    return per, (sum(per) / len(per) if per else 0.0)
+
+
+# --------------------------------------------------------------------------
+# TTC1 train image (src/serialization.cpp:68-129): "TTC1", u8 core count,
+# per core u64 r_left, n, r_right + little-endian f64 payload, u64 boundary
+# count + u64 boundaries.
+# --------------------------------------------------------------------------
+
+
+def serialize(tt: TensorTrain) -> bytes:
+    """serialization.cpp:68-87."""
+    out = bytearray(b"TTC1")
+    out.append(tt.num_cores() & 0xFF)
+    for c in tt.cores:
+        out += np.array([c.r_left, c.n, c.r_right], dtype="<u8").tobytes()
+        out += np.ravel(c.data, order="F").astype("<f8").tobytes()
+    out += np.array([len(tt.batch_boundaries)], dtype="<u8").tobytes()
+    out += np.array(tt.batch_boundaries, dtype="<u8").tobytes()
+    return bytes(out)
+
+
+def deserialize(data: bytes) -> TensorTrain:
+    """serialization.cpp:89-129 (same checks, same messages)."""
+    pos = 0
+
+    def need(n):
+        if pos + n > len(data):
+            raise FormatError("truncated train data")
+
+    def u64():
+        nonlocal pos
+        need(8)
+        v = int.from_bytes(data[pos:pos + 8], "little")
+        pos += 8
+        return v
+
+    need(4)
+    if data[:4] != b"TTC1":
+        raise FormatError("bad magic: not a TTC1 train file")
+    pos = 4
+    need(1)
+    nd = data[pos]
+    pos += 1
+    if nd < 1:
+        raise FormatError("train file declares zero cores")
+    cores = []
+    prev = 1
+    for _ in range(nd):
+        rl, n, rr = u64(), u64(), u64()
+        if rl < 1 or n < 1 or rr < 1:
+            raise FormatError("core extents must be positive")
+        if rl != prev:
+            raise FormatError("bond ranks of adjacent cores disagree")
+        if rl * n * rr > len(data) // 8 + 1:
+            raise FormatError("truncated train data")
+        cnt = rl * n * rr
+        need(8 * cnt)
+        vals = np.frombuffer(data, dtype="<f8", count=cnt, offset=pos).astype(np.float64)
+        pos += 8 * cnt
+        if not np.all(np.isfinite(vals)):
+            raise NumericError("non-finite element rejected at core construction")
+        cores.append(TTCore(np.asfortranarray(np.reshape(vals, (rl, n, rr), order="F"))))
+        prev = rr
+    if prev != 1:
+        raise FormatError("last core must close the chain with rank 1")
+    nb = u64()
+    bounds = [u64() for _ in range(nb)]
+    if pos != len(data):
+        raise FormatError("trailing bytes after train data")
+    try:
+        probe = TensorTrain(cores, 0, list(bounds))
+        return TensorTrain(cores, probe.measure_ortho_count(), list(bounds))
+    except DimensionError as e:
+        raise FormatError(str(e)) from None
+
+
+# --------------------------------------------------------------------------
+# TTB1 batch file (src/stream_io.cpp:123-204): "TTB1", u8 mode count,
+# u64 extents, little-endian f64 payload (first-index-fastest).
+# --------------------------------------------------------------------------
+
+
+def write_batch(t: np.ndarray, path: str) -> None:
+    """stream_io.cpp:123-137."""
+    out = bytearray(b"TTB1")
+    out.append(t.ndim & 0xFF)
+    out += np.array(t.shape, dtype="<u8").tobytes()
+    out += np.ravel(t, order="F").astype("<f8").tobytes()
+    with open(path, "wb") as f:
+        f.write(bytes(out))
+
+
+def read_batch(path: str) -> np.ndarray:
+    """stream_io.cpp:139-187."""
+    with open(path, "rb") as f:
+        data = f.read()
+    if len(data) < 4 or data[:4] != b"TTB1":
+        if len(data) < 4:
+            raise FormatError("truncated batch file " + path)
+        raise FormatError("bad magic: " + path + " is not a TTB1 batch")
+    if len(data) < 5:
+        raise FormatError("truncated batch file " + path)
+    nd = data[4]
+    if nd < 1:
+        raise FormatError("batch file declares zero modes")
+    pos = 5
+    if len(data) < pos + 8 * nd:
+        raise FormatError("truncated batch file " + path)
+    shape = [int.from_bytes(data[pos + 8 * i:pos + 8 * i + 8], "little") for i in range(nd)]
+    pos += 8 * nd
+    count = int(np.prod(shape)) if shape else 0
+    if len(data) - pos != count * 8:
+        raise FormatError("payload length disagrees with declared shape in " + path)
+    vals = np.frombuffer(data, dtype="<f8", count=count, offset=pos).astype(np.float64)
+    if any(e < 1 for e in shape):
+        raise DimensionError("tensor extent must be >= 1")
+    if not np.all(np.isfinite(vals)):
+        raise NumericError("non-finite element rejected at tensor construction")
+    return np.asfortranarray(np.reshape(vals, shape, order="F"))
+
+
+def list_stream(directory: str) -> List[str]:
+    """stream_io.cpp:189-204: .ttb files in lexicographic filename order."""
+    import os
+
+    if not os.path.isdir(directory):
+        raise FormatError("stream path is not a directory: " + directory)
+    files = [os.path.join(directory, f) for f in os.listdir(directory)
+             if f.endswith(".ttb") and os.path.isfile(os.path.join(directory, f))]
+    return sorted(files, key=lambda p: os.path.basename(p))

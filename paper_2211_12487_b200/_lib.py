@@ -85,6 +85,23 @@ SIGNATURES = [
     ("ttg_per_obs_errors", ctypes.c_int, [_P, _P, _DP, ctypes.c_int, _I64P, ctypes.c_int, _DP]),
     ("ttg_project", ctypes.c_int, [_P, _P, _DP, ctypes.c_int, _I64P, ctypes.c_int, _DP]),
     ("ttg_reconstruct", ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int64, _DP, ctypes.c_int]),
+    # metrics (metrics.hpp), checkpoint (serialization.hpp), ingest (stream_io.hpp)
+    ("ttg_compression_ratio", ctypes.c_int, [_P, _DP]),
+    ("ttg_rre", ctypes.c_int, [_P, _P, _DP, ctypes.c_int, _I64P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _DP,
+                               ctypes.POINTER(ctypes.c_int)]),
+    ("ttg_rpe", ctypes.c_int, [_P, _P, _DP, ctypes.c_int, _I64P, ctypes.c_int, _DP, ctypes.POINTER(ctypes.c_int)]),
+    ("ttg_tt_measure_ortho_count", ctypes.c_int, [_P, _P, ctypes.c_double, _I64P]),
+    ("ttg_tt_serialize", ctypes.c_int, [_P, _P, ctypes.c_void_p, ctypes.c_int64, _I64P]),
+    ("ttg_tt_deserialize", ctypes.c_int, [_P, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(_P)]),
+    ("ttg_tt_save_ttc", ctypes.c_int, [_P, _P, ctypes.c_char_p]),
+    ("ttg_tt_load_ttc", ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_P)]),
+    ("ttg_write_batch", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_int, _DP]),
+    ("ttg_read_batch", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.POINTER(ctypes.c_int), _DP, ctypes.c_int64,
+                                      _I64P]),
+    ("ttg_stream_open", ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_P)]),
+    ("ttg_stream_count", ctypes.c_int64, [_P]),
+    ("ttg_stream_next", ctypes.c_int, [_P, ctypes.POINTER(_DP), _I64P, ctypes.POINTER(ctypes.c_int)]),
+    ("ttg_stream_close", ctypes.c_int, [_P]),
 ]
 
 _lib = None

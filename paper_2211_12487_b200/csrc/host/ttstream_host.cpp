@@ -12,6 +12,9 @@
 
 #include "ttg.h"
 #include "ttstream/tt_ice_star.hpp"
+#include "ttstream/metrics.hpp"
+#include "ttstream/serialization.hpp"
+#include "ttstream/stream_io.hpp"
 
 namespace ttstream {
 
@@ -541,6 +544,202 @@ std::pair<TensorTrain, UpdateReport> tt_ice_star_update(const TensorTrain& tt, c
                                              static_cast<int>(s.v.size()), eps_des, &h, &rep));
     });
     return {TensorTrain::from_device(dev), to_report(rep)};
+}
+
+// ---------------------------------------------------------------------------
+// device-pointer overloads (a device-resident increment avoids
+// the PCIe copy; y is first-index-fastest float64 in device memory)
+// ---------------------------------------------------------------------------
+namespace {
+std::vector<int64_t> shape_vec(std::span<const Index> shape) { return {shape.begin(), shape.end()}; }
+}  // namespace
+
+std::pair<TensorTrain, UpdateReport> tt_ice_update(const TensorTrain& tt, const double* y_device,
+                                                   std::span<const Index> shape, double eps_des) {
+    if (eps_des <= 0.0) throw NumericError("eps_des must be positive");
+    if (!tt.fully_orthonormal()) throw StateError("incremental update requires a fully orthonormal train");
+    auto dev = tt.device();
+    auto sv = shape_vec(shape);
+    ttg_report rep{};
+    detail::run_update(dev, [&] {
+        detail::check(ttg_tt_ice_update(detail::context(), dev->h, y_device, TTG_DEVICE, sv.data(),
+                                        static_cast<int>(sv.size()), eps_des, &rep));
+    });
+    return {TensorTrain::from_device(dev), to_report(rep)};
+}
+
+std::pair<TensorTrain, UpdateReport> tt_ice_bootstrap(const double* y_device, std::span<const Index> shape,
+                                                      double eps_des) {
+    auto sv = shape_vec(shape);
+    ttg_report rep{};
+    auto dev = std::make_shared<detail::DeviceTrain>();
+    detail::check(ttg_bootstrap(detail::context(), y_device, TTG_DEVICE, sv.data(), static_cast<int>(sv.size()),
+                                eps_des, &dev->h, &rep));
+    return {TensorTrain::from_device(dev), to_report(rep)};
+}
+
+std::pair<TensorTrain, UpdateReport> tt_ice_star_update(const TensorTrain& tt, const double* y_device,
+                                                        std::span<const Index> shape, double eps_des,
+                                                        const HeuristicConfig& cfg) {
+    if (eps_des <= 0.0) throw NumericError("eps_des must be positive");
+    if (cfg.occupancy_threshold <= 0.0 || cfg.occupancy_threshold > 1.0)
+        throw ConfigError("occupancy threshold must lie in (0, 1]");
+    if (!tt.fully_orthonormal()) throw StateError("projection requires a fully orthonormal train");
+    auto dev = tt.device();
+    auto sv = shape_vec(shape);
+    ttg_heuristics h;
+    ttg_heuristics_default(&h);
+    h.occupancy_threshold = cfg.occupancy_threshold;
+    h.skip_enabled = cfg.skip_enabled;
+    h.subselect_enabled = cfg.subselect_enabled;
+    h.skip_statistic = cfg.skip_statistic == SkipStatistic::kMean ? TTG_SKIP_MEAN : TTG_SKIP_FULL_BATCH;
+    h.use_approx_tolerance = cfg.use_approx_tolerance;
+    ttg_report rep{};
+    detail::run_update(dev, [&] {
+        detail::check(ttg_tt_ice_star_update(detail::context(), dev->h, y_device, TTG_DEVICE, sv.data(),
+                                             static_cast<int>(sv.size()), eps_des, &h, &rep));
+    });
+    return {TensorTrain::from_device(dev), to_report(rep)};
+}
+
+// ---------------------------------------------------------------------------
+// metrics (metrics.cpp:7-68) on the device
+// ---------------------------------------------------------------------------
+double compression_ratio(const TensorTrain& tt) {
+    double elements = 1.0;
+    for (Index n : tt.mode_sizes()) elements *= static_cast<double>(n);
+    return elements / static_cast<double>(tt.param_count());
+}
+
+double rre(const TensorTrain& tt, const DenseTensor& x_ref, Index obs_begin, Index obs_end, bool* zero_reference) {
+    if (zero_reference) *zero_reference = false;
+    if (obs_begin < 0 || obs_end > tt.obs_count() || obs_begin > obs_end)
+        throw IndexError("observation range out of bounds");
+    auto dev = tt.device();
+    Shape s(x_ref);
+    double out = 0.0;
+    int zr = 0;
+    detail::check(ttg_rre(detail::context(), dev->h, x_ref.data(), TTG_HOST, s.v.data(), static_cast<int>(s.v.size()),
+                          obs_begin, obs_end, &out, &zr));
+    if (zero_reference) *zero_reference = zr != 0;
+    return out;
+}
+
+double rre(const TensorTrain& tt, const DenseTensor& x_ref, bool* zero_reference) {
+    return rre(tt, x_ref, 0, tt.obs_count(), zero_reference);
+}
+
+double rpe(const TensorTrain& tt, const DenseTensor& unseen, bool* zero_reference) {
+    if (zero_reference) *zero_reference = false;
+    if (!tt.fully_orthonormal()) throw StateError("projection requires a fully orthonormal train");
+    auto dev = tt.device();
+    Shape s(unseen);
+    double out = 0.0;
+    int zr = 0;
+    detail::check(ttg_rpe(detail::context(), dev->h, unseen.data(), TTG_HOST, s.v.data(), static_cast<int>(s.v.size()),
+                          &out, &zr));
+    if (zero_reference) *zero_reference = zr != 0;
+    return out;
+}
+
+IncrementErrors mean_rre_per_increment(const TensorTrain& tt, std::span<const DenseTensor> refs) {
+    if (static_cast<Index>(refs.size()) != tt.num_increments())
+        throw DimensionError("need one reference per stored increment");
+    IncrementErrors out;
+    double sum = 0.0;
+    for (Index k = 0; k < tt.num_increments(); ++k) {
+        const auto [begin, end] = tt.increment_range(k);
+        const auto& ref = refs[static_cast<std::size_t>(k)];
+        if (ref.shape().back() != end - begin)
+            throw DimensionError("reference observation count does not match increment");
+        const double e = rre(tt, ref, begin, end);
+        out.per_increment.push_back(e);
+        sum += e;
+    }
+    out.mean = out.per_increment.empty() ? 0.0 : sum / static_cast<double>(out.per_increment.size());
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// TTC1 (serialization.cpp:68-152) from / into device state
+// ---------------------------------------------------------------------------
+std::vector<std::uint8_t> serialize(const TensorTrain& tt) {
+    auto dev = tt.device();
+    int64_t len = 0;
+    detail::check(ttg_tt_serialize(detail::context(), dev->h, nullptr, 0, &len));
+    std::vector<std::uint8_t> out(static_cast<std::size_t>(len));
+    detail::check(ttg_tt_serialize(detail::context(), dev->h, out.data(), len, &len));
+    return out;
+}
+
+TensorTrain deserialize(std::span<const std::uint8_t> bytes) {
+    auto dev = std::make_shared<detail::DeviceTrain>();
+    detail::check(ttg_tt_deserialize(detail::context(), bytes.data(), static_cast<int64_t>(bytes.size()), &dev->h));
+    return TensorTrain::from_device(dev);
+}
+
+void save_ttc(const TensorTrain& tt, const std::filesystem::path& path) {
+    auto dev = tt.device();
+    detail::check(ttg_tt_save_ttc(detail::context(), dev->h, path.string().c_str()));
+}
+
+TensorTrain load_ttc(const std::filesystem::path& path) {
+    auto dev = std::make_shared<detail::DeviceTrain>();
+    detail::check(ttg_tt_load_ttc(detail::context(), path.string().c_str(), &dev->h));
+    return TensorTrain::from_device(dev);
+}
+
+// ---------------------------------------------------------------------------
+// TTB1 (stream_io.cpp:123-204)
+// ---------------------------------------------------------------------------
+void write_batch(const DenseTensor& t, const std::filesystem::path& path) {
+    Shape s(t);
+    const int st = ttg_write_batch(path.string().c_str(), s.v.data(), static_cast<int>(s.v.size()), t.data());
+    if (st != TTG_OK) detail::throw_status(st, ttg_last_error(nullptr));
+}
+
+DenseTensor read_batch(const std::filesystem::path& path) {
+    std::vector<int64_t> shape(255);
+    int nd = 0;
+    int64_t count = 0;
+    int st = ttg_read_batch(path.string().c_str(), shape.data(), &nd, nullptr, 0, &count);
+    if (st != TTG_OK) detail::throw_status(st, ttg_last_error(nullptr));
+    std::vector<double> data(static_cast<std::size_t>(count));
+    st = ttg_read_batch(path.string().c_str(), shape.data(), &nd, data.data(), count, &count);
+    if (st != TTG_OK) detail::throw_status(st, ttg_last_error(nullptr));
+    return DenseTensor(std::vector<Index>(shape.begin(), shape.begin() + nd), std::move(data));
+}
+
+std::vector<std::filesystem::path> list_stream(const std::filesystem::path& dir) {
+    if (!std::filesystem::is_directory(dir)) throw FormatError("stream path is not a directory: " + dir.string());
+    std::vector<std::filesystem::path> files;
+    for (const auto& entry : std::filesystem::directory_iterator(dir))
+        if (entry.is_regular_file() && entry.path().extension() == ".ttb") files.push_back(entry.path());
+    std::sort(files.begin(), files.end(), [](const auto& a, const auto& b) { return a.filename() < b.filename(); });
+    return files;
+}
+
+struct DeviceStreamReader::Impl {
+    ttg_stream* s = nullptr;
+};
+
+DeviceStreamReader::DeviceStreamReader(const std::filesystem::path& dir) : impl_(std::make_unique<Impl>()) {
+    detail::check(ttg_stream_open(detail::context(), dir.string().c_str(), &impl_->s));
+}
+
+DeviceStreamReader::~DeviceStreamReader() {
+    if (impl_ && impl_->s) ttg_stream_close(impl_->s);
+}
+
+Index DeviceStreamReader::size() const { return ttg_stream_count(impl_->s); }
+
+const double* DeviceStreamReader::next(std::vector<Index>& shape) {
+    const double* y = nullptr;
+    std::vector<int64_t> sh(255);
+    int nd = 0;
+    detail::check(ttg_stream_next(impl_->s, &y, sh.data(), &nd));
+    shape.assign(sh.begin(), sh.begin() + nd);
+    return y;
 }
 
 }  // namespace ttstream

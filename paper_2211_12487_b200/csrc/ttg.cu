@@ -24,8 +24,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ttg.h"
@@ -33,6 +35,7 @@
 #include "ttg_kernels.cuh"
 #include "ttg_misc.cuh"
 #include "ttg_syev.cuh"
+#include "ttg_io.cuh"
 
 namespace {
 
@@ -961,12 +964,14 @@ bool project_ws16(ttg_ctx* c, const double* X, int a, long long L, const double*
   const int r8 = ttg::round_up(r, 8), NB = r8 / 8, nks = (a + 15) / 16;
   const size_t nfr = (size_t)nks * NB * 128;
   const size_t stage = sizeof(double) * (size_t)nks * 16 * ttg::kTC;
-  const size_t fixed = 1024 + sizeof(double) * (nfr + (size_t)4 * 16 * 32);
+  const size_t fixed = 1024 + sizeof(double) * (nfr + (size_t)4 * 16 * r8);
   const size_t cap = (size_t)c->smem_optin - 1024;
   int nst = 2;
   if (fixed + 2 * stage > cap) return false;
-  if (2 * (fixed + 2 * stage) > 220 * 1024)  // one CTA / SM: deepen the ring
+  if (2 * (fixed + 2 * stage) > 220 * 1024) {  // one CTA / SM: deepen the ring
     while (nst < 4 && fixed + (nst + 1) * stage <= cap) ++nst;
+  }
+  if (std::getenv("TTG_WS16_NST")) nst = std::max(2, std::min(4, std::atoi(std::getenv("TTG_WS16_NST"))));
   const size_t smem = fixed + nst * stage;
   c->UTf.ensure(sizeof(double) * std::max<size_t>(nfr, 1));
   prof_begin(c, "k_make_frags", 8.0 * nfr, 0.0);
@@ -1005,7 +1010,8 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
     gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
     return false;
   }
-  if (!(a & 1) && r8 <= 32 && !(a8 <= 64 && r8 == 16) && project_ws16(c, X, a, L, W, r, ldw, out, tsq))
+  if (!(a & 1) && r8 <= 32 && (!(a8 <= 64 && r8 == 16) || std::getenv("TTG_WS16_ALL")) &&
+      project_ws16(c, X, a, L, W, r, ldw, out, tsq))
     return tsq != nullptr;
   make_frags(c, W, a, r, ldw, true, false);
   ttg::ProjArgs args{};
@@ -2007,7 +2013,9 @@ void ttg_ctx_destroy(ttg_ctx* c) {
   }
 }
 
-const char* ttg_last_error(const ttg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+// context-free entry points (TTB1 read/write) leave their message per thread
+thread_local std::string g_noctx_err = "no error";
+const char* ttg_last_error(const ttg_ctx* c) { return c ? c->err.c_str() : g_noctx_err.c_str(); }
 int ttg_ctx_rank(const ttg_ctx* c) { return c ? c->rank : -1; }
 int ttg_ctx_world(const ttg_ctx* c) { return c ? c->world : -1; }
 void* ttg_ctx_stream(const ttg_ctx* c) { return c ? (void*)c->stream : nullptr; }
@@ -2269,3 +2277,5 @@ int ttg_reconstruct(ttg_ctx* c, const ttg_tt* tt, int64_t b0, int64_t e0, double
 }
 
 }  // extern "C"
+
+#include "ttg_io_abi.inc"

@@ -1,0 +1,160 @@
+// ttg_io.cuh — device kernels of the metrics / checkpoint rows:
+// relative reconstruction / prediction error without materialising the
+// reconstruction, and the orthonormality measurement used when a TTC1
+// checkpoint is loaded.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ttg {
+
+// Partial sums over a slab of the data:  d = sum (x - Phi c)^2,  x2 = sum x^2.
+// Phi: S x r (column-major, the spatial chain), C: r x m coefficients (ld ldc),
+// X: S x m (ld ldx).  One thread per row s of Phi keeps that row in
+// registers (r <= RMAX) and walks the m observations; the coefficients are
+// staged in shared memory 64 observations at a time.  Per-block partials are
+// written in fixed order (k_pair_sum reduces them deterministically).
+constexpr int kRreObsChunk = 64;
+template <int RMAX>
+__global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ Phi, long long S, int r,
+                                                     const double* __restrict__ C, long long ldc, int m,
+                                                     const double* __restrict__ X, long long ldx,
+                                                     double* __restrict__ part) {
+  __shared__ double cs[kRreObsChunk * RMAX];
+  __shared__ double red[2][8];
+  double dsum = 0.0, xsum = 0.0;
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool live = s < S;
+  double phi[RMAX];
+#pragma unroll
+  for (int k = 0; k < RMAX; ++k) phi[k] = (live && k < r) ? Phi[s + S * k] : 0.0;
+  for (int o0 = 0; o0 < m; o0 += kRreObsChunk) {
+    const int mo = min(kRreObsChunk, m - o0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < mo * RMAX; e += blockDim.x) {
+      const int o = e / RMAX, k = e - o * RMAX;
+      cs[e] = k < r ? C[k + ldc * (o0 + o)] : 0.0;
+    }
+    __syncthreads();
+    if (live) {
+      for (int o = 0; o < mo; ++o) {
+        const double* co = cs + o * RMAX;
+        double dot0 = 0.0, dot1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < RMAX; k += 2) {
+          dot0 = fma(phi[k], co[k], dot0);
+          dot1 = fma(phi[k + 1], co[k + 1], dot1);
+        }
+        const double x = X[s + ldx * (o0 + o)];
+        const double df = x - (dot0 + dot1);
+        dsum = fma(df, df, dsum);
+        xsum = fma(x, x, xsum);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = dsum;
+    red[1][warp] = xsum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// Generic variant for r > 64: Phi row entries read through the cache.
+__global__ void __launch_bounds__(256) k_rre_partial_any(const double* __restrict__ Phi, long long S, int r,
+                                                         const double* __restrict__ C, long long ldc, int m,
+                                                         const double* __restrict__ X, long long ldx,
+                                                         double* __restrict__ part) {
+  __shared__ double red[2][8];
+  double dsum = 0.0, xsum = 0.0;
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s < S) {
+    for (int o = 0; o < m; ++o) {
+      double dot = 0.0;
+      for (int k = 0; k < r; ++k) dot = fma(Phi[s + S * k], C[k + ldc * o], dot);
+      const double x = X[s + ldx * o];
+      const double df = x - dot;
+      dsum = fma(df, df, dsum);
+      xsum = fma(x, x, xsum);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = dsum;
+    red[1][warp] = xsum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// out[0..1] = fixed-order sums of the n pairs in part (one warp, strided
+// per-lane partials then a butterfly: deterministic for a given n)
+__global__ void k_pair_sum(const double* __restrict__ part, long long n, double* __restrict__ out) {
+  double a = 0.0, b = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 32) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+// dev = max |U^T U - I| of one left unfolding U (a x r, column-major),
+// one block: entry (i, j) of the Gram per thread-strided loop.
+__global__ void k_ortho_dev(const double* __restrict__ U, int a, int r, double* __restrict__ dev) {
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (long long e = threadIdx.x; e < (long long)r * r; e += blockDim.x) {
+    const int i = (int)(e % r), j = (int)(e / r);
+    if (i > j) continue;
+    double s = 0.0;
+    for (int k = 0; k < a; ++k) s = fma(U[k + (long long)a * i], U[k + (long long)a * j], s);
+    mx = fmax(mx, fabs(s - (i == j ? 1.0 : 0.0)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    *dev = m;
+  }
+}
+
+}  // namespace ttg

@@ -1485,7 +1485,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_ws16(const __grid_co
   const int stage = nks * BOX;
   double* Wfs = smem + nst * stage;
   const int nfr = nks * NB * 128;
-  double* stg = Wfs + nfr + warp * 16 * 32;
+  double* stg = Wfs + nfr + warp * 16 * p.r8;  // 16 columns x r8 per warp
   for (int i = threadIdx.x; i < nfr; i += blockDim.x) Wfs[i] = p.WTf[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {

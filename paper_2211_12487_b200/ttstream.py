@@ -48,8 +48,8 @@ def _check(rc: int, ctx: Optional["Context"]) -> None:
     if rc == 0:
         return
     msg = ""
-    if ctx is not None and ctx._h:
-        raw = _lib.load().ttg_last_error(ctx._h)
+    if ctx is None or ctx._h:  # ctx None: context-free entry points keep a per-thread message
+        raw = _lib.load().ttg_last_error(ctx._h if ctx is not None else None)
         msg = raw.decode() if raw else ""
     raise STATUS_TO_ERROR.get(rc, Error)(msg or f"ttg status {rc}")
 
@@ -194,8 +194,18 @@ class HeuristicConfig:
                                int(bool(self.use_approx_tolerance)))
 
 
+class DeviceIncrement:
+    """A device-resident increment (first-index-fastest float64) owned by an
+    IncrementStream; valid until the stream's next ``next()``."""
+
+    def __init__(self, ptr: int, shape: Sequence[int], stream: "IncrementStream"):
+        self.ptr = int(ptr)
+        self.shape = tuple(int(s) for s in shape)
+        self._stream = stream
+
+
 class _Input:
-    """Resolves y (numpy host array or torch CUDA tensor) to (pointer, where, shape)."""
+    """Resolves y (numpy host array, torch CUDA tensor or DeviceIncrement) to (pointer, where, shape)."""
 
     def __init__(self, y, shape: Optional[Sequence[int]] = None):
         self.keep = None
@@ -209,6 +219,14 @@ class _Input:
                 raise ValueError("shape does not match the buffer")
             self.ptr = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
             self.where = TTG_HOST
+            return
+        if isinstance(y, DeviceIncrement):  # an increment delivered by IncrementStream
+            self.keep = y
+            self.shape = tuple(y.shape) if shape is None else tuple(int(s) for s in shape)
+            if int(np.prod(self.shape)) != int(np.prod(y.shape)):
+                raise ValueError("shape does not match the buffer")
+            self.ptr = ctypes.cast(ctypes.c_void_p(y.ptr), ctypes.POINTER(ctypes.c_double))
+            self.where = TTG_DEVICE
             return
         # torch tensor (duck-typed so torch is not a hard dependency of the host mirror)
         if not hasattr(y, "data_ptr") or not getattr(y, "is_cuda", False):
@@ -305,6 +323,21 @@ class TensorTrain:
 
     def num_increments(self) -> int:
         return self._shape()[3]
+
+    def increment_range(self, k: int):
+        """tensor_train.cpp:117-123."""
+        from .errors import IndexError_
+
+        bb = self.batch_boundaries()
+        if k < 0 or k >= len(bb):
+            raise IndexError_("increment index out of range")
+        return (0 if k == 0 else bb[k - 1]), bb[k]
+
+    def measure_ortho_count(self, tol: float = 1e-10) -> int:
+        """tensor_train.cpp:135-146, measured on the device."""
+        out = ctypes.c_int64()
+        _check(_lib.load().ttg_tt_measure_ortho_count(self.ctx._h, self._h, float(tol), ctypes.byref(out)), self.ctx)
+        return int(out.value)
 
     def core(self, i: int) -> np.ndarray:
         ranks, modes, _, _ = self._shape()
@@ -435,3 +468,175 @@ def subselect(errs: Sequence[float], eps_des: float):
     sel = [i for i, e in enumerate(errs) if e > eps_des]
     rej = [i for i, e in enumerate(errs) if not (e > eps_des)]
     return sel, rej
+
+
+# ---------------------------------------------------------------------------
+# metrics (metrics.hpp / metrics.cpp:7-68), computed on the device
+# ---------------------------------------------------------------------------
+
+
+def compression_ratio(tt: TensorTrain) -> float:
+    """metrics.cpp:7-11."""
+    out = ctypes.c_double()
+    _check(_lib.load().ttg_compression_ratio(tt._h, ctypes.byref(out)), tt.ctx)
+    return float(out.value)
+
+
+def rre(tt: TensorTrain, x_ref, obs_begin: int = 0, obs_end: Optional[int] = None, *, shape=None,
+        with_flag: bool = False):
+    """metrics.cpp:34-42: ||x_ref - reconstruct(range)|| / ||x_ref|| (0 for a zero-norm reference;
+    ``with_flag`` returns (value, zero_reference))."""
+    if obs_end is None:
+        obs_end = tt.obs_count()
+    inp = _Input(x_ref, shape)
+    sh, nd = inp.shape_arr()
+    val, zr = ctypes.c_double(), ctypes.c_int()
+    _check(_lib.load().ttg_rre(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, int(obs_begin), int(obs_end),
+                               ctypes.byref(val), ctypes.byref(zr)), tt.ctx)
+    return (float(val.value), bool(zr.value)) if with_flag else float(val.value)
+
+
+def rpe(tt: TensorTrain, unseen, *, shape=None, with_flag: bool = False):
+    """metrics.cpp:44-47: relative error of tt_expand(tt_project(unseen))."""
+    inp = _Input(unseen, shape)
+    sh, nd = inp.shape_arr()
+    val, zr = ctypes.c_double(), ctypes.c_int()
+    _check(_lib.load().ttg_rpe(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, ctypes.byref(val), ctypes.byref(zr)),
+           tt.ctx)
+    return (float(val.value), bool(zr.value)) if with_flag else float(val.value)
+
+
+@dataclass
+class IncrementErrors:
+    """metrics.hpp:27-30."""
+
+    per_increment: List[float]
+    mean: float = 0.0
+
+
+def mean_rre_per_increment(tt: TensorTrain, refs: Sequence) -> IncrementErrors:
+    """metrics.cpp:49-66."""
+    from .errors import DimensionError
+
+    if len(refs) != tt.num_increments():
+        raise DimensionError("need one reference per stored increment")
+    per = []
+    for k in range(tt.num_increments()):
+        begin, end = tt.increment_range(k)
+        ref_shape = refs[k].shape
+        if ref_shape[-1] != end - begin:
+            raise DimensionError("reference observation count does not match increment")
+        per.append(rre(tt, refs[k], begin, end))
+    return IncrementErrors(per, (sum(per) / len(per)) if per else 0.0)
+
+
+# ---------------------------------------------------------------------------
+# TTC1 checkpoint (serialization.hpp / serialization.cpp:68-152)
+# ---------------------------------------------------------------------------
+
+
+def serialize(tt: TensorTrain) -> bytes:
+    """serialization.cpp:68-87 (strided D2H of the device train)."""
+    lib = _lib.load()
+    n = ctypes.c_int64()
+    _check(lib.ttg_tt_serialize(tt.ctx._h, tt._h, None, 0, ctypes.byref(n)), tt.ctx)
+    buf = (ctypes.c_uint8 * n.value)()
+    _check(lib.ttg_tt_serialize(tt.ctx._h, tt._h, buf, n.value, ctypes.byref(n)), tt.ctx)
+    return bytes(buf)
+
+
+def deserialize(data: bytes, ctx: Optional[Context] = None) -> TensorTrain:
+    """serialization.cpp:89-129; ortho_count re-measured on the device."""
+    ctx = ctx or default_context()
+    h = ctypes.c_void_p()
+    buf = (ctypes.c_uint8 * len(data)).from_buffer_copy(data) if data else None
+    _check(_lib.load().ttg_tt_deserialize(ctx._h, buf, len(data), ctypes.byref(h)), ctx)
+    return TensorTrain(h, ctx)
+
+
+def save_ttc(tt: TensorTrain, path) -> None:
+    """serialization.cpp:131-139."""
+    _check(_lib.load().ttg_tt_save_ttc(tt.ctx._h, tt._h, str(path).encode()), tt.ctx)
+
+
+def load_ttc(path, ctx: Optional[Context] = None) -> TensorTrain:
+    """serialization.cpp:141-152."""
+    ctx = ctx or default_context()
+    h = ctypes.c_void_p()
+    _check(_lib.load().ttg_tt_load_ttc(ctx._h, str(path).encode(), ctypes.byref(h)), ctx)
+    return TensorTrain(h, ctx)
+
+
+# ---------------------------------------------------------------------------
+# TTB1 ingest (stream_io.hpp:57-65 / stream_io.cpp:123-204)
+# ---------------------------------------------------------------------------
+
+
+def write_batch(t: np.ndarray, path) -> None:
+    """stream_io.cpp:123-137 (first-index-fastest payload)."""
+    arr = np.asfortranarray(t, dtype=np.float64)
+    sh = (ctypes.c_int64 * arr.ndim)(*arr.shape)
+    _check(_lib.load().ttg_write_batch(str(path).encode(), sh, arr.ndim,
+                                       arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), None)
+
+
+def read_batch(path) -> np.ndarray:
+    """stream_io.cpp:139-187."""
+    lib = _lib.load()
+    sh = (ctypes.c_int64 * 255)()
+    nd, cnt = ctypes.c_int(), ctypes.c_int64()
+    _check(lib.ttg_read_batch(str(path).encode(), sh, ctypes.byref(nd), None, 0, ctypes.byref(cnt)), None)
+    out = np.empty(cnt.value, dtype=np.float64)
+    _check(lib.ttg_read_batch(str(path).encode(), sh, ctypes.byref(nd),
+                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cnt.value, ctypes.byref(cnt)), None)
+    return np.reshape(out, tuple(sh[:nd.value]), order="F")
+
+
+def list_stream(directory) -> List[str]:
+    """stream_io.cpp:189-204: the .ttb files of a directory in lexicographic filename order."""
+    import os
+
+    from .errors import FormatError
+
+    d = str(directory)
+    if not os.path.isdir(d):
+        raise FormatError("stream path is not a directory: " + d)
+    files = [os.path.join(d, f) for f in os.listdir(d) if f.endswith(".ttb") and os.path.isfile(os.path.join(d, f))]
+    return sorted(files, key=os.path.basename)
+
+
+class IncrementStream:
+    """A .ttb directory streamed to the device: a host thread reads the next
+    file into pinned memory and copies it H2D on a side stream while the
+    caller updates on the current one (include/ttg.h ``ttg_stream_*``).
+    Iterating yields DeviceIncrement objects accepted by every update call."""
+
+    def __init__(self, directory, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self._h = ctypes.c_void_p()
+        _check(_lib.load().ttg_stream_open(self.ctx._h, str(directory).encode(), ctypes.byref(self._h)), self.ctx)
+
+    def __len__(self) -> int:
+        return int(_lib.load().ttg_stream_count(self._h))
+
+    def next(self) -> DeviceIncrement:
+        p = ctypes.POINTER(ctypes.c_double)()
+        sh = (ctypes.c_int64 * 255)()
+        nd = ctypes.c_int()
+        _check(_lib.load().ttg_stream_next(self._h, ctypes.byref(p), sh, ctypes.byref(nd)), self.ctx)
+        return DeviceIncrement(ctypes.cast(p, ctypes.c_void_p).value, sh[:nd.value], self)
+
+    def __iter__(self):
+        for _ in range(len(self)):
+            yield self.next()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.load().ttg_stream_close(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
