@@ -96,6 +96,8 @@ int ttg_ctx_create(int device, ttg_ctx** out);
 int ttg_nccl_unique_id(uint8_t out[128]);
 int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[128], ttg_ctx** out);
 void ttg_ctx_destroy(ttg_ctx* ctx);
+/* ctx = NULL: the message of the calling thread's last context-free call (ttg_read_batch /
+ * ttg_write_batch). */
 const char* ttg_last_error(const ttg_ctx* ctx);
 int ttg_ctx_rank(const ttg_ctx* ctx);
 int ttg_ctx_world(const ttg_ctx* ctx);

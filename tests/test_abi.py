@@ -77,7 +77,12 @@ def test_null_arguments_return_status_without_gpu(lib):
     L = _lib.load()
     assert L.ttg_ctx_create(0, None) == 10  # TTG_E_ARGUMENT
     assert L.ttg_tt_num_cores(None) == -1
-    assert L.ttg_last_error(None) == b"null context"
+    # ctx NULL: the message of the calling thread's last context-free call (TTB1)
+    import ctypes
+
+    nd, cnt = ctypes.c_int(), ctypes.c_int64()
+    assert L.ttg_read_batch(b"/nonexistent/x.ttb", None, ctypes.byref(nd), None, 0, ctypes.byref(cnt)) == 4
+    assert L.ttg_last_error(None).startswith(b"cannot open")
 
 
 def test_host_mirror_pure_helpers():
