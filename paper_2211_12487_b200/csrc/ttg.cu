@@ -18,7 +18,11 @@
 #include <cudaTypedefs.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
