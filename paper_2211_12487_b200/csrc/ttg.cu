@@ -339,6 +339,21 @@ constexpr int kFastMax = 128;  // a8 / r8 limit of the fused DMMA tiles
 // ---- residual Gram -----------------------------------------------------------
 constexpr int kFastMax1 = 256;  // a8 limit of the single-buffered DMMA tiles
 
+// fixed-order two-stage reduction of nx per-CTA partials into c->G (a x a)
+void gram_reduce(ttg_ctx* c, int nx, int layout, int ld, int a, double* G) {
+  const long long n = (long long)a * a;
+  const int xs = std::max(1, std::min(32, nx / 8));
+  c->Mtmp.ensure(sizeof(double) * (size_t)(xs * n));
+  const int gxb = (int)std::min<long long>((n + 255) / 256, 1024);
+  prof_begin(c, "k_gram_reduce", 8.0 * (double)nx * n / 2, (double)nx * n / 2);
+  ttg::k_gram_reduce_s1<<<dim3(gxb, xs), 256, 0, c->stream>>>(c->partials.as<double>(), nx, layout, ld, a,
+                                                               c->Mtmp.as<double>());
+  post_launch(c);
+  prof_begin(c, "k_gram_reduce", 8.0 * (double)xs * n / 2, (double)xs * n / 2);
+  ttg::k_gram_reduce_s2<<<gxb, 256, 0, c->stream>>>(c->Mtmp.as<double>(), xs, a, G);
+  post_launch(c);
+}
+
 template <int WBR, int WBC, bool PRE, bool DB>
 void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem, int npairs) {
   auto kern = ttg::k_gram_resid<WBR, WBC, PRE, DB>;
@@ -362,10 +377,8 @@ void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem, int npair
   post_launch(c);
   const int a = args.a;
   const long long n = (long long)a * a;
-  prof_begin(c, "k_gram_reduce", 8.0 * npairs * gx * SBD * SBD, (double)gx * a * a);
-  ttg::k_gram_reduce<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, SBD, a,
-                                                                      c->G.as<double>());
-  post_launch(c);
+  (void)n;
+  gram_reduce(c, gx, 0, SBD, a, c->G.as<double>());
 }
 
 // The current unfolding cur_i (a_i x L_i) over a stored buffer:
@@ -493,7 +506,7 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
 
 
 // ---- raw Gram (SYRK) ---------------------------------------------------------
-template <int MAXT>
+template <int MAXT, int NCW = ttg::kConsumerWarps>
 void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) {
   constexpr int SBD = 128;
   const bool two = npairs > 1;  // some pairs carry two slices
@@ -505,8 +518,9 @@ void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) 
   else nst = (int)std::max<size_t>(1, std::min<size_t>(ttg::kMaxStages, (216 * 1024) / stage));
   args.nst = nst;
   const size_t smem = nst * stage;
-  auto kern = ttg::k_syrk<MAXT>;
-  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, ttg::kSyrkThreads, smem));
+  auto kern = ttg::k_syrk<MAXT, NCW>;
+  constexpr int threads = (NCW + 1) * 32;
+  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, threads, smem));
   long long want = std::max<long long>(1, (long long)c->num_sms * occ / npairs);
   int gx = (int)std::min<long long>(want, std::max<long long>(1, args.n_tiles));
   c->partials.ensure(sizeof(double) * (size_t)npairs * gx * SBD * SBD);
@@ -515,14 +529,12 @@ void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) 
   std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
   const double Ls = (double)args.L * sel_frac;
   prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
-  kern<<<dim3(gx, npairs), ttg::kSyrkThreads, smem, c->stream>>>(args);
+  kern<<<dim3(gx, npairs), threads, smem, c->stream>>>(args);
   post_launch(c);
   const int a = args.a;
   const long long n = (long long)a * a;
-  prof_begin(c, "k_gram_reduce", 8.0 * npairs * gx * SBD * SBD, (double)gx * a * a);
-  ttg::k_gram_reduce<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, SBD, a,
-                                                                      c->G.as<double>());
-  post_launch(c);
+  (void)n;
+  gram_reduce(c, gx, 0, SBD, a, c->G.as<double>());
 }
 
 // 2-D tensor map of X (a x L, column-major) with 16 x 64 boxes and 128-byte
@@ -570,10 +582,8 @@ void launch_syrk2_t(ttg_ctx* c, const CUtensorMap& tm, ttg::Syrk2Args args, int 
   kern<<<dim3(gx, parts), ttg::kSyrkThreads, smem, c->stream>>>(tm, args);
   post_launch(c);
   const long long n = (long long)args.a * args.a;
-  prof_begin(c, "k_gram_reduce", 8.0 * gx * args.a8 * args.a8, (double)gx * n);
-  ttg::k_gram_reduce2<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, args.a8, args.a,
-                                                                       c->G.as<double>());
-  post_launch(c);
+  (void)n;
+  gram_reduce(c, gx, 1, args.a8, args.a, c->G.as<double>());
 }
 
 // Warp-specialised m16n8k16 SYRK (k_syrk_ws16) for even a <= 128 into c->G.
@@ -611,10 +621,8 @@ void launch_syrk_ws16_t(ttg_ctx* c, const CUtensorMap& tm, ttg::Syrk2Args args, 
   kern<<<gx, threads, smem, c->stream>>>(tm, args);
   post_launch(c);
   const long long n = (long long)args.a * args.a;
-  prof_begin(c, "k_gram_reduce", 8.0 * gx * args.a8 * args.a8, (double)gx * n);
-  ttg::k_gram_reduce2<<<grid_for(n, 256, 4096), 256, 0, c->stream>>>(c->partials.as<double>(), gx, args.a8, args.a,
-                                                                       c->G.as<double>());
-  post_launch(c);
+  (void)n;
+  gram_reduce(c, gx, 1, args.a8, args.a, c->G.as<double>());
 }
 
 bool syrk_ws16(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
@@ -1936,7 +1944,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
         (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
         (const void*)ttg::k_syrk<8>, (const void*)ttg::k_syrk2<1>, (const void*)ttg::k_syrk2<2>,
-        (const void*)ttg::k_syrk2<3>, (const void*)ttg::k_gram_reduce2, (const void*)ttg::k_make_frags16,
+        (const void*)ttg::k_syrk2<3>, (const void*)ttg::k_gram_reduce2, (const void*)ttg::k_gram_reduce_s1, (const void*)ttg::k_gram_reduce_s2, (const void*)ttg::k_make_frags16,
         (const void*)ttg::k_project_ws16<4, 1>, (const void*)ttg::k_project_ws16<4, 2>,
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,

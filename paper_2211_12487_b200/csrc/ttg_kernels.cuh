@@ -533,8 +533,8 @@ __device__ __forceinline__ void syrk_issue(const SyrkArgs& p, long long q0, int 
 // full[s] / empty[s] mbarriers per ring stage; no block-wide barrier in the
 // main loop.
 
-template <int MAXT>
-__global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
+template <int MAXT, int NCW = kConsumerWarps>
+__global__ void __launch_bounds__((NCW + 1) * 32) k_syrk(SyrkArgs p) {
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ double red8[kConsumerWarps + 1];
@@ -552,13 +552,13 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
   if (threadIdx.x == 0)
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], NCW);
     }
   __syncthreads();
   auto Ti_of = [&](int s) { return smem + (size_t)s * per_stage; };
   auto Tj_of = [&](int s) { return two ? smem + (size_t)s * per_stage + (size_t)ldt * kTC : smem + (size_t)s * per_stage; };
 
-  if (warp == kConsumerWarps) {  // ---- producer ----
+  if (warp == NCW) {  // ---- producer ----
     int it = 0;
     for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
       const int st = it % nst;
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
   bool okA1[MAXT], okB1[MAXT], live[MAXT];
 #pragma unroll
   for (int u = 0; u < MAXT; ++u) {
-    const int idx = warp + kConsumerWarps * u;
+    const int idx = warp + NCW * u;
     live[u] = idx < ntiles;
     int ta = 0, tb = 0;
     if (two) {
@@ -648,15 +648,17 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
     mbar_wait(&full[st], (unsigned)((it / nst) & 1));
     const double* Ti = Ti_of(st);
     const double* Tj = Tj_of(st);
-    if (p.tsumsq) {  // per-(tile, warp) sum of squares (single full-height slice only)
-      double sq = 0.0;
-      for (int e = lane + 32 * warp; e < nri * kTC; e += 32 * kConsumerWarps) {
-        const int c = e / nri, r = e - c * nri;
-        const double vv = Ti[r + ldt * c];
-        sq = fma(vv, vv, sq);
+    if (p.tsumsq) {  // per-(tile, 8 virtual warps) sums of squares (single full-height slice only)
+      for (int v = warp; v < kConsumerWarps; v += NCW) {
+        double sq = 0.0;
+        for (int e = lane + 32 * v; e < nri * kTC; e += 32 * kConsumerWarps) {
+          const int c = e / nri, r = e - c * nri;
+          const double vv = Ti[r + ldt * c];
+          sq = fma(vv, vv, sq);
+        }
+        sq = warp_sum(sq);
+        if (lane == 0) p.tsumsq[tile * kConsumerWarps + v] = sq;
       }
-      sq = warp_sum(sq);
-      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = sq;
     }
 #pragma unroll
     for (int u = 0; u < MAXT; ++u) {
@@ -691,6 +693,54 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk(SyrkArgs p) {
         out[r + SBD * c] = acc[u][x][y][0];
         out[r + SBD * (c + 1)] = acc[u][x][y][1];
       }
+  }
+}
+
+// Two-stage fixed-order reduction of per-CTA Gram partials (hundreds of
+// CTAs): stage 1 sums x-chunks of the partials for every lower-triangle
+// element (blockIdx.y = chunk, four independent accumulators), stage 2 sums
+// the chunks in order and mirrors the result.  layout 0: k_syrk super-tile
+// pairs (ld sbd, pair py = I(I+1)/2 + J, CTA stride npairs-major); layout 1:
+// one a8 x a8 partial per CTA.
+__global__ void k_gram_reduce_s1(const double* __restrict__ partials, int nx, int layout, int ld, int a,
+                                 double* __restrict__ tmp) {
+  const int xs = gridDim.y, y = blockIdx.y;
+  const int x0 = (int)((long long)nx * y / xs), x1 = (int)((long long)nx * (y + 1) / xs);
+  const long long n = (long long)a * a;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % a), j = (int)(e / a);
+    if (i < j) continue;
+    long long base, stride;
+    if (layout == 0) {
+      const int I = i / ld, J = j / ld;
+      const int py = I * (I + 1) / 2 + J;
+      stride = (long long)ld * ld;
+      base = (long long)py * nx * stride + (i - I * ld) + (long long)ld * (j - J * ld);
+    } else {
+      stride = (long long)ld * ld;
+      base = i + (long long)ld * j;
+    }
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int x = x0;
+    for (; x + 3 < x1; x += 4) {
+      s0 += partials[base + stride * x];
+      s1 += partials[base + stride * (x + 1)];
+      s2 += partials[base + stride * (x + 2)];
+      s3 += partials[base + stride * (x + 3)];
+    }
+    for (; x < x1; ++x) s0 += partials[base + stride * x];
+    tmp[(long long)y * n + e] = (s0 + s1) + (s2 + s3);
+  }
+}
+__global__ void k_gram_reduce_s2(const double* __restrict__ tmp, int xs, int a, double* __restrict__ G) {
+  const long long n = (long long)a * a;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % a), j = (int)(e / a);
+    if (i < j) continue;
+    double s = 0.0;
+    for (int y = 0; y < xs; ++y) s += tmp[(long long)y * n + e];
+    G[e] = s;
+    G[j + (long long)a * i] = s;
   }
 }
 
