@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libttg.so")
+# TTG_LIB overrides the in-tree build (A/B timing of two builds on one box)
+LIB_PATH = os.environ.get("TTG_LIB") or os.path.join(_HERE, "libttg.so")
 
 MAX_CORES = 32
 
