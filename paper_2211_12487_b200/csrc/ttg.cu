@@ -516,6 +516,10 @@ void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) 
   if (3 * 2 * stage <= 220 * 1024) nst = 2;
   else if (2 * 3 * stage <= 220 * 1024) nst = 3;
   else nst = (int)std::max<size_t>(1, std::min<size_t>(ttg::kMaxStages, (216 * 1024) / stage));
+  if (const char* e = std::getenv("TTG_SYRK_NST")) {  // tuning override (kept only when it fits)
+    const int want = std::atoi(e);
+    if (want >= 1 && want <= ttg::kMaxStages && want * stage <= 220 * 1024) nst = want;
+  }
   args.nst = nst;
   const size_t smem = nst * stage;
   auto kern = ttg::k_syrk<MAXT, NCW>;
