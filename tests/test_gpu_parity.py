@@ -77,6 +77,14 @@ def test_wide_unfoldings(ctx, algo):
     run_stream(ctx, s, 6, algo)
 
 
+@pytest.mark.parametrize("algo", ["ice", "star"])
+def test_ranks_17_to_20(ctx, algo):
+    """Bond ranks 17..19 (projections with two MMA n-blocks + DFMA rows, r8 = 24
+    paths): modes 6^5, batch 40, true rank 17."""
+    s = Stream(3, seed=21, modes=(6,) * 5, batch=40, true_rank=17)
+    run_stream(ctx, s, 6, algo)
+
+
 def test_cfg1_video_small_batch(ctx):
     """BASELINE configs[1] shape (14,15,16,10,3) at batch 10, 6 increments."""
     s = Stream(1, seed=0, batch=10)
