@@ -125,7 +125,7 @@ struct ttg_ctx {
   int num_sms = 148;
   size_t smem_optin = 232448;
   // workspaces (grow-only)
-  DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, Uf, Upad, scratch, eigres, on2, sumsq_part,
+  DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, UTt, Uf, Upad, scratch, eigres, on2, sumsq_part,
       scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2], tsq, psif, wcomb, psi[2],
       spsi[2], scoeffs, matbuf, tmp, Craw, small[4];
   std::vector<DevBuf> scur;       // TT-ICE* stats-chain intermediates (reused by the sweep)
@@ -1019,9 +1019,106 @@ bool project_ws16(ttg_ctx* c, const double* X, int a, long long L, const double*
   return true;
 }
 
+// K-chunked projection (k_project_kc) for even a and r <= 34: n-blocks of 8
+// rows by DMMA plus a DFMA tail of 1-2 rows when r = 8 NB + {1, 2}.  Tall
+// sources (a > 64) stream in 64-row stages with the accumulators held in
+// registers.  False when the operand does not qualify.
+template <int NCW, int NB, int T>
+void* kc_kernel() {
+  return (void*)ttg::k_project_kc<NCW, NB, T>;
+}
+template <int NCW>
+void* kc_pick_t(int NB, int T) {
+  switch (NB * 3 + T) {
+    case 3: return kc_kernel<NCW, 1, 0>();
+    case 4: return kc_kernel<NCW, 1, 1>();
+    case 5: return kc_kernel<NCW, 1, 2>();
+    case 6: return kc_kernel<NCW, 2, 0>();
+    case 7: return kc_kernel<NCW, 2, 1>();
+    case 8: return kc_kernel<NCW, 2, 2>();
+    case 9: return kc_kernel<NCW, 3, 0>();
+    case 10: return kc_kernel<NCW, 3, 1>();
+    case 11: return kc_kernel<NCW, 3, 2>();
+    case 12: return kc_kernel<NCW, 4, 0>();
+    case 13: return kc_kernel<NCW, 4, 1>();
+    case 14: return kc_kernel<NCW, 4, 2>();
+  }
+  return nullptr;
+}
+void* kc_pick(int ncw, int NB, int T) { return ncw == 8 ? kc_pick_t<8>(NB, T) : kc_pick_t<4>(NB, T); }
+
+bool project_kc(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
+                double* tsq) {
+  if (std::getenv("TTG_NO_KC") || (a & 1) || r > 34 || r < 1) return false;
+  int NB = (r + 7) / 8, T = 0;
+  if (r > 8 && (r % 8 == 1 || r % 8 == 2) && !std::getenv("TTG_NO_TAIL")) {
+    NB = r / 8;
+    T = r % 8;
+  }
+  if (NB > 4) return false;
+  // 8 consumer warps (128-column tiles, 2 warps per SM sub-partition) for
+  // tall sources; 4 (64-column tiles, 2 CTAs / SM) when the whole tile fits
+  const int nks = (a + 15) / 16;
+  int ncw = nks > 4 ? 8 : 4;
+  if (std::getenv("TTG_KC_NCW")) ncw = std::atoi(std::getenv("TTG_KC_NCW")) == 8 ? 8 : 4;
+  const int tc = 16 * ncw;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, X, a, L, tc)) return false;
+  const int kc = std::min(nks, std::getenv("TTG_KC") ? std::max(1, std::atoi(std::getenv("TTG_KC"))) : 4);
+  const size_t nfr = (size_t)nks * NB * 128, ntl = (size_t)nks * T * 16;
+  const size_t stage = sizeof(double) * (size_t)kc * 16 * tc;
+  const size_t fixed = 1024 + sizeof(double) * (nfr + ntl + (size_t)ncw * 16 * (8 * NB + T));
+  const size_t cap = (size_t)c->smem_optin - 1024;
+  if (fixed + 2 * stage > cap) return false;
+  int nst = 2;
+  if (2 * (fixed + 2 * stage) > 220 * 1024) {  // one CTA / SM: deepen the ring
+    while (nst < ttg::kProjStages && fixed + (nst + 1) * stage <= cap) ++nst;
+  } else {
+    while (nst < ttg::kProjStages && 2 * (fixed + (nst + 1) * stage) <= 220 * 1024 && (nst + 1) * kc <= 2 * nks) ++nst;
+  }
+  if (std::getenv("TTG_KC_NST")) nst = std::max(2, std::min(ttg::kProjStages, std::atoi(std::getenv("TTG_KC_NST"))));
+  const size_t smem = fixed + nst * stage;
+  if (smem > cap) return false;
+  c->UTf.ensure(sizeof(double) * std::max<size_t>(nfr, 1));
+  prof_begin(c, "k_make_frags16", 8.0 * nfr, 0.0);
+  ttg::k_make_frags16<<<grid_for((long long)nfr, 256, 256), 256, 0, c->stream>>>(W, a, r, ldw, nks, NB,
+                                                                                 c->UTf.as<double>());
+  post_launch(c);
+  if (T) {
+    c->UTt.ensure(sizeof(double) * std::max<size_t>(ntl, 1));
+    prof_begin(c, "k_make_tail", 8.0 * ntl, 0.0);
+    ttg::k_make_tail<<<grid_for((long long)ntl, 256, 64), 256, 0, c->stream>>>(W, a, ldw, nks, 8 * NB, T,
+                                                                               c->UTt.as<double>());
+    post_launch(c);
+  }
+  ttg::ProjArgs args{};
+  args.src = ttg::TileSrc{X, a, L, nullptr, 1};
+  args.a8 = ttg::round_up(a, 8);
+  args.WTf = c->UTf.as<double>();
+  args.WTt = T ? c->UTt.as<double>() : nullptr;
+  args.r = r;
+  args.r8 = 8 * NB + T;
+  args.out = out;
+  args.tsumsq = tsq;
+  args.n_tiles = (L + tc - 1) / tc;
+  args.nst = nst;
+  args.kc = kc;
+  auto kern = reinterpret_cast<void (*)(const CUtensorMap, ttg::ProjArgs)>(kc_pick(ncw, NB, T));
+  const int threads = (ncw + 1) * 32;
+  const int occ = std::max(kernel_occupancy((const void*)kern, kern, threads, smem), 1);
+  const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
+  prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
+  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  post_launch(c);
+  return true;
+}
+
 bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
              double* tsq = nullptr) {
   const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
+  if (project_kc(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;
   if (a8 > kFastMax1 || r8 > kFastMax) {
     gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
     return false;
@@ -1515,8 +1612,18 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
   return out;
 }
 
-// Projection of Y through the train's current cores (same fusion plan as the
-// sweep).  cache=true keeps the materialised intermediates (c->scur) and the
+// projection-only chains fuse further: the next projection reads the same
+// buffer through the combined interface when k_project_kc takes it (even rows
+// <= kProjFuseMax, r <= 34), so Y -> r_3 x L_3 at cfg3 is one pass (no cur_2).
+constexpr int kProjFuseMax = 512;
+bool can_fuse_proj(const Src& s, int64_t n_i, int64_t n_next, int64_t r_next) {
+  const int64_t rows = s.As * n_i * n_next;
+  if (std::getenv("TTG_NO_PROJ_FUSE")) return rows <= kFastMax && r_next <= kFastMax;
+  return rows <= kProjFuseMax && !(rows & 1) && r_next <= 34;
+}
+
+// Projection of Y through the train's current cores (projection-only fusion
+// plan, can_fuse_proj).  cache=true keeps the materialised intermediates (c->scur) and the
 // coefficients (c->scoeffs) for reuse by a following TT-ICE* sweep.
 const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, bool cache, Norms& nm) {
   const int d = tt->d;
@@ -1536,7 +1643,7 @@ const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64
     if (i + 1 < d) {
       const int64_t n_next = tt->modes[i + 1];
       const int64_t rr = tt->ranks[i + 2];
-      if (can_fuse(src, n_i, r, n_next, rr)) {
+      if (can_fuse_proj(src, n_i, n_next, rr)) {
         const double* psi = src.Psi ? combine_psi(c, src, n_i, Ui, r, c->spsi[pf]) : Ui;
         if (src.Psi) pf ^= 1;
         src = Src{src.S, src.As * n_i, L, psi, r};
@@ -1952,7 +2059,12 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_ws16<4, 1>, (const void*)ttg::k_project_ws16<4, 2>,
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
-        (const void*)ttg::k_sum_vec};
+        (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail};
+    for (int nb = 1; nb <= 4; ++nb)
+      for (int t = 0; t <= 2; ++t) {
+        CK(cudaFuncGetAttributes(&fa, kc_pick(4, nb, t)));
+        CK(cudaFuncGetAttributes(&fa, kc_pick(8, nb, t)));
+      }
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));
   }
   CK(cudaMallocHost((void**)&c->h_eig, sizeof(ttg::EigResult)));

@@ -890,6 +890,8 @@ struct ProjArgs {
   long long n_tiles;
   int frag_smem;      // stage W^T fragments in shared memory
   int nst;            // ring stages (k_project_ring)
+  int kc;             // k-steps (16-row boxes) per ring stage (k_project_kc)
+  const double* WTt;  // DFMA tail weights (k_make_tail layout, k_project_kc)
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
@@ -1610,6 +1612,178 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_ws16(const __grid_co
         const int row = 8 * nb + 2 * t + (i & 1);
         if (row < p.r) stg[row + p.r * (g + 8 * (i >> 1))] = acc[nb][i];
       }
+    __syncwarp();
+    const long long colw = tile * TC + 16 * warp;
+    const int nval = (int)max(0LL, min(16LL, p.src.L - colw));
+    double* dst = p.out + colw * p.r;
+    const int n = nval * p.r;
+    for (int e = lane; e < n; e += 32) dst[e] = stg[e];
+    if (want_ss) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ss0 += __shfl_xor_sync(0xffffffffu, ss0, o);
+        ss1 += __shfl_xor_sync(0xffffffffu, ss1, o);
+      }
+      if (lane == 0) {
+        const long long c64 = colw >> 6;
+        const int grp = (int)((colw & 63) >> 3);
+        p.tsumsq[c64 * kConsumerWarps + grp] = ss0;
+        p.tsumsq[c64 * kConsumerWarps + grp + 1] = ss1;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// W columns [c0, c0 + T) (the rows of out past the 8 NB DMMA rows) for the
+// DFMA tail of k_project_kc:  Wt[((b T + j) 4 + t) 4 + q] = W[16b + 4q + t][c0 + j]
+// (zero past a), so lane (g, t) reads its four k values of box b as two double2.
+__global__ void k_make_tail(const double* __restrict__ W, int a, int ld, int nks, int c0, int T,
+                            double* __restrict__ Wt) {
+  const int n = nks * T * 16;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int q = e & 3, t = (e >> 2) & 3, f = e >> 4;
+    const int j = f % T, b = f / T;
+    const int row = 16 * b + 4 * q + t;
+    Wt[e] = row < a ? W[row + (long long)ld * (c0 + j)] : 0.0;
+  }
+}
+
+// K-chunked warp-specialised projection out (r x L) = W^T X for any even a
+// (the whole pre-projected chain of several modes, a = 512 at cfg3, in one
+// pass over Y).  A tile is TC = 16 NCW columns; its ceil(a/16) boxes stream
+// through the ring kc boxes per stage while each consumer warp keeps its 16
+// columns' accumulators in registers across the stages (so the ring depth
+// does not shrink with a).  Rows of out: 8 NB by m16n8k16 DMMA (W fragments
+// k-step-major in smem, as k_project_ws16) plus T = r - 8 NB in {1, 2} by DFMA
+// on the A fragments already in registers (W tail in smem, k_make_tail):
+// r = 17 costs 2 + 1/8 n-blocks of FP64 work instead of padding to 24.
+// The tail partial sums are reduced over the 4 lanes t of a column group.
+template <int NCW, int NB, int T>
+__global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  constexpr int TC = 16 * NCW, BOX = 16 * TC;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kProjStages], empty[kProjStages];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nst = p.nst, kc = p.kc;
+  const int nks = (p.src.a + 15) >> 4;
+  const int nch = (nks + kc - 1) / kc;
+  const int stage = kc * BOX;
+  double* Wfs = smem + nst * stage;
+  const int nfr = nks * NB * 128;
+  double* Wts = Wfs + nfr;
+  const int ntl = nks * T * 16;
+  double* stg = Wts + ntl + warp * 16 * (8 * NB + T);  // 16 columns x r per warp
+  for (int i = threadIdx.x; i < nfr; i += blockDim.x) Wfs[i] = p.WTf[i];
+  for (int i = threadIdx.x; i < ntl; i += blockDim.x) Wts[i] = p.WTt[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long grid = gridDim.x;
+  if (warp == NCW) {  // ---- producer ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      int it = 0, s = 0;
+      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+        for (int ch = 0; ch < nch; ++ch, ++it) {
+          if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
+          const int b0 = ch * kc, nb = min(kc, nks - b0);
+          mbar_expect_tx(&full[s], (unsigned)nb * BOX * 8u);
+          for (int b = 0; b < nb; ++b)
+            tma_load_2d(smem + s * stage + b * BOX, &tm, 16 * (b0 + b), (int)(tile * TC), &full[s]);
+          if (++s == nst) s = 0;
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  int osw[8];
+  {
+    const int hsw = (t >> 1) ^ g;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) osw[i] = (16 * warp + g + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
+  }
+  const bool want_ss = p.tsumsq != nullptr;
+  int st = 0;
+  unsigned ph = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+    double acc[NB][4];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0;
+    double tacc[T > 0 ? T : 1][2];
+#pragma unroll
+    for (int j = 0; j < (T > 0 ? T : 1); ++j) tacc[j][0] = tacc[j][1] = 0.0;
+    double ss0 = 0.0, ss1 = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+      mbar_wait(&full[st], ph);
+      const double* ab = smem + st * stage;
+      const int b0 = ch * kc, nb_ch = min(kc, nks - b0);
+      const double* wb = Wfs + lane + b0 * NB * 128;
+      const double* wt = Wts + b0 * T * 16 + 4 * t;
+      for (int bb = 0; bb < nb_ch; ++bb, ab += BOX, wb += NB * 128, wt += T * 16) {
+        double av[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = ab[osw[i]];
+        if (want_ss) {
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            ss0 = fma(av[i], av[i], ss0);
+            ss1 = fma(av[i + 1], av[i + 1], ss1);
+          }
+        }
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          double bw[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) bw[i] = wb[(nb * 4 + i) * 32];
+          dmma16(acc[nb], av, bw);
+        }
+#pragma unroll
+        for (int j = 0; j < T; ++j) {
+          const double2 w01 = *reinterpret_cast<const double2*>(wt + j * 16);
+          const double2 w23 = *reinterpret_cast<const double2*>(wt + j * 16 + 2);
+          tacc[j][0] = fma(av[0], w01.x, tacc[j][0]);
+          tacc[j][1] = fma(av[1], w01.x, tacc[j][1]);
+          tacc[j][0] = fma(av[2], w01.y, tacc[j][0]);
+          tacc[j][1] = fma(av[3], w01.y, tacc[j][1]);
+          tacc[j][0] = fma(av[4], w23.x, tacc[j][0]);
+          tacc[j][1] = fma(av[5], w23.x, tacc[j][1]);
+          tacc[j][0] = fma(av[6], w23.y, tacc[j][0]);
+          tacc[j][1] = fma(av[7], w23.y, tacc[j][1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+      if (++st == nst) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 8 * nb + 2 * t + (i & 1);
+        if (row < p.r) stg[row + p.r * (g + 8 * (i >> 1))] = acc[nb][i];
+      }
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = tacc[j][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (t == 0) stg[8 * NB + j + p.r * (g + 8 * h)] = v;
+      }
+    }
     __syncwarp();
     const long long colw = tile * TC + 16 * warp;
     const int nval = (int)max(0LL, min(16LL, p.src.L - colw));
