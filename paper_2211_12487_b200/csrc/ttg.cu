@@ -721,6 +721,32 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
   args.sel = sel;
   args.cpo = cpo;
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  CUtensorMap tmk;
+  if ((nb == 7 || nb == 8) && !std::getenv("TTG_NO_KX") && (!sel || cpo % ttg::kTC == 0) &&
+      make_tmap(&tmk, X, a, L)) {  // k-split SYRK, one CTA / SM
+    constexpr int SBD = 128;
+    args.tsumsq = tsq;
+    const size_t stage = sizeof(double) * 4 * 16 * ttg::kTC;
+    int nst = 6;
+    if (const char* e = std::getenv("TTG_KX_NST")) nst = std::max(2, std::min(ttg::kMaxStages + 4, std::atoi(e)));
+    args.nst = nst;
+    const size_t smem = nst * stage + 1024;
+    auto kern = ttg::k_syrk_kx<8>;
+    constexpr int threads = (ttg::kConsumerWarps + 1) * 32;
+    const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, threads, smem));
+    const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+    c->partials.ensure(sizeof(double) * (size_t)gx * SBD * SBD);
+    args.partials = c->partials.as<double>();
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", a);
+    const double Ls = (double)L * sel_frac;
+    prof_begin(c, nm, 8.0 * a * Ls, Ls * (double)a * a);
+    kern<<<gx, threads, smem, c->stream>>>(tmk, args);
+    post_launch(c);
+    gram_reduce(c, gx, 0, SBD, a, c->G.as<double>());
+    allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+    return tsq != nullptr;
+  }
   // 2x2-block tiles per super-tile: T(T+1)/2 (diagonal) or T^2 (off-diagonal), T <= 8
   if (nb <= 16) {
     args.ldt = ttg::smem_ld(a8);
@@ -2059,7 +2085,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_ws16<4, 1>, (const void*)ttg::k_project_ws16<4, 2>,
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
-        (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail};
+        (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>};
     for (int nb = 1; nb <= 4; ++nb)
       for (int t = 0; t <= 2; ++t) {
         CK(cudaFuncGetAttributes(&fa, kc_pick(4, nb, t)));

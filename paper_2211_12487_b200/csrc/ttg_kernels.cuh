@@ -166,6 +166,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
 // Issue the loads of tile [q0, q0+kTC) into T.  Uniform call by all threads.
 // tma: bulk path (a even); else cp.async 8-byte path (caller commits/waits).
@@ -696,6 +707,145 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_syrk(SyrkArgs p) {
   }
 }
 
+// K-split SYRK for a8 = 8 NBK <= 64 (one super-tile): every consumer warp
+// accumulates ALL NBK(NBK+1)/2 lower 8x8 blocks (m8n8k4) over its own 8
+// columns of each 64-column tile.  The m8n8k4 A and B fragments of row block
+// b are the same value per lane (X[8b+g][k+t]), so a k-step is NBK
+// shared-memory loads for NBK(NBK+1)/2 DMMAs, every warp does the same work
+// (no triangle-tiling imbalance, no padded 16x16 tiles: 36 blocks for a = 64
+// instead of 40), and the accumulators give the DMMA pipe ample independent
+// work.  Tiles arrive by tensor-map TMA (16 x 64 boxes, 128-byte swizzle; one
+// instruction per 8 KB box, rows >= a zero-filled); since a Gram is a sum
+// over k, lane t of warp w reads column 8w + 2h + {0,1,4,5}[t] at sub-step h,
+// which makes the fragment loads conflict-free under the swizzle.
+// Unselected tiles (selection is tile-aligned) are skipped by producer and
+// consumers alike.  One CTA per SM (registers).  The 8 warps' partial Grams
+// are summed in shared memory in warp order (deterministic) and written as one
+// SBD x SBD partial per CTA (gram_reduce layout 0).
+template <int NBK>
+__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) k_syrk_kx(const __grid_constant__ CUtensorMap tm,
+                                                                          SyrkArgs p) {
+  constexpr int NBL = NBK * (NBK + 1) / 2;
+  constexpr int NCW = kConsumerWarps;
+  constexpr int SBD = 128;
+  constexpr int NBOX = (NBK + 1) / 2;
+  constexpr int BOX = 16 * kTC;
+  constexpr int STAGE = NBOX * BOX;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxStages + 4], empty[kMaxStages + 4];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nst = p.nst;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto selected = [&](long long tile) {
+    return p.sel == nullptr || p.sel[(tile * kTC) / p.cpo] != 0;
+  };
+
+  if (warp == NCW) {  // ---- producer ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      int it = 0, s = 0;
+      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        if (!selected(tile)) continue;
+        if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
+        mbar_expect_tx(&full[s], (unsigned)STAGE * 8u);
+#pragma unroll
+        for (int b = 0; b < NBOX; ++b) tma_load_2d(smem + s * STAGE + b * BOX, &tm, 16 * b, (int)(tile * kTC), &full[s]);
+        ++it;
+        if (++s == nst) s = 0;
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  double acc[NBL][2];
+#pragma unroll
+  for (int u = 0; u < NBL; ++u) acc[u][0] = acc[u][1] = 0.0;
+  int off[2][2];  // [h][b & 1]
+  {
+    const int tp = (t & 1) + 4 * (t >> 1);  // {0, 1, 4, 5}
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 8 * warp + 2 * h + tp;
+#pragma unroll
+      for (int bp = 0; bp < 2; ++bp) off[h][bp] = c * 16 + ((((4 * bp + (g >> 1)) ^ (c & 7))) << 1) + (g & 1);
+    }
+  }
+  int st = 0;
+  unsigned ph = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    if (!selected(tile)) continue;
+    mbar_wait(&full[st], ph);
+    const double* Ti = smem + st * STAGE;
+    if (p.tsumsq) {  // per-(tile, 8-column group) sums of squares: group = this warp's columns
+      double sq = 0.0;
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b)
+#pragma unroll
+        for (int e = lane; e < 128; e += 32) {
+          const double vv = Ti[b * BOX + 128 * warp + e];
+          sq = fma(vv, vv, sq);
+        }
+      sq = warp_sum(sq);
+      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = sq;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double f[NBK];
+#pragma unroll
+      for (int b = 0; b < NBK; ++b) f[b] = Ti[(b >> 1) * BOX + off[h][b & 1]];
+      int u = 0;
+#pragma unroll
+      for (int bi = 0; bi < NBK; ++bi)
+#pragma unroll
+        for (int bj = 0; bj <= bi; ++bj, ++u) dmma(acc[u][0], acc[u][1], f[bi], f[bj]);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+    if (++st == nst) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  // ordered cross-warp sum in shared memory (the ring is idle: every stage was consumed)
+  double* buf = smem;  // 8 NBK x 8 NBK, ld 8 NBK
+  constexpr int LD = 8 * NBK;
+  for (int w = 0; w < NCW; ++w) {
+    asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");
+    if (warp == w) {
+      int u = 0;
+#pragma unroll
+      for (int bi = 0; bi < NBK; ++bi)
+#pragma unroll
+        for (int bj = 0; bj <= bi; ++bj, ++u) {
+          double* e = buf + (8 * bi + g) + LD * (8 * bj + 2 * t);
+          if (w == 0) {
+            e[0] = acc[u][0];
+            e[LD] = acc[u][1];
+          } else {
+            e[0] += acc[u][0];
+            e[LD] += acc[u][1];
+          }
+        }
+    }
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");
+  double* out = p.partials + (long long)blockIdx.x * SBD * SBD;
+  for (int e = threadIdx.x; e < LD * LD; e += NCW * 32) {
+    const int r = e % LD, c = e / LD;
+    if ((r >> 3) >= (c >> 3)) out[r + SBD * c] = buf[r + LD * c];
+  }
+}
+
 // Two-stage fixed-order reduction of per-CTA Gram partials (hundreds of
 // CTAs): stage 1 sums x-chunks of the partials for every lower-triangle
 // element (blockIdx.y = chunk, four independent accumulators), stage 2 sums
@@ -1050,17 +1200,6 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
 // B-fragment pattern (4 consecutive rows x 8 columns) conflict-free without
 // padding, so the smem image is dense and every byte moved is payload.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
-  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
 // Projection out (r x L) = W^T X with tensor-map TMA tiles of TC columns
 // (TC = 64, or 32 for tall operands so that two CTAs with two stages each fit
