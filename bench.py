@@ -155,6 +155,54 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def survey_increment_roofline(modes, b_local, reports, step_ms, world=1, tau=0.8, bw_gbs=8000.0,
+                              p_tflops=PEAK_FP64_TFLOPS):
+    """Per-increment roofline of SURVEY.md §8(d) with each increment's actual
+    ranks, |D| and occupancy-gated modes: skip path F = F_proj(old) + 3N,
+    B = 8N; update path F = F_proj(old) + 3N + F_ice(D) + F_proj(new),
+    B = 8N + B_ice(D) + 8N, with
+      F_proj = sum_i 2 r_i M_i,
+      F_ice  = 2 N_D + sum_i [4 r_i^old M_i + a_i M_i (SVD modes only) + 2 r_i^new M_i],
+      B_ice  = 8 (2 M_1 + 2 sum_{i>=2} M_i)   (M_i over the |D| selected columns).
+    T_roof = max(B / BW, F / P_FP64) per increment (BW 8 TB/s as the north
+    star states, P = the measured FP64 DMMA peak); returns the fraction
+    sum T_roof / sum T_measured and the totals."""
+    d = len(modes)
+    S = int(np.prod(modes))
+
+    def M(i, rl, cols):  # a_i * L_i for step i (0-based) with left rank rl and `cols` observations
+        return rl * modes[i] * int(np.prod(modes[i + 1:])) * cols
+
+    def f_proj(ranks, cols):
+        return sum(2.0 * ranks[i + 1] * M(i, ranks[i], cols) for i in range(d))
+
+    t_roof = t_meas = 0.0
+    for r, ms in zip(reports, step_ms):
+        old, new = list(r.ranks_before), list(r.ranks_after)
+        N = S * b_local
+        D = r.obs_used / world
+        if r.obs_used == 0:
+            F, B = f_proj(old, b_local) + 3.0 * N, 8.0 * N
+        else:
+            fice, mb = 2.0 * S * D, 0.0
+            for i in range(d):
+                rl_new = new[i]
+                a = rl_new * modes[i]
+                m = M(i, rl_new, D)
+                if old[i + 1] / a < tau:  # SVD ran (occupancy on the padded core)
+                    fice += 4.0 * old[i + 1] * m + a * m
+                fice += 2.0 * new[i + 1] * m
+                mb += 2.0 * m
+            F = f_proj(old, b_local) + 3.0 * N + fice + f_proj(new, b_local)
+            B = 8.0 * N + 8.0 * mb + 8.0 * N
+        t_roof += max(B / (bw_gbs * 1e9), F / (p_tflops * 1e12))
+        t_meas += ms * 1e-3
+    return {"frac": t_roof / t_meas if t_meas else None, "t_roof_ms": t_roof * 1e3, "t_meas_ms": t_meas * 1e3,
+            "bw_gbs": bw_gbs, "p_fp64_tflops": p_tflops,
+            "def": "SURVEY.md 8(d) algorithmic bytes/flops per increment (actual ranks, |D|, occupancy-gated "
+                   "modes), T_roof = max(B/BW, F/P) summed over the timed increments / their device time"}
+
+
 def workload_config(args, batch_override=None, world=1):
     b = batch_override or args.batch
     return {"workload": "cfg3 TT-ICE* stream (BASELINE configs[3]; configs[4] at 8 GPUs)",
@@ -309,7 +357,10 @@ def our_arm(args):
                                     "ms/step with events vs the headline region without them)",
                      "algorithmic_bytes_per_launch": dom["bytes"] / dom["launches"],
                      "algorithmic_flops_per_launch": dom["flops"] / dom["launches"]})
-        # whole-step roofline: sum over kernels of max(bytes/BW, flops/peak)
+        # kernel-level step roofline: sum over the LAUNCHED kernels of
+        # max(bytes/BW, flops/peak) with each kernel's own traffic (how close
+        # each launch runs to its own bound; the SURVEY per-increment
+        # roofline is "increment_roofline" below)
         t_roof = sum(max(s["bytes"] / (hbm * 1e9), s["flops"] / (PEAK_FP64_TFLOPS * 1e12)) for s in kstats)
         roof["step_roofline_frac"] = t_roof / (ms_prof * 1e-3)
 
@@ -358,7 +409,8 @@ def our_arm(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg3 generator, DESIGN.md §6)",
             "config": workload_config(args, world=world),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "roofline": roof, "increment_roofline": survey_increment_roofline(MODES, b, reports, step_ms, world),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "per_gpu_gbs": value / world,
             "steps_detail": [{"obs_used": r.obs_used, "ranks": r.ranks_after, "modes_updated": r.modes_updated,
                               "device_ms": round(dt, 3), "call_ms": round(r.seconds * 1e3, 3)}

@@ -699,6 +699,75 @@ bool syrk2(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, 
   return true;
 }
 
+// k-split SYRK for 64 < a8 <= 160 (k_syrk_kp): parts P per NBK so that a warp
+// holds at most 40 lower blocks
+constexpr int kp_parts(int nbk) {
+  const int nbl = nbk * (nbk + 1) / 2;
+  return (nbl + 1) / 2 <= 40 ? 2 : (nbl + 3) / 4 <= 44 ? 4 : 8;
+}
+template <int NBK>
+void* kp_kernel() {
+  return (void*)ttg::k_syrk_kp<NBK, kp_parts(NBK)>;
+}
+void* kp_pick(int nbk) {
+  switch (nbk) {
+    case 9: return kp_kernel<9>();
+    case 10: return kp_kernel<10>();
+    case 11: return kp_kernel<11>();
+    case 12: return kp_kernel<12>();
+    case 13: return kp_kernel<13>();
+    case 14: return kp_kernel<14>();
+    case 15: return kp_kernel<15>();
+    case 16: return kp_kernel<16>();
+    case 17: return kp_kernel<17>();
+    case 18: return kp_kernel<18>();
+    case 19: return kp_kernel<19>();
+    case 20: return kp_kernel<20>();
+  }
+  return nullptr;
+}
+
+bool syrk_kp(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
+             double* tsq) {
+  const int a8 = ttg::round_up(a, 8), nbk = a8 / 8;
+  // measured: 8 parts (NBK >= 19) re-load too many fragments per DMMA and lose
+  // to k_syrk2; up to 4 parts win (a = 136: 0.16 vs 0.24 ms per 1.1 GB)
+  if (std::getenv("TTG_NO_KP") || tsq || (a & 1) || nbk < 9 || nbk > 18 || kp_parts(nbk) > 4 ||
+      (sel && cpo % ttg::kTC != 0))
+    return false;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, X, a, L)) return false;
+  const size_t stage = sizeof(double) * 1024 * (size_t)((nbk + 1) / 2);
+  const size_t cap = (size_t)c->smem_optin - 1024;
+  int nst = (int)std::min<size_t>(4, (cap - 1024) / stage);
+  if (const char* e = std::getenv("TTG_KP_NST")) nst = std::min(nst, std::max(2, std::atoi(e)));
+  if (nst < 2) return false;
+  ttg::SyrkArgs args{};
+  args.X = X;
+  args.a = a;
+  args.a8 = a8;
+  args.L = L;
+  args.sel = sel;
+  args.cpo = cpo;
+  args.nst = nst;
+  args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  const size_t smem = nst * stage + 1024;
+  auto kern = reinterpret_cast<void (*)(const CUtensorMap, ttg::SyrkArgs)>(kp_pick(nbk));
+  constexpr int threads = ttg::kConsumerWarps * 32;
+  const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, threads, smem));
+  const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  c->partials.ensure(sizeof(double) * (size_t)gx * a8 * a8);
+  args.partials = c->partials.as<double>();
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", a);
+  const double Ls = (double)L * sel_frac;
+  prof_begin(c, nm, 8.0 * a * Ls, Ls * (double)a * a);
+  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  post_launch(c);
+  gram_reduce(c, gx, 1, a8, a, c->G.as<double>());
+  return true;
+}
+
 // C = sum over selected columns x x^T -> c->G (a x a); returns whether per-tile
 // sums of squares were produced
 bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
@@ -709,7 +778,8 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
     gram_src(c, Src{X, a, L, nullptr, a}, 1, nullptr, 0, sel, cpo, sel_frac, tsq);
     return tsq != nullptr && ttg::round_up(a, 8) <= kFastMax1;
   }
-  if (syrk_ws16(c, X, a, L, sel, cpo, sel_frac, tsq) || syrk2(c, X, a, L, sel, cpo, sel_frac, tsq)) {
+  if (syrk_kp(c, X, a, L, sel, cpo, sel_frac, tsq) || syrk_ws16(c, X, a, L, sel, cpo, sel_frac, tsq) ||
+      syrk2(c, X, a, L, sel, cpo, sel_frac, tsq)) {
     allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
     return tsq != nullptr;
   }
@@ -2086,6 +2156,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>};
+    for (int nbk = 9; nbk <= 20; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
     for (int nb = 1; nb <= 4; ++nb)
       for (int t = 0; t <= 2; ++t) {
         CK(cudaFuncGetAttributes(&fa, kc_pick(4, nb, t)));

@@ -846,6 +846,174 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) k_syrk_kx(const 
   }
 }
 
+// K-split SYRK for 64 < a8 = 8 NBK <= 160 (k_syrk_kx generalised): the
+// NBK(NBK+1)/2 lower 8x8 blocks are cut into P contiguous row-major parts and
+// the 8 column groups of a 64-column tile into KS = 8 / P slices; warp
+// (part, slice) accumulates its part's blocks (<= 40) over its slice's
+// columns.  Each part is its own unrolled code path (template PART) so block
+// indices and fragment registers stay static.  Per sub-step a warp loads the
+// row-block fragments its part touches (<= NBK, conflict-free permuted-k
+// layout of k_syrk_kx) for its DMMAs.  Slices of a part are summed in order
+// into the per-CTA a8 x a8 partial (gram_reduce layout 1).
+__host__ __device__ constexpr int kp_row_of(int u) {
+  int bi = 0;
+  while ((bi + 1) * (bi + 2) / 2 <= u) ++bi;
+  return bi;
+}
+
+// TMA producer state of k_syrk_kp (thread 0 of the CTA; no separate
+// producer warp, so the 8 consumer warps may use 255 registers)
+struct KpProducer {
+  long long tile;
+  int it, s;
+};
+template <int NBOX>
+__device__ __forceinline__ void kp_produce(const CUtensorMap* tm, const SyrkArgs& p, double* smem, uint64_t* full,
+                                           uint64_t* empty, KpProducer& pr) {
+  constexpr int BOX = 16 * kTC, STAGE = NBOX * BOX;
+  while (pr.tile < p.n_tiles && p.sel != nullptr && p.sel[(pr.tile * kTC) / p.cpo] == 0) pr.tile += gridDim.x;
+  if (pr.tile >= p.n_tiles) return;
+  if (pr.it >= p.nst) mbar_wait(&empty[pr.s], (unsigned)(((pr.it / p.nst) - 1) & 1));
+  mbar_expect_tx(&full[pr.s], (unsigned)STAGE * 8u);
+#pragma unroll
+  for (int b = 0; b < NBOX; ++b) tma_load_2d(smem + pr.s * STAGE + b * BOX, tm, 16 * b, (int)(pr.tile * kTC), &full[pr.s]);
+  pr.tile += gridDim.x;
+  ++pr.it;
+  if (++pr.s == p.nst) pr.s = 0;
+}
+
+template <int NBK, int P, int PART>
+__device__ __forceinline__ void syrk_kp_part(const CUtensorMap* tm, const SyrkArgs& p, double* smem, uint64_t* full,
+                                             uint64_t* empty, int slice) {
+  constexpr int KS = 8 / P;
+  constexpr int NBL = NBK * (NBK + 1) / 2;
+  constexpr int U0 = PART * NBL / P, U1 = (PART + 1) * NBL / P, NU = U1 - U0;
+  constexpr int BI0 = kp_row_of(U0), BJ0 = U0 - BI0 * (BI0 + 1) / 2;
+  constexpr int BI1 = kp_row_of(U1 - 1);
+  // rows whose fragments this part needs: bj spans 0..BI1 once a full row is
+  // covered, else BJ0..BI0 plus the row itself
+  constexpr int RLO = (BI1 > BI0) ? 0 : BJ0;
+  constexpr int RHI = BI1;
+  constexpr int NF = RHI - RLO + 1;
+  constexpr int NBOX = (NBK + 1) / 2;
+  constexpr int BOX = 16 * kTC;
+  constexpr int STAGE = NBOX * BOX;
+  constexpr int NQ = 8 / KS;  // column groups per slice
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int tp = (t & 1) + 4 * (t >> 1);
+  const bool producer = threadIdx.x == 0;
+  KpProducer pr{blockIdx.x, 0, 0};
+  if (producer)
+    for (int k = 0; k < p.nst; ++k) kp_produce<NBOX>(tm, p, smem, full, empty, pr);
+  __syncwarp();
+  int base[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int bp = 0; bp < 2; ++bp) {
+      const int c7 = 2 * h + tp;
+      base[h][bp] = c7 * 16 + (((4 * bp + (g >> 1)) ^ c7) << 1) + (g & 1);
+    }
+  double acc[NU][2];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) acc[u][0] = acc[u][1] = 0.0;
+  const int nst = p.nst;
+  int st = 0;
+  unsigned ph = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    if (p.sel != nullptr && p.sel[(tile * kTC) / p.cpo] == 0) continue;
+    mbar_wait(&full[st], ph);
+    const double* Ti = smem + st * STAGE;
+#pragma unroll
+    for (int qi = 0; qi < NQ; ++qi) {
+      const int q = slice + KS * qi;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double f[NF];
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const int b = RLO + k;
+          f[k] = Ti[(b >> 1) * BOX + 128 * q + base[h][b & 1]];
+        }
+        int bi = BI0, bj = BJ0;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          dmma(acc[u][0], acc[u][1], f[bi - RLO], f[bj - RLO]);
+          if (++bj > bi) {
+            ++bi;
+            bj = 0;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+    if (++st == nst) {
+      st = 0;
+      ph ^= 1u;
+    }
+    // refill the stage just consumed (waits for the other warps to release it;
+    // in steady state warp 0 is the last to get there)
+    if (producer) kp_produce<NBOX>(tm, p, smem, full, empty, pr);
+    __syncwarp();
+  }
+  // slices of this part add into the CTA's partial in slice order
+  const int a8 = 8 * NBK;
+  double* out = p.partials + (long long)blockIdx.x * a8 * a8;
+  for (int s = 0; s < KS; ++s) {
+    __syncthreads();
+    if (slice == s) {
+      int bi = BI0, bj = BJ0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        double* e = out + (8 * bi + g) + (long long)a8 * (8 * bj + 2 * t);
+        if (s == 0) {
+          e[0] = acc[u][0];
+          e[a8] = acc[u][1];
+        } else {
+          e[0] += acc[u][0];
+          e[a8] += acc[u][1];
+        }
+        if (++bj > bi) {
+          ++bi;
+          bj = 0;
+        }
+      }
+    }
+  }
+}
+
+template <int NBK, int P>
+__global__ void __launch_bounds__(kConsumerWarps * 32, 1) k_syrk_kp(const __grid_constant__ CUtensorMap tm,
+                                                                    SyrkArgs p) {
+  constexpr int KS = 8 / P;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[8], empty[8];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tm);
+  }
+  __syncthreads();
+  const int part = warp / KS, slice = warp % KS;
+  switch (part) {
+    case 0: syrk_kp_part<NBK, P, 0>(&tm, p, smem, full, empty, slice); break;
+    case 1: if constexpr (P > 1) syrk_kp_part<NBK, P, (P > 1 ? 1 : 0)>(&tm, p, smem, full, empty, slice); break;
+    case 2: if constexpr (P > 2) syrk_kp_part<NBK, P, (P > 2 ? 2 : 0)>(&tm, p, smem, full, empty, slice); break;
+    case 3: if constexpr (P > 3) syrk_kp_part<NBK, P, (P > 3 ? 3 : 0)>(&tm, p, smem, full, empty, slice); break;
+    case 4: if constexpr (P > 4) syrk_kp_part<NBK, P, (P > 4 ? 4 : 0)>(&tm, p, smem, full, empty, slice); break;
+    case 5: if constexpr (P > 5) syrk_kp_part<NBK, P, (P > 5 ? 5 : 0)>(&tm, p, smem, full, empty, slice); break;
+    case 6: if constexpr (P > 6) syrk_kp_part<NBK, P, (P > 6 ? 6 : 0)>(&tm, p, smem, full, empty, slice); break;
+    default: if constexpr (P > 7) syrk_kp_part<NBK, P, (P > 7 ? 7 : 0)>(&tm, p, smem, full, empty, slice); break;
+  }
+}
+
 // Two-stage fixed-order reduction of per-CTA Gram partials (hundreds of
 // CTAs): stage 1 sums x-chunks of the partials for every lower-triangle
 // element (blockIdx.y = chunk, four independent accumulators), stage 2 sums
