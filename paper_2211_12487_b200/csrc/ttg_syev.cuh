@@ -523,6 +523,153 @@ __device__ int warp_sym_eig(const double* Hs, int k, double* theta, double* Wv, 
   return sweep;
 }
 
+// One thread: cyclic Jacobi on the symmetric k x k (k <= 4) Hs held in
+// registers (same rotation formula and skip thresholds as warp_sym_eig; the
+// k = 4 Rayleigh-Ritz problem is latency-bound, and one thread avoids the
+// shuffle chains of the warp version).  Output as warp_sym_eig.
+__device__ int thread_sym_eig4(const double* Hs, int k, double* theta, double* Wv) {
+  double h[4][4], w[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      h[i][j] = (i < k && j < k) ? 0.5 * (Hs[i + k * j] + Hs[j + k * i]) : 0.0;
+      w[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    double hmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) hmax = fmax(hmax, fabs(h[i][i]));
+    const double floor_abs = 8.881784197001252e-16 * hmax;
+    bool rotated = false;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p + 1; q < 4; ++q) {
+        const double hpp = h[p][p], hqq = h[q][q], hpq = h[p][q];
+        if (q < k && fabs(hpq) > floor_abs && fabs(hpq) > 1e-15 * sqrt(fabs(hpp * hqq))) {
+          const double zeta = (hqq - hpp) / (2.0 * hpq);
+          const double az = fabs(zeta);
+          const double t = az > 1e150 ? 0.5 / zeta : copysign(1.0, zeta) / (az + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(t, t, 1.0));
+          const double sn = c * t;
+          rotated = true;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {  // rows p, q
+            const double x = h[p][j], y = h[q][j];
+            h[p][j] = c * x - sn * y;
+            h[q][j] = sn * x + c * y;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // columns p, q of H and W
+            const double x = h[i][p], y = h[i][q];
+            h[i][p] = c * x - sn * y;
+            h[i][q] = sn * x + c * y;
+            const double u = w[i][p], v = w[i][q];
+            w[i][p] = c * u - sn * v;
+            w[i][q] = sn * u + c * v;
+          }
+        }
+      }
+    if (!rotated) break;
+  }
+  // stable descending sort of the diagonal
+  double d[4];
+  int pos[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i] = h[i][i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int ps = 0;
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+      if (y < k) ps += (d[y] > d[i] || (d[y] == d[i] && y < i)) ? 1 : 0;
+    pos[i] = ps;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < k) {
+      theta[pos[i]] = d[i];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (r < k) Wv[r + k * pos[i]] = w[r][i];
+    }
+  return sweep;
+}
+
+// block_cholqr2 for k <= 4 with the k x k Cholesky in one thread's registers
+// (fewer barriers / warp-serial steps; same column-scaled CholQR2 numerics)
+__device__ void block_cholqr2_4(double* X, int a, int k, double* S, double* Ri) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int e = warp; e < 16; e += nw) {
+      const int i = e & 3, j = e >> 2;
+      if (i > j || j >= k) continue;
+      double s0 = 0.0, s1 = 0.0;
+      int r = lane;
+      for (; r + 32 < a; r += 64) {
+        s0 = fma(X[r + (size_t)a * i], X[r + (size_t)a * j], s0);
+        s1 = fma(X[r + 32 + (size_t)a * i], X[r + 32 + (size_t)a * j], s1);
+      }
+      if (r < a) s0 = fma(X[r + (size_t)a * i], X[r + (size_t)a * j], s0);
+      const double sacc = warp_sum(s0 + s1);
+      if (lane == 0) S[i + 4 * j] = sacc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double m[4][4], dsc[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dsc[i] = (i < k && S[i + 4 * i] > 0.0) ? 1.0 / sqrt(S[i + 4 * i]) : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[i][j] = (i <= j && j < k) ? S[i + 4 * j] * dsc[i] * dsc[j] : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        if (jj < k) {
+          const double piv = m[jj][jj];
+          const double rjj = piv > 1e-28 ? sqrt(piv) : 0.0;
+          const double inv = rjj > 0.0 ? 1.0 / rjj : 0.0;
+          Ri[4 + jj] = inv;
+#pragma unroll
+          for (int l = 0; l < 4; ++l)
+            if (l >= jj) m[jj][l] = (l == jj) ? rjj : m[jj][l] * inv;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int l = 0; l < 4; ++l)
+              if (i > jj && i <= l) m[i][l] -= m[jj][i] * m[jj][l];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        Ri[i] = dsc[i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) S[i + 4 * j] = m[i][j];
+      }
+    }
+    __syncthreads();
+    for (int r = tid; r < a; r += blockDim.x) {
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < k) {
+          double t = X[r + (size_t)a * j] * Ri[j];
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm)
+            if (mm < j) t -= v[mm] * S[mm + 4 * j];
+          v[j] = t * Ri[4 + j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < k) X[r + (size_t)a * j] = v[j];
+    }
+    __syncthreads();
+  }
+}
+
 // Orthonormalise the k (<= kSubK) columns of X (a x k, ld a) in place:
 // column-scaled Cholesky QR, twice (X D R^-1 with D = diag(X^T X)^-1/2, so the
 // Gram matrix factored is unit-diagonal and CholQR2 is stable up to
@@ -635,7 +782,8 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
     return;
   }
   const long long ts2 = clock64();
-  block_cholqr2<K>(X, Z, a, k, Sq, Rq);
+  if constexpr (K == 4) block_cholqr2_4(X, a, k, Sq, Rq);
+  else block_cholqr2<K>(X, Z, a, k, Sq, Rq);
   const long long t1 = clock64();
   double prev_res = 1e300;
   long long ph[4] = {0, 0, 0, 0};
@@ -646,18 +794,30 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
     // Z = G X: one thread per row i (G[i + a*j] over consecutive i is
     // conflict-free, X[j + a*c] is a broadcast), K independent chains
     for (int i = tid; i < a; i += blockDim.x) {
-      double acc[K];
+      // two interleaved partial sums per column (even / odd j), loads batched
+      double acc[K], acc2[K];
 #pragma unroll
-      for (int c = 0; c < K; ++c) acc[c] = 0.0;
-      for (int j = 0; j < a; ++j) {
-        const double gij = G[i + (size_t)a * j];
+      for (int c = 0; c < K; ++c) acc[c] = acc2[c] = 0.0;
+      int j = 0;
+#pragma unroll 4
+      for (; j + 1 < a; j += 2) {
+        const double g0 = G[i + (size_t)a * j], g1 = G[i + (size_t)a * (j + 1)];
 #pragma unroll
         for (int c = 0; c < K; ++c)
-          if (c < k) acc[c] = fma(gij, X[j + (size_t)a * c], acc[c]);
+          if (c < k) {
+            acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
+            acc2[c] = fma(g1, X[j + 1 + (size_t)a * c], acc2[c]);
+          }
+      }
+      if (j < a) {
+        const double g0 = G[i + (size_t)a * j];
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+          if (c < k) acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
       }
 #pragma unroll
       for (int c = 0; c < K; ++c)
-        if (c < k) Z[i + (size_t)a * c] = acc[c];
+        if (c < k) Z[i + (size_t)a * c] = acc[c] + acc2[c];
     }
     __syncthreads();
     long long tq1 = clock64();
@@ -671,7 +831,9 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
     }
     __syncthreads();
     long long tq2 = clock64();
-    if (warp == 0) {
+    if constexpr (K == 4) {
+      if (tid == 0) jac_sweeps += thread_sym_eig4(H, k, theta, Wv);
+    } else if (warp == 0) {
       const int nsw = warp_sym_eig<K>(H, k, theta, Wv, Wt);
       if (lane == 0) jac_sweeps += nsw;
     }
@@ -736,7 +898,8 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
       X[e] = s;
     }
     __syncthreads();
-    block_cholqr2<K>(X, Z, a, k, Sq, Rq);
+    if constexpr (K == 4) block_cholqr2_4(X, a, k, Sq, Rq);
+    else block_cholqr2<K>(X, Z, a, k, Sq, Rq);
   }
   const int rank = s_rank;
   if (tid == 0) {
