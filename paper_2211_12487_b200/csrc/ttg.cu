@@ -145,6 +145,7 @@ struct ttg_ctx {
     cudaEvent_t e0, e1;
   };
   bool profiling = false;
+  bool pdl = true;  // programmatic dependent launch (launch_k); off under TTG_NO_PDL and for world > 1
   std::vector<KStat> kstats;
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> evpool;
@@ -195,6 +196,24 @@ cudaEvent_t get_event(ttg_ctx* c) {
   cudaEvent_t e;
   CK(cudaEventCreate(&e));
   return e;
+}
+
+// Every library kernel launch: programmatic stream serialization (PDL, see
+// ttg_pdl.cuh) when enabled on the context and no per-kernel timing events
+// sit between launches; errors surface in post_launch.
+template <typename... KArgs, typename... Args>
+void launch_k(ttg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (c->pdl && !c->profiling) ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 // Call before every kernel launch: accounts the launch under `name` with its
@@ -293,10 +312,10 @@ void obs_norms(ttg_ctx* c, const double* Y, long long S, int b) {
   c->scal.ensure(sizeof(double) * 16);
   dim3 grid(nchunk, b);
   prof_begin(c, "k_sumsq_obs", 8.0 * S * b, 2.0 * S * b);
-  ttg::k_sumsq_obs<<<grid, 256, 0, c->stream>>>(Y, S, nchunk, c->sumsq_part.as<double>());
+  launch_k(c, ttg::k_sumsq_obs, grid, 256, 0, Y, S, nchunk, c->sumsq_part.as<double>());
   post_launch(c);
   prof_begin(c, "k_sumsq_finalize", 8.0 * nchunk * b, 0.0);
-  ttg::k_sumsq_finalize<<<1, 256, 0, c->stream>>>(c->sumsq_part.as<double>(), nchunk, b,
+  launch_k(c, ttg::k_sumsq_finalize, 1, 256, 0, c->sumsq_part.as<double>(), nchunk, b,
                                                    c->on2.as<double>(), c->scal.as<double>());
   post_launch(c);
   allreduce_sum(c, c->scal.as<double>(), 1);
@@ -316,7 +335,7 @@ void make_frags(ttg_ctx* c, const double* U, int a, int r, int ld, bool need_ut,
   c->UTf.ensure(sizeof(double) * std::max<size_t>(n1, 1));
   c->Uf.ensure(sizeof(double) * std::max<size_t>(n2, 1));
   prof_begin(c, "k_make_frags", 8.0 * (n1 + n2), 0.0);
-  ttg::k_make_frags<<<grid_for(n1 + n2, 256, 1024), 256, 0, c->stream>>>(
+  launch_k(c, ttg::k_make_frags, grid_for(n1 + n2, 256, 1024), 256, 0, 
       U, a, r, ld, a8, r8, need_ut ? c->UTf.as<double>() : nullptr, need_u ? c->Uf.as<double>() : nullptr);
   post_launch(c);
 }
@@ -330,7 +349,7 @@ void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
   if (grid.y > 65535) fail(TTG_E_RESOURCE, "generic gemm: m too large");
   prof_begin(c, "k_gemm", 8.0 * (m * k + k * n + m * n), 2.0 * m * n * k);
-  ttg::k_gemm<TA, TB><<<grid, dim3(32, 32), 0, c->stream>>>(A, lda, B, ldb, C, ldc, m, n, k, alpha, beta);
+  launch_k(c, ttg::k_gemm<TA, TB>, grid, dim3(32, 32), 0, A, lda, B, ldb, C, ldc, m, n, k, alpha, beta);
   post_launch(c);
 }
 
@@ -346,11 +365,11 @@ void gram_reduce(ttg_ctx* c, int nx, int layout, int ld, int a, double* G) {
   c->Mtmp.ensure(sizeof(double) * (size_t)(xs * n));
   const int gxb = (int)std::min<long long>((n + 255) / 256, 1024);
   prof_begin(c, "k_gram_reduce", 8.0 * (double)nx * n / 2, (double)nx * n / 2);
-  ttg::k_gram_reduce_s1<<<dim3(gxb, xs), 256, 0, c->stream>>>(c->partials.as<double>(), nx, layout, ld, a,
+  launch_k(c, ttg::k_gram_reduce_s1, dim3(gxb, xs), 256, 0, c->partials.as<double>(), nx, layout, ld, a,
                                                                c->Mtmp.as<double>());
   post_launch(c);
   prof_begin(c, "k_gram_reduce", 8.0 * (double)xs * n / 2, (double)xs * n / 2);
-  ttg::k_gram_reduce_s2<<<gxb, 256, 0, c->stream>>>(c->Mtmp.as<double>(), xs, a, G);
+  launch_k(c, ttg::k_gram_reduce_s2, gxb, 256, 0, c->Mtmp.as<double>(), xs, a, G);
   post_launch(c);
 }
 
@@ -373,7 +392,7 @@ void launch_gram_t(ttg_ctx* c, const ttg::GramArgs& args, size_t smem, int npair
     std::snprintf(nm, sizeof nm, "%s[a=%d,r=%d]", PRE ? "k_gram_resid_pre" : "k_gram_resid", args.a, args.r_old);
     prof_begin(c, nm, 8.0 * args.src.a * Ls, Ls * (4.0 * r_ * a_ + a_ * a_));
   }
-  kern<<<dim3(gx, npairs), ttg::kThreads, smem, c->stream>>>(a2);
+  launch_k(c, kern, dim3(gx, npairs), ttg::kThreads, smem, a2);
   post_launch(c);
   const int a = args.a;
   const long long n = (long long)a * a;
@@ -426,7 +445,7 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
     const size_t nf = (size_t)(rc8 / 8) * (As8 / 4) * 32;
     c->psif.ensure(sizeof(double) * nf);
     prof_begin(c, "k_make_frags", 8.0 * nf, 0.0);
-    ttg::k_make_frags<<<grid_for((long long)nf, 256, 1024), 256, 0, c->stream>>>(
+    launch_k(c, ttg::k_make_frags, grid_for((long long)nf, 256, 1024), 256, 0, 
         s.Psi, (int)s.As, (int)s.r, (int)s.As, As8, rc8, c->psif.as<double>(), nullptr);
     post_launch(c);
     args.src = ttg::TileSrc{s.S, src_rows, L, sel, cpo};
@@ -496,7 +515,7 @@ bool gram_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, c
   }
   if (sel) {
     prof_begin(c, "k_mask_cols", 16.0 * a * L, 0.0);
-    ttg::k_mask_cols<<<grid_for((long long)a * L, 256, 4096), 256, 0, c->stream>>>(R, a, L, sel, cpo);
+    launch_k(c, ttg::k_mask_cols, grid_for((long long)a * L, 256, 4096), 256, 0, R, a, L, sel, cpo);
     post_launch(c);
   }
   gemm<false, true>(c, R, a, R, a, c->G.as<double>(), a, a, a, L, 1.0, 0.0);
@@ -533,7 +552,7 @@ void launch_syrk_t(ttg_ctx* c, ttg::SyrkArgs args, int npairs, double sel_frac) 
   std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
   const double Ls = (double)args.L * sel_frac;
   prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
-  kern<<<dim3(gx, npairs), threads, smem, c->stream>>>(args);
+  launch_k(c, kern, dim3(gx, npairs), threads, smem, args);
   post_launch(c);
   const int a = args.a;
   const long long n = (long long)a * a;
@@ -583,7 +602,7 @@ void launch_syrk2_t(ttg_ctx* c, const CUtensorMap& tm, ttg::Syrk2Args args, int 
   std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
   const double Ls = (double)args.L * sel_frac;
   prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
-  kern<<<dim3(gx, parts), ttg::kSyrkThreads, smem, c->stream>>>(tm, args);
+  launch_k(c, kern, dim3(gx, parts), ttg::kSyrkThreads, smem, tm, args);
   post_launch(c);
   const long long n = (long long)args.a * args.a;
   (void)n;
@@ -622,7 +641,7 @@ void launch_syrk_ws16_t(ttg_ctx* c, const CUtensorMap& tm, ttg::Syrk2Args args, 
   std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", args.a);
   const double Ls = (double)args.L * sel_frac;
   prof_begin(c, nm, 8.0 * args.a * Ls, Ls * (double)args.a * args.a);
-  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  launch_k(c, kern, gx, threads, smem, tm, args);
   post_launch(c);
   const long long n = (long long)args.a * args.a;
   (void)n;
@@ -762,7 +781,7 @@ bool syrk_kp(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel
   std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", a);
   const double Ls = (double)L * sel_frac;
   prof_begin(c, nm, 8.0 * a * Ls, Ls * (double)a * a);
-  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  launch_k(c, kern, gx, threads, smem, tm, args);
   post_launch(c);
   gram_reduce(c, gx, 1, a8, a, c->G.as<double>());
   return true;
@@ -811,7 +830,7 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
     std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", a);
     const double Ls = (double)L * sel_frac;
     prof_begin(c, nm, 8.0 * a * Ls, Ls * (double)a * a);
-    kern<<<gx, threads, smem, c->stream>>>(tmk, args);
+    launch_k(c, kern, gx, threads, smem, tmk, args);
     post_launch(c);
     gram_reduce(c, gx, 0, SBD, a, c->G.as<double>());
     allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
@@ -855,7 +874,7 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
   c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
   double* Q = c->wcomb.as<double>();
   prof_begin(c, "k_build_q", 8.0 * rows * a, 2.0 * rows * a * std::max(r_old, 1) * (s.Psi ? s.r : 1));
-  ttg::k_build_q<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, s.Psi ? (int)s.As : (int)s.r, (int)s.r,
+  launch_k(c, ttg::k_build_q, grid_for(rows * a, 256, 1024), 256, 0, s.Psi, s.Psi ? (int)s.As : (int)s.r, (int)s.r,
                                                                         (int)n, U, r_old, Q);
   post_launch(c);
   c->small[0].ensure(sizeof(double) * (size_t)(rows * a));
@@ -868,7 +887,7 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
   c->scal.ensure(sizeof(double) * 16);
   // (C is exactly symmetric: the SYRK reduction mirrors its lower triangle)
   prof_begin(c, "k_symmetrize_trace", 16.0 * a * a, 0.0);
-  ttg::k_symmetrize_trace<<<grid_for(a * a, 256, 64), 256, 0, c->stream>>>(G, (int)a, c->Craw.as<double>(), (int)rows,
+  launch_k(c, ttg::k_symmetrize_trace, grid_for(a * a, 256, 64), 256, 0, G, (int)a, c->Craw.as<double>(), (int)rows,
                                                                           c->scal.as<double>() + 4);
   post_launch(c);
   return did;
@@ -913,7 +932,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         char nm[64];
         std::snprintf(nm, sizeof nm, "k_syev_top[a=%d]", a);
         prof_begin(c, nm, 16.0 * a * a, 2.0 * a * a * K);
-        kern<<<1, ttg::kSubThreads, smem_s, c->stream>>>(sa);
+        launch_k(c, kern, 1, ttg::kSubThreads, smem_s, sa);
         post_launch(c);
         c->d2h += sizeof(EigResult);
         CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
@@ -943,7 +962,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
       char nm[64];
       std::snprintf(nm, sizeof nm, "k_syev[a=%d]", a);
       prof_begin(c, nm, 16.0 * a * a, 4.0 / 3.0 * a * a * a);
-      ttg::k_syev<<<1, ttg::kSyevThreads, smem, c->stream>>>(args);
+      launch_k(c, ttg::k_syev, 1, ttg::kSyevThreads, smem, args);
       post_launch(c);
     }
   } else {
@@ -973,7 +992,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     }
     kernel_occupancy((const void*)ttg::k_jacobi_eig, ttg::k_jacobi_eig, ttg::kEigThreads, smem);
     prof_begin(c, "k_jacobi_eig", 16.0 * a * a, 0.0);
-    ttg::k_jacobi_eig<<<1, ttg::kEigThreads, smem, c->stream>>>(args);
+    launch_k(c, ttg::k_jacobi_eig, 1, ttg::kEigThreads, smem, args);
     post_launch(c);
   }
   c->d2h += sizeof(EigResult);
@@ -1018,21 +1037,21 @@ EigResult accurate_eig(ttg_ctx* c, const double* X, int a, long long L, const do
   c->partials.ensure(sizeof(double) * (size_t)gx * a * a);
   args.Tout = c->partials.as<double>();
   prof_begin(c, "k_tsqr_local", 8.0 * a * L, (double)L * (4.0 * r_old * a + 2.0 * a * a));
-  ttg::k_tsqr_local<<<gx, ttg::kThreads, smem, c->stream>>>(args);
+  launch_k(c, ttg::k_tsqr_local, gx, ttg::kThreads, smem, args);
   post_launch(c);
   c->scratch.ensure(sizeof(double) * (size_t)a * a);
   c->G.ensure(sizeof(double) * (size_t)a * a);
   size_t smem2 = sizeof(double) * (size_t)a * a;
   kernel_occupancy((const void*)ttg::k_tsqr_combine, ttg::k_tsqr_combine, 1024, smem2);
   prof_begin(c, "k_tsqr_combine", 16.0 * gx * a * a, 2.0 * gx * a * a * a);
-  ttg::k_tsqr_combine<<<1, 1024, smem2, c->stream>>>(c->partials.as<double>(), gx, a, c->scratch.as<double>(),
+  launch_k(c, ttg::k_tsqr_combine, 1, 1024, smem2, c->partials.as<double>(), gx, a, c->scratch.as<double>(),
                                                      c->G.as<double>());
   post_launch(c);
   if (c->world > 1) {
     c->partials.ensure(sizeof(double) * (size_t)c->world * a * a);
     NK(ncclAllGather(c->G.p, c->partials.p, (size_t)a * a, ncclDouble, c->comm, c->stream));
     prof_begin(c, "k_tsqr_combine", 16.0 * c->world * a * a, 2.0 * c->world * a * a * a);
-    ttg::k_tsqr_combine<<<1, 1024, smem2, c->stream>>>(c->partials.as<double>(), c->world, a,
+    launch_k(c, ttg::k_tsqr_combine, 1, 1024, smem2, c->partials.as<double>(), c->world, a,
                                                        c->scratch.as<double>(), c->G.as<double>());
     post_launch(c);
   }
@@ -1054,7 +1073,7 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
   ttg::AppendArgs args{Upad, c->UR.as<double>(), a, r_old, r_R, out, c->scratch.as<double>(),
                        c->eigres.as<EigResult>()};
   prof_begin(c, "k_append", 8.0 * a * (2.0 * r_old + 2.0 * r_R), 2.0 * a * (r_old + r_R) * (r_old + r_R));
-  ttg::k_append<<<1, 1024, 0, c->stream>>>(args);
+  launch_k(c, ttg::k_append, 1, 1024, 0, args);
   post_launch(c);
   c->d2h += sizeof(EigResult);
   CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
@@ -1087,7 +1106,7 @@ bool project_ws16(ttg_ctx* c, const double* X, int a, long long L, const double*
   const size_t smem = fixed + nst * stage;
   c->UTf.ensure(sizeof(double) * std::max<size_t>(nfr, 1));
   prof_begin(c, "k_make_frags", 8.0 * nfr, 0.0);
-  ttg::k_make_frags16<<<grid_for((long long)nfr, 256, 256), 256, 0, c->stream>>>(W, a, r, ldw, nks, NB,
+  launch_k(c, ttg::k_make_frags16, grid_for((long long)nfr, 256, 256), 256, 0, W, a, r, ldw, nks, NB,
                                                                                  c->UTf.as<double>());
   post_launch(c);
   ttg::ProjArgs args{};
@@ -1110,7 +1129,7 @@ bool project_ws16(ttg_ctx* c, const double* X, int a, long long L, const double*
   char nm[64];
   std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
   prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
-  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  launch_k(c, kern, gx, threads, smem, tm, args);
   post_launch(c);
   return true;
 }
@@ -1177,13 +1196,13 @@ bool project_kc(ttg_ctx* c, const double* X, int a, long long L, const double* W
   if (smem > cap) return false;
   c->UTf.ensure(sizeof(double) * std::max<size_t>(nfr, 1));
   prof_begin(c, "k_make_frags16", 8.0 * nfr, 0.0);
-  ttg::k_make_frags16<<<grid_for((long long)nfr, 256, 256), 256, 0, c->stream>>>(W, a, r, ldw, nks, NB,
+  launch_k(c, ttg::k_make_frags16, grid_for((long long)nfr, 256, 256), 256, 0, W, a, r, ldw, nks, NB,
                                                                                  c->UTf.as<double>());
   post_launch(c);
   if (T) {
     c->UTt.ensure(sizeof(double) * std::max<size_t>(ntl, 1));
     prof_begin(c, "k_make_tail", 8.0 * ntl, 0.0);
-    ttg::k_make_tail<<<grid_for((long long)ntl, 256, 64), 256, 0, c->stream>>>(W, a, ldw, nks, 8 * NB, T,
+    launch_k(c, ttg::k_make_tail, grid_for((long long)ntl, 256, 64), 256, 0, W, a, ldw, nks, 8 * NB, T,
                                                                                c->UTt.as<double>());
     post_launch(c);
   }
@@ -1206,7 +1225,7 @@ bool project_kc(ttg_ctx* c, const double* X, int a, long long L, const double* W
   char nm[64];
   std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
   prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
-  kern<<<gx, threads, smem, c->stream>>>(tm, args);
+  launch_k(c, kern, gx, threads, smem, tm, args);
   post_launch(c);
   return true;
 }
@@ -1251,7 +1270,7 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
     char nm0[64];
     std::snprintf(nm0, sizeof nm0, "k_project[a=%d,r=%d]", a, r);
     prof_begin(c, nm0, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
-    k0<<<gx0, ttg::kThreads, smem0, c->stream>>>(args);
+    launch_k(c, k0, gx0, ttg::kThreads, smem0, args);
     post_launch(c);
     return tsq != nullptr;
   }
@@ -1294,7 +1313,7 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
       char nm[64];
       std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
       prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
-      kern<<<gx, ttg::kThreads, smem, c->stream>>>(tm, args);
+      launch_k(c, kern, gx, ttg::kThreads, smem, tm, args);
       post_launch(c);
       return tsq != nullptr;
     }
@@ -1317,7 +1336,7 @@ bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, i
   char nm[64];
   std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
   prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
-  kern<<<gx, ttg::kThreads, smem, c->stream>>>(args);
+  launch_k(c, kern, gx, ttg::kThreads, smem, args);
   post_launch(c);
   return tsq != nullptr;
 }
@@ -1345,7 +1364,7 @@ const double* materialise(ttg_ctx* c, const Src& s, int64_t n, DevBuf& dst) {
   const int64_t rows = s.As * n, a = s.r * n;
   c->wcomb.ensure(sizeof(double) * (size_t)(rows * a));
   prof_begin(c, "k_kron_eye", 8.0 * rows * a, 0.0);
-  ttg::k_kron_eye<<<grid_for(rows * a, 256, 1024), 256, 0, c->stream>>>(s.Psi, (int)s.As, (int)s.r, (int)n,
+  launch_k(c, ttg::k_kron_eye, grid_for(rows * a, 256, 1024), 256, 0, s.Psi, (int)s.As, (int)s.r, (int)n,
                                                                          c->wcomb.as<double>());
   post_launch(c);
   const long long L = s.Ls / n;
@@ -1448,7 +1467,7 @@ double sumsq_device(ttg_ctx* c, const double* x, long long n) {
   c->scal.ensure(sizeof(double) * 16);
   dim3 grid(1, 1);
   prof_begin(c, "k_sumsq_obs", 8.0 * n, 2.0 * n);
-  ttg::k_sumsq_obs<<<grid, 256, 0, c->stream>>>(x, n, 1, c->sumsq_part.as<double>());
+  launch_k(c, ttg::k_sumsq_obs, grid, 256, 0, x, n, 1, c->sumsq_part.as<double>());
   post_launch(c);
   return read_scalar(c, c->sumsq_part.as<double>());
 }
@@ -1508,11 +1527,11 @@ void norms_finish(ttg_ctx* c, Norms& nm, int64_t rows, bool produced) {
     c->scal.ensure(sizeof(double) * 16);
     const long long tpo = nm.S / (rows * ttg::kTC);
     prof_begin(c, "k_tiles_to_obs", 8.0 * tpo * ttg::kConsumerWarps * nm.b, 0.0);
-    ttg::k_tiles_to_obs<<<(unsigned)nm.b, 256, 0, c->stream>>>(c->tsq.as<double>(), tpo, (int)nm.b,
+    launch_k(c, ttg::k_tiles_to_obs, (unsigned)nm.b, 256, 0, c->tsq.as<double>(), tpo, (int)nm.b,
                                                                  c->on2.as<double>(), nullptr);
     post_launch(c);
     prof_begin(c, "k_sum_vec", 8.0 * nm.b, 0.0);
-    ttg::k_sum_vec<<<1, 32, 0, c->stream>>>(c->on2.as<double>(), (int)nm.b, c->scal.as<double>());
+    launch_k(c, ttg::k_sum_vec, 1, 32, 0, c->on2.as<double>(), (int)nm.b, c->scal.as<double>());
     post_launch(c);
     allreduce_sum(c, c->scal.as<double>(), 1);
   }
@@ -1655,7 +1674,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         c->cur[flip].ensure(sizeof(double) * (size_t)std::max<long long>(r_new * L, 1));
         const long long tot = r_new * L;
         prof_begin(c, "k_merge_rows", 8.0 * (double)(2 * r_new) * L, 0.0);
-        ttg::k_merge_rows<<<grid_for(tot, 256, 8 * c->num_sms), 256, 0, c->stream>>>(
+        launch_k(c, ttg::k_merge_rows, grid_for(tot, 256, 8 * c->num_sms), 256, 0, 
             c->scur[i + 1].as<double>(), (int)r_old, c->tmp.as<double>(), (int)r_new, L, c->cur[flip].as<double>());
         post_launch(c);
         src = Src{c->cur[flip].as<double>(), r_new, L, nullptr, r_new};
@@ -1677,7 +1696,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         const int64_t tot = r_new * n_next * rr_old;
         c->Upad.ensure(sizeof(double) * (size_t)std::max<int64_t>(tot, 1));
         prof_begin(c, "k_pad_core", 16.0 * tot, 0.0);
-        ttg::k_pad_core<<<grid_for(tot, 256, 1024), 256, 0, c->stream>>>(
+        launch_k(c, ttg::k_pad_core, grid_for(tot, 256, 1024), 256, 0, 
             tt->cores[i + 1].as<double>(), (int)rl_old, (int)n_next, (int)rr_old, (int)r_new, c->Upad.as<double>());
         post_launch(c);
         Upad = c->Upad.as<double>();
@@ -1795,7 +1814,7 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
     ia.out = c->iface[0].as<double>();
     kernel_occupancy((const void*)ttg::k_iface_all, ttg::k_iface_all, 1024, ismem);
     prof_begin(c, "k_iface", 8.0 * core_tot, flops);
-    ttg::k_iface_all<<<1, 1024, ismem, c->stream>>>(ia);
+    launch_k(c, ttg::k_iface_all, 1, 1024, ismem, ia);
     post_launch(c);
     return c->iface[0].as<double>();
   }
@@ -1806,12 +1825,12 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
     const int rl = (int)tt->ranks[i], n = (int)tt->modes[i], rr = (int)tt->ranks[i + 1];
     const long long t1 = (long long)rl * n * rr;
     prof_begin(c, "k_iface", 8.0 * t1, 2.0 * t1 * rl);
-    ttg::k_iface_step1<<<grid_for(t1, 256, 1024), 256, 0, c->stream>>>(c->iface[f].as<double>(),
+    launch_k(c, ttg::k_iface_step1, grid_for(t1, 256, 1024), 256, 0, c->iface[f].as<double>(),
                                                                         tt->cores[i].as<double>(), rl, n, rr,
                                                                         c->Mtmp.as<double>());
     post_launch(c);
     prof_begin(c, "k_iface", 8.0 * rr * rr, 2.0 * rr * rr * n * rl);
-    ttg::k_iface_step2<<<grid_for((long long)rr * rr, 128, 1024), 128, 0, c->stream>>>(
+    launch_k(c, ttg::k_iface_step2, grid_for((long long)rr * rr, 128, 1024), 128, 0, 
         c->Mtmp.as<double>(), tt->cores[i].as<double>(), rl, n, rr, c->iface[f ^ 1].as<double>());
     post_launch(c);
     f ^= 1;
@@ -1833,11 +1852,11 @@ void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double
   c->rn2.ensure(sizeof(double) * b);
   c->stats.ensure(sizeof(ttg::StarStats));
   prof_begin(c, "k_coef_stats", 8.0 * r * b, 2.0 * r * r * b);
-  ttg::k_coef_stats<<<grid_for(b, 128, 1024), 128, 0, c->stream>>>(coeffs, r, (int)b, M, c->cn2.as<double>(),
+  launch_k(c, ttg::k_coef_stats, grid_for(b, 128, 1024), 128, 0, coeffs, r, (int)b, M, c->cn2.as<double>(),
                                                                    c->cmc.as<double>());
   post_launch(c);
   prof_begin(c, "k_star_local", 32.0 * b, 10.0 * b);
-  ttg::k_star_local<<<1, 256, 0, c->stream>>>(c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
+  launch_k(c, ttg::k_star_local, 1, 256, 0, c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
                                              (int)b, eps, c->errs.as<double>(), c->rn2.as<double>(),
                                              c->stats.as<ttg::StarStats>());
   post_launch(c);
@@ -1986,7 +2005,7 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
     rep->eps_target = delta;
     c->sel.ensure((size_t)b);
     prof_begin(c, "k_star_mask", 9.0 * b, 0.0);
-    ttg::k_star_mask<<<grid_for(b, 256, 64), 256, 0, c->stream>>>(c->errs.as<double>(), (int)b, eps_des,
+    launch_k(c, ttg::k_star_mask, grid_for(b, 256, 64), 256, 0, c->errs.as<double>(), (int)b, eps_des,
                                                                     cfg.subselect_enabled, c->sel.as<uint8_t>());
     post_launch(c);
     SweepOpts o;
@@ -2115,6 +2134,7 @@ void ttg_heuristics_default(ttg_heuristics* h) {
 static int ctx_init(ttg_ctx* c, int device) {
   CK(cudaSetDevice(device));
   c->device = device;
+  c->pdl = std::getenv("TTG_NO_PDL") == nullptr;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
@@ -2200,6 +2220,7 @@ int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[1
     ctx_init(c, device);
     c->rank = rank;
     c->world = world;
+    if (world > 1) c->pdl = false;  // NCCL kernels interleave in the stream
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
     NK(ncclCommInitRank(&c->comm, world, id, rank));

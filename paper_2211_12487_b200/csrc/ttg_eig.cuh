@@ -11,6 +11,7 @@
 // lambda_j v_j, so lambda_j = |w_j| and v_j = w_j / lambda_j — no V matrix is
 // kept, which lets a <= 165 live entirely in shared memory.
 #pragma once
+#include "ttg_pdl.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -55,6 +56,7 @@ struct EigArgs {
 };
 
 __global__ void __launch_bounds__(kEigThreads) k_jacobi_eig(EigArgs p) {
+  griddep_wait();
   extern __shared__ __align__(16) double esm[];
   const int a = p.a;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -237,6 +239,7 @@ __device__ double block_sum(double v, double* red) {
 }
 
 __global__ void __launch_bounds__(1024) k_append(AppendArgs p) {
+  griddep_wait();
   __shared__ double red[33];
   const int a = p.a, r0 = p.r_old, rr = p.r_R, rn = r0 + rr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;

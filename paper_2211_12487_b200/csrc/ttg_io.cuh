@@ -3,6 +3,7 @@
 // reconstruction, and the orthonormality measurement used when a TTC1
 // checkpoint is loaded.
 #pragma once
+#include "ttg_pdl.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -20,6 +21,7 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
                                                      const double* __restrict__ C, long long ldc, int m,
                                                      const double* __restrict__ X, long long ldx,
                                                      double* __restrict__ part) {
+  griddep_wait();
   __shared__ double cs[kRreObsChunk * RMAX];
   __shared__ double red[2][8];
   double dsum = 0.0, xsum = 0.0;
@@ -79,6 +81,7 @@ __global__ void __launch_bounds__(256) k_rre_partial_any(const double* __restric
                                                          const double* __restrict__ C, long long ldc, int m,
                                                          const double* __restrict__ X, long long ldx,
                                                          double* __restrict__ part) {
+  griddep_wait();
   __shared__ double red[2][8];
   double dsum = 0.0, xsum = 0.0;
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(256) k_rre_partial_any(const double* __restric
 // out[0..1] = fixed-order sums of the n pairs in part (one warp, strided
 // per-lane partials then a butterfly: deterministic for a given n)
 __global__ void k_pair_sum(const double* __restrict__ part, long long n, double* __restrict__ out) {
+  griddep_wait();
   double a = 0.0, b = 0.0;
   for (long long i = threadIdx.x; i < n; i += 32) {
     a += part[2 * i];
@@ -136,6 +140,7 @@ __global__ void k_pair_sum(const double* __restrict__ part, long long n, double*
 // dev = max |U^T U - I| of one left unfolding U (a x r, column-major),
 // one block: entry (i, j) of the Gram per thread-strided loop.
 __global__ void k_ortho_dev(const double* __restrict__ U, int a, int r, double* __restrict__ dev) {
+  griddep_wait();
   __shared__ double red[32];
   double mx = 0.0;
   for (long long e = threadIdx.x; e < (long long)r * r; e += blockDim.x) {

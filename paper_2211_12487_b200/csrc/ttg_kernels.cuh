@@ -12,6 +12,7 @@
 // Fragment layouts of m8n8k4 (row.col), lane = 4*g + t:
 //   A (8x4):  A[g][t]          B (4x8): B[t][g]          C (8x8): C[g][2t], C[g][2t+1]
 #pragma once
+#include "ttg_pdl.cuh"
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -341,6 +342,7 @@ struct GramArgs {
 
 template <int WBR, int WBC, bool PRE, bool DB>
 __global__ void __launch_bounds__(kThreads) k_gram_resid(GramArgs p) {
+  griddep_wait();
   extern __shared__ __align__(16) double smem[];
   __shared__ double red8[kThreads / 32];
   __shared__ __align__(8) uint64_t bars[2];
@@ -546,6 +548,7 @@ __device__ __forceinline__ void syrk_issue(const SyrkArgs& p, long long q0, int 
 
 template <int MAXT, int NCW = kConsumerWarps>
 __global__ void __launch_bounds__((NCW + 1) * 32) k_syrk(SyrkArgs p) {
+  griddep_wait();
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ double red8[kConsumerWarps + 1];
@@ -725,6 +728,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_syrk(SyrkArgs p) {
 template <int NBK>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) k_syrk_kx(const __grid_constant__ CUtensorMap tm,
                                                                           SyrkArgs p) {
+  griddep_wait();
   constexpr int NBL = NBK * (NBK + 1) / 2;
   constexpr int NCW = kConsumerWarps;
   constexpr int SBD = 128;
@@ -987,6 +991,7 @@ __device__ __forceinline__ void syrk_kp_part(const CUtensorMap* tm, const SyrkAr
 template <int NBK, int P>
 __global__ void __launch_bounds__(kConsumerWarps * 32, 1) k_syrk_kp(const __grid_constant__ CUtensorMap tm,
                                                                     SyrkArgs p) {
+  griddep_wait();
   constexpr int KS = 8 / P;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[8], empty[8];
@@ -1022,6 +1027,7 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, 1) k_syrk_kp(const __grid
 // one a8 x a8 partial per CTA.
 __global__ void k_gram_reduce_s1(const double* __restrict__ partials, int nx, int layout, int ld, int a,
                                  double* __restrict__ tmp) {
+  griddep_wait();
   const int xs = gridDim.y, y = blockIdx.y;
   const int x0 = (int)((long long)nx * y / xs), x1 = (int)((long long)nx * (y + 1) / xs);
   const long long n = (long long)a * a;
@@ -1051,6 +1057,7 @@ __global__ void k_gram_reduce_s1(const double* __restrict__ partials, int nx, in
   }
 }
 __global__ void k_gram_reduce_s2(const double* __restrict__ tmp, int xs, int a, double* __restrict__ G) {
+  griddep_wait();
   const long long n = (long long)a * a;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(e % a), j = (int)(e / a);
@@ -1066,6 +1073,7 @@ __global__ void k_gram_reduce_s2(const double* __restrict__ tmp, int xs, int a, 
 // a x a matrix G (column-major).
 __global__ void k_gram_reduce(const double* __restrict__ partials, int nx, int sbd, int a,
                               double* __restrict__ G) {
+  griddep_wait();
   long long n = (long long)a * a;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
@@ -1148,6 +1156,7 @@ struct TsqrArgs {
 
 // per-CTA T of the residual columns it owns (grid-stride over 64-column tiles)
 __global__ void __launch_bounds__(kThreads) k_tsqr_local(TsqrArgs p) {
+  griddep_wait();
   extern __shared__ __align__(16) double smem[];
   __shared__ double red[33];
   const int a = p.src.a, ldt = p.ldt, ldp = p.ldp;
@@ -1177,6 +1186,7 @@ __global__ void __launch_bounds__(kThreads) k_tsqr_local(TsqrArgs p) {
 // T <- R-factor of the stacked factors Ts[0..n-1] (each a x a), fixed order.
 __global__ void __launch_bounds__(1024) k_tsqr_combine(const double* __restrict__ Ts, int n, int a,
                                                       double* __restrict__ scratch, double* __restrict__ T) {
+  griddep_wait();
   extern __shared__ __align__(16) double sm2[];
   __shared__ double red[33];
   double* Tf = sm2;  // a x a
@@ -1229,6 +1239,7 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // (a8 <= 256).
 template <bool DB, bool REGW>
 __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
+  griddep_wait();
   extern __shared__ __align__(16) double smem[];
   __shared__ double red8[kThreads / 32];
   __shared__ __align__(8) uint64_t bars[2];
@@ -1382,6 +1393,7 @@ __global__ void __launch_bounds__(kThreads) k_project(ProjArgs p) {
 constexpr int kProjStages = 8;
 template <bool REGW, int TC>
 __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  griddep_wait();
   static_assert(TC == 64 || TC == 32, "tile width");
   __shared__ double red_ss[4];
   constexpr int CW = TC / 8;   // column warps
@@ -1565,6 +1577,7 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
 // k halves are summed through shared memory.  Same ring / barrier protocol and
 // output layout as k_project_tma.
 __global__ void __launch_bounds__(kThreads) k_project_w2(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  griddep_wait();
   constexpr int TC = 64, BOX = 16 * TC;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kProjStages];
@@ -1698,6 +1711,7 @@ __global__ void __launch_bounds__(kThreads) k_project_w2(const __grid_constant__
 // block, contiguous in out) and stored coalesced; optional per-(tile, 8-column
 // group) input sums of squares.
 __global__ void __launch_bounds__(kThreads) k_project_m16(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  griddep_wait();
   constexpr int TC = 64, BOX = 16 * TC;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kProjStages];
@@ -1810,6 +1824,7 @@ __global__ void __launch_bounds__(kThreads) k_project_m16(const __grid_constant_
 // (lane = 4g + t), zero outside W; b < nks = ceil(a/16), nb < NB = r8/8.
 __global__ void k_make_frags16(const double* __restrict__ W, int a, int r, int ld, int nks, int NB,
                                double* __restrict__ Wm) {
+  griddep_wait();
   const long long n = (long long)nks * NB * 128;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     const int lane = (int)(e & 31), i = (int)((e >> 5) & 3);
@@ -1833,6 +1848,7 @@ __global__ void k_make_frags16(const double* __restrict__ W, int a, int r, int l
 // group) input sums of squares.
 template <int NCW, int NB>
 __global__ void __launch_bounds__((NCW + 1) * 32) k_project_ws16(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  griddep_wait();
   constexpr int TC = 16 * NCW, BOX = 16 * TC;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kProjStages], empty[kProjStages];
@@ -1947,6 +1963,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_ws16(const __grid_co
 // (zero past a), so lane (g, t) reads its four k values of box b as two double2.
 __global__ void k_make_tail(const double* __restrict__ W, int a, int ld, int nks, int c0, int T,
                             double* __restrict__ Wt) {
+  griddep_wait();
   const int n = nks * T * 16;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int q = e & 3, t = (e >> 2) & 3, f = e >> 4;
@@ -1968,6 +1985,7 @@ __global__ void k_make_tail(const double* __restrict__ W, int a, int ld, int nks
 // The tail partial sums are reduced over the 4 lanes t of a column group.
 template <int NCW, int NB, int T>
 __global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  griddep_wait();
   constexpr int TC = 16 * NCW, BOX = 16 * TC;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kProjStages], empty[kProjStages];
@@ -2125,6 +2143,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_cons
 constexpr int kBoxStages = 16;
 template <int MRMAX, bool REGW>
 __global__ void __launch_bounds__(kSyrkThreads) k_project_box(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  griddep_wait();
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kBoxStages], empty[kBoxStages];
   double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -2296,6 +2315,7 @@ struct Syrk2Args {
 
 template <int MAXT>
 __global__ void __launch_bounds__(kSyrkThreads) k_syrk2(const __grid_constant__ CUtensorMap tm, Syrk2Args p) {
+  griddep_wait();
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -2436,6 +2456,7 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk2(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 template <int NCW, int MAXG>
 __global__ void __launch_bounds__((NCW + 1) * 32) k_syrk_ws16(const __grid_constant__ CUtensorMap tm, Syrk2Args p) {
+  griddep_wait();
   constexpr int BOX = 1024;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxStages + 4], empty[kMaxStages + 4];
@@ -2583,6 +2604,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_syrk_ws16(const __grid_const
 
 // G (a x a, symmetric) = sum over the nx CTA partials (lower triangle read)
 __global__ void k_gram_reduce2(const double* __restrict__ partials, int nx, int a8, int a, double* __restrict__ G) {
+  griddep_wait();
   const long long n = (long long)a * a;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     int i = (int)(e % a), j = (int)(e / a);
@@ -2598,6 +2620,7 @@ __global__ void k_gram_reduce2(const double* __restrict__ partials, int nx, int 
 // observations): one block per observation, fixed assignment + fixed tree
 __global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_per_obs, int nobs,
                                double* __restrict__ on2, double* __restrict__ unused) {
+  griddep_wait();
   __shared__ double red[32];
   const long long per_obs = tiles_per_obs * kConsumerWarps;
   const int o = blockIdx.x;
@@ -2617,6 +2640,7 @@ __global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_pe
 
 // total = sum_o v[o] in observation order (one thread: the reference's order)
 __global__ void k_sum_vec(const double* __restrict__ v, int n, double* __restrict__ total) {
+  griddep_wait();
   if (threadIdx.x != 0) return;
   double s = 0.0;
   for (int i = 0; i < n; ++i) s += v[i];
@@ -2634,6 +2658,7 @@ __global__ void __launch_bounds__(1024) k_gemm(const double* __restrict__ A, lon
                                                const double* __restrict__ B, long long ldb, double* C,
                                                long long ldc, long long m, long long n, long long k,
                                                double alpha, double beta) {
+  griddep_wait();
   __shared__ double As[32][33];  // As[kk][i]
   __shared__ double Bs[32][33];  // Bs[j][kk]
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -2670,6 +2695,7 @@ __global__ void __launch_bounds__(1024) k_gemm(const double* __restrict__ A, lon
 // zero the columns of observations that are not selected
 __global__ void k_mask_cols(double* __restrict__ X, int a, long long L, const uint8_t* __restrict__ sel,
                             long long cpo) {
+  griddep_wait();
   long long n = (long long)a * L;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {

@@ -2,6 +2,7 @@
 // core padding, TT-ICE* per-observation statistics and decisions, and the
 // expansion used by reconstruct.
 #pragma once
+#include "ttg_pdl.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -14,6 +15,7 @@ namespace ttg {
 // ([a8/8][r8/4][32]); zero outside the matrix.
 __global__ void k_make_frags(const double* __restrict__ U, int a, int r, int ld, int a8, int r8,
                              double* __restrict__ UTf, double* __restrict__ Uf) {
+  griddep_wait();
   const int KA = a8 / 4, KR = r8 / 4;
   const long long n1 = (long long)(r8 / 8) * KA * 32;
   const long long n2 = (long long)(a8 / 8) * KR * 32;
@@ -41,6 +43,7 @@ __global__ void k_make_frags(const double* __restrict__ U, int a, int r, int ld,
 // Per-observation partial sums of squares: block (chunk, obs).
 __global__ void k_sumsq_obs(const double* __restrict__ Y, long long S, int nchunk,
                             double* __restrict__ part) {
+  griddep_wait();
   __shared__ double red[33];
   const int o = blockIdx.y, c = blockIdx.x;
   long long cs = (S + nchunk - 1) / nchunk;
@@ -68,6 +71,7 @@ __global__ void k_sumsq_obs(const double* __restrict__ Y, long long S, int nchun
 // on2[o] = sum of chunk partials (fixed order); out_total = sum_o on2[o].
 __global__ void k_sumsq_finalize(const double* __restrict__ part, int nchunk, int nobs,
                                  double* __restrict__ on2, double* __restrict__ total) {
+  griddep_wait();
   double s = 0.0;
   for (int o = threadIdx.x; o < nobs; o += blockDim.x) {
     double v = 0.0;
@@ -84,6 +88,7 @@ __global__ void k_sumsq_finalize(const double* __restrict__ part, int nchunk, in
 // pad_core (tt_ice.cpp:43-58): core (r_old x n x r_right) -> (r_new x n x r_right)
 __global__ void k_pad_core(const double* __restrict__ core, int r_old, int n, int r_right, int r_new,
                            double* __restrict__ out) {
+  griddep_wait();
   long long tot = (long long)r_new * n * r_right;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
        e += (long long)gridDim.x * blockDim.x) {
@@ -96,6 +101,7 @@ __global__ void k_pad_core(const double* __restrict__ core, int r_old, int n, in
 // M_new = sum_j G_j^T M G_j  (G_j = core[:, j, :], r_l x r_r), two steps via scratch T.
 __global__ void k_iface_step1(const double* __restrict__ M, const double* __restrict__ core, int rl,
                               int n, int rr, double* __restrict__ T) {
+  griddep_wait();
   // T[p', j, q] = sum_p M[p', p] core[p, j, q]
   long long tot = (long long)rl * n * rr;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
@@ -109,6 +115,7 @@ __global__ void k_iface_step1(const double* __restrict__ M, const double* __rest
 }
 __global__ void k_iface_step2(const double* __restrict__ T, const double* __restrict__ core, int rl,
                               int n, int rr, double* __restrict__ Mn) {
+  griddep_wait();
   // Mn[q, q'] = sum_{j, p'} core[p', j, q] T[p', j, q']
   long long tot = (long long)rr * rr;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
@@ -140,6 +147,7 @@ struct IfaceArgs {
 // column walks of the second contraction hit distinct banks (m is often a
 // multiple of 16).
 __global__ void __launch_bounds__(1024) k_iface_all(IfaceArgs a) {
+  griddep_wait();
   extern __shared__ double sm[];
   double* Mb[2] = {sm, sm + a.rmax * a.rmax};
   double* T = sm + 2 * a.rmax * a.rmax;
@@ -207,6 +215,7 @@ __global__ void __launch_bounds__(1024) k_iface_all(IfaceArgs a) {
 // One thread per element; (K U)[i, k] is formed inline (r_old r FMA).
 __global__ void k_build_q(const double* __restrict__ Psi, int As, int r, int n, const double* __restrict__ U,
                           int r_old, double* __restrict__ Q) {
+  griddep_wait();
   const int rows = As * n, a = r * n;
   const long long tot = (long long)rows * a;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
@@ -233,6 +242,7 @@ __global__ void k_build_q(const double* __restrict__ Psi, int As, int r, int n, 
 // cn2[o] = |c_o|^2, cmc[o] = c_o^T M c_o  (c: r x b, ld r)
 __global__ void k_coef_stats(const double* __restrict__ C, int r, int b, const double* __restrict__ M,
                              double* __restrict__ cn2, double* __restrict__ cmc) {
+  griddep_wait();
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < b; o += gridDim.x * blockDim.x) {
     const double* c = C + (long long)r * o;
     double s = 0.0, m = 0.0;
@@ -259,6 +269,7 @@ __global__ void __launch_bounds__(256) k_star_local(const double* __restrict__ o
                                                     const double* __restrict__ cmc, int b, double eps,
                                                     double* __restrict__ errs, double* __restrict__ rn2_out,
                                                     StarStats* st) {
+  griddep_wait();
   // per-observation values in parallel (256 at a time, staged in shared
   // memory), the nine decision sums by one thread in observation order (the
   // reference's loop order, so the sums are bit-identical to a serial pass)
@@ -300,6 +311,7 @@ __global__ void __launch_bounds__(256) k_star_local(const double* __restrict__ o
 
 // W = I_n (x) Psi  ((As*n) x (r*n), block diagonal)
 __global__ void k_kron_eye(const double* __restrict__ Psi, int As, int r, int n, double* __restrict__ W) {
+  griddep_wait();
   const long long rows = (long long)As * n, tot = rows * r * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
        e += (long long)gridDim.x * blockDim.x) {
@@ -313,6 +325,7 @@ __global__ void k_kron_eye(const double* __restrict__ Psi, int As, int r, int n,
 // out (rn x L) = [old (ro x L) ; add ((rn - ro) x L)] row-interleaved per column
 __global__ void k_merge_rows(const double* __restrict__ old, int ro, const double* __restrict__ add, int rn,
                              long long L, double* __restrict__ out) {
+  griddep_wait();
   const int ra = rn - ro;
   const long long tot = (long long)rn * L;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
@@ -327,6 +340,7 @@ __global__ void k_merge_rows(const double* __restrict__ old, int ro, const doubl
 // block 0 also writes trace(Tsrc) -> *tr (Tsrc: nt x nt; G's diagonal is not
 // modified, so Tsrc may be G; fixed warp-tree order, deterministic).
 __global__ void k_symmetrize_trace(double* __restrict__ G, int a, const double* Tsrc, int nt, double* __restrict__ tr) {
+  griddep_wait();
   const long long n = (long long)a * a;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(e % a), j = (int)(e / a);
@@ -348,6 +362,7 @@ __global__ void k_symmetrize_trace(double* __restrict__ G, int a, const double* 
 // selection mask (err > eps, or all when subselect is off)
 __global__ void k_star_mask(const double* __restrict__ errs, int b, double eps, int subselect,
                             uint8_t* __restrict__ sel) {
+  griddep_wait();
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < b; o += gridDim.x * blockDim.x)
     sel[o] = subselect ? (errs[o] > eps ? 1 : 0) : 1;
 }

@@ -14,6 +14,7 @@
 // O(a) block barriers.  Accuracy: eigenvalues to eps |G| absolute,
 // eigenvectors to eps |G| / gap — the same as a Jacobi solve of G.
 #pragma once
+#include "ttg_pdl.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -80,6 +81,7 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
 }
 
 __global__ void __launch_bounds__(kSyevThreads) k_syev(SyevArgs p) {
+  griddep_wait();
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[33];
   __shared__ int s_rank, s_done;
@@ -740,6 +742,7 @@ __device__ void block_cholqr2(double* X, double* Y, int a, int k, double* S, dou
 
 template <int K>
 __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
+  griddep_wait();
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[64];
   __shared__ double H[K * K], Wv[K * K], theta[K], resn[K];
