@@ -722,7 +722,7 @@ bool syrk2(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, 
 // holds at most 40 lower blocks
 constexpr int kp_parts(int nbk) {
   const int nbl = nbk * (nbk + 1) / 2;
-  return (nbl + 1) / 2 <= 40 ? 2 : (nbl + 3) / 4 <= 44 ? 4 : 8;
+  return nbl <= 40 ? 1 : (nbl + 1) / 2 <= 40 ? 2 : (nbl + 3) / 4 <= 44 ? 4 : 8;
 }
 template <int NBK>
 void* kp_kernel() {
@@ -730,6 +730,8 @@ void* kp_kernel() {
 }
 void* kp_pick(int nbk) {
   switch (nbk) {
+    case 7: return kp_kernel<7>();
+    case 8: return kp_kernel<8>();
     case 9: return kp_kernel<9>();
     case 10: return kp_kernel<10>();
     case 11: return kp_kernel<11>();
@@ -751,14 +753,15 @@ bool syrk_kp(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel
   const int a8 = ttg::round_up(a, 8), nbk = a8 / 8;
   // measured: 8 parts (NBK >= 19) re-load too many fragments per DMMA and lose
   // to k_syrk2; up to 4 parts win (a = 136: 0.16 vs 0.24 ms per 1.1 GB)
-  if (std::getenv("TTG_NO_KP") || tsq || (a & 1) || nbk < 9 || nbk > 18 || kp_parts(nbk) > 4 ||
+  if (std::getenv("TTG_NO_KP") || tsq || (a & 1) || nbk < (std::getenv("TTG_KP8") ? 7 : 9) || nbk > 18 ||
+      kp_parts(nbk) > 4 ||
       (sel && cpo % ttg::kTC != 0))
     return false;
   CUtensorMap tm;
   if (!make_tmap(&tm, X, a, L)) return false;
   const size_t stage = sizeof(double) * 1024 * (size_t)((nbk + 1) / 2);
   const size_t cap = (size_t)c->smem_optin - 1024;
-  int nst = (int)std::min<size_t>(4, (cap - 1024) / stage);
+  int nst = (int)std::min<size_t>(6, (cap - 1024) / stage);
   if (const char* e = std::getenv("TTG_KP_NST")) nst = std::min(nst, std::max(2, std::atoi(e)));
   if (nst < 2) return false;
   ttg::SyrkArgs args{};
@@ -810,6 +813,11 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
   args.sel = sel;
   args.cpo = cpo;
   args.n_tiles = (L + ttg::kTC - 1) / ttg::kTC;
+  // measured at a = 64: k_syrk_kx 1.17 ms, k_syrk_kp<8, 1> 1.32 ms per 4.3 GB
+  if ((nb == 7 || nb == 8) && std::getenv("TTG_KP8") && syrk_kp(c, X, a, L, sel, cpo, sel_frac, tsq)) {
+    allreduce_sum(c, c->G.as<double>(), (size_t)a * a);
+    return false;
+  }
   CUtensorMap tmk;
   if ((nb == 7 || nb == 8) && !std::getenv("TTG_NO_KX") && (!sel || cpo % ttg::kTC == 0) &&
       make_tmap(&tmk, X, a, L)) {  // k-split SYRK, one CTA / SM
@@ -2176,7 +2184,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>};
-    for (int nbk = 9; nbk <= 20; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
+    for (int nbk = 7; nbk <= 20; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
     for (int nb = 1; nb <= 4; ++nb)
       for (int t = 0; t <= 2; ++t) {
         CK(cudaFuncGetAttributes(&fa, kc_pick(4, nb, t)));
