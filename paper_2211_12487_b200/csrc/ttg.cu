@@ -145,6 +145,8 @@ struct ttg_ctx {
     cudaEvent_t e0, e1;
   };
   bool profiling = false;
+  uint64_t iface_gen = 0;
+  const double* iface_ptr = nullptr;
   bool pdl = true;  // programmatic dependent launch (launch_k); off under TTG_NO_PDL and for world > 1
   std::vector<KStat> kstats;
   std::vector<Pending> pending;
@@ -163,6 +165,11 @@ struct ttg_tt {
   int64_t rc = 0, oc = 0, n_obs = 0;
   int64_t ortho_count = 0;
   std::vector<int64_t> bounds;
+  uint64_t gen = next_gen();  // bumped whenever the cores may change (caches keyed on it)
+  static uint64_t next_gen() {
+    static std::atomic<uint64_t> g{0};
+    return ++g;
+  }
 };
 
 namespace {
@@ -1170,38 +1177,65 @@ void* kc_pick_t(int NB, int T) {
 }
 void* kc_pick(int ncw, int NB, int T) { return ncw == 8 ? kc_pick_t<8>(NB, T) : kc_pick_t<4>(NB, T); }
 
+struct KcPlan {
+  int NB = 0, T = 0, ncw = 0, kc = 0, nst = 0, nks = 0;
+  size_t smem = 0, nfr = 0, ntl = 0;
+};
+
+// Shared-memory plan of k_project_kc for (a, r): 8 consumer warps (128-column
+// tiles, two warps per SM sub-partition) for tall sources, 4 (64-column
+// tiles, two CTAs / SM) when the whole tile fits a stage or the 8-warp ring
+// does not fit next to the W fragments; false when neither fits.
+bool kc_plan(const ttg_ctx* c, int a, int r, KcPlan& P) {
+  if (std::getenv("TTG_NO_KC") || (a & 1) || r > 34 || r < 1) return false;
+  P.NB = (r + 7) / 8;
+  P.T = 0;
+  if (r > 8 && (r % 8 == 1 || r % 8 == 2) && !std::getenv("TTG_NO_TAIL")) {
+    P.NB = r / 8;
+    P.T = r % 8;
+  }
+  if (P.NB > 4) return false;
+  P.nks = (a + 15) / 16;
+  P.nfr = (size_t)P.nks * P.NB * 128;
+  P.ntl = (size_t)P.nks * P.T * 16;
+  const size_t cap = (size_t)c->smem_optin - 1024;
+  int order[2] = {P.nks > 4 ? 8 : 4, P.nks > 4 ? 4 : 8};
+  if (const char* e = std::getenv("TTG_KC_NCW")) order[0] = order[1] = std::atoi(e) == 8 ? 8 : 4;
+  for (int ncw : order) {
+    for (int kcw : {4, 2}) {
+      const int kc = std::min(P.nks, std::getenv("TTG_KC") ? std::max(1, std::atoi(std::getenv("TTG_KC"))) : kcw);
+      const int tc = 16 * ncw;
+      const size_t stage = sizeof(double) * (size_t)kc * 16 * tc;
+      const size_t fixed = 1024 + sizeof(double) * (P.nfr + P.ntl + (size_t)ncw * 16 * (8 * P.NB + P.T));
+      if (fixed + 2 * stage > cap) continue;
+      int nst = 2;
+      if (2 * (fixed + 2 * stage) > 220 * 1024) {  // one CTA / SM: deepen the ring
+        while (nst < ttg::kProjStages && fixed + (nst + 1) * stage <= cap) ++nst;
+      } else {
+        while (nst < ttg::kProjStages && 2 * (fixed + (nst + 1) * stage) <= 220 * 1024 && (nst + 1) * kc <= 2 * P.nks)
+          ++nst;
+      }
+      if (const char* e = std::getenv("TTG_KC_NST")) nst = std::max(2, std::min(ttg::kProjStages, std::atoi(e)));
+      if (fixed + nst * stage > cap) continue;
+      P.ncw = ncw;
+      P.kc = kc;
+      P.nst = nst;
+      P.smem = fixed + nst * stage;
+      return true;
+    }
+  }
+  return false;
+}
+
 bool project_kc(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
                 double* tsq) {
-  if (std::getenv("TTG_NO_KC") || (a & 1) || r > 34 || r < 1) return false;
-  int NB = (r + 7) / 8, T = 0;
-  if (r > 8 && (r % 8 == 1 || r % 8 == 2) && !std::getenv("TTG_NO_TAIL")) {
-    NB = r / 8;
-    T = r % 8;
-  }
-  if (NB > 4) return false;
-  // 8 consumer warps (128-column tiles, 2 warps per SM sub-partition) for
-  // tall sources; 4 (64-column tiles, 2 CTAs / SM) when the whole tile fits
-  const int nks = (a + 15) / 16;
-  int ncw = nks > 4 ? 8 : 4;
-  if (std::getenv("TTG_KC_NCW")) ncw = std::atoi(std::getenv("TTG_KC_NCW")) == 8 ? 8 : 4;
+  KcPlan P;
+  if (!kc_plan(c, a, r, P)) return false;
+  const int NB = P.NB, T = P.T, ncw = P.ncw, nks = P.nks, kc = P.kc, nst = P.nst;
+  const size_t nfr = P.nfr, ntl = P.ntl, smem = P.smem;
   const int tc = 16 * ncw;
   CUtensorMap tm;
   if (!make_tmap(&tm, X, a, L, tc)) return false;
-  const int kc = std::min(nks, std::getenv("TTG_KC") ? std::max(1, std::atoi(std::getenv("TTG_KC"))) : 4);
-  const size_t nfr = (size_t)nks * NB * 128, ntl = (size_t)nks * T * 16;
-  const size_t stage = sizeof(double) * (size_t)kc * 16 * tc;
-  const size_t fixed = 1024 + sizeof(double) * (nfr + ntl + (size_t)ncw * 16 * (8 * NB + T));
-  const size_t cap = (size_t)c->smem_optin - 1024;
-  if (fixed + 2 * stage > cap) return false;
-  int nst = 2;
-  if (2 * (fixed + 2 * stage) > 220 * 1024) {  // one CTA / SM: deepen the ring
-    while (nst < ttg::kProjStages && fixed + (nst + 1) * stage <= cap) ++nst;
-  } else {
-    while (nst < ttg::kProjStages && 2 * (fixed + (nst + 1) * stage) <= 220 * 1024 && (nst + 1) * kc <= 2 * nks) ++nst;
-  }
-  if (std::getenv("TTG_KC_NST")) nst = std::max(2, std::min(ttg::kProjStages, std::atoi(std::getenv("TTG_KC_NST"))));
-  const size_t smem = fixed + nst * stage;
-  if (smem > cap) return false;
   c->UTf.ensure(sizeof(double) * std::max<size_t>(nfr, 1));
   prof_begin(c, "k_make_frags16", 8.0 * nfr, 0.0);
   launch_k(c, ttg::k_make_frags16, grid_for((long long)nfr, 256, 256), 256, 0, W, a, r, ldw, nks, NB,
@@ -1559,6 +1593,7 @@ bool can_fuse(const Src& s, int64_t n_i, int64_t r_new, int64_t n_next, int64_t 
 
 SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm) {
   SweepOut out;
+  tt->gen = ttg_tt::next_gen();  // the sweep rewrites the cores
   const int d = tt->d;
   const int64_t S = prod(tt->modes);
   std::vector<int64_t> old_ranks = tt->ranks;
@@ -1739,10 +1774,11 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
 // buffer through the combined interface when k_project_kc takes it (even rows
 // <= kProjFuseMax, r <= 34), so Y -> r_3 x L_3 at cfg3 is one pass (no cur_2).
 constexpr int kProjFuseMax = 512;
-bool can_fuse_proj(const Src& s, int64_t n_i, int64_t n_next, int64_t r_next) {
+bool can_fuse_proj(const ttg_ctx* c, const Src& s, int64_t n_i, int64_t n_next, int64_t r_next) {
   const int64_t rows = s.As * n_i * n_next;
   if (std::getenv("TTG_NO_PROJ_FUSE")) return rows <= kFastMax && r_next <= kFastMax;
-  return rows <= kProjFuseMax && !(rows & 1) && r_next <= 34;
+  KcPlan P;
+  return rows <= kProjFuseMax && kc_plan(c, (int)rows, (int)r_next, P);
 }
 
 // Projection of Y through the train's current cores (projection-only fusion
@@ -1766,7 +1802,7 @@ const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64
     if (i + 1 < d) {
       const int64_t n_next = tt->modes[i + 1];
       const int64_t rr = tt->ranks[i + 2];
-      if (can_fuse_proj(src, n_i, n_next, rr)) {
+      if (can_fuse_proj(c, src, n_i, n_next, rr)) {
         const double* psi = src.Psi ? combine_psi(c, src, n_i, Ui, r, c->spsi[pf]) : Ui;
         if (src.Psi) pf ^= 1;
         src = Src{src.S, src.As * n_i, L, psi, r};
@@ -1795,7 +1831,16 @@ const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64
 }
 
 // M = Phi^T Phi of the spatial chain -> returns device pointer (r_d x r_d)
+const double* interface_gram_compute(ttg_ctx* c, const ttg_tt* tt);
+// cached per train generation: a TT-ICE* skip step leaves the cores as they
+// were, so the next increment's statistics reuse Phi^T Phi
 const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
+  if (c->iface_gen == tt->gen && c->iface_ptr && !std::getenv("TTG_NO_IFACE_CACHE")) return c->iface_ptr;
+  c->iface_ptr = interface_gram_compute(c, tt);
+  c->iface_gen = tt->gen;
+  return c->iface_ptr;
+}
+const double* interface_gram_compute(ttg_ctx* c, const ttg_tt* tt) {
   int64_t rmax = 1;
   for (auto r : tt->ranks) rmax = std::max(rmax, r);
   int64_t nmax = 1;
@@ -1805,7 +1850,8 @@ const double* interface_gram(ttg_ctx* c, const ttg_tt* tt) {
   c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
   size_t core_tot = 0;
   for (int i = 0; i < tt->d; ++i) core_tot += (size_t)((tt->ranks[i] * tt->modes[i] + 1) * tt->ranks[i + 1]);
-  const size_t ismem = sizeof(double) * ((size_t)(2 * rmax * rmax + (rmax * nmax + 1) * rmax) + core_tot);
+  (void)core_tot;
+  const size_t ismem = sizeof(double) * (size_t)(2 * rmax * rmax + 2 * (rmax * nmax + 1) * rmax);
   if (tt->d <= ttg::kIfaceMaxModes && ismem <= 200 * 1024) {  // one launch for the whole chain
     ttg::IfaceArgs ia{};
     ia.d = tt->d;

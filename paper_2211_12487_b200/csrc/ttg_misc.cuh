@@ -151,26 +151,21 @@ __global__ void __launch_bounds__(1024) k_iface_all(IfaceArgs a) {
   extern __shared__ double sm[];
   double* Mb[2] = {sm, sm + a.rmax * a.rmax};
   double* T = sm + 2 * a.rmax * a.rmax;
-  double* Cs0 = T + (a.rmax * a.nmax + 1) * a.rmax;
-  {
-    double* dst = Cs0;
-    for (int i = 0; i < a.d; ++i) {
-      const int m = a.rl[i] * a.n[i], t1 = m * a.rr[i];
-      const double* __restrict__ src = a.cores[i];
-      for (int e = threadIdx.x; e < t1; e += blockDim.x) {
-        const int q = e / m, x = e - q * m;
-        dst[x + (m + 1) * q] = __ldg(src + e);
-      }
-      dst += (m + 1) * a.rr[i];
-    }
-  }
+  double* Cs0 = T + (a.rmax * a.nmax + 1) * a.rmax;  // the current core (ld m + 1), staged per mode
   if (threadIdx.x == 0) Mb[0][0] = 1.0;
-  __syncthreads();
   int f = 0;
   const double* Cs = Cs0;
   for (int i = 0; i < a.d; ++i) {
     const int rl = a.rl[i], n = a.n[i], rr = a.rr[i];
     const int m = rl * n, t1 = m * rr, ms = m + 1;
+    {
+      const double* __restrict__ src = a.cores[i];
+      for (int e = threadIdx.x; e < t1; e += blockDim.x) {
+        const int q = e / m, x = e - q * m;
+        Cs0[x + ms * q] = __ldg(src + e);
+      }
+    }
+    __syncthreads();
     const double* M = Mb[f];
     // T[p', j, q] = sum_p M[p', p] core[p, j, q]
     for (int e = threadIdx.x; e < t1; e += blockDim.x) {
@@ -205,7 +200,6 @@ __global__ void __launch_bounds__(1024) k_iface_all(IfaceArgs a) {
       Mn[e] = (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
-    Cs += ms * rr;
     f ^= 1;
   }
 }
