@@ -882,6 +882,18 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
   const int64_t rows = s.Psi ? s.As * n : s.r * n, a = s.r * n;
   const long long L = s.Ls / n;
   const bool did = syrk(c, s.S, (int)rows, L, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
+  c->scal.ensure(sizeof(double) * 16);
+  const size_t pcp_smem = sizeof(double) * (size_t)(a * a + 2 * a * std::max(r_old, 1) + r_old * r_old);
+  // (Y = W - U M / 2 keeps <= 4 elements per thread in registers: a r <= 2048)
+  if (!s.Psi && pcp_smem + 1024 <= (size_t)c->smem_optin && a * r_old <= 4 * 512 && !std::getenv("TTG_NO_PCP")) {
+    // one CTA: G = P C P in place (rank-r form), trace(C) for the guard
+    kernel_occupancy((const void*)ttg::k_pcp, ttg::k_pcp, 512, pcp_smem);
+    prof_begin(c, "k_pcp", 16.0 * a * a, 4.0 * a * a * std::max(r_old, 1));
+    launch_k(c, ttg::k_pcp, 1, 512, pcp_smem, (const double*)c->G.as<double>(), (int)a, U, r_old, c->G.as<double>(),
+             c->scal.as<double>() + 4);
+    post_launch(c);
+    return did;
+  }
   c->Craw.ensure(sizeof(double) * (size_t)(rows * rows));
   CK(cudaMemcpyAsync(c->Craw.p, c->G.p, sizeof(double) * rows * rows, cudaMemcpyDeviceToDevice, c->stream));
   // G = Q^T C Q with Q = K P (one element-wise kernel, two GEMMs): the same
@@ -2229,7 +2241,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_ws16<4, 1>, (const void*)ttg::k_project_ws16<4, 2>,
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
-        (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>};
+        (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>, (const void*)ttg::k_pcp};
     for (int nbk = 7; nbk <= 20; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
     for (int nb = 1; nb <= 4; ++nb)
       for (int t = 0; t <= 2; ++t) {

@@ -733,7 +733,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_syrk(SyrkArgs p) {
 // instead of 40), and the accumulators give the DMMA pipe ample independent
 // work.  Tiles arrive by tensor-map TMA (16 x 64 boxes, 128-byte swizzle; one
 // instruction per 8 KB box, rows >= a zero-filled); since a Gram is a sum
-// over k, lane t of warp w reads column 8w + 2h + {0,1,4,5}[t] at sub-step h,
+// over k, lane t of warp w reads column 8w + 2t + h at sub-step h (k permuted),
 // which makes the fragment loads conflict-free under the swizzle.
 // Unselected tiles (selection is tile-aligned) are skipped by producer and
 // consumers alike.  One CTA per SM (registers).  The 8 warps' partial Grams
@@ -790,10 +790,11 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) k_syrk_kx(const 
   for (int u = 0; u < NBL; ++u) acc[u][0] = acc[u][1] = 0.0;
   int off[2][2];  // [h][b & 1]
   {
-    const int tp = (t & 1) + 4 * (t >> 1);  // {0, 1, 4, 5}
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int c = 8 * warp + 2 * h + tp;
+      // k column 2t + h of the warp's 8: each half-warp (g < 4 / g >= 4)
+      // then covers 16 distinct 8-byte banks under the swizzle
+      const int c = 8 * warp + 2 * t + h;
 #pragma unroll
       for (int bp = 0; bp < 2; ++bp) off[h][bp] = c * 16 + ((((4 * bp + (g >> 1)) ^ (c & 7))) << 1) + (g & 1);
     }
@@ -919,7 +920,6 @@ __device__ __forceinline__ void syrk_kp_part(const CUtensorMap* tm, const SyrkAr
   constexpr int NQ = 8 / KS;  // column groups per slice
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int tp = (t & 1) + 4 * (t >> 1);
   const bool producer = threadIdx.x == 0;
   KpProducer pr{blockIdx.x, 0, 0};
   if (producer)
@@ -930,7 +930,7 @@ __device__ __forceinline__ void syrk_kp_part(const CUtensorMap* tm, const SyrkAr
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int bp = 0; bp < 2; ++bp) {
-      const int c7 = 2 * h + tp;
+      const int c7 = 2 * t + h;  // conflict-free per half-warp (see k_syrk_kx)
       base[h][bp] = c7 * 16 + (((4 * bp + (g >> 1)) ^ c7) << 1) + (g & 1);
     }
   double acc[NU][2];
@@ -1899,11 +1899,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_ws16(const __grid_co
     return;
   }
   // ---- consumers ----
+  // MMA row g of the A fragment (a tile column) lives in physical column
+  // pg = pi(g) = 2 (g & 3) + (g >> 2) of its 8-column group: 64-bit shared
+  // loads are served per half-warp (lanes g < 4 / g >= 4), and this spreads
+  // each half-warp over all 8 swizzle chunks of a 128-byte row (16 distinct
+  // 8-byte banks per half: 2 wavefronts instead of 4).
+  const int pg = ((g & 3) << 1) | (g >> 2);
   int osw[8];
   {
-    const int hsw = (t >> 1) ^ g;
+    const int hsw = (t >> 1) ^ pg;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) osw[i] = (16 * warp + g + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
+    for (int i = 0; i < 8; ++i) osw[i] = (16 * warp + pg + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
   }
   const double* wl = Wfs + lane;
   const bool want_ss = p.tsumsq != nullptr;
@@ -1947,7 +1953,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_ws16(const __grid_co
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = 8 * nb + 2 * t + (i & 1);
-        if (row < p.r) stg[row + p.r * (g + 8 * (i >> 1))] = acc[nb][i];
+        if (row < p.r) stg[row + p.r * (pg + 8 * (i >> 1))] = acc[nb][i];
       }
     __syncwarp();
     const long long colw = tile * TC + 16 * warp;
@@ -2044,11 +2050,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_cons
     return;
   }
   // ---- consumers ----
+  // MMA row g of the A fragment (a tile column) lives in physical column
+  // pg = pi(g) = 2 (g & 3) + (g >> 2) of its 8-column group: 64-bit shared
+  // loads are served per half-warp (lanes g < 4 / g >= 4), and this spreads
+  // each half-warp over all 8 swizzle chunks of a 128-byte row (16 distinct
+  // 8-byte banks per half: 2 wavefronts instead of 4).
+  const int pg = ((g & 3) << 1) | (g >> 2);
   int osw[8];
   {
-    const int hsw = (t >> 1) ^ g;
+    const int hsw = (t >> 1) ^ pg;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) osw[i] = (16 * warp + g + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
+    for (int i = 0; i < 8; ++i) osw[i] = (16 * warp + pg + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
   }
   const bool want_ss = p.tsumsq != nullptr;
   int st = 0;
@@ -2111,7 +2123,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_cons
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = 8 * nb + 2 * t + (i & 1);
-        if (row < p.r) stg[row + p.r * (g + 8 * (i >> 1))] = acc[nb][i];
+        if (row < p.r) stg[row + p.r * (pg + 8 * (i >> 1))] = acc[nb][i];
       }
 #pragma unroll
     for (int j = 0; j < T; ++j) {
@@ -2120,7 +2132,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_cons
         double v = tacc[j][h];
         v += __shfl_xor_sync(0xffffffffu, v, 1);
         v += __shfl_xor_sync(0xffffffffu, v, 2);
-        if (t == 0) stg[8 * NB + j + p.r * (g + 8 * h)] = v;
+        if (t == 0) stg[8 * NB + j + p.r * (pg + 8 * h)] = v;
       }
     }
     __syncwarp();

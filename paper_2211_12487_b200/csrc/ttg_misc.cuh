@@ -353,6 +353,108 @@ __global__ void k_symmetrize_trace(double* __restrict__ G, int a, const double* 
   }
 }
 
+// Residual Gram from the raw Gram in one CTA (no pre-projection, K = I):
+//   G = P C P = C - (U Y^T + Y U^T),  W = C U,  M = sym(U^T W),  Y = W - M' ,
+// with M' = U M / 2, so that U Y^T + Y U^T = U W^T + W U^T - U M U^T.
+// Rank-r work (a^2 r) instead of the two dense a^3 GEMMs of the Q^T C Q form;
+// only the lower triangle is formed and mirrored (G exactly symmetric);
+// trace(C) goes to *tr for the raw-Gram accuracy guard.  C and G may alias.
+// Shared memory: U and W / Y, a x r each.
+__global__ void __launch_bounds__(512) k_pcp(const double* C, int a, const double* __restrict__ U, int r,
+                                             double* G, double* __restrict__ tr) {
+  griddep_wait();
+  extern __shared__ double psm[];
+  double* Cs = psm;              // a x a (staged C)
+  double* Us = Cs + a * a;       // a x r
+  double* Ws = Us + a * r;       // a x r (W, then Y)
+  double* Ms = Ws + a * r;       // r x r
+  const int tid = threadIdx.x, nt = blockDim.x;
+  {
+    const long long n = (long long)a * a;
+    for (long long e = tid; e < n; e += nt) Cs[e] = C[e];
+    for (int e = tid; e < a * r; e += nt) Us[e] = U[e];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    double s = 0.0;
+    for (int i = tid; i < a; i += 32) s += Cs[i + a * i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (tid == 0) *tr = s;
+  }
+  // W = C U: work item = (row i, 4-column chunk), two partial sums per column
+  const int nch = (r + 3) / 4;
+  for (int w = tid; w < a * nch; w += nt) {
+    const int i = w % a, k0 = (w / a) * 4;
+    double acc[4], acc2[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = acc2[q] = 0.0;
+    int j = 0;
+    for (; j + 1 < a; j += 2) {
+      const double c0 = Cs[i + a * j], c1 = Cs[i + a * (j + 1)];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (k0 + q < r) {
+          acc[q] = fma(c0, Us[j + a * (k0 + q)], acc[q]);
+          acc2[q] = fma(c1, Us[j + 1 + a * (k0 + q)], acc2[q]);
+        }
+    }
+    if (j < a) {
+      const double c0 = Cs[i + a * j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (k0 + q < r) acc[q] = fma(c0, Us[j + a * (k0 + q)], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (k0 + q < r) Ws[i + a * (k0 + q)] = acc[q] + acc2[q];
+  }
+  __syncthreads();
+  // M = U^T W (r x r), symmetrised below
+  for (int e = tid; e < r * r; e += nt) {
+    const int k = e % r, l = e / r;
+    double s0 = 0.0, s1 = 0.0;
+    int j = 0;
+    for (; j + 1 < a; j += 2) {
+      s0 = fma(Us[j + a * k], Ws[j + a * l], s0);
+      s1 = fma(Us[j + 1 + a * k], Ws[j + 1 + a * l], s1);
+    }
+    if (j < a) s0 = fma(Us[j + a * k], Ws[j + a * l], s0);
+    Ms[e] = s0 + s1;
+  }
+  __syncthreads();
+  // Y = W - U sym(M) / 2: work item (row i, column l); all reads of W precede
+  // the barrier, writes go to the element's own slot after it
+  double ynew[4];
+  int nmine = 0;
+  for (int w = tid; w < a * r && nmine < 4; w += nt, ++nmine) {
+    const int i = w % a, l = w / a;
+    double s = 0.0;
+    for (int k = 0; k < r; ++k) s = fma(Us[i + a * k], 0.5 * (Ms[k + r * l] + Ms[l + r * k]), s);
+    ynew[nmine] = Ws[i + a * l] - 0.5 * s;
+  }
+  __syncthreads();
+  {
+    int m = 0;
+    for (int w = tid; w < a * r && m < 4; w += nt, ++m) Ws[w] = ynew[m];
+  }
+  __syncthreads();
+  // lower triangle of G = C - (U Y^T + Y U^T), mirrored (exactly symmetric)
+  const long long n = (long long)a * a;
+  for (long long e = tid; e < n; e += nt) {
+    const int i = (int)(e % a), j = (int)(e / a);
+    if (i > j) continue;
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < r; ++k) {
+      s1 = fma(Us[i + a * k], Ws[j + a * k], s1);
+      s2 = fma(Ws[i + a * k], Us[j + a * k], s2);
+    }
+    const double g = Cs[i + a * j] - (s1 + s2);
+    G[i + (long long)a * j] = g;
+    G[j + (long long)a * i] = g;
+  }
+}
+
 // selection mask (err > eps, or all when subselect is off)
 __global__ void k_star_mask(const double* __restrict__ errs, int b, double eps, int subselect,
                             uint8_t* __restrict__ sel) {
