@@ -1224,8 +1224,7 @@ bool kc_plan(const ttg_ctx* c, int a, int r, KcPlan& P) {
       if (2 * (fixed + 2 * stage) > 220 * 1024) {  // one CTA / SM: deepen the ring
         while (nst < ttg::kProjStages && fixed + (nst + 1) * stage <= cap) ++nst;
       } else {
-        while (nst < ttg::kProjStages && 2 * (fixed + (nst + 1) * stage) <= 220 * 1024 && (nst + 1) * kc <= 2 * P.nks)
-          ++nst;
+        while (nst < ttg::kProjStages && 2 * (fixed + (nst + 1) * stage) <= 220 * 1024) ++nst;
       }
       if (const char* e = std::getenv("TTG_KC_NST")) nst = std::max(2, std::min(ttg::kProjStages, std::atoi(e)));
       if (fixed + nst * stage > cap) continue;
