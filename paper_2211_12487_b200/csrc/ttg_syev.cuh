@@ -747,6 +747,7 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
   __shared__ double red[64];
   __shared__ double H[K * K], Wv[K * K], theta[K], resn[K];
   __shared__ double Sq[K * K], Rq[2 * K], Wt[72];
+  __shared__ double zpart[128 * K];  // second-half partial sums of Z = G X (a <= 128)
   __shared__ int s_state, s_rank;
   __shared__ double s_tail;
   const long long t0 = clock64();
@@ -796,31 +797,44 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
     long long tq0 = clock64();
     // Z = G X: one thread per row i (G[i + a*j] over consecutive i is
     // conflict-free, X[j + a*c] is a broadcast), K independent chains
-    for (int i = tid; i < a; i += blockDim.x) {
-      // two interleaved partial sums per column (even / odd j), loads batched
-      double acc[K], acc2[K];
+    {
+      // a <= 128: two threads per row (j halves; the second half's partial
+      // sums go through zpart), else one thread per row; two interleaved
+      // partial sums per column, loads batched
+      const int tpr = (2 * a <= (int)blockDim.x) ? 2 : 1;
+      const int jh = tpr == 2 ? (a + 1) / 2 : a;
+      for (int w = tid; w < a * tpr; w += blockDim.x) {
+        const int i = w % a, part = w / a;
+        const int j0 = part * jh, j1 = part ? a : jh;
+        double acc[K], acc2[K];
 #pragma unroll
-      for (int c = 0; c < K; ++c) acc[c] = acc2[c] = 0.0;
-      int j = 0;
+        for (int c = 0; c < K; ++c) acc[c] = acc2[c] = 0.0;
+        int j = j0;
 #pragma unroll 4
-      for (; j + 1 < a; j += 2) {
-        const double g0 = G[i + (size_t)a * j], g1 = G[i + (size_t)a * (j + 1)];
+        for (; j + 1 < j1; j += 2) {
+          const double g0 = G[i + (size_t)a * j], g1 = G[i + (size_t)a * (j + 1)];
+#pragma unroll
+          for (int c = 0; c < K; ++c)
+            if (c < k) {
+              acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
+              acc2[c] = fma(g1, X[j + 1 + (size_t)a * c], acc2[c]);
+            }
+        }
+        if (j < j1) {
+          const double g0 = G[i + (size_t)a * j];
+#pragma unroll
+          for (int c = 0; c < K; ++c)
+            if (c < k) acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
+        }
+        double* dst = part ? zpart : Z;
 #pragma unroll
         for (int c = 0; c < K; ++c)
-          if (c < k) {
-            acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
-            acc2[c] = fma(g1, X[j + 1 + (size_t)a * c], acc2[c]);
-          }
+          if (c < k) dst[i + (size_t)a * c] = acc[c] + acc2[c];
       }
-      if (j < a) {
-        const double g0 = G[i + (size_t)a * j];
-#pragma unroll
-        for (int c = 0; c < K; ++c)
-          if (c < k) acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
+      if (tpr == 2) {
+        __syncthreads();
+        for (int e = tid; e < a * k; e += blockDim.x) Z[e] += zpart[e];
       }
-#pragma unroll
-      for (int c = 0; c < K; ++c)
-        if (c < k) Z[i + (size_t)a * c] = acc[c] + acc2[c];
     }
     __syncthreads();
     long long tq1 = clock64();
