@@ -727,41 +727,37 @@ bool syrk2(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, 
 
 // k-split SYRK for 64 < a8 <= 160 (k_syrk_kp): parts P per NBK so that a warp
 // holds at most 40 lower blocks
+constexpr int kp_nbl(int nbk) { return nbk * (nbk + 1) / 2; }
+// parts per CTA: a warp holds at most 40-44 lower blocks
 constexpr int kp_parts(int nbk) {
-  const int nbl = nbk * (nbk + 1) / 2;
-  return nbl <= 40 ? 1 : (nbl + 1) / 2 <= 40 ? 2 : (nbl + 3) / 4 <= 44 ? 4 : 8;
+  return kp_nbl(nbk) <= 40 ? 1 : (kp_nbl(nbk) + 1) / 2 <= 40 ? 2 : 4;
+}
+// CTAs per tile set
+constexpr int kp_py(int nbk) {
+  return kp_parts(nbk) < 4 ? 1 : (kp_nbl(nbk) + 4 * 44 - 1) / (4 * 44);
 }
 template <int NBK>
 void* kp_kernel() {
-  return (void*)ttg::k_syrk_kp<NBK, kp_parts(NBK)>;
+  return (void*)ttg::k_syrk_kp<NBK, kp_parts(NBK), kp_py(NBK)>;
 }
-void* kp_pick(int nbk) {
-  switch (nbk) {
-    case 7: return kp_kernel<7>();
-    case 8: return kp_kernel<8>();
-    case 9: return kp_kernel<9>();
-    case 10: return kp_kernel<10>();
-    case 11: return kp_kernel<11>();
-    case 12: return kp_kernel<12>();
-    case 13: return kp_kernel<13>();
-    case 14: return kp_kernel<14>();
-    case 15: return kp_kernel<15>();
-    case 16: return kp_kernel<16>();
-    case 17: return kp_kernel<17>();
-    case 18: return kp_kernel<18>();
-    case 19: return kp_kernel<19>();
-    case 20: return kp_kernel<20>();
+constexpr int kKpMaxNbk = 28;
+template <int NBK>
+void* kp_pick_t(int nbk) {
+  if constexpr (NBK > kKpMaxNbk) {
+    return nullptr;
+  } else {
+    return nbk == NBK ? kp_kernel<NBK>() : kp_pick_t<NBK + 1>(nbk);
   }
-  return nullptr;
 }
+void* kp_pick(int nbk) { return nbk >= 7 ? kp_pick_t<7>(nbk) : nullptr; }
 
 bool syrk_kp(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, long long cpo, double sel_frac,
              double* tsq) {
   const int a8 = ttg::round_up(a, 8), nbk = a8 / 8;
-  // measured: 8 parts (NBK >= 19) re-load too many fragments per DMMA and lose
-  // to k_syrk2; up to 4 parts win (a = 136: 0.16 vs 0.24 ms per 1.1 GB)
-  if (std::getenv("TTG_NO_KP") || tsq || (a & 1) || nbk < (std::getenv("TTG_KP8") ? 7 : 9) || nbk > 18 ||
-      kp_parts(nbk) > 4 ||
+  // measured: 8 warp-parts per CTA re-load too many fragments per DMMA and
+  // lose to k_syrk2; up to 4 parts win (a = 136: 0.16 vs 0.24 ms per 1.1 GB);
+  // larger triangles add CTAs per tile set (kp_py) instead
+  if (std::getenv("TTG_NO_KP") || tsq || (a & 1) || nbk < (std::getenv("TTG_KP8") ? 7 : 9) || nbk > kKpMaxNbk ||
       (sel && cpo % ttg::kTC != 0))
     return false;
   CUtensorMap tm;
@@ -784,14 +780,21 @@ bool syrk_kp(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel
   auto kern = reinterpret_cast<void (*)(const CUtensorMap, ttg::SyrkArgs)>(kp_pick(nbk));
   constexpr int threads = ttg::kConsumerWarps * 32;
   const int occ = std::max(1, kernel_occupancy((const void*)kern, kern, threads, smem));
-  const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  int py = 1;
+  switch (nbk) {  // CTAs per tile set of this instantiation
+#define KP_PY(N) case N: py = kp_py(N); break;
+    KP_PY(7) KP_PY(8) KP_PY(9) KP_PY(10) KP_PY(11) KP_PY(12) KP_PY(13) KP_PY(14) KP_PY(15) KP_PY(16) KP_PY(17)
+    KP_PY(18) KP_PY(19) KP_PY(20) KP_PY(21) KP_PY(22) KP_PY(23) KP_PY(24) KP_PY(25) KP_PY(26) KP_PY(27) KP_PY(28)
+#undef KP_PY
+  }
+  const int gx = (int)std::max<long long>(1, std::min<long long>((long long)c->num_sms * occ / py, args.n_tiles));
   c->partials.ensure(sizeof(double) * (size_t)gx * a8 * a8);
   args.partials = c->partials.as<double>();
   char nm[64];
   std::snprintf(nm, sizeof nm, "k_syrk[a=%d]", a);
   const double Ls = (double)L * sel_frac;
   prof_begin(c, nm, 8.0 * a * Ls, Ls * (double)a * a);
-  launch_k(c, kern, gx, threads, smem, tm, args);
+  launch_k(c, kern, dim3(gx, py), threads, smem, tm, args);
   post_launch(c);
   gram_reduce(c, gx, 1, a8, a, c->G.as<double>());
   return true;
@@ -2241,7 +2244,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>, (const void*)ttg::k_pcp};
-    for (int nbk = 7; nbk <= 20; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
+    for (int nbk = 7; nbk <= kKpMaxNbk; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
     for (int nb = 1; nb <= 4; ++nb)
       for (int t = 0; t <= 2; ++t) {
         CK(cudaFuncGetAttributes(&fa, kc_pick(4, nb, t)));

@@ -901,12 +901,11 @@ __device__ __forceinline__ void kp_produce(const CUtensorMap* tm, const SyrkArgs
   if (++pr.s == p.nst) pr.s = 0;
 }
 
-template <int NBK, int P, int PART>
+template <int NBK, int NPART, int KS, int PART>
 __device__ __forceinline__ void syrk_kp_part(const CUtensorMap* tm, const SyrkArgs& p, double* smem, uint64_t* full,
                                              uint64_t* empty, int slice) {
-  constexpr int KS = 8 / P;
   constexpr int NBL = NBK * (NBK + 1) / 2;
-  constexpr int U0 = PART * NBL / P, U1 = (PART + 1) * NBL / P, NU = U1 - U0;
+  constexpr int U0 = PART * NBL / NPART, U1 = (PART + 1) * NBL / NPART, NU = U1 - U0;
   constexpr int BI0 = kp_row_of(U0), BJ0 = U0 - BI0 * (BI0 + 1) / 2;
   constexpr int BI1 = kp_row_of(U1 - 1);
   // rows whose fragments this part needs: bj spans 0..BI1 once a full row is
@@ -1002,10 +1001,22 @@ __device__ __forceinline__ void syrk_kp_part(const CUtensorMap* tm, const SyrkAr
   }
 }
 
-template <int NBK, int P>
+template <int NBK, int NPART, int KS, int I>
+__device__ __forceinline__ void kp_dispatch(int part, const CUtensorMap* tm, const SyrkArgs& p, double* smem,
+                                            uint64_t* full, uint64_t* empty, int slice) {
+  if constexpr (I < NPART) {
+    if (part == I) syrk_kp_part<NBK, NPART, KS, I>(tm, p, smem, full, empty, slice);
+    else kp_dispatch<NBK, NPART, KS, I + 1>(part, tm, p, smem, full, empty, slice);
+  }
+}
+
+// P parts per CTA (8 / P column slices each) and PY CTAs per tile set
+// (blockIdx.y): the lower blocks are cut into P * PY parts; the PY CTAs of a
+// column x stream the same tiles at the same time (the second read hits L2)
+// and write disjoint blocks of the same per-x partial.
+template <int NBK, int P, int PY>
 __global__ void __launch_bounds__(kConsumerWarps * 32, 1) k_syrk_kp(const __grid_constant__ CUtensorMap tm,
                                                                     SyrkArgs p) {
-  griddep_wait();
   constexpr int KS = 8 / P;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[8], empty[8];
@@ -1020,17 +1031,8 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, 1) k_syrk_kp(const __grid
     tma_prefetch_desc(&tm);
   }
   __syncthreads();
-  const int part = warp / KS, slice = warp % KS;
-  switch (part) {
-    case 0: syrk_kp_part<NBK, P, 0>(&tm, p, smem, full, empty, slice); break;
-    case 1: if constexpr (P > 1) syrk_kp_part<NBK, P, (P > 1 ? 1 : 0)>(&tm, p, smem, full, empty, slice); break;
-    case 2: if constexpr (P > 2) syrk_kp_part<NBK, P, (P > 2 ? 2 : 0)>(&tm, p, smem, full, empty, slice); break;
-    case 3: if constexpr (P > 3) syrk_kp_part<NBK, P, (P > 3 ? 3 : 0)>(&tm, p, smem, full, empty, slice); break;
-    case 4: if constexpr (P > 4) syrk_kp_part<NBK, P, (P > 4 ? 4 : 0)>(&tm, p, smem, full, empty, slice); break;
-    case 5: if constexpr (P > 5) syrk_kp_part<NBK, P, (P > 5 ? 5 : 0)>(&tm, p, smem, full, empty, slice); break;
-    case 6: if constexpr (P > 6) syrk_kp_part<NBK, P, (P > 6 ? 6 : 0)>(&tm, p, smem, full, empty, slice); break;
-    default: if constexpr (P > 7) syrk_kp_part<NBK, P, (P > 7 ? 7 : 0)>(&tm, p, smem, full, empty, slice); break;
-  }
+  const int part = (int)blockIdx.y * P + warp / KS, slice = warp % KS;
+  kp_dispatch<NBK, P * PY, KS, 0>(part, &tm, p, smem, full, empty, slice);
 }
 
 // Two-stage fixed-order reduction of per-CTA Gram partials (hundreds of
