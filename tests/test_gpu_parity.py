@@ -85,6 +85,16 @@ def test_ranks_17_to_20(ctx, algo):
     run_stream(ctx, s, 6, algo)
 
 
+@pytest.mark.parametrize("true_rank", [22, 27])
+def test_high_ranks_multi_cta_gram(ctx, true_rank):
+    """Bond ranks 22..29 at n = 8: mode-3 unfoldings a = 176..232 (k-split
+    SYRK with 2 or 3 CTAs per tile set, then the k_syrk2 fallback above
+    a = 224) and the 512-row statistics projection with r > 18 (NB = 3 plans,
+    DFMA tails); modes 8^5, batch 24, TT-ICE*."""
+    s = Stream(3, seed=31, modes=(8,) * 5, batch=24, true_rank=true_rank)
+    run_stream(ctx, s, 5, "star")
+
+
 def test_cfg1_video_small_batch(ctx):
     """BASELINE configs[1] shape (14,15,16,10,3) at batch 10, 6 increments."""
     s = Stream(1, seed=0, batch=10)
