@@ -95,6 +95,17 @@ int ttg_ctx_create(int device, ttg_ctx** out);
  * 128-byte ncclUniqueId produced by ttg_nccl_unique_id on rank 0. */
 int ttg_nccl_unique_id(uint8_t out[128]);
 int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[128], ttg_ctx** out);
+/* Multi-rank context whose exchanges go through caller-supplied HOST
+ * collectives instead of NCCL (another transport, or several ranks sharing
+ * one GPU in tests): the library copies the operand to host memory, calls the
+ * function, and copies the result back.  allreduce: element-wise sum of `n`
+ * doubles in place over all ranks; allgather: `bytes` from every rank,
+ * concatenated in rank order into `recv` (world * bytes).  Both return 0 on
+ * success; a nonzero return surfaces as TTG_E_NCCL. */
+typedef int (*ttg_host_allreduce_fn)(void* user, double* buf, int64_t n);
+typedef int (*ttg_host_allgather_fn)(void* user, const void* send, int64_t bytes, void* recv);
+int ttg_ctx_create_hostcoll(int device, int rank, int world, ttg_host_allreduce_fn allreduce,
+                            ttg_host_allgather_fn allgather, void* user, ttg_ctx** out);
 void ttg_ctx_destroy(ttg_ctx* ctx);
 /* ctx = NULL: the message of the calling thread's last context-free call (ttg_read_batch /
  * ttg_write_batch). */

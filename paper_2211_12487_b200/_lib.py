@@ -46,6 +46,10 @@ class Heuristics(ctypes.Structure):
     ]
 
 
+# host-collective callbacks (ttg_host_allreduce_fn / ttg_host_allgather_fn)
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+HOST_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+
 # (name, restype, argtypes) for every symbol of include/ttg.h
 _P = ctypes.c_void_p
 _I64P = ctypes.POINTER(ctypes.c_int64)
@@ -55,6 +59,7 @@ SIGNATURES = [
     ("ttg_ctx_create", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_P)]),
     ("ttg_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
     ("ttg_ctx_create_dist", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_P)]),
+    ("ttg_ctx_create_hostcoll", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P, ctypes.POINTER(_P)]),
     ("ttg_ctx_destroy", None, [_P]),
     ("ttg_last_error", ctypes.c_char_p, [_P]),
     ("ttg_ctx_rank", ctypes.c_int, [_P]),

@@ -118,6 +118,11 @@ struct ttg_ctx {
   int device = 0;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  // host collectives (ttg_ctx_create_hostcoll) instead of NCCL when set
+  ttg_host_allreduce_fn host_ar = nullptr;
+  ttg_host_allgather_fn host_ag = nullptr;
+  void* host_user = nullptr;
+  std::vector<uint8_t> host_coll_buf;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
@@ -306,7 +311,32 @@ int grid_for(long long n, int threads, int max_blocks) {
 
 void allreduce_sum(ttg_ctx* c, double* d, size_t n) {
   if (c->world <= 1) return;
+  if (c->host_ar) {  // host transport: D2H, exchange, H2D (stream-ordered)
+    c->host_coll_buf.resize(sizeof(double) * n);
+    double* h = reinterpret_cast<double*>(c->host_coll_buf.data());
+    CK(cudaMemcpyAsync(h, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->host_ar(c->host_user, h, (int64_t)n) != 0) fail(TTG_E_NCCL, "host all-reduce failed");
+    CK(cudaMemcpyAsync(d, h, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
   NK(ncclAllReduce(d, d, n, ncclDouble, ncclSum, c->comm, c->stream));
+}
+
+// recv (world x n doubles, rank order) <- send (n doubles) from every rank
+void allgather(ttg_ctx* c, const double* send, double* recv, size_t n) {
+  if (c->host_ag) {
+    std::vector<double> hs(n), hr(n * (size_t)c->world);
+    CK(cudaMemcpyAsync(hs.data(), send, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->host_ag(c->host_user, hs.data(), (int64_t)(sizeof(double) * n), hr.data()) != 0)
+      fail(TTG_E_NCCL, "host all-gather failed");
+    CK(cudaMemcpyAsync(recv, hr.data(), sizeof(double) * n * c->world, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
+  NK(ncclAllGather(send, recv, n, ncclDouble, c->comm, c->stream));
 }
 
 // ---- norms ---------------------------------------------------------------
@@ -1079,7 +1109,7 @@ EigResult accurate_eig(ttg_ctx* c, const double* X, int a, long long L, const do
   post_launch(c);
   if (c->world > 1) {
     c->partials.ensure(sizeof(double) * (size_t)c->world * a * a);
-    NK(ncclAllGather(c->G.p, c->partials.p, (size_t)a * a, ncclDouble, c->comm, c->stream));
+    allgather(c, c->G.as<double>(), c->partials.as<double>(), (size_t)a * a);
     prof_begin(c, "k_tsqr_combine", 16.0 * c->world * a * a, 2.0 * c->world * a * a * a);
     launch_k(c, ttg::k_tsqr_combine, 1, 1024, smem2, c->partials.as<double>(), c->world, a,
                                                        c->scratch.as<double>(), c->G.as<double>());
@@ -1481,7 +1511,7 @@ void append_last_core(ttg_ctx* c, ttg_tt* tt, const double* coeffs, int r, int64
   const double* src = coeffs;
   if (c->world > 1) {
     c->coeffs_all.ensure(sizeof(double) * (size_t)r * bg);
-    NK(ncclAllGather(coeffs, c->coeffs_all.p, (size_t)r * b_local, ncclDouble, c->comm, c->stream));
+    allgather(c, coeffs, c->coeffs_all.as<double>(), (size_t)r * b_local);
     src = c->coeffs_all.as<double>();
   }
   int64_t need_rc = std::max<int64_t>(r, 1), need_oc = tt->n_obs + bg;
@@ -2295,6 +2325,29 @@ int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[1
   });
   if (rc != TTG_OK) {
     fprintf(stderr, "ttg_ctx_create_dist: %s\n", c->err.c_str());
+    ttg_ctx_destroy(c);
+    *out = nullptr;
+    return rc;
+  }
+  *out = c;
+  return TTG_OK;
+}
+
+int ttg_ctx_create_hostcoll(int device, int rank, int world, ttg_host_allreduce_fn allreduce,
+                            ttg_host_allgather_fn allgather_fn, void* user, ttg_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world || (world > 1 && (!allreduce || !allgather_fn)))
+    return TTG_E_ARGUMENT;
+  auto c = new ttg_ctx();
+  int rc = guard(c, [&] {
+    ctx_init(c, device);
+    c->rank = rank;
+    c->world = world;
+    c->host_ar = allreduce;
+    c->host_ag = allgather_fn;
+    c->host_user = user;
+  });
+  if (rc != TTG_OK) {
+    fprintf(stderr, "ttg_ctx_create_hostcoll: %s\n", c->err.c_str());
     ttg_ctx_destroy(c);
     *out = nullptr;
     return rc;

@@ -71,6 +71,42 @@ class Context:
         self._h = h
         self.device = device
 
+    @classmethod
+    def with_host_collectives(cls, device: int, rank: int, world: int, allreduce, allgather) -> "Context":
+        """Multi-rank context over caller-supplied host collectives
+        (include/ttg.h ttg_ctx_create_hostcoll): ``allreduce(a)`` sums the
+        float64 array ``a`` in place over the ranks; ``allgather(b)`` returns
+        the uint8 arrays ``b`` of all ranks concatenated in rank order."""
+        lib = _lib.load()
+        self = cls.__new__(cls)
+        self._h = None
+        self.device = device
+
+        def ar(_user, buf, n):
+            try:
+                allreduce(np.ctypeslib.as_array(buf, shape=(int(n),)))
+                return 0
+            except Exception:  # surfaces as TTG_E_NCCL
+                return 1
+
+        def ag(_user, send, nbytes, recv):
+            try:
+                nb = int(nbytes)
+                snd = np.ctypeslib.as_array(ctypes.cast(send, ctypes.POINTER(ctypes.c_uint8)), shape=(nb,)).copy()
+                rcv = np.ctypeslib.as_array(ctypes.cast(recv, ctypes.POINTER(ctypes.c_uint8)), shape=(nb * world,))
+                rcv[:] = np.asarray(allgather(snd), dtype=np.uint8).reshape(-1)
+                return 0
+            except Exception:
+                return 1
+
+        self._callbacks = (_lib.HOST_ALLREDUCE_FN(ar), _lib.HOST_ALLGATHER_FN(ag))  # kept alive with the context
+        h = ctypes.c_void_p()
+        rc = lib.ttg_ctx_create_hostcoll(device, rank, world, ctypes.cast(self._callbacks[0], ctypes.c_void_p),
+                                         ctypes.cast(self._callbacks[1], ctypes.c_void_p), None, ctypes.byref(h))
+        _check(rc, None)
+        self._h = h
+        return self
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = ctypes.create_string_buffer(128)
