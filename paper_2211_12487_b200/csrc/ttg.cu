@@ -132,7 +132,7 @@ struct ttg_ctx {
   // workspaces (grow-only)
   DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, UTt, Uf, Upad, scratch, eigres, on2, sumsq_part,
       scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2], tsq, psif, wcomb, psi[2],
-      spsi[2], scoeffs, matbuf, tmp, Craw, small[4];
+      spsi[2], scoeffs, matbuf, tmp, Craw, small[4], gcount;
   std::vector<DevBuf> scur;       // TT-ICE* stats-chain intermediates (reused by the sweep)
   std::vector<bool> stat_has;
   ttg::EigResult* h_eig = nullptr;
@@ -960,6 +960,8 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
   c->UR.ensure(sizeof(double) * (size_t)a * a);
   c->lam.ensure(sizeof(double) * a);
   c->eigres.ensure(sizeof(EigResult));
+  c->scal.ensure(sizeof(double) * 16);
+  bool fast_done = false;
   if (!factor) {
     ttg::SyevArgs args{};
     args.G = c->G.as<double>();
@@ -994,8 +996,9 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         prof_begin(c, nm, 16.0 * a * a, 2.0 * a * a * K);
         launch_k(c, kern, 1, ttg::kSubThreads, smem_s, sa);
         post_launch(c);
-        c->d2h += sizeof(EigResult);
+        c->d2h += sizeof(EigResult) + sizeof(double);
         CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_scal + 8, c->scal.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         done = c->h_eig->converged != 0;
         if (std::getenv("TTG_DEBUG"))
@@ -1007,6 +1010,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
                        c->h_eig->t_phase[3] & 0xffffffffll, c->h_eig->t_phase[3] >> 32);
       }
     }
+    fast_done = done;
     if (!done) {
       size_t vec = sizeof(double) * (size_t)7 * a;
       size_t smem = sizeof(double) * (size_t)a * a + vec;
@@ -1055,9 +1059,12 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     launch_k(c, ttg::k_jacobi_eig, 1, ttg::kEigThreads, smem, args);
     post_launch(c);
   }
-  c->d2h += sizeof(EigResult);
-  CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  if (!fast_done) {
+    c->d2h += sizeof(EigResult) + sizeof(double);
+    CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_scal + 8, c->scal.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
   EigResult r = *c->h_eig;
   if (std::getenv("TTG_DEBUG"))
     std::fprintf(stderr,
@@ -1131,14 +1138,19 @@ bool needs_accurate(const EigResult& er) {
 int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* out) {
   c->scratch.ensure(sizeof(double) * ((size_t)a * r_R + (size_t)(r_old + 1) * (r_R + 1) + 16));
   ttg::AppendArgs args{Upad, c->UR.as<double>(), a, r_old, r_R, out, c->scratch.as<double>(),
-                       c->eigres.as<EigResult>()};
+                       c->eigres.as<EigResult>(), c->gcount.as<int>()};
   prof_begin(c, "k_append", 8.0 * a * (2.0 * r_old + 2.0 * r_R), 2.0 * a * (r_old + r_R) * (r_old + r_R));
   launch_k(c, ttg::k_append, 1, 1024, 0, args);
   post_launch(c);
-  c->d2h += sizeof(EigResult);
-  CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  return c->h_eig->guard;
+  return 0;  // the guard count is read once per update (guards_read), not per mode
+}
+
+// Guard count of the last sweep: copied to the pinned slot after the sweep and
+// valid after the caller's next stream synchronisation.
+int* guards_slot(ttg_ctx* c) { return reinterpret_cast<int*>(c->h_scal + 12); }
+void guards_fetch(ttg_ctx* c) {
+  c->d2h += sizeof(int);
+  CK(cudaMemcpyAsync(guards_slot(c), c->gcount.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
 }
 
 // ---- projection --------------------------------------------------------------
@@ -1547,7 +1559,8 @@ void fill_report_ranks(int64_t* dst, const ttg_tt* tt) {
   dst[tt->d + 1] = 1;
 }
 
-double sumsq_device(ttg_ctx* c, const double* x, long long n) {
+// |x|^2 -> c->h_scal[0], valid after the caller's next stream synchronisation
+void sumsq_device_async(ttg_ctx* c, const double* x, long long n) {
   // reuse the per-observation kernel with one "observation"
   c->sumsq_part.ensure(sizeof(double) * 64);
   c->scal.ensure(sizeof(double) * 16);
@@ -1555,7 +1568,14 @@ double sumsq_device(ttg_ctx* c, const double* x, long long n) {
   prof_begin(c, "k_sumsq_obs", 8.0 * n, 2.0 * n);
   launch_k(c, ttg::k_sumsq_obs, grid, 256, 0, x, n, 1, c->sumsq_part.as<double>());
   post_launch(c);
-  return read_scalar(c, c->sumsq_part.as<double>());
+  c->d2h += sizeof(double);
+  CK(cudaMemcpyAsync(c->h_scal, c->sumsq_part.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+}
+
+double sumsq_device(ttg_ctx* c, const double* x, long long n) {
+  sumsq_device_async(c, x, n);
+  CK(cudaStreamSynchronize(c->stream));
+  return c->h_scal[0];
 }
 
 // ---- the TT-ICE / TT-ICE* sweep -----------------------------------------------
@@ -1638,6 +1658,8 @@ bool can_fuse(const Src& s, int64_t n_i, int64_t r_new, int64_t n_next, int64_t 
 SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm) {
   SweepOut out;
   tt->gen = ttg_tt::next_gen();  // the sweep rewrites the cores
+  c->gcount.ensure(sizeof(int));
+  CK(cudaMemsetAsync(c->gcount.p, 0, sizeof(int), c->stream));
   const int d = tt->d;
   const int64_t S = prod(tt->modes);
   std::vector<int64_t> old_ranks = tt->ranks;
@@ -1690,7 +1712,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       if (raw && er.rank > 0 && r_old > 0) {  // no projector (empty basis): C is G exactly
         // raw-Gram cancellation costs ~eps*tr(C)/gap in the kept vectors: keep
         // it only for directions carrying >= 1e-3 of the source energy
-        const double trC = read_scalar(c, c->scal.as<double>() + 4);
+        const double trC = c->h_scal[8];  // trace(C), fetched with the eigen result
         if (er.lam_min_kept < 1e-3 * trC) {
           gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, nullptr);
           er = eig(c, (int)a, kmax, dsrc, dmult);
@@ -1811,6 +1833,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     if (i + 1 == d) out.r_d = (int)r_new;
     trace("sweep:mode advanced");
   }
+  guards_fetch(c);
   return out;
 }
 
@@ -2020,7 +2043,7 @@ void do_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t
   append_last_core(c, tt, so.coeffs, so.r_d, b);
   fill_report_ranks(rep->ranks_after, tt);
   rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(so.discarded_sq) / y_norm;
-  rep->guard_reorthogonalised = so.guards;
+  rep->guard_reorthogonalised = *guards_slot(c);  // fetched by the sweep, valid after read_scalar's sync
   rep->modes_updated = so.modes_updated;
   rep->seconds = tm.stop();
 }
@@ -2119,7 +2142,6 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
     so = sweep(c, tt, Y, b, o, nm);
     coeffs = so.coeffs;
     r_d = so.r_d;
-    rep->guard_reorthogonalised = so.guards;
     rep->modes_updated = so.modes_updated;
   }
   trace("star:sweep done");
@@ -2128,10 +2150,13 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   fill_report_ranks(rep->ranks_after, tt);
   // estimate: Pythagoras on the appended coefficients (tt_ice_star.cpp:297-300)
   const double* csrc = c->world > 1 ? c->coeffs_all.as<double>() : coeffs;
-  const double kept_sq = sumsq_device(c, csrc, (long long)r_d * bg);
+  // |c|^2 and the guard count ride on the timer's synchronisation (one host sync)
+  sumsq_device_async(c, csrc, (long long)r_d * bg);
+  rep->seconds = tm.stop();
+  const double kept_sq = c->h_scal[0];
+  if (n_sel > 0) rep->guard_reorthogonalised = *guards_slot(c);
   const double lost_sq = std::max(ysq - kept_sq, 0.0);
   rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(lost_sq) / y_norm;
-  rep->seconds = tm.stop();
   trace("star:end");
   g_trace = nullptr;
 }

@@ -201,6 +201,7 @@ struct AppendArgs {
   double* out;         // a x (r_old + r_R)
   double* scratch;     // a x r_R + r_R
   EigResult* res;
+  int* guard_count;    // incremented when the guard fires (read once per update: no host sync per mode)
 };
 
 __device__ void block_max_reduce(double& v, double* red) {
@@ -259,7 +260,11 @@ __global__ void __launch_bounds__(1024) k_append(AppendArgs p) {
     dev = fmax(dev, fabs(s - (ci == cj ? 1.0 : 0.0)));
   }
   block_max_reduce(dev, red);
-  if (threadIdx.x == 0) { p.res->dev = dev; p.res->guard = (dev > 1e-10) ? 1 : 0; }
+  if (threadIdx.x == 0) {
+    p.res->dev = dev;
+    p.res->guard = (dev > 1e-10) ? 1 : 0;
+    if (dev > 1e-10 && p.guard_count) atomicAdd(p.guard_count, 1);
+  }
   if (!(dev > 1e-10)) return;
 
   // corrected = U_R - U_pad (U_pad^T U_R)   -> scratch (a x rr)
