@@ -17,6 +17,7 @@
 // solve on identical bytes.
 #include <cudaTypedefs.h>
 #include <nccl.h>
+#include <cublas_v2.h>
 
 #include <fcntl.h>
 #include <unistd.h>
@@ -125,6 +126,7 @@ struct ttg_ctx {
   std::vector<uint8_t> host_coll_buf;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cublasHandle_t blas = nullptr;  // plain large GEMMs only (gemm() below); created on first use
   std::string err;
   int64_t launches = 0;
   int num_sms = 148;
@@ -379,10 +381,33 @@ void make_frags(ttg_ctx* c, const double* U, int a, int r, int ld, bool need_ut,
 
 // ---- generic GEMM (any size) ------------------------------------------------
 // (defined below; forward declaration for the raw-Gram path)
+// Generic GEMM C = alpha op(A) op(B) + beta C (column-major).  Small shapes
+// (every a x a / Psi combination of the sweep) run the fixed-order k_gemm;
+// large plain GEMMs (the high-rank projections, r > 34, of tt_project and
+// wide unfoldings: >= kBlasFlops) go to cuBLAS DGEMM on the library stream.
+constexpr double kBlasFlops = 1e8;
 template <bool TA, bool TB>
 void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
           long long m, long long n, long long k, double alpha, double beta) {
   if (m == 0 || n == 0) return;
+  if (2.0 * m * n * k >= kBlasFlops && m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31) && !std::getenv("TTG_NO_BLAS")) {
+    if (!c->blas) {
+      if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasCreate failed");
+    }
+    if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasSetStream failed");
+    prof_begin(c, "cublas_dgemm", 8.0 * (m * k + k * n + m * n), 2.0 * m * n * k);
+    const cublasStatus_t st = cublasDgemm(c->blas, TA ? CUBLAS_OP_T : CUBLAS_OP_N, TB ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                          (int)m, (int)n, (int)k, &alpha, A, (int)lda, B, (int)ldb, &beta, C, (int)ldc);
+    if (st != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasDgemm failed (status " + std::to_string((int)st) + ")");
+    CK(cudaGetLastError());
+    if (c->profiling && c->cur_idx >= 0) {
+      cudaEvent_t e1 = get_event(c);
+      CK(cudaEventRecord(e1, c->stream));
+      c->pending.push_back({c->cur_idx, c->cur_e0, e1});
+    }
+    c->cur_idx = -1;
+    return;
+  }
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
   if (grid.y > 65535) fail(TTG_E_RESOURCE, "generic gemm: m too large");
   prof_begin(c, "k_gemm", 8.0 * (m * k + k * n + m * n), 2.0 * m * n * k);
@@ -916,13 +941,16 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
   const long long L = s.Ls / n;
   const bool did = syrk(c, s.S, (int)rows, L, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
   c->scal.ensure(sizeof(double) * 16);
-  const size_t pcp_smem = sizeof(double) * (size_t)(a * a + 2 * a * std::max(r_old, 1) + r_old * r_old);
-  // (Y = W - U M / 2 keeps <= 4 elements per thread in registers: a r <= 2048)
-  if (!s.Psi && pcp_smem + 1024 <= (size_t)c->smem_optin && a * r_old <= 4 * 512 && !std::getenv("TTG_NO_PCP")) {
+  const int64_t a8 = ttg::round_up((int)a, 8), r8 = ttg::round_up(std::max(r_old, 1), 8);
+  const size_t pcp_smem = sizeof(double) * (size_t)(a8 * a8 + 2 * a8 * r8 + r_old * r_old);
+  // (Y = W - U M / 2 keeps <= 8 elements per thread in registers: a r <= 4096;
+  // W = C U holds four 8-column accumulator blocks: r <= 32)
+  if (!s.Psi && pcp_smem + 1024 <= (size_t)c->smem_optin && a * r_old <= 8 * ttg::kPcpThreads && r_old <= 32 &&
+      !std::getenv("TTG_NO_PCP")) {
     // one CTA: G = P C P in place (rank-r form), trace(C) for the guard
-    kernel_occupancy((const void*)ttg::k_pcp, ttg::k_pcp, 512, pcp_smem);
+    kernel_occupancy((const void*)ttg::k_pcp, ttg::k_pcp, ttg::kPcpThreads, pcp_smem);
     prof_begin(c, "k_pcp", 16.0 * a * a, 4.0 * a * a * std::max(r_old, 1));
-    launch_k(c, ttg::k_pcp, 1, 512, pcp_smem, (const double*)c->G.as<double>(), (int)a, U, r_old, c->G.as<double>(),
+    launch_k(c, ttg::k_pcp, 1, ttg::kPcpThreads, pcp_smem, (const double*)c->G.as<double>(), (int)a, U, r_old, c->G.as<double>(),
              c->scal.as<double>() + 4);
     post_launch(c);
     return did;
@@ -1637,7 +1665,7 @@ void norms_finish(ttg_ctx* c, Norms& nm, int64_t rows, bool produced) {
                                                                  c->on2.as<double>(), nullptr);
     post_launch(c);
     prof_begin(c, "k_sum_vec", 8.0 * nm.b, 0.0);
-    launch_k(c, ttg::k_sum_vec, 1, 32, 0, c->on2.as<double>(), (int)nm.b, c->scal.as<double>());
+    launch_k(c, ttg::k_sum_vec, 1, 256, 0, c->on2.as<double>(), (int)nm.b, c->scal.as<double>());
     post_launch(c);
     allreduce_sum(c, c->scal.as<double>(), 1);
   }
@@ -1841,11 +1869,23 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
 // buffer through the combined interface when k_project_kc takes it (even rows
 // <= kProjFuseMax, r <= 34), so Y -> r_3 x L_3 at cfg3 is one pass (no cur_2).
 constexpr int kProjFuseMax = 512;
-bool can_fuse_proj(const ttg_ctx* c, const Src& s, int64_t n_i, int64_t n_next, int64_t r_next) {
+// Without a k_project_kc plan (r > 34) the fused step is a plain GEMM; fuse
+// when its per-column time max(F/P, B/BW) beats materialising cur_{i+1}
+// (the projection at mode i plus the next one): at full-rank early modes
+// (r_i = a_i) fusion removes a whole write + read of the increment.
+bool can_fuse_proj(const ttg_ctx* c, const Src& s, int64_t n_i, int64_t r_i, int64_t n_next, int64_t r_next) {
   const int64_t rows = s.As * n_i * n_next;
   if (std::getenv("TTG_NO_PROJ_FUSE")) return rows <= kFastMax && r_next <= kFastMax;
+  if (rows > kProjFuseMax) return false;
   KcPlan P;
-  return rows <= kProjFuseMax && kc_plan(c, (int)rows, (int)r_next, P);
+  if (kc_plan(c, (int)rows, (int)r_next, P)) return true;
+  const double Pf = 30e12, BW = 6e12;  // sustained FP64 / HBM rates (profiles/r01_box_probe.log)
+  auto t = [&](double f, double b) { return std::max(f / Pf, b / BW); };
+  const double src_rows = (double)s.As * n_i;  // rows of the current source per sub-column
+  const double fused = t(2.0 * rows * r_next, 8.0 * rows);
+  const double staged = t(2.0 * n_next * src_rows * r_i, 8.0 * (rows + r_i * n_next)) +
+                        t(2.0 * r_i * n_next * r_next, 8.0 * r_i * n_next);
+  return fused <= staged;
 }
 
 // Projection of Y through the train's current cores (projection-only fusion
@@ -1869,7 +1909,7 @@ const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64
     if (i + 1 < d) {
       const int64_t n_next = tt->modes[i + 1];
       const int64_t rr = tt->ranks[i + 2];
-      if (can_fuse_proj(c, src, n_i, n_next, rr)) {
+      if (can_fuse_proj(c, src, n_i, r, n_next, rr)) {
         const double* psi = src.Psi ? combine_psi(c, src, n_i, Ui, r, c->spsi[pf]) : Ui;
         if (src.Psi) pf ^= 1;
         src = Src{src.S, src.As * n_i, L, psi, r};
@@ -1973,7 +2013,7 @@ void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double
   c->rn2.ensure(sizeof(double) * b);
   c->stats.ensure(sizeof(ttg::StarStats));
   prof_begin(c, "k_coef_stats", 8.0 * r * b, 2.0 * r * r * b);
-  launch_k(c, ttg::k_coef_stats, grid_for(b, 128, 1024), 128, 0, coeffs, r, (int)b, M, c->cn2.as<double>(),
+  launch_k(c, ttg::k_coef_stats, grid_for(32 * b, 256, 1024), 256, 0, coeffs, r, (int)b, M, c->cn2.as<double>(),
                                                                    c->cmc.as<double>());
   post_launch(c);
   prof_begin(c, "k_star_local", 32.0 * b, 10.0 * b);
@@ -2384,6 +2424,7 @@ int ttg_ctx_create_hostcoll(int device, int rank, int world, ttg_host_allreduce_
 void ttg_ctx_destroy(ttg_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->blas) cublasDestroy(c->blas);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_eig) cudaFreeHost(c->h_eig);
   if (c->h_scal) cudaFreeHost(c->h_scal);

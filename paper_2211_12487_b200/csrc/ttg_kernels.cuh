@@ -2669,10 +2669,20 @@ __global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_pe
 // total = sum_o v[o] in observation order (one thread: the reference's order)
 __global__ void k_sum_vec(const double* __restrict__ v, int n, double* __restrict__ total) {
   griddep_wait();
-  if (threadIdx.x != 0) return;
+  // the block stages chunks (coalesced, many loads in flight); thread 0 adds
+  // them in index order, so the sum is bit-identical to a serial pass
+  __shared__ double buf[1024];
   double s = 0.0;
-  for (int i = 0; i < n; ++i) s += v[i];
-  *total = s;
+  for (int base = 0; base < n; base += 1024) {
+    const int m = min(1024, n - base);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < m; i += blockDim.x) buf[i] = __ldg(v + base + i);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < m; ++i) s += buf[i];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = s;
 }
 
 // ---------------------------------------------------------------------------

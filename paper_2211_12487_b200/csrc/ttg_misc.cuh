@@ -233,21 +233,35 @@ __global__ void k_build_q(const double* __restrict__ Psi, int As, int r, int n, 
   }
 }
 
-// cn2[o] = |c_o|^2, cmc[o] = c_o^T M c_o  (c: r x b, ld r)
+// cn2[o] = |c_o|^2, cmc[o] = c_o^T M c_o  (c: r x b, ld r).  One warp per
+// observation: lane i forms (M c)_i for rows i, i + 32, ... (coalesced column
+// reads of M, c broadcast), then two fixed-order warp sums.
 __global__ void k_coef_stats(const double* __restrict__ C, int r, int b, const double* __restrict__ M,
                              double* __restrict__ cn2, double* __restrict__ cmc) {
   griddep_wait();
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < b; o += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < b; o += nwarp) {
     const double* c = C + (long long)r * o;
     double s = 0.0, m = 0.0;
-    for (int i = 0; i < r; ++i) {
-      s = fma(c[i], c[i], s);
-      double mi = 0.0;
-      for (int k = 0; k < r; ++k) mi = fma(M[i + (long long)r * k], c[k], mi);
-      m = fma(c[i], mi, m);
+    for (int i = lane; i < r; i += 32) {
+      const double ci = __ldg(c + i);
+      double mi0 = 0.0, mi1 = 0.0;
+      int k = 0;
+      for (; k + 1 < r; k += 2) {
+        mi0 = fma(__ldg(M + i + (long long)r * k), __ldg(c + k), mi0);
+        mi1 = fma(__ldg(M + i + (long long)r * (k + 1)), __ldg(c + k + 1), mi1);
+      }
+      if (k < r) mi0 = fma(__ldg(M + i + (long long)r * k), __ldg(c + k), mi0);
+      s = fma(ci, ci, s);
+      m = fma(ci, mi0 + mi1, m);
     }
-    cn2[o] = s;
-    cmc[o] = m;
+    s = warp_sum(s);
+    m = warp_sum(m);
+    if (lane == 0) {
+      cn2[o] = s;
+      cmc[o] = m;
+    }
   }
 }
 
@@ -264,43 +278,51 @@ __global__ void __launch_bounds__(256) k_star_local(const double* __restrict__ o
                                                     double* __restrict__ errs, double* __restrict__ rn2_out,
                                                     StarStats* st) {
   griddep_wait();
-  // per-observation values in parallel (256 at a time, staged in shared
-  // memory), the nine decision sums by one thread in observation order (the
-  // reference's loop order, so the sums are bit-identical to a serial pass)
-  __shared__ double s_err[256], s_on2[256], s_rn2[256];
-  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  // Per observation (in parallel): err and the nine sum terms, each the value
+  // the reference's loop adds or +0.0 when its condition is false (adding
+  // +0.0 is exact).  Then lane t < 9 of warp 0 adds row t in observation order,
+  // so every sum is bit-identical to one serial pass.  Terms: 0 err (on > 0),
+  // 1 count (on > 0), 2 rn^2, 3 on^2 (on = sqrt(on2): the reference squares
+  // the root), 4 (err on)^2 (err <= eps), 5 on2 (err > eps), 6 count
+  // (err > eps), 7 count (err <= eps), 8 err (err <= eps).
+  constexpr int kLd = 257;  // odd stride: the nine lanes read distinct banks
+  __shared__ double s_term[9 * kLd];
+  double acc = 0.0;
+  const int t = threadIdx.x;
   for (int base = 0; base < b; base += 256) {
-    const int o = base + threadIdx.x;
+    const int o = base + t;
     if (o < b) {
-      const double on = sqrt(on2[o]);
+      const double o2 = on2[o];
+      const double on = sqrt(o2);
       // |y - Phi c|^2 = |y|^2 - 2|c|^2 + c^T (Phi^T Phi) c   (c = Phi^T y)
-      double rsq = on2[o] - 2.0 * cn2[o] + cmc[o];
+      double rsq = o2 - 2.0 * cn2[o] + cmc[o];
       if (rsq < 0.0) rsq = 0.0;
       const double rn = sqrt(rsq);
       const double err = (on == 0.0) ? 0.0 : rn / on;
       errs[o] = err;
       rn2_out[o] = rn * rn;
-      s_err[threadIdx.x] = err;
-      s_on2[threadIdx.x] = on2[o];
-      s_rn2[threadIdx.x] = rn * rn;
+      const double rj = err * on;
+      const bool pos = on > 0.0, sel = err > eps;
+      s_term[0 * kLd + t] = pos ? err : 0.0;
+      s_term[1 * kLd + t] = pos ? 1.0 : 0.0;
+      s_term[2 * kLd + t] = rn * rn;
+      s_term[3 * kLd + t] = on * on;
+      s_term[4 * kLd + t] = sel ? 0.0 : rj * rj;
+      s_term[5 * kLd + t] = sel ? o2 : 0.0;
+      s_term[6 * kLd + t] = sel ? 1.0 : 0.0;
+      s_term[7 * kLd + t] = sel ? 0.0 : 1.0;
+      s_term[8 * kLd + t] = sel ? 0.0 : err;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      const int m = min(256, b - base);
-      for (int q = 0; q < m; ++q) {
-        const double err = s_err[q], o2 = s_on2[q], r2 = s_rn2[q];
-        const double on = sqrt(o2);
-        if (on > 0.0) { s[0] += err; s[1] += 1.0; }
-        s[2] += r2;
-        s[3] += on * on;
-        if (err > eps) { s[5] += o2; s[6] += 1.0; }
-        else { const double r = err * on; s[4] += r * r; s[7] += 1.0; s[8] += err; }
-      }
+    const int m = min(256, b - base);
+    if (t < 9) {
+      const double* row = s_term + t * kLd;
+#pragma unroll 8
+      for (int q = 0; q < m; ++q) acc += row[q];
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0)
-    for (int i = 0; i < 9; ++i) st->sums[i] = s[i];
+  if (t < 9) st->sums[t] = acc;
 }
 
 // W = I_n (x) Psi  ((As*n) x (r*n), block diagonal)
@@ -356,58 +378,63 @@ __global__ void k_symmetrize_trace(double* __restrict__ G, int a, const double* 
 // Residual Gram from the raw Gram in one CTA (no pre-projection, K = I):
 //   G = P C P = C - (U Y^T + Y U^T),  W = C U,  M = sym(U^T W),  Y = W - M' ,
 // with M' = U M / 2, so that U Y^T + Y U^T = U W^T + W U^T - U M U^T.
-// Rank-r work (a^2 r) instead of the two dense a^3 GEMMs of the Q^T C Q form;
-// only the lower triangle is formed and mirrored (G exactly symmetric);
+// Rank-r work (a^2 r) instead of the two dense a^3 GEMMs of the Q^T C Q form.
+// W = C U and the rank-2r update [U Y][Y U]^T run on DMMA (m8n8k4, one 8-row
+// block per warp task); only the lower 8 x 8 blocks of G are formed (the
+// diagonal blocks' lower halves) and mirrored, so G is exactly symmetric;
 // trace(C) goes to *tr for the raw-Gram accuracy guard.  C and G may alias.
-// Shared memory: U and W / Y, a x r each.
-__global__ void __launch_bounds__(512) k_pcp(const double* C, int a, const double* __restrict__ U, int r,
-                                             double* G, double* __restrict__ tr) {
+// Shared memory (zero-padded to multiples of 8, leading dimension a8):
+// C (a8 x a8), U and W / Y (a8 x r8 each), M (r x r).  Needs a r <= 8 * 512.
+constexpr int kPcpThreads = 512;
+__global__ void __launch_bounds__(kPcpThreads) k_pcp(const double* C, int a, const double* __restrict__ U, int r,
+                                                     double* G, double* __restrict__ tr) {
   griddep_wait();
   extern __shared__ double psm[];
-  double* Cs = psm;              // a x a (staged C)
-  double* Us = Cs + a * a;       // a x r
-  double* Ws = Us + a * r;       // a x r (W, then Y)
-  double* Ms = Ws + a * r;       // r x r
+  const int a8 = (a + 7) & ~7, r8 = (r + 7) & ~7;
+  double* Cs = psm;                       // a8 x a8
+  double* Us = Cs + (size_t)a8 * a8;      // a8 x r8
+  double* Ws = Us + (size_t)a8 * r8;      // a8 x r8 (W, then Y)
+  double* Ms = Ws + (size_t)a8 * r8;      // r x r
   const int tid = threadIdx.x, nt = blockDim.x;
-  {
-    const long long n = (long long)a * a;
-    for (long long e = tid; e < n; e += nt) Cs[e] = C[e];
-    for (int e = tid; e < a * r; e += nt) Us[e] = U[e];
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  {  // staging by columns, one warp per column (zero-padded rows / columns)
+#pragma unroll 2
+    for (int j = warp; j < a8; j += nwarp)
+#pragma unroll 4
+      for (int i = lane; i < a8; i += 32) Cs[i + a8 * j] = (i < a && j < a) ? __ldg(C + i + (long long)a * j) : 0.0;
+    for (int k = warp; k < r8; k += nwarp)
+#pragma unroll 4
+      for (int i = lane; i < a8; i += 32) Us[i + a8 * k] = (i < a && k < r) ? __ldg(U + i + (long long)a * k) : 0.0;
   }
   __syncthreads();
   if (tid < 32) {
     double s = 0.0;
-    for (int i = tid; i < a; i += 32) s += Cs[i + a * i];
+    for (int i = tid; i < a; i += 32) s += Cs[i + a8 * i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (tid == 0) *tr = s;
   }
-  // W = C U: work item = (row i, 4-column chunk), two partial sums per column
-  const int nch = (r + 3) / 4;
-  for (int w = tid; w < a * nch; w += nt) {
-    const int i = w % a, k0 = (w / a) * 4;
-    double acc[4], acc2[4];
+  // W = C U: task = 8-row block ib; accumulators for every 8-column block
+  const int nbr = a8 / 8, nbc = r8 / 8;  // nbc <= 4 (r <= 32)
+  for (int ib = warp; ib < nbr; ib += nwarp) {
+    double acc[4][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = acc2[q] = 0.0;
-    int j = 0;
-    for (; j + 1 < a; j += 2) {
-      const double c0 = Cs[i + a * j], c1 = Cs[i + a * (j + 1)];
+    for (int jb = 0; jb < 4; ++jb) acc[jb][0] = acc[jb][1] = 0.0;
+    const double* crow = Cs + ib * 8 + g;
+#pragma unroll 2
+    for (int k0 = 0; k0 < a8; k0 += 4) {
+      const double av = crow[(size_t)a8 * (k0 + t)];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (k0 + q < r) {
-          acc[q] = fma(c0, Us[j + a * (k0 + q)], acc[q]);
-          acc2[q] = fma(c1, Us[j + 1 + a * (k0 + q)], acc2[q]);
-        }
-    }
-    if (j < a) {
-      const double c0 = Cs[i + a * j];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (k0 + q < r) acc[q] = fma(c0, Us[j + a * (k0 + q)], acc[q]);
+      for (int jb = 0; jb < 4; ++jb)
+        if (jb < nbc) dmma(acc[jb][0], acc[jb][1], av, Us[(k0 + t) + (size_t)a8 * (jb * 8 + g)]);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (k0 + q < r) Ws[i + a * (k0 + q)] = acc[q] + acc2[q];
+    for (int jb = 0; jb < 4; ++jb)
+      if (jb < nbc) {
+        Ws[ib * 8 + g + (size_t)a8 * (jb * 8 + 2 * t)] = acc[jb][0];
+        Ws[ib * 8 + g + (size_t)a8 * (jb * 8 + 2 * t + 1)] = acc[jb][1];
+      }
   }
   __syncthreads();
   // M = U^T W (r x r), symmetrised below
@@ -416,42 +443,57 @@ __global__ void __launch_bounds__(512) k_pcp(const double* C, int a, const doubl
     double s0 = 0.0, s1 = 0.0;
     int j = 0;
     for (; j + 1 < a; j += 2) {
-      s0 = fma(Us[j + a * k], Ws[j + a * l], s0);
-      s1 = fma(Us[j + 1 + a * k], Ws[j + 1 + a * l], s1);
+      s0 = fma(Us[j + a8 * k], Ws[j + a8 * l], s0);
+      s1 = fma(Us[j + 1 + a8 * k], Ws[j + 1 + a8 * l], s1);
     }
-    if (j < a) s0 = fma(Us[j + a * k], Ws[j + a * l], s0);
+    if (j < a) s0 = fma(Us[j + a8 * k], Ws[j + a8 * l], s0);
     Ms[e] = s0 + s1;
   }
   __syncthreads();
   // Y = W - U sym(M) / 2: work item (row i, column l); all reads of W precede
   // the barrier, writes go to the element's own slot after it
-  double ynew[4];
-  int nmine = 0;
-  for (int w = tid; w < a * r && nmine < 4; w += nt, ++nmine) {
-    const int i = w % a, l = w / a;
-    double s = 0.0;
-    for (int k = 0; k < r; ++k) s = fma(Us[i + a * k], 0.5 * (Ms[k + r * l] + Ms[l + r * k]), s);
-    ynew[nmine] = Ws[i + a * l] - 0.5 * s;
+  double ynew[8];
+  {
+    int nmine = 0;
+    for (int w = tid; w < a * r && nmine < 8; w += nt, ++nmine) {
+      const int i = w % a, l = w / a;
+      double s = 0.0;
+      for (int k = 0; k < r; ++k) s = fma(Us[i + a8 * k], 0.5 * (Ms[k + r * l] + Ms[l + r * k]), s);
+      ynew[nmine] = Ws[i + a8 * l] - 0.5 * s;
+    }
   }
   __syncthreads();
   {
     int m = 0;
-    for (int w = tid; w < a * r && m < 4; w += nt, ++m) Ws[w] = ynew[m];
+    for (int w = tid; w < a * r && m < 8; w += nt, ++m) Ws[(w % a) + a8 * (w / a)] = ynew[m];
   }
   __syncthreads();
-  // lower triangle of G = C - (U Y^T + Y U^T), mirrored (exactly symmetric)
-  const long long n = (long long)a * a;
-  for (long long e = tid; e < n; e += nt) {
-    const int i = (int)(e % a), j = (int)(e / a);
-    if (i > j) continue;
-    double s1 = 0.0, s2 = 0.0;
-    for (int k = 0; k < r; ++k) {
-      s1 = fma(Us[i + a * k], Ws[j + a * k], s1);
-      s2 = fma(Ws[i + a * k], Us[j + a * k], s2);
+  // lower 8 x 8 blocks of G = C - [U Y][Y U]^T (k over 2 r8), mirrored
+  const int nlow = nbr * (nbr + 1) / 2;
+  for (int blk = warp; blk < nlow; blk += nwarp) {
+    int ib = 0;
+    while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
+    const int jb = blk - ib * (ib + 1) / 2;
+    double d0 = 0.0, d1 = 0.0;
+    const int i = ib * 8 + g, jrow = jb * 8 + g;
+#pragma unroll 2
+    for (int k0 = 0; k0 < r8; k0 += 4) {  // U_i . Y_j
+      dmma(d0, d1, Us[i + (size_t)a8 * (k0 + t)], Ws[jrow + (size_t)a8 * (k0 + t)]);
     }
-    const double g = Cs[i + a * j] - (s1 + s2);
-    G[i + (long long)a * j] = g;
-    G[j + (long long)a * i] = g;
+#pragma unroll 2
+    for (int k0 = 0; k0 < r8; k0 += 4) {  // Y_i . U_j
+      dmma(d0, d1, Ws[i + (size_t)a8 * (k0 + t)], Us[jrow + (size_t)a8 * (k0 + t)]);
+    }
+    const double dv[2] = {d0, d1};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = jb * 8 + 2 * t + h;
+      if (i < a && j < a && (ib != jb || i >= j)) {
+        const double gv = Cs[i + (size_t)a8 * j] - dv[h];
+        G[i + (long long)a * j] = gv;
+        G[j + (long long)a * i] = gv;
+      }
+    }
   }
 }
 

@@ -529,6 +529,34 @@ __device__ int warp_sym_eig(const double* Hs, int k, double* theta, double* Wv, 
 // registers (same rotation formula and skip thresholds as warp_sym_eig; the
 // k = 4 Rayleigh-Ritz problem is latency-bound, and one thread avoids the
 // shuffle chains of the warp version).  Output as warp_sym_eig.
+// Rotation (c, s) zeroing h_pq of the 2 x 2 block [[hpp, hpq], [hpq, hqq]]:
+// t = sign(d) e / (|d| + sqrt(d^2 + e^2)) with d = hqq - hpp, e = 2 hpq (the
+// tan of the smaller angle, one division and one square root), c = 1/sqrt(1+t^2).
+// Same skip rule as warp_sym_eig (|h_pq| <= 1e-15 sqrt|h_pp h_qq| or <= the
+// absolute floor), tested on squares.  Returns false (c = 1, s = 0) if skipped.
+__device__ __forceinline__ bool jacobi_rot(double hpp, double hqq, double hpq, double floor_abs, bool active,
+                                           double& c, double& sn) {
+  c = 1.0;
+  sn = 0.0;
+  if (!active || !(fabs(hpq) > floor_abs) || !(hpq * hpq > 1e-30 * fabs(hpp * hqq))) return false;
+  double dd = hqq - hpp, e = 2.0 * hpq;
+  const double m = fmax(fabs(dd), fabs(e));
+  if (m > 1e150) {  // exact power-of-two rescale keeps d^2 + e^2 finite
+    dd *= 0x1p-600;
+    e *= 0x1p-600;
+  }
+  const double t = copysign(1.0, dd) * e / (fabs(dd) + sqrt(fma(dd, dd, e * e)));
+  c = rsqrt(fma(t, t, 1.0));
+  sn = c * t;
+  return true;
+}
+
+// One thread: Jacobi on the symmetric k x k (k <= 4) Hs held in registers,
+// round-robin order: each round rotates two disjoint pairs, (0,1)(2,3),
+// (0,2)(1,3), (0,3)(1,2), whose angles depend only on their own 2 x 2 blocks,
+// so the two rotation chains run side by side (the k = 4 Rayleigh-Ritz problem
+// is latency-bound).  Stops after a sweep without rotations.  Output as
+// warp_sym_eig.
 __device__ int thread_sym_eig4(const double* Hs, int k, double* theta, double* Wv) {
   double h[4][4], w[4][4];
 #pragma unroll
@@ -546,34 +574,36 @@ __device__ int thread_sym_eig4(const double* Hs, int k, double* theta, double* W
     const double floor_abs = 8.881784197001252e-16 * hmax;
     bool rotated = false;
 #pragma unroll
-    for (int p = 0; p < 3; ++p)
+    for (int rd = 0; rd < 3; ++rd) {
+      const int p1 = 0, q1 = rd + 1;                       // (0,1) (0,2) (0,3)
+      const int p2 = rd == 0 ? 2 : 1, q2 = rd == 2 ? 2 : 3;  // (2,3) (1,3) (1,2)
+      double c1, s1, c2, s2;
+      const bool r1 = jacobi_rot(h[p1][p1], h[q1][q1], h[p1][q1], floor_abs, q1 < k, c1, s1);
+      const bool r2 = jacobi_rot(h[p2][p2], h[q2][q2], h[p2][q2], floor_abs, q2 < k, c2, s2);
+      if (!(r1 || r2)) continue;
+      rotated = true;
 #pragma unroll
-      for (int q = p + 1; q < 4; ++q) {
-        const double hpp = h[p][p], hqq = h[q][q], hpq = h[p][q];
-        if (q < k && fabs(hpq) > floor_abs && fabs(hpq) > 1e-15 * sqrt(fabs(hpp * hqq))) {
-          const double zeta = (hqq - hpp) / (2.0 * hpq);
-          const double az = fabs(zeta);
-          const double t = az > 1e150 ? 0.5 / zeta : copysign(1.0, zeta) / (az + sqrt(fma(zeta, zeta, 1.0)));
-          const double c = rsqrt(fma(t, t, 1.0));
-          const double sn = c * t;
-          rotated = true;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {  // rows p, q
-            const double x = h[p][j], y = h[q][j];
-            h[p][j] = c * x - sn * y;
-            h[q][j] = sn * x + c * y;
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {  // columns p, q of H and W
-            const double x = h[i][p], y = h[i][q];
-            h[i][p] = c * x - sn * y;
-            h[i][q] = sn * x + c * y;
-            const double u = w[i][p], v = w[i][q];
-            w[i][p] = c * u - sn * v;
-            w[i][q] = sn * u + c * v;
-          }
-        }
+      for (int j = 0; j < 4; ++j) {  // rows p, q of both pairs
+        const double x1 = h[p1][j], y1 = h[q1][j], x2 = h[p2][j], y2 = h[q2][j];
+        h[p1][j] = c1 * x1 - s1 * y1;
+        h[q1][j] = s1 * x1 + c1 * y1;
+        h[p2][j] = c2 * x2 - s2 * y2;
+        h[q2][j] = s2 * x2 + c2 * y2;
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // columns p, q of H and W
+        const double x1 = h[i][p1], y1 = h[i][q1], x2 = h[i][p2], y2 = h[i][q2];
+        h[i][p1] = c1 * x1 - s1 * y1;
+        h[i][q1] = s1 * x1 + c1 * y1;
+        h[i][p2] = c2 * x2 - s2 * y2;
+        h[i][q2] = s2 * x2 + c2 * y2;
+        const double u1 = w[i][p1], v1 = w[i][q1], u2 = w[i][p2], v2 = w[i][q2];
+        w[i][p1] = c1 * u1 - s1 * v1;
+        w[i][q1] = s1 * u1 + c1 * v1;
+        w[i][p2] = c2 * u2 - s2 * v2;
+        w[i][q2] = s2 * u2 + c2 * v2;
+      }
+    }
     if (!rotated) break;
   }
   // stable descending sort of the diagonal

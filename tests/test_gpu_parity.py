@@ -288,3 +288,28 @@ def test_upload_roundtrip_and_update(ctx):
     tr, rr = O.tt_ice_star_update(tr, y, 0.1)
     compare_reports(rg, rr, star=True)
     compare_trains(tg, tr)
+
+
+@pytest.mark.parametrize("R", [24, 48, 64, 128])
+def test_project_fixed_cores_high_rank(ctx, R):
+    """tt_project through pre-built orthonormal cores with bond ranks up to 128
+    (BASELINE configs[4] companion sweep shapes at batch 2): the r > 34 paths
+    (k_project_tma, fused plain GEMMs on cuBLAS, the fusion cost model)
+    against the oracle, coefficients within 1e-10 relative."""
+    modes, b = (8,) * 7, 2
+    rng = np.random.default_rng(100 + R)
+    r = [1]
+    for i in range(1, len(modes) + 1):
+        r.append(min(R, 8 ** i, 8 ** (len(modes) - i) * b))
+    cores = []
+    for i, n in enumerate(modes):
+        q, _ = np.linalg.qr(rng.standard_normal((r[i] * n, r[i + 1])))
+        cores.append(np.reshape(q, (r[i], n, r[i + 1]), order="F"))
+    cores.append(np.reshape(rng.standard_normal((r[-1], 1)), (r[-1], 1, 1), order="F"))
+    tg = TensorTrain.upload(cores, ortho_count=len(modes), batch_boundaries=[1], ctx=ctx)
+    tr = O.TensorTrain([O.TTCore(np.asfortranarray(c)) for c in cores], len(modes), [1])
+    y = np.asfortranarray(rng.standard_normal(modes + (b,)))
+    cg = tt_project(tg, y)
+    cr = O.tt_project(tr, y)
+    assert cg.shape == cr.shape
+    assert np.linalg.norm(cg - cr) <= TOL * np.linalg.norm(cr)
