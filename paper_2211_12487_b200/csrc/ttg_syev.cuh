@@ -771,7 +771,7 @@ __device__ void block_cholqr2(double* X, double* Y, int a, int k, double* S, dou
 }
 
 template <int K>
-__global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
+__global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
   griddep_wait();
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[64];
@@ -796,15 +796,28 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
     if ((n & 1) && tid == 0) G[n - 1] = p.G[n - 1];
   }
   const long long ts1 = clock64();
-  // deterministic pseudo-random start block
-  for (int e = tid; e < a * k; e += blockDim.x) {
-    unsigned long long h = 0x9E3779B97F4A7C15ull * (unsigned long long)(e + 1);
+  // deterministic pseudo-random orthonormal start block: k columns of the
+  // Householder reflector I - 2 v v^T / v^T v (v pseudo-random), at pivots
+  // spread over the rows -- orthonormal by construction, so no initial QR
+  __syncthreads();  // G staged
+  double vpart = 0.0, gpart = 0.0;
+  for (int i = tid; i < a; i += blockDim.x) {
+    unsigned long long h = 0x9E3779B97F4A7C15ull * (unsigned long long)(i + 1);
     h ^= h >> 31; h *= 0xbf58476d1ce4e5b9ull; h ^= h >> 27;
-    X[e] = (double)(h >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    const double vi = (double)(h >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    Z[i] = vi;
+    vpart = fma(vi, vi, vpart);
+    gpart += G[i + (size_t)a * i];
+  }
+  const double vv = block_sum_all(vpart, red);
+  __syncthreads();
+  const double trace = block_sum_all(gpart, red);  // fixed order: identical on every thread
+  for (int e = tid; e < a * k; e += blockDim.x) {
+    const int i = e % a, c = e / a;
+    const int piv = (int)(((long long)c * a) / k);
+    X[e] = (i == piv ? 1.0 : 0.0) - 2.0 * Z[i] * (Z[piv] / vv);
   }
   __syncthreads();
-  double trace = 0.0;
-  for (int i = 0; i < a; ++i) trace += G[i + (size_t)a * i];
   const double delta = p.delta_src ? p.delta_mult * sqrt(*p.delta_src) : p.delta_mult;
   const long long kcap = p.kmax < a ? p.kmax : a;
   if (tid == 0) { s_state = 0; s_rank = 0; s_tail = trace; }
@@ -816,8 +829,6 @@ __global__ void __launch_bounds__(kSubThreads) k_syev_top(SyevArgs p) {
     return;
   }
   const long long ts2 = clock64();
-  if constexpr (K == 4) block_cholqr2_4(X, a, k, Sq, Rq);
-  else block_cholqr2<K>(X, Z, a, k, Sq, Rq);
   const long long t1 = clock64();
   double prev_res = 1e300;
   long long ph[4] = {0, 0, 0, 0};
