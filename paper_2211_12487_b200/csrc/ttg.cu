@@ -941,8 +941,7 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
   const long long L = s.Ls / n;
   const bool did = syrk(c, s.S, (int)rows, L, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
   c->scal.ensure(sizeof(double) * 16);
-  const int64_t a8 = ttg::round_up((int)a, 8), r8 = ttg::round_up(std::max(r_old, 1), 8);
-  const size_t pcp_smem = sizeof(double) * (size_t)(a8 * a8 + 2 * a8 * r8 + r_old * r_old);
+  const size_t pcp_smem = sizeof(double) * ttg::pcp_smem_doubles((int)a, r_old);
   // (Y = W - U M / 2 keeps <= 8 elements per thread in registers: a r <= 4096;
   // W = C U holds four 8-column accumulator blocks: r <= 32)
   if (!s.Psi && pcp_smem + 1024 <= (size_t)c->smem_optin && a * r_old <= 8 * ttg::kPcpThreads && r_old <= 32 &&

@@ -379,38 +379,64 @@ __global__ void k_symmetrize_trace(double* __restrict__ G, int a, const double* 
 //   G = P C P = C - (U Y^T + Y U^T),  W = C U,  M = sym(U^T W),  Y = W - M' ,
 // with M' = U M / 2, so that U Y^T + Y U^T = U W^T + W U^T - U M U^T.
 // Rank-r work (a^2 r) instead of the two dense a^3 GEMMs of the Q^T C Q form.
-// W = C U and the rank-2r update [U Y][Y U]^T run on DMMA (m8n8k4, one 8-row
-// block per warp task); only the lower 8 x 8 blocks of G are formed (the
-// diagonal blocks' lower halves) and mirrored, so G is exactly symmetric;
-// trace(C) goes to *tr for the raw-Gram accuracy guard.  C and G may alias.
-// Shared memory (zero-padded to multiples of 8, leading dimension a8):
-// C (a8 x a8), U and W / Y (a8 x r8 each), M (r x r).  Needs a r <= 8 * 512.
+// W = C U, M = U^T W and the rank-2r update [U Y][Y U]^T run on DMMA
+// (m8n8k4); only the lower 8 x 8 blocks of G are formed (the diagonal
+// blocks' lower halves) and mirrored, so G is exactly symmetric; trace(C) goes
+// to *tr for the raw-Gram accuracy guard.  C and G may alias.
+// Shared memory, zero-padded to multiples of 8 with leading dimension
+// ld = pcp_ld(a8) (== 4 mod 16 doubles: the fragment loads of a half-warp,
+// rows g + 4 t, hit 16 distinct banks; with ld = a8 = 112 every column
+// started in the same bank and the phases ran 4-13-way conflicted):
+// C (ld x a8), U and W / Y (ld x r8 each), M (r8 x r8).  Needs a r <= 8 x
+// threads and r <= 32.
 constexpr int kPcpThreads = 512;
+__host__ __device__ constexpr int pcp_ld(int a8) { return a8 + ((20 - a8 % 16) % 16); }
+__host__ __device__ constexpr size_t pcp_smem_doubles(int a, int r) {
+  return (size_t)pcp_ld((a + 7) & ~7) * (((a + 7) & ~7) + 2 * (((r > 1 ? r : 1) + 7) & ~7)) +
+         (size_t)(((r > 1 ? r : 1) + 7) & ~7) * (((r > 1 ? r : 1) + 7) & ~7);
+}
 __global__ void __launch_bounds__(kPcpThreads) k_pcp(const double* C, int a, const double* __restrict__ U, int r,
                                                      double* G, double* __restrict__ tr) {
   griddep_wait();
   extern __shared__ double psm[];
-  const int a8 = (a + 7) & ~7, r8 = (r + 7) & ~7;
-  double* Cs = psm;                       // a8 x a8
-  double* Us = Cs + (size_t)a8 * a8;      // a8 x r8
-  double* Ws = Us + (size_t)a8 * r8;      // a8 x r8 (W, then Y)
-  double* Ms = Ws + (size_t)a8 * r8;      // r x r
+  const int a8 = (a + 7) & ~7, r8 = (r + 7) & ~7, ld = pcp_ld(a8);
+  double* Cs = psm;                       // ld x a8
+  double* Us = Cs + (size_t)ld * a8;      // ld x r8
+  double* Ws = Us + (size_t)ld * r8;      // ld x r8 (W, then Y)
+  double* Ms = Ws + (size_t)ld * r8;      // r8 x r8
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   const int g = lane >> 2, t = lane & 3;
-  {  // staging by columns, one warp per column (zero-padded rows / columns)
-#pragma unroll 2
-    for (int j = warp; j < a8; j += nwarp)
-#pragma unroll 4
-      for (int i = lane; i < a8; i += 32) Cs[i + a8 * j] = (i < a && j < a) ? __ldg(C + i + (long long)a * j) : 0.0;
-    for (int k = warp; k < r8; k += nwarp)
-#pragma unroll 4
-      for (int i = lane; i < a8; i += 32) Us[i + a8 * k] = (i < a && k < r) ? __ldg(U + i + (long long)a * k) : 0.0;
+  {  // staging: contiguous loads batched in registers (8 in flight per thread),
+     // then scattered into the padded layout; padding rows / columns zeroed
+    const int n = a * a, m = a * r;
+    for (int base = tid; base < n + m; base += 8 * nt) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = base + q * nt;
+        v[q] = e < n ? __ldg(C + e) : (e < n + m ? __ldg(U + (e - n)) : 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = base + q * nt;
+        if (e < n) Cs[(e % a) + ld * (e / a)] = v[q];
+        else if (e < n + m) Us[((e - n) % a) + ld * ((e - n) / a)] = v[q];
+      }
+    }
+    for (int e = tid; e < a8 * a8; e += nt) {
+      const int i = e % a8, j = e / a8;
+      if (i >= a || j >= a) Cs[i + ld * j] = 0.0;
+    }
+    for (int e = tid; e < a8 * r8; e += nt) {
+      const int i = e % a8, k = e / a8;
+      if (i >= a || k >= r) Us[i + ld * k] = 0.0;
+    }
   }
   __syncthreads();
   if (tid < 32) {
     double s = 0.0;
-    for (int i = tid; i < a; i += 32) s += Cs[i + a8 * i];
+    for (int i = tid; i < a; i += 32) s += Cs[i + ld * i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (tid == 0) *tr = s;
@@ -424,30 +450,28 @@ __global__ void __launch_bounds__(kPcpThreads) k_pcp(const double* C, int a, con
     const double* crow = Cs + ib * 8 + g;
 #pragma unroll 2
     for (int k0 = 0; k0 < a8; k0 += 4) {
-      const double av = crow[(size_t)a8 * (k0 + t)];
+      const double av = crow[(size_t)ld * (k0 + t)];
 #pragma unroll
       for (int jb = 0; jb < 4; ++jb)
-        if (jb < nbc) dmma(acc[jb][0], acc[jb][1], av, Us[(k0 + t) + (size_t)a8 * (jb * 8 + g)]);
+        if (jb < nbc) dmma(acc[jb][0], acc[jb][1], av, Us[(k0 + t) + (size_t)ld * (jb * 8 + g)]);
     }
 #pragma unroll
     for (int jb = 0; jb < 4; ++jb)
       if (jb < nbc) {
-        Ws[ib * 8 + g + (size_t)a8 * (jb * 8 + 2 * t)] = acc[jb][0];
-        Ws[ib * 8 + g + (size_t)a8 * (jb * 8 + 2 * t + 1)] = acc[jb][1];
+        Ws[ib * 8 + g + (size_t)ld * (jb * 8 + 2 * t)] = acc[jb][0];
+        Ws[ib * 8 + g + (size_t)ld * (jb * 8 + 2 * t + 1)] = acc[jb][1];
       }
   }
   __syncthreads();
-  // M = U^T W (r x r), symmetrised below
-  for (int e = tid; e < r * r; e += nt) {
-    const int k = e % r, l = e / r;
-    double s0 = 0.0, s1 = 0.0;
-    int j = 0;
-    for (; j + 1 < a; j += 2) {
-      s0 = fma(Us[j + a8 * k], Ws[j + a8 * l], s0);
-      s1 = fma(Us[j + 1 + a8 * k], Ws[j + 1 + a8 * l], s1);
-    }
-    if (j < a) s0 = fma(Us[j + a8 * k], Ws[j + a8 * l], s0);
-    Ms[e] = s0 + s1;
+  // M = U^T W (r8 x r8, padded entries zero): one 8 x 8 block per warp task
+  for (int blk = warp; blk < nbc * nbc; blk += nwarp) {
+    const int kb = blk % nbc, lb = blk / nbc;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll 2
+    for (int k0 = 0; k0 < a8; k0 += 4)
+      dmma(d0, d1, Us[(k0 + t) + (size_t)ld * (kb * 8 + g)], Ws[(k0 + t) + (size_t)ld * (lb * 8 + g)]);
+    Ms[kb * 8 + g + r8 * (lb * 8 + 2 * t)] = d0;
+    Ms[kb * 8 + g + r8 * (lb * 8 + 2 * t + 1)] = d1;
   }
   __syncthreads();
   // Y = W - U sym(M) / 2: work item (row i, column l); all reads of W precede
@@ -458,14 +482,14 @@ __global__ void __launch_bounds__(kPcpThreads) k_pcp(const double* C, int a, con
     for (int w = tid; w < a * r && nmine < 8; w += nt, ++nmine) {
       const int i = w % a, l = w / a;
       double s = 0.0;
-      for (int k = 0; k < r; ++k) s = fma(Us[i + a8 * k], 0.5 * (Ms[k + r * l] + Ms[l + r * k]), s);
-      ynew[nmine] = Ws[i + a8 * l] - 0.5 * s;
+      for (int k = 0; k < r; ++k) s = fma(Us[i + ld * k], 0.5 * (Ms[k + r8 * l] + Ms[l + r8 * k]), s);
+      ynew[nmine] = Ws[i + ld * l] - 0.5 * s;
     }
   }
   __syncthreads();
   {
     int m = 0;
-    for (int w = tid; w < a * r && m < 8; w += nt, ++m) Ws[(w % a) + a8 * (w / a)] = ynew[m];
+    for (int w = tid; w < a * r && m < 8; w += nt, ++m) Ws[(w % a) + ld * (w / a)] = ynew[m];
   }
   __syncthreads();
   // lower 8 x 8 blocks of G = C - [U Y][Y U]^T (k over 2 r8), mirrored
@@ -478,18 +502,18 @@ __global__ void __launch_bounds__(kPcpThreads) k_pcp(const double* C, int a, con
     const int i = ib * 8 + g, jrow = jb * 8 + g;
 #pragma unroll 2
     for (int k0 = 0; k0 < r8; k0 += 4) {  // U_i . Y_j
-      dmma(d0, d1, Us[i + (size_t)a8 * (k0 + t)], Ws[jrow + (size_t)a8 * (k0 + t)]);
+      dmma(d0, d1, Us[i + (size_t)ld * (k0 + t)], Ws[jrow + (size_t)ld * (k0 + t)]);
     }
 #pragma unroll 2
     for (int k0 = 0; k0 < r8; k0 += 4) {  // Y_i . U_j
-      dmma(d0, d1, Ws[i + (size_t)a8 * (k0 + t)], Us[jrow + (size_t)a8 * (k0 + t)]);
+      dmma(d0, d1, Ws[i + (size_t)ld * (k0 + t)], Us[jrow + (size_t)ld * (k0 + t)]);
     }
     const double dv[2] = {d0, d1};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int j = jb * 8 + 2 * t + h;
       if (i < a && j < a && (ib != jb || i >= j)) {
-        const double gv = Cs[i + (size_t)a8 * j] - dv[h];
+        const double gv = Cs[i + (size_t)ld * j] - dv[h];
         G[i + (long long)a * j] = gv;
         G[j + (long long)a * i] = gv;
       }
