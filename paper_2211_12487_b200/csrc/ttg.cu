@@ -275,6 +275,29 @@ void prof_flush(ttg_ctx* c) {
   c->pending.clear();
 }
 
+// per-block shared-memory limit of the current device (opt-in)
+int prop_smem_optin() {
+  static int v = [] {
+    int dev = 0, x = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return x;
+  }();
+  return v;
+}
+
+// dynamic shared memory a kernel may still request (opt-in limit minus its static shared memory)
+size_t dyn_smem_cap(const void* kern) {
+  static std::vector<std::pair<const void*, size_t>> cache;
+  for (const auto& e : cache)
+    if (e.first == kern) return e.second;
+  cudaFuncAttributes fa{};
+  CK(cudaFuncGetAttributes(&fa, kern));
+  const size_t cap = (size_t)prop_smem_optin() - fa.sharedSizeBytes;
+  cache.push_back({kern, cap});
+  return cap;
+}
+
 // cudaFuncSetAttribute / occupancy queries are driver calls: cache them per
 // (kernel, dynamic smem) so the per-increment host path stays short.
 template <class K>
@@ -292,6 +315,12 @@ int kernel_occupancy(const void* key, K kern, int threads, size_t smem) {
   for (const auto& a : attr)
     if (a.first == key) have = a.second;
   if (smem > have) {
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, kern));
+    if (fa.sharedSizeBytes + smem > (size_t)prop_smem_optin())
+      fail(TTG_E_RESOURCE, "kernel shared memory plan exceeds the per-block limit: dynamic " + std::to_string(smem) +
+                               " + static " + std::to_string(fa.sharedSizeBytes) + " > " +
+                               std::to_string(prop_smem_optin()) + " (" + std::to_string(threads) + " threads)");
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool found = false;
     for (auto& a : attr)
@@ -1010,7 +1039,9 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         const size_t sub_vec = sizeof(double) * (size_t)2 * a * K;
         size_t smem_s = sizeof(double) * (size_t)a * a + sub_vec;
         ttg::SyevArgs sa = args;
-        if (smem_s <= c->smem_optin) {
+        const size_t kcap = dyn_smem_cap(K == 4 ? (const void*)ttg::k_syev_top<4> : (const void*)ttg::k_syev_top<8>);
+        if (sub_vec > kcap) break;  // even the block vectors do not fit: full solver
+        if (smem_s <= kcap) {
           sa.in_smem = 1;
         } else {
           sa.in_smem = 0;
@@ -1041,7 +1072,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     if (!done) {
       size_t vec = sizeof(double) * (size_t)7 * a;
       size_t smem = sizeof(double) * (size_t)a * a + vec;
-      if (smem <= c->smem_optin) {
+      if (smem <= dyn_smem_cap((const void*)ttg::k_syev)) {
         args.in_smem = 1;
       } else {
         args.in_smem = 0;
@@ -1071,7 +1102,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     args.lam = c->lam.as<double>();
     args.res = c->eigres.as<EigResult>();
     size_t smem;
-    if (need_smem <= c->smem_optin) {
+    if (need_smem <= dyn_smem_cap((const void*)ttg::k_jacobi_eig)) {
       args.in_smem = 1;
       args.Wg = nullptr;
       smem = need_smem;

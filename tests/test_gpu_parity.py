@@ -313,3 +313,19 @@ def test_project_fixed_cores_high_rank(ctx, R):
     cr = O.tt_project(tr, y)
     assert cg.shape == cr.shape
     assert np.linalg.norm(cg - cr) <= TOL * np.linalg.norm(cr)
+
+
+def test_bootstrap_tall_unfolding_full_solver(ctx):
+    """a = 2048 rows: the block-8 subspace vectors no longer fit shared memory
+    (2 a 8 doubles > the opt-in limit), so the solver goes straight from the
+    failed block-4 attempt to the full tridiagonal solver (configs[1] reaches
+    a ~ 2000 at its bootstrap)."""
+    rng = np.random.default_rng(7)
+    u = np.linalg.qr(rng.standard_normal((2048, 40)))[0]
+    v = rng.standard_normal((40, 300)) * np.logspace(0, -2, 40)[:, None]
+    y = np.asfortranarray(u @ v + 1e-4 * rng.standard_normal((2048, 300)))
+    tg, rg = tt_ice_bootstrap(y, 0.05, ctx=ctx)
+    tr, rr = O.tt_ice_bootstrap(y, 0.05)
+    compare_reports(rg, rr)
+    compare_trains(tg, tr)
+    assert tg.ranks()[1] > 8
