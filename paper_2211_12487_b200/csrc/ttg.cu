@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 #include <nccl.h>
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 
 #include <fcntl.h>
 #include <unistd.h>
@@ -127,6 +128,8 @@ struct ttg_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cublasHandle_t blas = nullptr;  // plain large GEMMs only (gemm() below); created on first use
+  cusolverDnHandle_t solver = nullptr;  // full eigen-decomposition of large a x a Grams (eig()); on first use
+  DevBuf sv_work, sv_evals, sv_info;
   std::string err;
   int64_t launches = 0;
   int num_sms = 148;
@@ -445,6 +448,8 @@ void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long
 }
 
 constexpr int kFastMax = 128;  // a8 / r8 limit of the fused DMMA tiles
+constexpr int kSolverLarge = 512;  // a from which a failed fast eigen-solve goes to cuSOLVER syevd
+constexpr int kFastSkip = 2048;    // a from which the block subspace attempt (G in global memory) is skipped
 
 // ---- residual Gram -----------------------------------------------------------
 constexpr int kFastMax1 = 256;  // a8 limit of the single-buffered DMMA tiles
@@ -1035,7 +1040,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     if (!std::getenv("TTG_FULL_EIG")) {
       // block of 4 first (the common case keeps 1-2 directions), then 8
       for (int K : {4, 8}) {
-        if (done) break;
+        if (done || a >= kFastSkip) break;  // very large a: straight to the full decomposition
         const size_t sub_vec = sizeof(double) * (size_t)2 * a * K;
         size_t smem_s = sizeof(double) * (size_t)a * a + sub_vec;
         ttg::SyevArgs sa = args;
@@ -1069,6 +1074,43 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
       }
     }
     fast_done = done;
+    if (!done && a >= kSolverLarge && !std::getenv("TTG_NO_CUSOLVER")) {
+      // large a: the one-CTA tridiagonalisation is latency-bound (a = 2488:
+      // 2 s); cuSOLVER syevd on a copy of G, then the rank rule / sign rule
+      // selection (k_syev_select)
+      if (!c->solver) {
+        if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(TTG_E_CUDA, "cusolverDnCreate failed");
+      }
+      if (cusolverDnSetStream(c->solver, c->stream) != CUSOLVER_STATUS_SUCCESS) fail(TTG_E_CUDA, "cusolverDnSetStream failed");
+      c->W.ensure(sizeof(double) * (size_t)a * a);
+      c->sv_evals.ensure(sizeof(double) * a);
+      c->sv_info.ensure(sizeof(int));
+      double* Q = c->W.as<double>();
+      CK(cudaMemcpyAsync(Q, c->G.p, sizeof(double) * (size_t)a * a, cudaMemcpyDeviceToDevice, c->stream));
+      int lwork = 0;
+      if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, a, Q, a,
+                                      c->sv_evals.as<double>(), &lwork) != CUSOLVER_STATUS_SUCCESS)
+        fail(TTG_E_CUDA, "cusolverDnDsyevd_bufferSize failed");
+      c->sv_work.ensure(sizeof(double) * (size_t)std::max(lwork, 1));
+      char nm[64];
+      std::snprintf(nm, sizeof nm, "cusolver_dsyevd[a=%d]", a);
+      prof_begin(c, nm, 16.0 * a * a, 4.0 * a * a * a);
+      if (cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, a, Q, a, c->sv_evals.as<double>(),
+                           c->sv_work.as<double>(), lwork, c->sv_info.as<int>()) != CUSOLVER_STATUS_SUCCESS)
+        fail(TTG_E_CUDA, "cusolverDnDsyevd failed");
+      CK(cudaGetLastError());
+      if (c->profiling && c->cur_idx >= 0) {
+        cudaEvent_t e1 = get_event(c);
+        CK(cudaEventRecord(e1, c->stream));
+        c->pending.push_back({c->cur_idx, c->cur_e0, e1});
+      }
+      c->cur_idx = -1;
+      prof_begin(c, "k_syev_select", 8.0 * a * a, 2.0 * a);
+      launch_k(c, ttg::k_syev_select, 1, 1024, 0, (const double*)c->G.as<double>(), a,
+               (const double*)c->sv_evals.as<double>(), (const double*)Q, (const int*)c->sv_info.as<int>(), args);
+      post_launch(c);
+      done = true;
+    }
     if (!done) {
       size_t vec = sizeof(double) * (size_t)7 * a;
       size_t smem = sizeof(double) * (size_t)a * a + vec;
@@ -1196,7 +1238,33 @@ bool needs_accurate(const EigResult& er) {
 int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* out) {
   c->scratch.ensure(sizeof(double) * ((size_t)a * r_R + (size_t)(r_old + 1) * (r_R + 1) + 16));
   ttg::AppendArgs args{Upad, c->UR.as<double>(), a, r_old, r_R, out, c->scratch.as<double>(),
-                       c->eigres.as<EigResult>(), c->gcount.as<int>()};
+                       c->eigres.as<EigResult>(), c->gcount.as<int>(), 0};
+  const int rn = r_old + r_R;
+  if ((double)a * rn * rn >= 5e7 && !std::getenv("TTG_NO_BLAS")) {
+    // large block: [U_pad U_R] by copies, its Gram C^T C by cuBLAS DSYRK, the
+    // deviation by a grid reduction; k_append then only runs the (rare)
+    // Householder correction when the guard fires
+    if (Upad != out && r_old > 0)
+      CK(cudaMemcpyAsync(out, Upad, sizeof(double) * (size_t)a * r_old, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(out + (size_t)a * r_old, c->UR.p, sizeof(double) * (size_t)a * r_R, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    c->small[1].ensure(sizeof(double) * (size_t)rn * rn);
+    double* S = c->small[1].as<double>();
+    if (!c->blas) {
+      if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasCreate failed");
+    }
+    if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasSetStream failed");
+    const double one = 1.0, zero = 0.0;
+    if (cublasDsyrk(c->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, rn, a, &one, out, a, &zero, S, rn) !=
+        CUBLAS_STATUS_SUCCESS)
+      fail(TTG_E_CUDA, "cublasDsyrk failed");
+    CK(cudaMemsetAsync(&c->eigres.as<EigResult>()->dev, 0, sizeof(double), c->stream));
+    prof_begin(c, "k_gram_dev", 8.0 * rn * rn, 0.0);
+    launch_k(c, ttg::k_gram_dev, grid_for((long long)rn * rn, 256, 2 * c->num_sms), 256, 0, (const double*)S, rn,
+             c->eigres.as<EigResult>());
+    post_launch(c);
+    args.precomputed = 1;
+  }
   prof_begin(c, "k_append", 8.0 * a * (2.0 * r_old + 2.0 * r_R), 2.0 * a * (r_old + r_R) * (r_old + r_R));
   launch_k(c, ttg::k_append, 1, 1024, 0, args);
   post_launch(c);
@@ -2455,6 +2523,7 @@ void ttg_ctx_destroy(ttg_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->blas) cublasDestroy(c->blas);
+  if (c->solver) cusolverDnDestroy(c->solver);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_eig) cudaFreeHost(c->h_eig);
   if (c->h_scal) cudaFreeHost(c->h_scal);

@@ -202,7 +202,31 @@ struct AppendArgs {
   double* scratch;     // a x r_R + r_R
   EigResult* res;
   int* guard_count;    // incremented when the guard fires (read once per update: no host sync per mode)
+  int precomputed;     // out already holds [U_pad U_R] and res->dev the Gram deviation (k_gram_dev)
 };
+
+// Gram deviation max |S_ij - delta_ij| over the lower triangle of S = C^T C
+// (n x n, from cuBLAS DSYRK) -> res->dev as an atomic max on the bit pattern
+// (non-negative doubles order like their bits); res->dev zeroed beforehand.
+__global__ void k_gram_dev(const double* __restrict__ S, int n, EigResult* res) {
+  griddep_wait();
+  __shared__ double red[32];
+  double m = 0.0;
+  const long long tot = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    if (i >= j) m = fmax(m, fabs(S[e] - (i == j ? 1.0 : 0.0)));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = fmax(b, red[w]);
+    atomicMax(reinterpret_cast<unsigned long long*>(&res->dev), (unsigned long long)__double_as_longlong(b));
+  }
+}
 
 __device__ void block_max_reduce(double& v, double* red) {
   v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 16));
@@ -244,22 +268,26 @@ __global__ void __launch_bounds__(1024) k_append(AppendArgs p) {
   __shared__ double red[33];
   const int a = p.a, r0 = p.r_old, rr = p.r_R, rn = r0 + rr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (long long e = threadIdx.x; e < (long long)a * rn; e += blockDim.x) {
-    long long c = e / a;
-    p.out[e] = (c < r0) ? p.Upad[e] : p.UR[e - (long long)r0 * a];
-  }
-  __syncthreads();
-  // Gram deviation of the combined block
   double dev = 0.0;
-  for (int pr = warp; pr < rn * rn; pr += nwarps) {
-    int ci = pr % rn, cj = pr / rn;
-    if (cj < ci) continue;
-    double s = 0.0;
-    for (int i = lane; i < a; i += 32) s = fma(p.out[(size_t)ci * a + i], p.out[(size_t)cj * a + i], s);
-    s = warp_sum(s);
-    dev = fmax(dev, fabs(s - (ci == cj ? 1.0 : 0.0)));
+  if (p.precomputed) {
+    dev = p.res->dev;
+  } else {
+    for (long long e = threadIdx.x; e < (long long)a * rn; e += blockDim.x) {
+      long long c = e / a;
+      p.out[e] = (c < r0) ? p.Upad[e] : p.UR[e - (long long)r0 * a];
+    }
+    __syncthreads();
+    // Gram deviation of the combined block
+    for (int pr = warp; pr < rn * rn; pr += nwarps) {
+      int ci = pr % rn, cj = pr / rn;
+      if (cj < ci) continue;
+      double s = 0.0;
+      for (int i = lane; i < a; i += 32) s = fma(p.out[(size_t)ci * a + i], p.out[(size_t)cj * a + i], s);
+      s = warp_sum(s);
+      dev = fmax(dev, fabs(s - (ci == cj ? 1.0 : 0.0)));
+    }
+    block_max_reduce(dev, red);
   }
-  block_max_reduce(dev, red);
   if (threadIdx.x == 0) {
     p.res->dev = dev;
     p.res->guard = (dev > 1e-10) ? 1 : 0;

@@ -1003,4 +1003,69 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
   }
 }
 
+// Rank rule, outputs and sign rule on a full eigen-decomposition of G
+// computed by cuSOLVER syevd (large a, where the one-CTA tridiagonal solver
+// is latency-bound): evals ascending, Q columns the eigenvectors (in place of
+// G's copy).  Same rule as k_syev: the smallest r <= kcap with
+// sqrt(trace(G) - sum_{j<r} lambda_j) <= delta ('>' keeps the smaller rank),
+// U_R = the top r eigenvectors with the largest-|.| entry (first index)
+// positive, lam = eigenvalues descending.  One CTA.
+__global__ void __launch_bounds__(1024) k_syev_select(const double* __restrict__ G, int a, const double* __restrict__ evals,
+                                                      const double* __restrict__ Q, const int* __restrict__ info,
+                                                      SyevArgs p) {
+  griddep_wait();
+  __shared__ double red[33];
+  __shared__ int s_rank;
+  __shared__ double s_tail, s_trace;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double tp = 0.0;
+  for (int i = tid; i < a; i += blockDim.x) tp += G[i + (size_t)a * i];
+  const double trace = block_sum_all(tp, red);
+  const double delta = p.delta_src ? p.delta_mult * sqrt(*p.delta_src) : p.delta_mult;
+  const long long kcap = p.kmax < a ? p.kmax : a;
+  if (tid == 0) {
+    double pre = 0.0;
+    int found = (int)kcap;
+    for (int r = 0; r <= a; ++r) {
+      if (r <= kcap && !(sqrt(fmax(trace - pre, 0.0)) > delta)) { found = r; break; }
+      if (r < a) pre += evals[a - 1 - r];
+    }
+    double pre2 = 0.0;
+    for (int r = 0; r < found; ++r) pre2 += evals[a - 1 - r];
+    s_rank = found;
+    s_tail = fmax(trace - pre2, 0.0);
+    s_trace = trace;
+  }
+  __syncthreads();
+  const int rank = s_rank;
+  for (int j = tid; j < a; j += blockDim.x) p.lam[j] = evals[a - 1 - j];
+  if (tid == 0) {
+    p.res->rank = rank;
+    p.res->tail_sq = s_tail;
+    p.res->delta = delta;
+    p.res->converged = (*info == 0) ? 1 : 0;
+    p.res->sweeps = 0;
+    p.res->lam_max = evals[a - 1];
+    p.res->lam_min_kept = rank > 0 ? evals[a - rank] : 0.0;
+    p.res->t_phase[0] = p.res->t_phase[1] = p.res->t_phase[2] = 0;
+    p.res->t_phase[3] = a;
+  }
+  for (int j = warp; j < rank; j += nw) {
+    const double* z = Q + (size_t)(a - 1 - j) * a;
+    double best = -1.0;
+    int bi = a;
+    for (int i = lane; i < a; i += 32) {
+      const double vv = fabs(z[i]);
+      if (vv > best) { best = vv; bi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double sgn = (z[bi] < 0.0) ? -1.0 : 1.0;
+    for (int i = lane; i < a; i += 32) p.UR[(size_t)j * a + i] = sgn * z[i];
+  }
+}
+
 }  // namespace ttg

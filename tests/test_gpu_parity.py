@@ -329,3 +329,26 @@ def test_bootstrap_tall_unfolding_full_solver(ctx):
     compare_reports(rg, rr)
     compare_trains(tg, tr)
     assert tg.ranks()[1] > 8
+
+
+def test_update_large_append_guard_path(ctx):
+    """a = 2048 rows, r_old ~ 150 kept directions + ~20 new ones: the appended
+    block [U_pad U_R] has a r_new^2 >= 5e7, so its Gram guard runs through
+    cuBLAS DSYRK + the grid deviation reduction (k_gram_dev) and the
+    eigen-solve through cuSOLVER; TT-ICE against the oracle."""
+    rng = np.random.default_rng(11)
+    basis = np.linalg.qr(rng.standard_normal((2048, 190)))[0]
+    spec = np.logspace(0, -1.5, 190)[:, None]
+    y0 = np.asfortranarray(basis[:, :150] @ (rng.standard_normal((150, 400)) * spec[:150]) +
+                           1e-6 * rng.standard_normal((2048, 400)))
+    y1 = np.asfortranarray(basis[:, 20:190] @ (rng.standard_normal((170, 300)) * spec[20:190]) +
+                           1e-6 * rng.standard_normal((2048, 300)))
+    tg, rg = tt_ice_bootstrap(y0, 1e-3, ctx=ctx)
+    tr, rr = O.tt_ice_bootstrap(y0, 1e-3)
+    compare_reports(rg, rr)
+    tg, rg = tt_ice_update(tg, y1, 1e-3)
+    tr, rr = O.tt_ice_update(tr, y1, 1e-3)
+    compare_reports(rg, rr)
+    compare_trains(tg, tr)
+    r = tg.ranks()[1]
+    assert 2048 * r * r >= 5e7, r
