@@ -127,6 +127,10 @@ struct ttg_ctx {
   std::vector<uint8_t> host_coll_buf;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // side stream: the interface Gram Phi^T Phi (one small CTA) runs beside the
+  // statistics pass instead of after it
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cublasHandle_t blas = nullptr;  // plain large GEMMs only (gemm() below); created on first use
   cusolverDnHandle_t solver = nullptr;  // full eigen-decomposition of large a x a Grams (eig()); on first use
   DevBuf sv_work, sv_evals, sv_info;
@@ -2101,9 +2105,34 @@ const double* interface_gram_compute(ttg_ctx* c, const ttg_tt* tt) {
 // current cores (cached for the sweep) + decisions' partial sums
 void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double eps) {
   Norms nm{true, Y, prod(tt->modes), b};
+  // a stale Phi^T Phi (the cores changed in the previous update) is computed
+  // on the side stream, concurrently with the statistics pass over Y
+  const double* M = nullptr;
+  const bool stale = !(c->iface_gen == tt->gen && c->iface_ptr) || std::getenv("TTG_NO_IFACE_CACHE");
+  if (stale && !c->profiling && !std::getenv("TTG_NO_SIDE")) {
+    // workspaces grow on the main stream (stream-ordered pool), before the fork
+    int64_t rmax = 1, nmax = 1;
+    for (auto r : tt->ranks) rmax = std::max(rmax, r);
+    for (auto n : tt->modes) nmax = std::max(nmax, n);
+    c->iface[0].ensure(sizeof(double) * rmax * rmax);
+    c->iface[1].ensure(sizeof(double) * rmax * rmax);
+    c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    std::swap(c->stream, c->side);
+    try {
+      M = interface_gram(c, tt);
+    } catch (...) {
+      std::swap(c->stream, c->side);
+      throw;
+    }
+    std::swap(c->stream, c->side);
+    CK(cudaEventRecord(c->ev_join, c->side));
+  }
   const double* coeffs = project_chain(c, tt, Y, b, /*cache=*/true, nm);
   if (nm.pending) norms_finish(c, nm, 0, false);
-  const double* M = interface_gram(c, tt);
+  if (M) CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  else M = interface_gram(c, tt);
   const int r = (int)tt->ranks[tt->d];
   c->cn2.ensure(sizeof(double) * b);
   c->cmc.ensure(sizeof(double) * b);
@@ -2399,6 +2428,9 @@ static int ctx_init(ttg_ctx* c, int device) {
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
   c->num_sms = prop.multiProcessorCount;
@@ -2530,6 +2562,12 @@ void ttg_ctx_destroy(ttg_ctx* c) {
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (auto& p : c->pending) {
     cudaEventDestroy(p.e0);
     cudaEventDestroy(p.e1);
