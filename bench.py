@@ -382,7 +382,10 @@ def our_arm(args):
         io0 = ctx.io_bytes()
         barrier()
         t0 = time.perf_counter()
+        ctx.prefetch(hosts[0])
         for j in range(e2e_steps):
+            if j + 1 < e2e_steps:
+                ctx.prefetch(hosts[j + 1])  # H2D of increment j+1 overlaps the update of j (ttg_prefetch)
             tt, rep = tt_ice_star_update(tt, hosts[j], EPS)
             _ = rep.batch_rel_error_estimate  # result read back on the host
         torch.cuda.synchronize()
@@ -394,7 +397,7 @@ def our_arm(args):
         io1 = ctx.io_bytes()
         e2e = {"value": inc_bytes * world * e2e_steps / el / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": (io1[0] - io0[0]) // e2e_steps, "d2h_bytes_per_step": (io1[1] - io0[1]) // e2e_steps,
-               "steps": e2e_steps, "path": "ttstream.tt_ice_star_update(numpy pinned host array) -> ttg C ABI (TTG_HOST)"}
+               "steps": e2e_steps, "path": "Context.prefetch(next pinned host increment) + ttstream.tt_ice_star_update(numpy pinned host array) -> ttg C ABI (TTG_HOST)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

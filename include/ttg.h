@@ -132,6 +132,15 @@ int ttg_ctx_reserve(ttg_ctx* ctx, int64_t bytes);
 /* Host<->device bytes moved by the context (H2D of host increments, D2H of
  * scalars/decisions). */
 int ttg_ctx_io_bytes(const ttg_ctx* ctx, int64_t* h2d, int64_t* d2h);
+/* Start copying a host increment (n doubles, ideally page-locked) to the
+ * device on the context's copy stream, into one of two staging slots; the next
+ * update / projection call given the same host pointer and size (where =
+ * TTG_HOST) consumes the staged copy instead of copying, so the PCIe transfer
+ * of increment k+1 overlaps the update of increment k.  The caller must not
+ * modify y until that consuming call has returned.  No reference counterpart:
+ * the in-memory analogue of the double-buffered stream reader
+ * (stream_io.cpp:123-204, ttg_stream_*). */
+int ttg_prefetch(ttg_ctx* ctx, const double* y, int64_t n);
 
 /* ---- device train ------------------------------------------------------- */
 /* Upload a host train: cores[i] is r_left[i]*n[i]*r_right[i] doubles,

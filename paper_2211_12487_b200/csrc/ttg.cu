@@ -131,6 +131,16 @@ struct ttg_ctx {
   // statistics pass instead of after it
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // ttg_prefetch: two staging slots filled on the copy stream
+  struct Prefetch {
+    DevBuf buf;
+    const double* src = nullptr;
+    int64_t n = 0;
+    cudaEvent_t ready = nullptr, freed = nullptr;
+    bool valid = false, used = false;
+  } pf[2];
+  cudaStream_t copy = nullptr;
+  int pf_next = 0, pf_inuse = -1;
   cublasHandle_t blas = nullptr;  // plain large GEMMs only (gemm() below); created on first use
   cusolverDnHandle_t solver = nullptr;  // full eigen-decomposition of large a x a Grams (eig()); on first use
   DevBuf sv_work, sv_evals, sv_info;
@@ -1611,6 +1621,15 @@ int64_t prod(const std::vector<int64_t>& v) {
 const double* stage_input(ttg_ctx* c, const double* y, int where, size_t n) {
   if (where == TTG_DEVICE) return y;
   if (where != TTG_HOST) fail(TTG_E_ARGUMENT, "where must be TTG_HOST or TTG_DEVICE");
+  for (int i = 0; i < 2; ++i) {  // consumed a ttg_prefetch slot: wait for its copy, no transfer here
+    auto& s = c->pf[i];
+    if (s.valid && s.src == y && s.n == (int64_t)n) {
+      CK(cudaStreamWaitEvent(c->stream, s.ready, 0));
+      s.valid = false;
+      c->pf_inuse = i;
+      return s.buf.as<double>();
+    }
+  }
   c->ystage.ensure(sizeof(double) * n);
   CK(cudaMemcpyAsync(c->ystage.p, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   c->h2d += (int64_t)(sizeof(double) * n);
@@ -2390,6 +2409,16 @@ int guard(ttg_ctx* c, auto&& fn) {
     }
     ~StreamScope() { g_alloc_stream = prev; }
   } scope(c);
+  struct PrefetchRelease {  // the consumed staging slot is free once the call's stream work is done
+    ttg_ctx* c;
+    ~PrefetchRelease() {
+      if (c && c->pf_inuse >= 0) {
+        cudaEventRecord(c->pf[c->pf_inuse].freed, c->stream);
+        c->pf[c->pf_inuse].used = true;
+        c->pf_inuse = -1;
+      }
+    }
+  } release{c};
   try {
     fn();
     return TTG_OK;
@@ -2429,6 +2458,11 @@ static int ctx_init(ttg_ctx* c, int device) {
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  for (auto& s : c->pf) {
+    CK(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
+  }
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   cudaDeviceProp prop;
@@ -2566,6 +2600,14 @@ void ttg_ctx_destroy(ttg_ctx* c) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);
   }
+  if (c->copy) {
+    cudaStreamSynchronize(c->copy);
+    cudaStreamDestroy(c->copy);
+  }
+  for (auto& s : c->pf) {
+    if (s.ready) cudaEventDestroy(s.ready);
+    if (s.freed) cudaEventDestroy(s.freed);
+  }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (auto& p : c->pending) {
@@ -2648,6 +2690,23 @@ int ttg_ctx_io_bytes(const ttg_ctx* c, int64_t* h2d, int64_t* d2h) {
   if (h2d) *h2d = c->h2d;
   if (d2h) *d2h = c->d2h;
   return TTG_OK;
+}
+
+int ttg_prefetch(ttg_ctx* c, const double* y, int64_t n) {
+  if (!c || !y || n < 0) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    const int i = c->pf_next;
+    c->pf_next ^= 1;
+    auto& s = c->pf[i];
+    if (s.used) CK(cudaStreamWaitEvent(c->copy, s.freed, 0));  // an earlier update may still read this slot
+    s.buf.ensure(sizeof(double) * (size_t)std::max<int64_t>(n, 1), false, c->copy);
+    CK(cudaMemcpyAsync(s.buf.p, y, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->copy));
+    CK(cudaEventRecord(s.ready, c->copy));
+    s.src = y;
+    s.n = n;
+    s.valid = true;
+    c->h2d += (int64_t)(sizeof(double) * n);
+  });
 }
 
 int ttg_ctx_synchronize(ttg_ctx* c) {

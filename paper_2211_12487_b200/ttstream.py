@@ -159,6 +159,20 @@ class Context:
         _check(_lib.load().ttg_ctx_io_bytes(self._h, ctypes.byref(h), ctypes.byref(d)), self)
         return h.value, d.value
 
+    def prefetch(self, y: np.ndarray) -> None:
+        """include/ttg.h ttg_prefetch: start the H2D copy of host increment ``y``
+        (float64, first-index-fastest, ideally pinned) on the copy stream; the
+        next update / projection given the same array consumes it, so the PCIe
+        transfer of increment k+1 overlaps the update of increment k.  ``y``
+        must not be modified until that call returns."""
+        if not isinstance(y, np.ndarray) or y.dtype != np.float64:
+            raise TypeError("prefetch takes a float64 numpy array")
+        arr = np.asfortranarray(y)
+        if arr is not y:
+            raise ValueError("prefetch needs the first-index-fastest array the update will be given")
+        self._prefetched = (getattr(self, "_prefetched", ()) + (arr,))[-2:]  # keep alive while in flight
+        _check(_lib.load().ttg_prefetch(self._h, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), arr.size), self)
+
     def synchronize(self) -> None:
         _check(_lib.load().ttg_ctx_synchronize(self._h), self)
 

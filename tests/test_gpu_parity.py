@@ -352,3 +352,24 @@ def test_update_large_append_guard_path(ctx):
     compare_trains(tg, tr)
     r = tg.ranks()[1]
     assert 2048 * r * r >= 5e7, r
+
+
+def test_prefetch_host_increments(ctx):
+    """ttg_prefetch: host increments staged on the copy stream and consumed by
+    the next update give bit-identical trains and reports to the plain host
+    path (and a prefetch of a different array is ignored)."""
+    st = Stream(3, seed=4, modes=(4,) * 5, batch=12)
+    ys = [np.asfortranarray(st.increment(k)) for k in range(5)]
+    ta, _ = tt_ice_bootstrap(ys[0], st.eps, ctx=ctx)
+    tb, _ = tt_ice_bootstrap(ys[0], st.eps, ctx=ctx)
+    other = np.asfortranarray(ys[1] + 1.0)
+    for k in range(1, 5):
+        ta, ra = tt_ice_star_update(ta, ys[k], st.eps)
+        if k < 4:
+            ctx.prefetch(ys[k + 1] if k % 2 else other)
+        if k == 1:
+            ctx.prefetch(ys[1])
+        tb, rb = tt_ice_star_update(tb, ys[k], st.eps)
+        assert ra.ranks_after == rb.ranks_after and ra.batch_rel_error_estimate == rb.batch_rel_error_estimate
+    for ca, cb in zip(ta.cores(), tb.cores()):
+        assert np.array_equal(ca, cb)
