@@ -224,14 +224,17 @@ def our_arm(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    # under torchrun the multi-GPU path runs at every N (at N = 1 too: NCCL
+    # context, one-rank communicator), so `torchrun --nproc-per-node 1` checks it
+    multi = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if multi:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2211_12487_b200 import Context, TensorTrain, tt_ice_bootstrap, tt_ice_star_update
     from paper_2211_12487_b200.streams import DeviceStream
 
-    if world > 1:
+    if multi:
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             idt.copy_(torch.frombuffer(bytearray(Context.nccl_unique_id()), dtype=torch.uint8))

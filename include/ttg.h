@@ -92,7 +92,8 @@ void ttg_heuristics_default(ttg_heuristics* h);
 int ttg_ctx_create(int device, ttg_ctx** out);
 /* Multi-GPU: one context per rank, batch axis sharded; Grams and scalars are
  * all-reduced, coefficient columns all-gathered over NCCL.  `nccl_id` is the
- * 128-byte ncclUniqueId produced by ttg_nccl_unique_id on rank 0. */
+ * 128-byte ncclUniqueId produced by ttg_nccl_unique_id on rank 0.  Every
+ * exchange of an NCCL context goes through NCCL, world 1 included. */
 int ttg_nccl_unique_id(uint8_t out[128]);
 int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[128], ttg_ctx** out);
 /* Multi-rank context whose exchanges go through caller-supplied HOST

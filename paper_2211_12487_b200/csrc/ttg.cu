@@ -171,7 +171,10 @@ struct ttg_ctx {
   bool profiling = false;
   uint64_t iface_gen = 0;
   const double* iface_ptr = nullptr;
-  bool pdl = true;  // programmatic dependent launch (launch_k); off under TTG_NO_PDL and for world > 1
+  bool pdl = true;  // programmatic dependent launch (launch_k); off under TTG_NO_PDL and on NCCL contexts
+  // exchange steps active: every NCCL context (world 1 included, so the single-GPU
+  // test exercises the NCCL transport) and host-collective contexts with world > 1
+  bool coll = false;
   std::vector<KStat> kstats;
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> evpool;
@@ -358,7 +361,7 @@ int grid_for(long long n, int threads, int max_blocks) {
 }
 
 void allreduce_sum(ttg_ctx* c, double* d, size_t n) {
-  if (c->world <= 1) return;
+  if (!c->coll) return;
   if (c->host_ar) {  // host transport: D2H, exchange, H2D (stream-ordered)
     c->host_coll_buf.resize(sizeof(double) * n);
     double* h = reinterpret_cast<double*>(c->host_coll_buf.data());
@@ -1228,7 +1231,7 @@ EigResult accurate_eig(ttg_ctx* c, const double* X, int a, long long L, const do
   launch_k(c, ttg::k_tsqr_combine, 1, 1024, smem2, c->partials.as<double>(), gx, a, c->scratch.as<double>(),
                                                      c->G.as<double>());
   post_launch(c);
-  if (c->world > 1) {
+  if (c->coll) {
     c->partials.ensure(sizeof(double) * (size_t)c->world * a * a);
     allgather(c, c->G.as<double>(), c->partials.as<double>(), (size_t)a * a);
     prof_begin(c, "k_tsqr_combine", 16.0 * c->world * a * a, 2.0 * c->world * a * a * a);
@@ -1653,7 +1656,7 @@ void check_train_vs_y(const ttg_tt* tt, const int64_t* shape, int ndim, bool sta
 
 // make sure the observation counts are equal on all ranks (sharded batch)
 int64_t global_obs(ttg_ctx* c, int64_t b) {
-  if (c->world <= 1) return b;
+  if (!c->coll) return b;
   c->scal.ensure(sizeof(double) * 16);
   double* d = c->scal.as<double>() + 8;
   double h[2] = {(double)b, (double)b * (double)b};
@@ -1670,7 +1673,7 @@ int64_t global_obs(ttg_ctx* c, int64_t b) {
 void append_last_core(ttg_ctx* c, ttg_tt* tt, const double* coeffs, int r, int64_t b_local) {
   int64_t bg = b_local * c->world;
   const double* src = coeffs;
-  if (c->world > 1) {
+  if (c->coll) {
     c->coeffs_all.ensure(sizeof(double) * (size_t)r * bg);
     allgather(c, coeffs, c->coeffs_all.as<double>(), (size_t)r * b_local);
     src = c->coeffs_all.as<double>();
@@ -2335,7 +2338,7 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
   trace("star:append last core");
   fill_report_ranks(rep->ranks_after, tt);
   // estimate: Pythagoras on the appended coefficients (tt_ice_star.cpp:297-300)
-  const double* csrc = c->world > 1 ? c->coeffs_all.as<double>() : coeffs;
+  const double* csrc = c->coll ? c->coeffs_all.as<double>() : coeffs;
   // |c|^2 and the guard count ride on the timer's synchronisation (one host sync)
   sumsq_device_async(c, csrc, (long long)r_d * bg);
   rep->seconds = tm.stop();
@@ -2389,7 +2392,7 @@ ttg_tt* do_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shap
     fill_report_ranks(rep->ranks_after, tt);
     for (int i = 0; i <= d + 1; ++i) rep->ranks_before[i] = 1;
     rep->eps_target = eps * y_norm / std::sqrt((double)(ndim - 1));
-    const double* src = c->world > 1 ? c->coeffs_all.as<double>() : so.coeffs;
+    const double* src = c->coll ? c->coeffs_all.as<double>() : so.coeffs;
     const double kept_sq = sumsq_device(c, src, (long long)so.r_d * bg);  // tt_norm (tensor_train.cpp:383-386)
     const double lost_sq = std::max(ysq - kept_sq, 0.0);
     rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(lost_sq) / y_norm;
@@ -2547,7 +2550,8 @@ int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[1
     ctx_init(c, device);
     c->rank = rank;
     c->world = world;
-    if (world > 1) c->pdl = false;  // NCCL kernels interleave in the stream
+    c->pdl = false;  // NCCL kernels interleave in the stream
+    c->coll = true;
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
     NK(ncclCommInitRank(&c->comm, world, id, rank));
@@ -2574,6 +2578,7 @@ int ttg_ctx_create_hostcoll(int device, int rank, int world, ttg_host_allreduce_
     c->host_ar = allreduce;
     c->host_ag = allgather_fn;
     c->host_user = user;
+    c->coll = world > 1;
   });
   if (rc != TTG_OK) {
     fprintf(stderr, "ttg_ctx_create_hostcoll: %s\n", c->err.c_str());

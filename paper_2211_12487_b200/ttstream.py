@@ -60,7 +60,7 @@ class Context:
     def __init__(self, device: int = 0, *, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
         lib = _lib.load()
         h = ctypes.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # an explicit id at world 1: NCCL transport on one GPU
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("multi-GPU context needs the 128-byte NCCL unique id")
             rc = lib.ttg_ctx_create_dist(device, rank, world, nccl_id, ctypes.byref(h))

@@ -113,3 +113,42 @@ def test_ranks_on_one_gpu_match_unsharded_oracle(algo, world):
     compare_reconstructions(tg, tr, list(enumerate(ys)))
     for p in procs:
         assert p.exitcode == 0
+
+
+@pytest.mark.parametrize("algo", ["ice", "star"])
+def test_nccl_transport_single_rank_matches_oracle(algo):
+    """The production NCCL transport (ttg_ctx_create_dist, ttg.cu allreduce_sum /
+    allgather) on a one-rank communicator: every exchange step of the multi-GPU
+    path runs through ncclAllReduce / ncclAllGather (an NCCL context always
+    takes them, world 1 included) with PDL off as on N > 1 GPUs.  Ranks after
+    every increment identical to the oracle, subspaces / reconstructions /
+    estimates within 1e-10."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle import ttstream_oracle as O
+    from paper_2211_12487_b200 import Context, tt_ice_bootstrap, tt_ice_star_update, tt_ice_update
+    from paper_2211_12487_b200.streams import Stream
+    from tests.parity_util import TOL, compare_reconstructions, compare_trains
+
+    ctx = Context(0, rank=0, world=1, nccl_id=Context.nccl_unique_id())
+    assert ctx.world == 1 and ctx.rank == 0
+    s = Stream(3, seed=5, modes=(6,) * 4, batch=16, true_rank=5)
+    ys = [s.increment(k) for k in range(N_INC)]
+    tt, rep = tt_ice_bootstrap(ys[0], s.eps, ctx=ctx)
+    tr, rr = O.tt_ice_bootstrap(ys[0], s.eps)
+    pairs = [(rep, rr)]
+    for y in ys[1:]:
+        tt, rep = (tt_ice_update if algo == "ice" else tt_ice_star_update)(tt, y, s.eps)
+        tr, rr = (O.tt_ice_update if algo == "ice" else O.tt_ice_star_update)(tr, y, s.eps)
+        pairs.append((rep, rr))
+    for rg, r in pairs:
+        assert list(rg.ranks_after) == list(r.ranks_after)
+        assert rg.obs_used == r.obs_used
+        assert abs(rg.batch_rel_error_estimate - r.batch_rel_error_estimate) <= max(TOL, 1e-8 * r.batch_rel_error_estimate)
+    tg = O.TensorTrain([O.TTCore(np.asfortranarray(c)) for c in tt.cores()], tt.ortho_count, tt.batch_boundaries())
+    compare_trains(tg, tr)
+    compare_reconstructions(tg, tr, list(enumerate(ys)))
+    tt.close()
+    ctx.close()
