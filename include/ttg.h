@@ -118,6 +118,14 @@ void* ttg_ctx_stream(const ttg_ctx* ctx);
 /* Number of ttg kernels launched by this context so far. */
 int64_t ttg_ctx_launch_count(const ttg_ctx* ctx);
 int ttg_ctx_synchronize(ttg_ctx* ctx);
+/* Ordering against a caller's CUDA stream (cudaStream_t as void*; NULL = the
+ * legacy default stream), no host synchronisation.  The context stream is
+ * non-blocking, so a device increment produced on another stream must be
+ * ordered before the update reads it (wait), and a device result written by
+ * the context (ttg_reconstruct into device memory) before the caller's stream
+ * reads it (join). */
+int ttg_ctx_wait_stream(ttg_ctx* ctx, void* stream);
+int ttg_ctx_join_stream(ttg_ctx* ctx, void* stream);
 /* Per-kernel accounting.  Launch counts and ALGORITHMIC bytes / flops per
  * launch are always kept; device time (CUDA events on the
  * context stream around each launch) only while profiling is on. */

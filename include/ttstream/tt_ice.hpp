@@ -30,6 +30,8 @@ std::pair<TensorTrain, UpdateReport> tt_ice_bootstrap(const DenseTensor& y, doub
 
 /// Device-pointer overloads (drop-in extension): y_device is a
 /// first-index-fastest float64 increment already in GPU memory (no PCIe copy).
+/// The library stream is non-blocking: a y_device written on another CUDA
+/// stream must be complete or ordered first (ttg_ctx_wait_stream, ttg.h).
 std::pair<TensorTrain, UpdateReport> tt_ice_update(const TensorTrain& tt, const double* y_device,
                                                    std::span<const Index> shape, double eps_des);
 std::pair<TensorTrain, UpdateReport> tt_ice_bootstrap(const double* y_device, std::span<const Index> shape,

@@ -67,6 +67,8 @@ SIGNATURES = [
     ("ttg_ctx_stream", ctypes.c_void_p, [_P]),
     ("ttg_ctx_launch_count", ctypes.c_int64, [_P]),
     ("ttg_ctx_synchronize", ctypes.c_int, [_P]),
+    ("ttg_ctx_wait_stream", ctypes.c_int, [_P, _P]),
+    ("ttg_ctx_join_stream", ctypes.c_int, [_P, _P]),
     ("ttg_ctx_set_profiling", ctypes.c_int, [_P, ctypes.c_int]),
     ("ttg_ctx_reset_stats", None, [_P]),
     ("ttg_ctx_num_kernel_stats", ctypes.c_int, [_P]),

@@ -131,6 +131,7 @@ struct ttg_ctx {
   // statistics pass instead of after it
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;  // ordering against caller streams
   // ttg_prefetch: two staging slots filled on the copy stream
   struct Prefetch {
     DevBuf buf;
@@ -2468,6 +2469,8 @@ static int ctx_init(ttg_ctx* c, int device) {
   }
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
   c->num_sms = prop.multiProcessorCount;
@@ -2615,6 +2618,8 @@ void ttg_ctx_destroy(ttg_ctx* c) {
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
   for (auto& p : c->pending) {
     cudaEventDestroy(p.e0);
     cudaEventDestroy(p.e1);
@@ -2716,6 +2721,22 @@ int ttg_prefetch(ttg_ctx* c, const double* y, int64_t n) {
 
 int ttg_ctx_synchronize(ttg_ctx* c) {
   return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int ttg_ctx_wait_stream(ttg_ctx* c, void* stream) {
+  if (!c) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    CK(cudaEventRecord(c->ev_in, (cudaStream_t)stream));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_in, 0));
+  });
+}
+
+int ttg_ctx_join_stream(ttg_ctx* c, void* stream) {
+  if (!c) return TTG_E_ARGUMENT;
+  return guard(c, [&] {
+    CK(cudaEventRecord(c->ev_out, c->stream));
+    CK(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_out, 0));
+  });
 }
 
 int ttg_tt_upload(ttg_ctx* c, int n_cores, const int64_t* r_left, const int64_t* n, const int64_t* r_right,

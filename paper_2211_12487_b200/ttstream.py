@@ -255,9 +255,12 @@ class DeviceIncrement:
 
 
 class _Input:
-    """Resolves y (numpy host array, torch CUDA tensor or DeviceIncrement) to (pointer, where, shape)."""
+    """Resolves y (numpy host array, torch CUDA tensor or DeviceIncrement) to (pointer, where, shape).
+    A torch tensor is ordered before the context's (non-blocking) stream reads
+    it: the context stream waits on torch's current stream (ttg_ctx_wait_stream,
+    no host sync)."""
 
-    def __init__(self, y, shape: Optional[Sequence[int]] = None):
+    def __init__(self, y, shape: Optional[Sequence[int]] = None, ctx: Optional["Context"] = None):
         self.keep = None
         if isinstance(y, np.ndarray):
             if y.dtype != np.float64:
@@ -298,6 +301,8 @@ class _Input:
         self.keep = y
         self.ptr = ctypes.cast(ctypes.c_void_p(y.data_ptr()), ctypes.POINTER(ctypes.c_double))
         self.where = TTG_DEVICE
+        if ctx is not None:
+            _check(_lib.load().ttg_ctx_wait_stream(ctx._h, torch.cuda.current_stream(y.device).cuda_stream), ctx)
 
     def shape_arr(self):
         return (ctypes.c_int64 * len(self.shape))(*self.shape), len(self.shape)
@@ -419,7 +424,7 @@ class TensorTrain:
 def tt_ice_bootstrap(y, eps_des: float, ctx: Optional[Context] = None, shape=None) -> Tuple[TensorTrain, UpdateReport]:
     """tt_ice.cpp:143-165: TT-SVD of the first increment (tt_svd.cpp:9-66), on device."""
     ctx = ctx or default_context()
-    inp = _Input(y, shape)
+    inp = _Input(y, shape, ctx)
     sh, nd = inp.shape_arr()
     h = ctypes.c_void_p()
     rep = _lib.Report()
@@ -430,7 +435,7 @@ def tt_ice_bootstrap(y, eps_des: float, ctx: Optional[Context] = None, shape=Non
 
 def tt_ice_update(tt: TensorTrain, y, eps_des: float, shape=None) -> Tuple[TensorTrain, UpdateReport]:
     """tt_ice.cpp:131-141 (uniform delta = eps_des |y|_F / sqrt(d)); updates ``tt`` in place."""
-    inp = _Input(y, shape)
+    inp = _Input(y, shape, tt.ctx)
     sh, nd = inp.shape_arr()
     rep = _lib.Report()
     _check(_lib.load().ttg_tt_ice_update(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, float(eps_des),
@@ -440,7 +445,7 @@ def tt_ice_update(tt: TensorTrain, y, eps_des: float, shape=None) -> Tuple[Tenso
 
 def tt_ice_update_with_tolerances(tt: TensorTrain, y, deltas: Sequence[float], shape=None):
     """tt_ice.cpp:60-129 (one absolute threshold per spatial mode)."""
-    inp = _Input(y, shape)
+    inp = _Input(y, shape, tt.ctx)
     sh, nd = inp.shape_arr()
     rep = _lib.Report()
     dl = (ctypes.c_double * max(len(deltas), 1))(*[float(x) for x in deltas])
@@ -452,7 +457,7 @@ def tt_ice_update_with_tolerances(tt: TensorTrain, y, deltas: Sequence[float], s
 def tt_ice_star_update(tt: TensorTrain, y, eps_des: float, cfg: Optional[HeuristicConfig] = None, shape=None):
     """tt_ice_star.cpp:171-303 (Algorithm 2); updates ``tt`` in place."""
     cfg = cfg or HeuristicConfig()
-    inp = _Input(y, shape)
+    inp = _Input(y, shape, tt.ctx)
     sh, nd = inp.shape_arr()
     rep = _lib.Report()
     h = cfg._to()
@@ -463,7 +468,7 @@ def tt_ice_star_update(tt: TensorTrain, y, eps_des: float, cfg: Optional[Heurist
 
 def per_obs_errors(tt: TensorTrain, y, shape=None) -> np.ndarray:
     """tt_ice_star.cpp:86-88."""
-    inp = _Input(y, shape)
+    inp = _Input(y, shape, tt.ctx)
     sh, nd = inp.shape_arr()
     out = np.empty(inp.shape[-1], dtype=np.float64)
     _check(_lib.load().ttg_per_obs_errors(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd,
@@ -473,7 +478,7 @@ def per_obs_errors(tt: TensorTrain, y, shape=None) -> np.ndarray:
 
 def tt_project(tt: TensorTrain, y, shape=None) -> np.ndarray:
     """tensor_train.cpp:195-226: r_d x n_obs latent coefficients."""
-    inp = _Input(y, shape)
+    inp = _Input(y, shape, tt.ctx)
     sh, nd = inp.shape_arr()
     r_d = tt.ranks()[-2]
     out = np.empty((r_d, inp.shape[-1]), dtype=np.float64, order="F")
@@ -493,8 +498,14 @@ def tt_reconstruct(tt: TensorTrain, obs_begin: int = 0, obs_end: Optional[int] =
         _check(_lib.load().ttg_reconstruct(tt.ctx._h, tt._h, int(obs_begin), int(obs_end),
                                            host.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), TTG_HOST), tt.ctx)
         return np.reshape(host, tuple(spatial) + (m,), order="F")
+    import torch
+
+    lib = _lib.load()
+    ts = torch.cuda.current_stream(out.device).cuda_stream
     ptr = ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_double))
-    _check(_lib.load().ttg_reconstruct(tt.ctx._h, tt._h, int(obs_begin), int(obs_end), ptr, TTG_DEVICE), tt.ctx)
+    _check(lib.ttg_ctx_wait_stream(tt.ctx._h, ts), tt.ctx)  # torch's pending use of ``out`` first
+    _check(lib.ttg_reconstruct(tt.ctx._h, tt._h, int(obs_begin), int(obs_end), ptr, TTG_DEVICE), tt.ctx)
+    _check(lib.ttg_ctx_join_stream(tt.ctx._h, ts), tt.ctx)  # torch reads ``out`` after the write
     return out
 
 
@@ -538,7 +549,7 @@ def rre(tt: TensorTrain, x_ref, obs_begin: int = 0, obs_end: Optional[int] = Non
     ``with_flag`` returns (value, zero_reference))."""
     if obs_end is None:
         obs_end = tt.obs_count()
-    inp = _Input(x_ref, shape)
+    inp = _Input(x_ref, shape, tt.ctx)
     sh, nd = inp.shape_arr()
     val, zr = ctypes.c_double(), ctypes.c_int()
     _check(_lib.load().ttg_rre(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, int(obs_begin), int(obs_end),
@@ -548,7 +559,7 @@ def rre(tt: TensorTrain, x_ref, obs_begin: int = 0, obs_end: Optional[int] = Non
 
 def rpe(tt: TensorTrain, unseen, *, shape=None, with_flag: bool = False):
     """metrics.cpp:44-47: relative error of tt_expand(tt_project(unseen))."""
-    inp = _Input(unseen, shape)
+    inp = _Input(unseen, shape, tt.ctx)
     sh, nd = inp.shape_arr()
     val, zr = ctypes.c_double(), ctypes.c_int()
     _check(_lib.load().ttg_rpe(tt.ctx._h, tt._h, inp.ptr, inp.where, sh, nd, ctypes.byref(val), ctypes.byref(zr)),

@@ -1,0 +1,122 @@
+"""GPU, BASELINE configs[3] at its FULL size (8^7 x 256 = 4.29 GB per
+increment, eps 0.01): properties that do not need the oracle to finish at this
+size (the oracle runs the same generator at batch <= 8 in test_gpu_parity.py).
+
+Per increment:
+* the device RRE of the increment against its own reconstruction (metrics.cpp
+  rre, computed by k_rre_partial from the cores alone) equals the report's
+  batch_rel_error_estimate (tt_ice.cpp:125-126 / tt_ice_star.cpp:297-300, a
+  different formula): |rre^2 - est^2| <= 1e-12 (both are differences of
+  537M-term sums of |Y|^2-sized terms);
+* TT-ICE: that error is within eps_des (Cor. 3.2);
+* the re-measured orthonormality (serialization.cpp:126-128 rule, 1e-10) covers
+  every spatial core;
+* Theorem 3.3 / Eq. 3.4: every old core entry is bit-identical after the update
+  and the padded rows of old columns are exactly zero; old last-core columns
+  are bit-identical;
+* TT-ICE*: the redundant increments of the stream (in-span re-samples) use no
+  observations and leave the ranks unchanged.
+Across runs: the same stream in a fresh context gives bit-identical cores, and
+the stream scaled by 2 (exact in FP64) gives the same ranks and cores.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MODES = (8,) * 7
+B = 256
+EPS = 0.01
+N_INC = 6
+
+
+def _run(ctx, algo, scale=1.0, check=True):
+    import torch
+
+    from paper_2211_12487_b200 import rre, tt_ice_bootstrap, tt_ice_star_update, tt_ice_update
+    from paper_2211_12487_b200.streams import DeviceStream
+
+    gen = DeviceStream(seed=7, modes=MODES)
+    shape = MODES + (B,)
+    d = len(MODES)
+    tt = None
+    prev_cores = None
+    prev_last = None
+    ranks_hist = []
+    for k in range(N_INC):
+        y = gen.increment(k, B)
+        if scale != 1.0:
+            y.mul_(scale)
+        if k == 0:
+            tt, rep = tt_ice_bootstrap(y, EPS, ctx=ctx, shape=shape)
+        elif algo == "ice":
+            tt, rep = tt_ice_update(tt, y, EPS, shape=shape)
+        else:
+            tt, rep = tt_ice_star_update(tt, y, EPS, shape=shape)
+        ranks_hist.append(list(rep.ranks_after))
+        cores = tt.cores()
+        if check:
+            b0, e0 = tt.increment_range(k)
+            assert (b0, e0) == (k * B, (k + 1) * B)
+            err = rre(tt, y, b0, e0, shape=shape)
+            est = rep.batch_rel_error_estimate
+            # both are differences of N-term sums of |Y|^2-sized terms (N = 537M):
+            # they agree to 1e-12 in relative energy, |err^2 - est^2| <= 1e-12
+            assert abs(err * err - est * est) <= 1e-12, (k, err, est)
+            print(f"{algo} k={k} rre={err:.15e} est={est:.15e} rel={abs(err - est) / err:.2e}")
+            if algo == "ice" or k == 0:
+                assert err <= EPS * (1 + 1e-12), (k, err)
+            assert tt.measure_ortho_count() == d == tt.ortho_count
+            if algo == "star" and k > 0 and gen.host.is_redundant(k):
+                assert rep.obs_used == 0 and list(rep.ranks_after) == list(rep.ranks_before), k
+            if prev_cores is not None:
+                for i in range(d):
+                    old, new = prev_cores[i], cores[i]
+                    rl, n, rr = old.shape
+                    assert new.shape[1] == n and new.shape[0] >= rl and new.shape[2] >= rr
+                    assert np.array_equal(new[:rl, :, :rr], old), (k, i)
+                    assert not np.any(new[rl:, :, :rr]), (k, i)
+                last = cores[d]
+                rl, nobs = prev_last.shape[0], prev_last.shape[1]
+                assert np.array_equal(last[:rl, :nobs, 0], prev_last[:, :, 0]), k
+                assert not np.any(last[rl:, :nobs, 0]), k
+        prev_cores = cores[:d]
+        prev_last = cores[d]
+        del y
+        torch.cuda.empty_cache()
+    out = (ranks_hist, tt.cores())
+    tt.close()
+    return out
+
+
+@pytest.mark.parametrize("algo", ["star", "ice"])
+def test_cfg3_full_size_properties(algo):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2211_12487_b200 import Context
+
+    ctx = Context(0)
+    ranks, cores = _run(ctx, algo)
+    assert ranks[-1][1] == 8 and all(r >= 12 for r in ranks[-1][2:-1])  # true rank 12 plus drift
+    for a, b in zip(ranks, ranks[1:]):
+        assert all(y >= x for x, y in zip(a, b))
+    ctx.close()
+    # bit-identical in a fresh context
+    ctx2 = Context(0)
+    ranks2, cores2 = _run(ctx2, algo, check=False)
+    ctx2.close()
+    assert ranks2 == ranks
+    for c1, c2 in zip(cores, cores2):
+        assert np.array_equal(c1, c2)
+    if algo == "star":
+        # scale by 2: every threshold and Gram scales exactly, so ranks and
+        # spatial cores are unchanged and the coefficients double
+        ctx3 = Context(0)
+        ranks3, cores3 = _run(ctx3, algo, scale=2.0, check=False)
+        ctx3.close()
+        assert ranks3 == ranks
+        for c1, c3 in zip(cores[:-1], cores3[:-1]):
+            assert np.max(np.abs(c1 - c3)) <= 1e-12
+        assert np.max(np.abs(2.0 * cores[-1] - cores3[-1])) <= 1e-12 * np.max(np.abs(cores3[-1]))
