@@ -224,9 +224,9 @@ def our_arm(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     dist = None
-    # under torchrun the multi-GPU path runs at every N (at N = 1 too: NCCL
-    # context, one-rank communicator), so `torchrun --nproc-per-node 1` checks it
-    multi = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    # --force-dist under torchrun runs the multi-GPU path at N = 1 too (NCCL
+    # context on a one-rank communicator, PDL off), so one GPU can check it
+    multi = world > 1 or (args.force_dist and "TORCHELASTIC_RUN_ID" in os.environ)
     if multi:
         import torch.distributed as dist
 
@@ -449,6 +449,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--clock-interval-ms", type=int, default=100)
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="under torchrun at N = 1: take the multi-GPU path (NCCL process group and context)")
     ap.add_argument("--kernels-out", default=None, help="write the full per-kernel table (JSON) here")
     args = ap.parse_args()
     if args.warmup < 3:
