@@ -77,6 +77,8 @@ def test_null_arguments_return_status_without_gpu(lib):
     L = _lib.load()
     assert L.ttg_ctx_create(0, None) == 10  # TTG_E_ARGUMENT
     assert L.ttg_tt_num_cores(None) == -1
+    assert L.ttg_ctx_wait_stream(None, None) == 10
+    assert L.ttg_ctx_join_stream(None, None) == 10
     # ctx NULL: the message of the calling thread's last context-free call (TTB1)
     import ctypes
 
