@@ -120,3 +120,63 @@ def test_cfg3_full_size_properties(algo):
         for c1, c3 in zip(cores[:-1], cores3[:-1]):
             assert np.max(np.abs(c1 - c3)) <= 1e-12
         assert np.max(np.abs(2.0 * cores[-1] - cores3[-1])) <= 1e-12 * np.max(np.abs(cores3[-1]))
+
+
+def _host_stream_properties(ctx, stream, n_inc, algo):
+    """The per-increment properties above over a host-generated stream (numpy
+    increments: the host path, H2D inside the call)."""
+    from paper_2211_12487_b200 import rre, tt_ice_bootstrap, tt_ice_star_update, tt_ice_update
+
+    eps = stream.eps
+    tt, prev, ranks = None, None, []
+    for k in range(n_inc):
+        y = stream.increment(k)
+        if k == 0:
+            tt, rep = tt_ice_bootstrap(y, eps, ctx=ctx)
+        elif algo == "ice":
+            tt, rep = tt_ice_update(tt, y, eps)
+        else:
+            tt, rep = tt_ice_star_update(tt, y, eps)
+        d = tt.spatial_dims()
+        b0, e0 = tt.increment_range(k)
+        assert e0 - b0 == y.shape[-1]
+        err = rre(tt, y, b0, e0)
+        est = rep.batch_rel_error_estimate
+        assert abs(err * err - est * est) <= 1e-12, (k, err, est)
+        if algo == "ice" or k == 0:
+            assert err <= eps * (1 + 1e-12), (k, err)
+        assert tt.measure_ortho_count() == d == tt.ortho_count
+        cores = tt.cores()
+        if prev is not None:
+            for i in range(d):
+                rl, n, rr = prev[i].shape
+                assert np.array_equal(cores[i][:rl, :, :rr], prev[i]), (k, i)
+                assert not np.any(cores[i][rl:, :, :rr]), (k, i)
+            rl, nobs = prev[d].shape[0], prev[d].shape[1]
+            assert np.array_equal(cores[d][:rl, :nobs, 0], prev[d][:, :, 0]), k
+        prev = cores
+        ranks.append(list(rep.ranks_after))
+    for a, b in zip(ranks, ranks[1:]):
+        assert all(y >= x for x, y in zip(a, b))
+    tt.close()
+    return ranks
+
+
+@pytest.mark.parametrize("algo", ["ice", "star"])
+def test_cfg1_video_full_size_properties(ctx, algo):
+    """BASELINE configs[1] at full size: 210x160x3 frames as 14x15x16x10x3,
+    batches of 100, all 40 increments, eps 0.1 (drift: ranks grow)."""
+    from paper_2211_12487_b200.streams import Stream
+
+    ranks = _host_stream_properties(ctx, Stream(1, seed=0), 40, algo)
+    assert ranks[-1] != ranks[0]
+
+
+def test_cfg2_simulation_full_size_properties(ctx):
+    """BASELINE configs[2] at full size: 64^3 x 3 velocity fields as
+    8^6 x 3, batches of 32, eps 0.05; the first 8 of its 50 increments (the
+    ranks reach the hundreds; the whole stream is timed by
+    tools/bench_configs.py)."""
+    from paper_2211_12487_b200.streams import Stream
+
+    _host_stream_properties(ctx, Stream(2, seed=0), 8, "star")
