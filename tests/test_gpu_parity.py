@@ -70,6 +70,14 @@ def test_cfg3_shape_star_midsize(ctx):
 
 
 @pytest.mark.parametrize("algo", ["ice", "star"])
+def test_cfg3_shape_batch16(ctx, algo):
+    """cfg3 shape 8^7 at batch 16 (268 MB increments), 6 increments: two drift
+    increments and two in-span (skip) increments after the bootstrap."""
+    s = Stream(3, seed=4, batch=16)
+    run_stream(ctx, s, 6, algo)
+
+
+@pytest.mark.parametrize("algo", ["ice", "star"])
 def test_wide_unfoldings(ctx, algo):
     """Unfoldings with 128 < r*n <= 256 rows (tensor-map SYRK, 32-column
     projection tiles) and odd/even row counts: modes 16^3 x 6, batch 16."""
