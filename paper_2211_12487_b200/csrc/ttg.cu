@@ -2553,7 +2553,10 @@ int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[1
     ctx_init(c, device);
     c->rank = rank;
     c->world = world;
-    c->pdl = false;  // NCCL kernels interleave in the stream
+    // NCCL kernels interleave in the stream: PDL off unless TTG_NCCL_PDL is set
+    // (our kernels never trigger early, so the opt-in is safe by construction;
+    // kept opt-in until measured at N > 1)
+    c->pdl = c->pdl && std::getenv("TTG_NCCL_PDL") != nullptr;
     c->coll = true;
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
