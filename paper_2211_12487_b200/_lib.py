@@ -123,6 +123,14 @@ def load() -> ctypes.CDLL:
         return _lib
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: the CUDA library must be built (no CPU fallback exists)")
+    # libttg.so needs libnccl.so.2.  torch bundles a newer NCCL under the same
+    # soname, and libtorch_cuda fails to load against the older system copy, so
+    # torch (the plumbing: device memory, streams) is loaded first; libttg's
+    # dependency then binds to the NCCL already in the process.
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     lib = ctypes.CDLL(LIB_PATH)
     for name, res, args in SIGNATURES:
         fn = getattr(lib, name)

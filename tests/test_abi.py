@@ -116,3 +116,15 @@ def test_sass_uses_fp64_tensor_cores():
     """The fused Gram / projection kernels are DMMA (FP64 tensor core) code."""
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in out
+
+
+def test_loading_the_library_before_torch_keeps_torch_importable():
+    """libttg.so depends on libnccl.so.2; loading it before torch must not bind
+    the process to the older system NCCL (libtorch_cuda then fails with an
+    undefined ncclDevCommCreate).  _lib.load() loads torch first."""
+    import subprocess
+    import sys
+
+    code = "from paper_2211_12487_b200 import _lib; _lib.load(); import torch; print('ok')"
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

@@ -381,3 +381,39 @@ def test_prefetch_host_increments(ctx):
         assert ra.ranks_after == rb.ranks_after and ra.batch_rel_error_estimate == rb.batch_rel_error_estimate
     for ca, cb in zip(ta.cores(), tb.cores()):
         assert np.array_equal(ca, cb)
+
+
+def test_device_io_ordered_against_torch_stream(ctx):
+    """Device increments produced by torch and device results consumed by torch
+    without any host synchronisation (ttg_ctx_wait_stream / ttg_ctx_join_stream):
+    a large torch kernel queue in front of the update and a torch read right
+    after tt_reconstruct(out=...) see the same bytes as the host path."""
+    import torch
+
+    s = Stream(3, seed=13, modes=(6,) * 5, batch=24, true_rank=5)
+    ys = [s.increment(k) for k in range(3)]
+    th, _ = tt_ice_bootstrap(ys[0], s.eps, ctx=ctx)
+    for y in ys[1:]:
+        th, _ = tt_ice_update(th, y, s.eps)
+    ref = tt_reconstruct(th, 0, th.obs_count())
+    cores_h = th.cores()
+    th.close()
+    td = None
+    for k, y in enumerate(ys):
+        dev = torch.from_numpy(np.ravel(y, order="F")).cuda()
+        big = torch.randn(1 << 26, device="cuda", dtype=torch.float64)  # keeps torch's stream busy
+        for _ in range(4):
+            big.mul_(1.0000001)
+        dev.mul_(2.0).mul_(0.5)  # the last writes of the increment are queued behind the big kernels
+        if k == 0:
+            td, _ = tt_ice_bootstrap(dev, s.eps, ctx=ctx, shape=y.shape)
+        else:
+            td, _ = tt_ice_update(td, dev, s.eps, shape=y.shape)
+        del big
+    for a, b in zip(td.cores(), cores_h):
+        assert np.array_equal(a, b)
+    out = torch.full((ref.size,), float("nan"), device="cuda", dtype=torch.float64)
+    tt_reconstruct(td, 0, td.obs_count(), out=out)
+    got = out.mul(1.0).cpu().numpy()  # a torch kernel reads the result first
+    assert np.array_equal(got, np.ravel(ref, order="F"))
+    td.close()
