@@ -28,11 +28,16 @@ What it restates (reference = /root/reference/proj, C++20 + Eigen):
 * ``write_batch`` / ``read_batch`` (TTB1) / ``list_stream``
                                 src/stream_io.cpp:123-204
 
-Parity status: the reference ships NO golden vectors and cannot be compiled
-here (Eigen3 is absent).  This oracle is therefore pinned
-only to the SPEC's known-answer examples and property tests (SPEC.md:121-129,
-212-214, 321, 344-348, 395-415, 514), checked in tests/test_oracle_kat.py.
-Against the reference itself: **parity unpinned** beyond those.
+Parity status: PINNED to the reference itself.  The reference library's own
+sources (/root/reference/proj/src/*.cpp) compile unchanged against the
+Eigen-API shim in oracle/eigen_shim (oracle/Makefile -> oracle/_ref/
+libttref.so, bound by oracle/ref_binding.py with this module's names);
+tests/test_ref_pin.py runs the same seeded bytes through both on cfg0, reduced
+cfg1/2/3, every TT-ICE* heuristic variant, the Appendix-B eps = 1e-8 cases, the
+edge cases and the SPEC known-answer examples, at the north-star bar.  The
+committed cfg0 golden fixtures are the reference's output.  The GPU parity
+tests use the reference library as their checker when it is present and this
+restatement otherwise.
 
 Eigen -> LAPACK mapping: Eigen::BDCSVD -> numpy.linalg.svd (LAPACK dgesdd,
 the same divide-and-conquer family); Eigen::HouseholderQR -> numpy.linalg.qr

@@ -1020,6 +1020,8 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, 1) k_syrk_kp(const __grid
   constexpr int KS = 8 / P;
   extern __shared__ __align__(1024) double smem_raw[];
   __shared__ __align__(8) uint64_t full[8], empty[8];
+  // X is the previous mode's projection output: wait for it (PDL launch).
+  griddep_wait();
   double* smem = align1024(smem_raw);
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {

@@ -1,20 +1,19 @@
 """Generate the committed golden fixtures under tests/golden/.
 
-The reference (C++20 + Eigen3) cannot be built in this image (Eigen3 is not
-installed, no network) and ships no golden vectors of its own
-(its test TUs are one-line stubs), so the fixtures here are:
+The reference ships no golden vectors of its own (its test TUs are one-line
+stubs), so the fixtures here are:
 
 * kat.json   -- the SPEC known-answer examples for the path's helper
                operations, each with the SPEC.md line it restates (inputs and
                expected outputs written from the SPEC text, not computed);
-* cfg0_ice.npz, cfg0_star.npz -- the CPU oracle (oracle/ttstream_oracle.py)
-               run over BASELINE configs[0] (64 increments of 8x8x8x8, batch 1,
-               eps 0.1; seeds 0 and 1): per-increment reports and the final
-               train, plus a SHA-256 of the generated input bytes so a change
-               of the seeded generator is caught.  These pin the oracle and the
-               CUDA path to a fixed answer across rounds (regression anchor);
-               they are oracle outputs, so parity against the reference itself
-               stays unpinned beyond kat.json.
+* cfg0_ice.npz, cfg0_star.npz -- the REFERENCE ITSELF (oracle/_ref/libttref.so:
+               /root/reference/proj/src compiled unchanged against the
+               Eigen-API shim, see oracle/Makefile) run over BASELINE
+               configs[0] (64 increments of 8x8x8x8, batch 1, eps 0.1; seeds 0
+               and 1): per-increment reports and the final train, plus a
+               SHA-256 of the generated input bytes so a change of the seeded
+               generator is caught.  They pin the numpy oracle and the CUDA
+               path to the reference's answer.
 
 usage: python tests/golden/make_golden.py
 """
@@ -29,7 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle import ttstream_oracle as O  # noqa: E402
+from oracle import ref_binding as R  # noqa: E402
 from paper_2211_12487_b200.streams import Stream  # noqa: E402
 
 N_INC = 64
@@ -70,10 +69,10 @@ def stream_fixture(algo, seed):
         y = np.asfortranarray(s.increment(k))
         h.update(y.tobytes(order="F"))
         ys.append(y)
-    tt, rep = O.tt_ice_bootstrap(ys[0], s.eps)
+    tt, rep = R.tt_ice_bootstrap(ys[0], s.eps)
     reps = [rep]
     for k in range(1, N_INC):
-        tt, rep = (O.tt_ice_update if algo == "ice" else O.tt_ice_star_update)(tt, ys[k], s.eps)
+        tt, rep = (R.tt_ice_update if algo == "ice" else R.tt_ice_star_update)(tt, ys[k], s.eps)
         reps.append(rep)
     out = {
         "input_sha256": np.frombuffer(h.digest(), dtype=np.uint8),
@@ -85,6 +84,7 @@ def stream_fixture(algo, seed):
         "batch_boundaries": np.array(tt.batch_boundaries, dtype=np.int64),
         "ortho_count": np.int64(tt.ortho_count),
         "n_cores": np.int64(len(tt.cores)),
+        "generator": np.array("reference proj/src via oracle/_ref/libttref.so"),
     }
     for i, c in enumerate(tt.cores):
         out[f"core{i}"] = np.asfortranarray(c.data)

@@ -9,14 +9,24 @@ errors within 1e-10 relative (FP64)"):
                               interface matrix Phi_k (basis-invariant subspace distance)
 * reconstructions           : |rec - rec_ref|_F / |rec_ref|_F <= 1e-10 per increment
 * per-increment rel. errors : |err - err_ref| <= 1e-10 (absolute difference of two relative errors)
+* report error estimates    : 1e-10 absolute; Pythagoras-form estimates on their square at 1e-13
+                              (see estimates_agree)
 """
 from __future__ import annotations
 
 import numpy as np
 
+from oracle import ref_binding as R
 from oracle import ttstream_oracle as O
 
 TOL = 1e-10
+
+# The checker of the GPU parity tests: the reference library itself
+# (oracle/_ref/libttref.so, proj/src compiled unchanged against the Eigen-API
+# shim) when it was built, else the numpy restatement, which
+# tests/test_ref_pin.py pins to the reference case by case.
+REF = R if R.available() else O
+REF_NAME = "reference (oracle/_ref)" if REF is R else "numpy oracle"
 
 
 def to_oracle(tt) -> O.TensorTrain:
@@ -67,11 +77,28 @@ def compare_reconstructions(tt_gpu_host: O.TensorTrain, tt_ref: O.TensorTrain, y
     return worst_rec, worst_err
 
 
+# Pythagoras-form estimates (bootstrap tt_ice.cpp:159-162 and TT-ICE*
+# tt_ice_star.cpp:297-300) are sqrt(max(1 - |c|^2/|y|^2, 0)): the SQUARE is
+# computed to a few ulps absolute, the root of a near-zero difference is not
+# (a noiseless stream gives 0 in one rounding and 3e-8 in another).  They are
+# compared on the square at 1e-13 absolute, i.e. 5e-11 in the estimate at the
+# 1e-3 errors of configs[3]; TT-ICE's sqrt(sum tail^2)/|y| (tt_ice.cpp:125-126)
+# at 1e-10 absolute.
+EST2_TOL = 1e-13
+
+
+def estimates_agree(a: float, b: float, pythagoras: bool, tol: float = TOL) -> bool:
+    if abs(a - b) <= tol:
+        return True
+    return pythagoras and abs(a * a - b * b) <= EST2_TOL
+
+
 def compare_reports(rg, rr, tol: float = TOL, star: bool = False):
     assert list(rg.ranks_after) == list(rr.ranks_after), f"report ranks {rg.ranks_after} vs {rr.ranks_after}"
     assert rg.obs_in_batch == rr.obs_in_batch
     assert rg.obs_used == rr.obs_used, f"obs_used {rg.obs_used} vs {rr.obs_used}"
-    assert abs(rg.batch_rel_error_estimate - rr.batch_rel_error_estimate) <= max(tol, 1e-8 * rr.batch_rel_error_estimate if star else tol), \
+    assert estimates_agree(rg.batch_rel_error_estimate, rr.batch_rel_error_estimate,
+                           pythagoras=star or rr.increment_index == 0, tol=tol), \
         f"estimate {rg.batch_rel_error_estimate!r} vs {rr.batch_rel_error_estimate!r}"
     if rr.eps_target != 0.0:
         assert abs(rg.eps_target - rr.eps_target) <= 1e-10 * abs(rr.eps_target), f"eps_target {rg.eps_target} vs {rr.eps_target}"

@@ -10,7 +10,7 @@ from paper_2211_12487_b200 import (FormatError, IncrementStream, NumericError, T
                                    deserialize, load_ttc, mean_rre_per_increment, rpe, rre, save_ttc, serialize,
                                    tt_ice_bootstrap, tt_ice_star_update, tt_ice_update, write_batch)
 from paper_2211_12487_b200.streams import Stream
-from tests.parity_util import TOL, compare_trains, to_oracle
+from tests.parity_util import REF, TOL, compare_trains, to_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -82,7 +82,7 @@ def test_ttc1_image_byte_identical_and_resume(ctx, tmp_path):
     # resume: the next update from the checkpoint equals the update from the live train
     y = s.increment(4)
     ta, ra = tt_ice_star_update(t3, y, s.eps)
-    tr, rr = O.tt_ice_star_update(O.deserialize(img), y, s.eps)
+    tr, rr = REF.tt_ice_star_update(O.deserialize(img), y, s.eps)
     assert list(ra.ranks_after) == list(rr.ranks_after)
     compare_trains(ta, tr)
 
@@ -124,9 +124,9 @@ def test_stream_reader_feeds_the_update(ctx, tmp_path):
     for y in ys[1:]:
         th, _ = tt_ice_star_update(th, y, s.eps)
     assert serialize(tg) == serialize(th)
-    tr, _ = O.tt_ice_bootstrap(ys[0], s.eps)
+    tr, _ = REF.tt_ice_bootstrap(ys[0], s.eps)
     for y in ys[1:]:
-        tr, _ = O.tt_ice_star_update(tr, y, s.eps)
+        tr, _ = REF.tt_ice_star_update(tr, y, s.eps)
     compare_trains(tg, tr)
     assert TOL > 0
 
@@ -154,9 +154,9 @@ def test_cpp_dropin_stream_checkpoint_metrics(tmp_path):
         parts = ln.split()
         lines[(parts[0], parts[1] if len(parts) == 3 else "")] = float(parts[-1]) if parts[0] != "errors" else parts[1]
     tg = O.deserialize((tmp_path / "out.ttc").read_bytes())
-    tr, _ = O.tt_ice_bootstrap(ys[0], s.eps)
+    tr, _ = REF.tt_ice_bootstrap(ys[0], s.eps)
     for y in ys[1:]:
-        tr, _ = O.tt_ice_star_update(tr, y, s.eps)
+        tr, _ = REF.tt_ice_star_update(tr, y, s.eps)
     compare_trains(tg, tr)
     per_ref, _ = O.mean_rre_per_increment(tg, ys)
     for k, e in enumerate(per_ref):

@@ -14,7 +14,7 @@ from paper_2211_12487_b200 import (ConfigError, DimensionError, HeuristicConfig,
                                    TensorTrain, per_obs_errors, tt_ice_bootstrap, tt_ice_star_update,
                                    tt_ice_update, tt_ice_update_with_tolerances, tt_project, tt_reconstruct)
 from paper_2211_12487_b200.streams import Stream
-from tests.parity_util import (TOL, compare_reconstructions, compare_reports, compare_trains, subspace_distance,
+from tests.parity_util import (REF, TOL, compare_reconstructions, compare_reports, compare_trains, subspace_distance,
                                to_oracle)
 
 pytestmark = pytest.mark.gpu
@@ -24,7 +24,7 @@ def run_stream(ctx, stream, n_inc, algo="ice", cfg=None, check_every=1, eps=None
     eps = eps if eps is not None else stream.eps
     y0 = stream.increment(0)
     tg, rg = tt_ice_bootstrap(y0, eps, ctx=ctx)
-    tr, rr = O.tt_ice_bootstrap(y0, eps)
+    tr, rr = REF.tt_ice_bootstrap(y0, eps)
     compare_reports(rg, rr)
     compare_trains(tg, tr)
     ys = [(0, y0)]
@@ -33,11 +33,11 @@ def run_stream(ctx, stream, n_inc, algo="ice", cfg=None, check_every=1, eps=None
         ys.append((k, y))
         if algo == "ice":
             tg, rg = tt_ice_update(tg, y, eps)
-            tr, rr = O.tt_ice_update(tr, y, eps)
+            tr, rr = REF.tt_ice_update(tr, y, eps)
         else:
             ocfg = O.HeuristicConfig(**vars(cfg)) if cfg else O.HeuristicConfig()
             tg, rg = tt_ice_star_update(tg, y, eps, cfg)
-            tr, rr = O.tt_ice_star_update(tr, y, eps, ocfg)
+            tr, rr = REF.tt_ice_star_update(tr, y, eps, ocfg)
         compare_reports(rg, rr, star=(algo != "ice"))
         if k % check_every == 0 or k == n_inc - 1:
             compare_trains(tg, tr)
@@ -142,14 +142,14 @@ def test_appendix_b_rank_recovery(ctx):
     ys = [np.reshape(phi @ rng.standard_normal((5, 10)), modes + (10,), order="F") for _ in range(50)]
     for algo in ("ice", "star"):
         tg, rg = tt_ice_bootstrap(ys[0], eps, ctx=ctx)
-        tr, _ = O.tt_ice_bootstrap(ys[0], eps)
+        tr, _ = REF.tt_ice_bootstrap(ys[0], eps)
         for k in range(1, 50):
             if algo == "ice":
                 tg, rg = tt_ice_update(tg, ys[k], eps)
-                tr, rr = O.tt_ice_update(tr, ys[k], eps)
+                tr, rr = REF.tt_ice_update(tr, ys[k], eps)
             else:
                 tg, rg = tt_ice_star_update(tg, ys[k], eps)
-                tr, rr = O.tt_ice_star_update(tr, ys[k], eps)
+                tr, rr = REF.tt_ice_star_update(tr, ys[k], eps)
             assert rg.ranks_after == rr.ranks_after
         assert tg.ranks() == [1, 2, 3, 5, 1]
         gh = to_oracle(tg)
@@ -177,13 +177,13 @@ def test_in_span_increment_adds_no_directions(ctx):
 def test_zero_increment(ctx):
     s = Stream(0, seed=5)
     tg, _ = tt_ice_bootstrap(s.increment(0, batch=4), 0.1, ctx=ctx)
-    tr, _ = O.tt_ice_bootstrap(s.increment(0, batch=4), 0.1)
+    tr, _ = REF.tt_ice_bootstrap(s.increment(0, batch=4), 0.1)
     z = np.zeros((8, 8, 8, 8, 3))
     tg, rg = tt_ice_update(tg, z, 0.1)
-    tr, rr = O.tt_ice_update(tr, z, 0.1)
+    tr, rr = REF.tt_ice_update(tr, z, 0.1)
     compare_reports(rg, rr)
     tg, rg = tt_ice_star_update(tg, z, 0.1)
-    tr, rr = O.tt_ice_star_update(tr, z, 0.1)
+    tr, rr = REF.tt_ice_star_update(tr, z, 0.1)
     compare_reports(rg, rr)
     assert rg.obs_used == 0
 
@@ -192,7 +192,7 @@ def test_bootstrap_rank_zero_placeholder(ctx):
     """tt_svd.cpp:42-47: eps >= 1 -> every mode rank 0 -> unit-column placeholder."""
     y = Stream(0, seed=6).increment(0, batch=3)
     tg, rg = tt_ice_bootstrap(y, 1.0, ctx=ctx)
-    tr, rr = O.tt_ice_bootstrap(y, 1.0)
+    tr, rr = REF.tt_ice_bootstrap(y, 1.0)
     compare_reports(rg, rr)
     compare_trains(tg, tr)
 
@@ -201,19 +201,19 @@ def test_with_tolerances_and_project_reconstruct(ctx):
     s = Stream(3, seed=8, modes=(4,) * 5, batch=9, true_rank=4)
     y0 = s.increment(0)
     tg, _ = tt_ice_bootstrap(y0, 0.05, ctx=ctx)
-    tr, _ = O.tt_ice_bootstrap(y0, 0.05)
+    tr, _ = REF.tt_ice_bootstrap(y0, 0.05)
     y = s.increment(2)
     deltas = [0.3, 0.2, 0.1, 0.05, 0.01]
     tg, rg = tt_ice_update_with_tolerances(tg, y, deltas)
-    tr, rr = O.tt_ice_update_with_tolerances(tr, y, deltas)
+    tr, rr = REF.tt_ice_update_with_tolerances(tr, y, deltas)
     compare_reports(rg, rr)
     compare_trains(tg, tr)
     y2 = s.increment(3)
     cg = tt_project(tg, y2)
-    cr = O.tt_project(tr, y2)
+    cr = REF.tt_project(tr, y2)
     assert np.linalg.norm(cg - cr) <= TOL * np.linalg.norm(cr)
     eg = per_obs_errors(tg, y2)
-    er = O.per_obs_errors(tr, y2)
+    er = REF.per_obs_errors(tr, y2)
     assert np.max(np.abs(eg - er)) <= 1e-9
     rec = tt_reconstruct(tg, 3, 12)
     rec_r = O.tt_reconstruct(tr, 3, 12)
@@ -287,13 +287,13 @@ def test_errors_mirror_reference(ctx):
 def test_upload_roundtrip_and_update(ctx):
     """A host train (oracle) uploaded through the ABI updates like the oracle."""
     s = Stream(0, seed=13)
-    tr, _ = O.tt_ice_bootstrap(s.increment(0, batch=3), 0.1)
+    tr, _ = REF.tt_ice_bootstrap(s.increment(0, batch=3), 0.1)
     tg = TensorTrain.upload([c.data for c in tr.cores], tr.ortho_count, tr.batch_boundaries, ctx=ctx)
     for a, b in zip(tg.cores(), tr.cores):
         assert np.array_equal(a, b.data)
     y = s.increment(1, batch=3)
     tg, rg = tt_ice_star_update(tg, y, 0.1)
-    tr, rr = O.tt_ice_star_update(tr, y, 0.1)
+    tr, rr = REF.tt_ice_star_update(tr, y, 0.1)
     compare_reports(rg, rr, star=True)
     compare_trains(tg, tr)
 
@@ -318,7 +318,7 @@ def test_project_fixed_cores_high_rank(ctx, R):
     tr = O.TensorTrain([O.TTCore(np.asfortranarray(c)) for c in cores], len(modes), [1])
     y = np.asfortranarray(rng.standard_normal(modes + (b,)))
     cg = tt_project(tg, y)
-    cr = O.tt_project(tr, y)
+    cr = REF.tt_project(tr, y)
     assert cg.shape == cr.shape
     assert np.linalg.norm(cg - cr) <= TOL * np.linalg.norm(cr)
 
@@ -333,7 +333,7 @@ def test_bootstrap_tall_unfolding_full_solver(ctx):
     v = rng.standard_normal((40, 300)) * np.logspace(0, -2, 40)[:, None]
     y = np.asfortranarray(u @ v + 1e-4 * rng.standard_normal((2048, 300)))
     tg, rg = tt_ice_bootstrap(y, 0.05, ctx=ctx)
-    tr, rr = O.tt_ice_bootstrap(y, 0.05)
+    tr, rr = REF.tt_ice_bootstrap(y, 0.05)
     compare_reports(rg, rr)
     compare_trains(tg, tr)
     assert tg.ranks()[1] > 8
@@ -352,10 +352,10 @@ def test_update_large_append_guard_path(ctx):
     y1 = np.asfortranarray(basis[:, 20:190] @ (rng.standard_normal((170, 300)) * spec[20:190]) +
                            1e-6 * rng.standard_normal((2048, 300)))
     tg, rg = tt_ice_bootstrap(y0, 1e-3, ctx=ctx)
-    tr, rr = O.tt_ice_bootstrap(y0, 1e-3)
+    tr, rr = REF.tt_ice_bootstrap(y0, 1e-3)
     compare_reports(rg, rr)
     tg, rg = tt_ice_update(tg, y1, 1e-3)
-    tr, rr = O.tt_ice_update(tr, y1, 1e-3)
+    tr, rr = REF.tt_ice_update(tr, y1, 1e-3)
     compare_reports(rg, rr)
     compare_trains(tg, tr)
     r = tg.ranks()[1]
