@@ -73,6 +73,13 @@ typedef struct ttg_report {
   double seconds; /* wall time (CUDA events) */
   int32_t guard_reorthogonalised; /* number of modes whose 1e-10 Gram guard fired */
   int32_t modes_updated;          /* modes whose basis grew */
+  /* numerics of the truncated SVDs (truncated_svd.cpp:29-94 is one backward-stable
+     BDCSVD; here a Gram eigen-solve with two fallbacks): */
+  int32_t accurate_modes;         /* modes solved on the unsquared factor (TSQR + Jacobi) */
+  int32_t raw_fallbacks;          /* modes whose raw-Gram result was recomputed from the explicit residual */
+  int32_t gram_only_unstable;     /* modes where the accuracy test asked for the factor path and none
+                                     applied (the result rests on the squared-condition Gram); 0 means
+                                     every decision was taken at full resolution */
 } ttg_report;
 
 /* Mirrors HeuristicConfig (tt_ice_star.hpp:14-20). */

@@ -31,6 +31,9 @@ class Report(ctypes.Structure):
         ("seconds", ctypes.c_double),
         ("guard_reorthogonalised", ctypes.c_int32),
         ("modes_updated", ctypes.c_int32),
+        ("accurate_modes", ctypes.c_int32),
+        ("raw_fallbacks", ctypes.c_int32),
+        ("gram_only_unstable", ctypes.c_int32),
     ]
 
 

@@ -17,8 +17,6 @@
 // solve on identical bytes.
 #include <cudaTypedefs.h>
 #include <nccl.h>
-#include <cublas_v2.h>
-#include <cusolverDn.h>
 
 #include <fcntl.h>
 #include <unistd.h>
@@ -42,6 +40,7 @@
 #include "ttg_misc.cuh"
 #include "ttg_syev.cuh"
 #include "ttg_io.cuh"
+#include "ttg_gemm.cuh"
 
 namespace {
 
@@ -142,9 +141,7 @@ struct ttg_ctx {
   } pf[2];
   cudaStream_t copy = nullptr;
   int pf_next = 0, pf_inuse = -1;
-  cublasHandle_t blas = nullptr;  // plain large GEMMs only (gemm() below); created on first use
-  cusolverDnHandle_t solver = nullptr;  // full eigen-decomposition of large a x a Grams (eig()); on first use
-  DevBuf sv_work, sv_evals, sv_info;
+  DevBuf trd;  // k_sytrd_grid panels, p, [d | e | tau], barrier
   std::string err;
   int64_t launches = 0;
   int num_sms = 148;
@@ -152,7 +149,7 @@ struct ttg_ctx {
   // workspaces (grow-only)
   DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, UTt, Uf, Upad, scratch, eigres, on2, sumsq_part,
       scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2], tsq, psif, wcomb, psi[2],
-      spsi[2], scoeffs, matbuf, tmp, Craw, small[4], gcount;
+      spsi[2], scoeffs, matbuf, tmp, Craw, small[4], gcount, gemm_ws, tallR, tallRg, tallXt, UR2;
   std::vector<DevBuf> scur;       // TT-ICE* stats-chain intermediates (reused by the sweep)
   std::vector<bool> stat_has;
   ttg::EigResult* h_eig = nullptr;
@@ -182,6 +179,7 @@ struct ttg_ctx {
   int cur_idx = -1;
   cudaEvent_t cur_e0 = nullptr;
   int64_t h2d = 0, d2h = 0;
+  bool shard_check = false;  // shard sizes ride on the next |Y|^2 all-reduce (global_obs)
 };
 
 struct ttg_tt {
@@ -407,13 +405,21 @@ void obs_norms(ttg_ctx* c, const double* Y, long long S, int b) {
   launch_k(c, ttg::k_sumsq_finalize, 1, 256, 0, c->sumsq_part.as<double>(), nchunk, b,
                                                    c->on2.as<double>(), c->scal.as<double>());
   post_launch(c);
-  allreduce_sum(c, c->scal.as<double>(), 1);
+  allreduce_sum(c, c->scal.as<double>(), 3);  // |Y|^2 and the shard-size check (global_obs)
 }
 
+// |Y|^2 (c->scal[0], all-reduced) to the host; on a sharded context also the
+// all-reduced shard sizes (scal[1..2], see global_obs), checked here.
 double read_scalar(ttg_ctx* c, const double* d) {
-  c->d2h += sizeof(double);
-  CK(cudaMemcpyAsync(c->h_scal, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  const int n = c->coll ? 3 : 1;
+  c->d2h += sizeof(double) * n;
+  CK(cudaMemcpyAsync(c->h_scal, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (c->shard_check) {
+    c->shard_check = false;
+    const double s = c->h_scal[1], s2 = c->h_scal[2];
+    if (s * s != s2 * c->world) fail(TTG_E_DIMENSION, "multi-GPU update needs the same batch shard size on every rank");
+  }
   return c->h_scal[0];
 }
 
@@ -430,43 +436,49 @@ void make_frags(ttg_ctx* c, const double* U, int a, int r, int ld, bool need_ut,
 }
 
 // ---- generic GEMM (any size) ------------------------------------------------
-// (defined below; forward declaration for the raw-Gram path)
-// Generic GEMM C = alpha op(A) op(B) + beta C (column-major).  Small shapes
-// (every a x a / Psi combination of the sweep) run the fixed-order k_gemm;
-// large plain GEMMs (the high-rank projections, r > 34, of tt_project and
-// wide unfoldings: >= kBlasFlops) go to cuBLAS DGEMM on the library stream.
-constexpr double kBlasFlops = 1e8;
+// C = alpha op(A) op(B) + beta C (column-major) on the DMMA GEMM (ttg_gemm.cuh):
+// every plain GEMM of the sweep, small or large.  Few output tiles with a long
+// k (R^T R, append Grams) split k over grid z with a fixed-order reduction.
 template <bool TA, bool TB>
 void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
           long long m, long long n, long long k, double alpha, double beta) {
   if (m == 0 || n == 0) return;
-  if (2.0 * m * n * k >= kBlasFlops && m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31) && !std::getenv("TTG_NO_BLAS")) {
-    if (!c->blas) {
-      if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasCreate failed");
-    }
-    if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasSetStream failed");
-    prof_begin(c, "cublas_dgemm", 8.0 * (m * k + k * n + m * n), 2.0 * m * n * k);
-    const cublasStatus_t st = cublasDgemm(c->blas, TA ? CUBLAS_OP_T : CUBLAS_OP_N, TB ? CUBLAS_OP_T : CUBLAS_OP_N,
-                                          (int)m, (int)n, (int)k, &alpha, A, (int)lda, B, (int)ldb, &beta, C, (int)ldc);
-    if (st != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasDgemm failed (status " + std::to_string((int)st) + ")");
-    CK(cudaGetLastError());
-    if (c->profiling && c->cur_idx >= 0) {
-      cudaEvent_t e1 = get_event(c);
-      CK(cudaEventRecord(e1, c->stream));
-      c->pending.push_back({c->cur_idx, c->cur_e0, e1});
-    }
-    c->cur_idx = -1;
-    return;
+  ttg::DgemmArgs a{A, lda, B, ldb, C, ldc, m, n, k, alpha, beta, 0, nullptr};
+  const bool big = m > 64;
+  const int bm = big ? 128 : 64;
+  const long long tiles_m = (m + bm - 1) / bm, tiles_n = (n + ttg::kGemmBN - 1) / ttg::kGemmBN;
+  if (tiles_m > 65535) fail(TTG_E_RESOURCE, "gemm: m too large");
+  const long long tiles = tiles_m * tiles_n;
+  const long long ksteps = (k + ttg::kGemmBK - 1) / ttg::kGemmBK;
+  int nz = 1;
+  if (tiles < 2LL * c->num_sms && ksteps >= 16) {
+    nz = (int)std::min<long long>({(2LL * c->num_sms + tiles - 1) / tiles, ksteps / 8, 64});
+    nz = std::max(nz, 1);
   }
-  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
-  if (grid.y > 65535) fail(TTG_E_RESOURCE, "generic gemm: m too large");
-  prof_begin(c, "k_gemm", 8.0 * (m * k + k * n + m * n), 2.0 * m * n * k);
-  launch_k(c, ttg::k_gemm<TA, TB>, grid, dim3(32, 32), 0, A, lda, B, ldb, C, ldc, m, n, k, alpha, beta);
+  a.kchunk = ((ksteps + nz - 1) / nz) * ttg::kGemmBK;
+  nz = (int)std::max<long long>(1, (k + a.kchunk - 1) / std::max<long long>(a.kchunk, 1));
+  if (k == 0) a.kchunk = ttg::kGemmBK;
+  if (nz > 1) {
+    c->gemm_ws.ensure(sizeof(double) * (size_t)nz * m * n);
+    a.ws = c->gemm_ws.as<double>();
+  }
+  auto kern = big ? ttg::k_dgemm<TA, TB, 128> : ttg::k_dgemm<TA, TB, 64>;
+  const size_t smem = big ? ttg::dgemm_smem<128>() : ttg::dgemm_smem<64>();
+  kernel_occupancy((const void*)kern, kern, bm * 2, smem);
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_dgemm[%c%c]", TA ? 'T' : 'N', TB ? 'T' : 'N');
+  prof_begin(c, nm, 8.0 * (m * k + k * n + m * n), 2.0 * m * n * k);
+  launch_k(c, kern, dim3((unsigned)tiles_n, (unsigned)tiles_m, (unsigned)nz), bm * 2, smem, a);
   post_launch(c);
+  if (nz > 1) {
+    prof_begin(c, "k_dgemm_reduce", 8.0 * (nz + 2.0) * m * n, (double)nz * m * n);
+    launch_k(c, ttg::k_dgemm_reduce, grid_for(m * n, 256, 4 * c->num_sms), 256, 0, (const double*)a.ws, nz, m, n, C,
+             ldc, alpha, beta);
+    post_launch(c);
+  }
 }
 
 constexpr int kFastMax = 128;  // a8 / r8 limit of the fused DMMA tiles
-constexpr int kSolverLarge = 512;  // a from which a failed fast eigen-solve goes to cuSOLVER syevd
 constexpr int kFastSkip = 2048;    // a from which the block subspace attempt (G in global memory) is skipped
 
 // ---- residual Gram -----------------------------------------------------------
@@ -1092,58 +1104,58 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
       }
     }
     fast_done = done;
-    if (!done && a >= kSolverLarge && !std::getenv("TTG_NO_CUSOLVER")) {
-      // large a: the one-CTA tridiagonalisation is latency-bound (a = 2488:
-      // 2 s); cuSOLVER syevd on a copy of G, then the rank rule / sign rule
-      // selection (k_syev_select)
-      if (!c->solver) {
-        if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(TTG_E_CUDA, "cusolverDnCreate failed");
-      }
-      if (cusolverDnSetStream(c->solver, c->stream) != CUSOLVER_STATUS_SUCCESS) fail(TTG_E_CUDA, "cusolverDnSetStream failed");
-      c->W.ensure(sizeof(double) * (size_t)a * a);
-      c->sv_evals.ensure(sizeof(double) * a);
-      c->sv_info.ensure(sizeof(int));
-      double* Q = c->W.as<double>();
-      CK(cudaMemcpyAsync(Q, c->G.p, sizeof(double) * (size_t)a * a, cudaMemcpyDeviceToDevice, c->stream));
-      int lwork = 0;
-      if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, a, Q, a,
-                                      c->sv_evals.as<double>(), &lwork) != CUSOLVER_STATUS_SUCCESS)
-        fail(TTG_E_CUDA, "cusolverDnDsyevd_bufferSize failed");
-      c->sv_work.ensure(sizeof(double) * (size_t)std::max(lwork, 1));
-      char nm[64];
-      std::snprintf(nm, sizeof nm, "cusolver_dsyevd[a=%d]", a);
-      prof_begin(c, nm, 16.0 * a * a, 4.0 * a * a * a);
-      if (cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, a, Q, a, c->sv_evals.as<double>(),
-                           c->sv_work.as<double>(), lwork, c->sv_info.as<int>()) != CUSOLVER_STATUS_SUCCESS)
-        fail(TTG_E_CUDA, "cusolverDnDsyevd failed");
-      CK(cudaGetLastError());
-      if (c->profiling && c->cur_idx >= 0) {
-        cudaEvent_t e1 = get_event(c);
-        CK(cudaEventRecord(e1, c->stream));
-        c->pending.push_back({c->cur_idx, c->cur_e0, e1});
-      }
-      c->cur_idx = -1;
-      prof_begin(c, "k_syev_select", 8.0 * a * a, 2.0 * a);
-      launch_k(c, ttg::k_syev_select, 1, 1024, 0, (const double*)c->G.as<double>(), a,
-               (const double*)c->sv_evals.as<double>(), (const double*)Q, (const int*)c->sv_info.as<int>(), args);
-      post_launch(c);
-      done = true;
-    }
     if (!done) {
       size_t vec = sizeof(double) * (size_t)7 * a;
       size_t smem = sizeof(double) * (size_t)a * a + vec;
       if (smem <= dyn_smem_cap((const void*)ttg::k_syev)) {
         args.in_smem = 1;
       } else {
-        args.in_smem = 0;
+        // G does not fit one CTA: tridiagonalise on the multi-CTA kernel
+        // (k_sytrd_grid, cooperative), then k_syev's eigenvalue / eigenvector
+        // phases on the result (reflectors in W, tri = [d | e | tau])
         c->W.ensure(sizeof(double) * (size_t)a * a);
+        CK(cudaMemcpyAsync(c->W.p, c->G.p, sizeof(double) * (size_t)a * a, cudaMemcpyDeviceToDevice, c->stream));
+        c->trd.ensure(sizeof(double) * ((size_t)2 * ttg::kTrdPanel * a + 4 * (size_t)a) + 64);
+        ttg::TrdArgs ta{};
+        ta.A = c->W.as<double>();
+        ta.a = a;
+        ta.V = c->trd.as<double>();
+        ta.W = ta.V + (size_t)ttg::kTrdPanel * a;
+        ta.pbuf = ta.W + (size_t)ttg::kTrdPanel * a;
+        ta.tri = ta.pbuf + a;
+        ta.bar = reinterpret_cast<unsigned*>(ta.tri + 3 * (size_t)a);
+        CK(cudaMemsetAsync(ta.bar, 0, 2 * sizeof(unsigned), c->stream));
+        const size_t tsm = sizeof(double) * 5 * (size_t)a;
+        const int occ = kernel_occupancy((const void*)ttg::k_sytrd_grid, ttg::k_sytrd_grid, ttg::kTrdThreads, tsm);
+        if (occ < 1) fail(TTG_E_RESOURCE, "tridiagonalisation kernel does not fit on an SM");
+        const int want = std::getenv("TTG_TRD_CTAS") ? std::atoi(std::getenv("TTG_TRD_CTAS")) : 32;
+        const int nblk = std::max(1, std::min({want, c->num_sms * occ, (a + 31) / 32}));
+        char nm[64];
+        std::snprintf(nm, sizeof nm, "k_sytrd_grid[a=%d]", a);
+        prof_begin(c, nm, 24.0 * a * a, 4.0 / 3.0 * a * a * a);
+        {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3((unsigned)nblk);
+          cfg.blockDim = dim3(ttg::kTrdThreads);
+          cfg.dynamicSmemBytes = tsm;
+          cfg.stream = c->stream;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeCooperative;  // co-residency of the grid barrier
+          at[0].val.cooperative = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          CK(cudaLaunchKernelEx(&cfg, ttg::k_sytrd_grid, ta));
+        }
+        post_launch(c);
+        args.in_smem = 0;
         args.Ag = c->W.as<double>();
+        args.tri = ta.tri;
         smem = vec;
       }
       kernel_occupancy((const void*)ttg::k_syev, ttg::k_syev, ttg::kSyevThreads, smem);
       char nm[64];
       std::snprintf(nm, sizeof nm, "k_syev[a=%d]", a);
-      prof_begin(c, nm, 16.0 * a * a, 4.0 / 3.0 * a * a * a);
+      prof_begin(c, nm, 16.0 * a * a, args.tri ? 2.0 * a * a : 4.0 / 3.0 * a * a * a);
       launch_k(c, ttg::k_syev, 1, ttg::kSyevThreads, smem, args);
       post_launch(c);
     }
@@ -1258,24 +1270,17 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
   ttg::AppendArgs args{Upad, c->UR.as<double>(), a, r_old, r_R, out, c->scratch.as<double>(),
                        c->eigres.as<EigResult>(), c->gcount.as<int>(), 0};
   const int rn = r_old + r_R;
-  if ((double)a * rn * rn >= 5e7 && !std::getenv("TTG_NO_BLAS")) {
-    // large block: [U_pad U_R] by copies, its Gram C^T C by cuBLAS DSYRK, the
-    // deviation by a grid reduction; k_append then only runs the (rare)
-    // Householder correction when the guard fires
+  if ((double)a * rn * rn >= 5e7) {
+    // large block: [U_pad U_R] by copies, its Gram C^T C on the DMMA GEMM
+    // (split-k, fixed order), the deviation by a grid reduction; k_append then
+    // only runs the (rare) Householder correction when the guard fires
     if (Upad != out && r_old > 0)
       CK(cudaMemcpyAsync(out, Upad, sizeof(double) * (size_t)a * r_old, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(out + (size_t)a * r_old, c->UR.p, sizeof(double) * (size_t)a * r_R, cudaMemcpyDeviceToDevice,
                        c->stream));
     c->small[1].ensure(sizeof(double) * (size_t)rn * rn);
     double* S = c->small[1].as<double>();
-    if (!c->blas) {
-      if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasCreate failed");
-    }
-    if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) fail(TTG_E_CUDA, "cublasSetStream failed");
-    const double one = 1.0, zero = 0.0;
-    if (cublasDsyrk(c->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, rn, a, &one, out, a, &zero, S, rn) !=
-        CUBLAS_STATUS_SUCCESS)
-      fail(TTG_E_CUDA, "cublasDsyrk failed");
+    gemm<true, false>(c, out, a, out, a, S, rn, rn, rn, a, 1.0, 0.0);
     CK(cudaMemsetAsync(&c->eigres.as<EigResult>()->dev, 0, sizeof(double), c->stream));
     prof_begin(c, "k_gram_dev", 8.0 * rn * rn, 0.0);
     launch_k(c, ttg::k_gram_dev, grid_for((long long)rn * rn, 256, 2 * c->num_sms), 256, 0, (const double*)S, rn,
@@ -1354,27 +1359,27 @@ bool project_ws16(ttg_ctx* c, const double* X, int a, long long L, const double*
 // rows by DMMA plus a DFMA tail of 1-2 rows when r = 8 NB + {1, 2}.  Tall
 // sources (a > 64) stream in 64-row stages with the accumulators held in
 // registers.  False when the operand does not qualify.
+// DFMA tail rows of k_project_kc: r = 8 NB + T with T <= kKcMaxTail costs
+// NB + T/8 n-blocks of FP64 work instead of NB + 1 (r = 19..20 no longer pay
+// for 24 rows).
+constexpr int kKcMaxTail = 4;
 template <int NCW, int NB, int T>
 void* kc_kernel() {
   return (void*)ttg::k_project_kc<NCW, NB, T>;
 }
+template <int NCW, int NB, int T>
+void* kc_pick_nb(int nb, int t) {
+  if constexpr (NB > 4) {
+    return nullptr;
+  } else if constexpr (T > kKcMaxTail) {
+    return kc_pick_nb<NCW, NB + 1, 0>(nb, t);
+  } else {
+    return (nb == NB && t == T) ? kc_kernel<NCW, NB, T>() : kc_pick_nb<NCW, NB, T + 1>(nb, t);
+  }
+}
 template <int NCW>
 void* kc_pick_t(int NB, int T) {
-  switch (NB * 3 + T) {
-    case 3: return kc_kernel<NCW, 1, 0>();
-    case 4: return kc_kernel<NCW, 1, 1>();
-    case 5: return kc_kernel<NCW, 1, 2>();
-    case 6: return kc_kernel<NCW, 2, 0>();
-    case 7: return kc_kernel<NCW, 2, 1>();
-    case 8: return kc_kernel<NCW, 2, 2>();
-    case 9: return kc_kernel<NCW, 3, 0>();
-    case 10: return kc_kernel<NCW, 3, 1>();
-    case 11: return kc_kernel<NCW, 3, 2>();
-    case 12: return kc_kernel<NCW, 4, 0>();
-    case 13: return kc_kernel<NCW, 4, 1>();
-    case 14: return kc_kernel<NCW, 4, 2>();
-  }
-  return nullptr;
+  return kc_pick_nb<NCW, 1, 0>(NB, T);
 }
 void* kc_pick(int ncw, int NB, int T) { return ncw == 8 ? kc_pick_t<8>(NB, T) : kc_pick_t<4>(NB, T); }
 
@@ -1391,7 +1396,8 @@ bool kc_plan(const ttg_ctx* c, int a, int r, KcPlan& P) {
   if (std::getenv("TTG_NO_KC") || (a & 1) || r > 34 || r < 1) return false;
   P.NB = (r + 7) / 8;
   P.T = 0;
-  if (r > 8 && (r % 8 == 1 || r % 8 == 2) && !std::getenv("TTG_NO_TAIL")) {
+  const int max_tail = std::getenv("TTG_KC_TAIL") ? std::atoi(std::getenv("TTG_KC_TAIL")) : kKcMaxTail;
+  if (r > 8 && r % 8 >= 1 && r % 8 <= std::min(max_tail, kKcMaxTail) && !std::getenv("TTG_NO_TAIL")) {
     P.NB = r / 8;
     P.T = r % 8;
   }
@@ -1615,6 +1621,79 @@ const double* materialise(ttg_ctx* c, const Src& s, int64_t n, DevBuf& dst) {
   return dst.as<double>();
 }
 
+// Collectives off while an already-gathered operand is processed (RAII).
+struct NoColl {
+  ttg_ctx* c;
+  bool prev;
+  explicit NoColl(ttg_ctx* cc) : c(cc), prev(cc->coll) { c->coll = false; }
+  ~NoColl() { c->coll = prev; }
+};
+
+// Tall unfolding a > 2 L (the reference's QR branch, truncated_svd.cpp:51-59):
+// R = cur - U (U^T cur) explicitly (a x L, selection applied; all-gathered
+// across ranks, L is small), the eigen-problem on the L x L side -- R^T R, or
+// the TSQR factor of R^T when the Gram cannot resolve the decision -- and
+// u_j = R v_j / |R v_j| with the sign rule (k_tall_u) into c->UR.  a can be
+// thousands (configs[2] modes 6-7: a ~ 3000, L = 96 / 32) at the cost of an
+// L x L eigen-solve; the accurate path needs L <= 128, not a.
+EigResult tall_eig(ttg_ctx* c, const Src& src, int64_t n_i, const double* U, int r_old, const uint8_t* sel,
+                   long long cpo, long long kmax, const double* dsrc, double dmult, int& accurate, int& unstable) {
+  const int64_t a = src.r * n_i;
+  const long long L = src.Ls / n_i;
+  const double* X = materialise(c, src, n_i, c->matbuf);
+  c->tallR.ensure(sizeof(double) * (size_t)std::max<long long>(a * L, 1));
+  double* R = c->tallR.as<double>();
+  CK(cudaMemcpyAsync(R, X, sizeof(double) * (size_t)(a * L), cudaMemcpyDeviceToDevice, c->stream));
+  if (r_old > 0) {
+    c->W.ensure(sizeof(double) * (size_t)std::max<long long>((long long)r_old * L, 1));
+    double* P = c->W.as<double>();
+    gemm<true, false>(c, U, a, X, a, P, r_old, r_old, L, a, 1.0, 0.0);   // P = U^T X
+    gemm<false, false>(c, U, a, P, r_old, R, a, a, L, r_old, -1.0, 1.0);  // R = X - U P
+  }
+  if (sel) {
+    prof_begin(c, "k_mask_cols", 16.0 * a * L, 0.0);
+    launch_k(c, ttg::k_mask_cols, grid_for((long long)a * L, 256, 4096), 256, 0, R, (int)a, L, sel, cpo);
+    post_launch(c);
+  }
+  const long long Lg = L * c->world;
+  double* Rg = R;
+  if (c->coll) {
+    c->tallRg.ensure(sizeof(double) * (size_t)(a * Lg));
+    Rg = c->tallRg.as<double>();
+    allgather(c, R, Rg, (size_t)(a * L));
+  }
+  NoColl nc(c);  // every rank now holds the same Rg: local, identical solves
+  c->G.ensure(sizeof(double) * (size_t)(Lg * Lg));
+  gemm<true, false>(c, Rg, a, Rg, a, c->G.as<double>(), Lg, Lg, Lg, a, 1.0, 0.0);  // R^T R (exactly symmetric)
+  EigResult er = eig(c, (int)Lg, kmax, dsrc, dmult);
+  if (needs_accurate(er)) {
+    if (accurate_supported((int)Lg, 0)) {
+      c->tallXt.ensure(sizeof(double) * (size_t)(a * Lg));
+      double* Xt = c->tallXt.as<double>();
+      prof_begin(c, "k_transpose", 16.0 * a * Lg, 0.0);
+      launch_k(c, ttg::k_transpose, dim3((unsigned)((Lg + 31) / 32), (unsigned)((a + 31) / 32)), dim3(32, 8), 0,
+               (const double*)Rg, (int)a, Lg, Xt);
+      post_launch(c);
+      er = accurate_eig(c, Xt, (int)Lg, a, nullptr, 0, (int)Lg, nullptr, 1, kmax, dsrc, dmult);
+      accurate++;
+    } else {
+      unstable++;
+      if (std::getenv("TTG_STRICT"))
+        fail(TTG_E_NUMERIC, "svd_trunc: threshold below the Gram eigen-solve's resolution on a tall " +
+                                std::to_string(a) + " x " + std::to_string(Lg) + " residual");
+    }
+  }
+  if (er.rank > 0) {
+    c->UR2.ensure(sizeof(double) * (size_t)(a * er.rank));
+    prof_begin(c, "k_tall_u", 8.0 * (a * Lg + a * er.rank), 2.0 * a * Lg * er.rank);
+    launch_k(c, ttg::k_tall_u, (unsigned)er.rank, 256, 0, (const double*)Rg, (int)a, (int)Lg,
+             (const double*)c->UR.as<double>(), c->UR2.as<double>());
+    post_launch(c);
+    std::swap(c->UR, c->UR2);
+  }
+  return er;
+}
+
 // ---- helpers -----------------------------------------------------------------
 int64_t prod(const std::vector<int64_t>& v) {
   int64_t p = 1;
@@ -1655,19 +1734,19 @@ void check_train_vs_y(const ttg_tt* tt, const int64_t* shape, int ndim, bool sta
     if (shape[i] != tt->modes[i]) fail(TTG_E_DIMENSION, "increment spatial shape does not match the train");
 }
 
-// make sure the observation counts are equal on all ranks (sharded batch)
+// Sharded batch: every rank must carry the same number of observations.  The
+// check rides on the first exchange of the update (the |Y|^2 all-reduce, which
+// carries b and b^2 in scal[1..2]) and is evaluated where |Y|^2 reaches the
+// host (read_scalar), before anything is mutated: no extra all-reduce or host
+// synchronisation per call.
 int64_t global_obs(ttg_ctx* c, int64_t b) {
   if (!c->coll) return b;
   c->scal.ensure(sizeof(double) * 16);
-  double* d = c->scal.as<double>() + 8;
-  double h[2] = {(double)b, (double)b * (double)b};
-  CK(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
-  allreduce_sum(c, d, 2);
-  CK(cudaMemcpyAsync(c->h_scal, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  double s = c->h_scal[0], s2 = c->h_scal[1];
-  if (s * s != s2 * c->world) fail(TTG_E_DIMENSION, "multi-GPU update needs the same batch shard size on every rank");
-  return (int64_t)s;
+  c->h_scal[14] = (double)b;
+  c->h_scal[15] = (double)b * (double)b;
+  CK(cudaMemcpyAsync(c->scal.as<double>() + 1, c->h_scal + 14, 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  c->shard_check = true;
+  return b * c->world;
 }
 
 // coefficients (r x b_local, compact) -> last core columns [n_obs, n_obs + b_global)
@@ -1752,6 +1831,8 @@ struct SweepOut {
   int modes_updated = 0;
   int accurate_modes = 0;
   int raw_fallbacks = 0;
+  int gram_only_unstable = 0;
+  int tall_modes = 0;
   bool cores_changed = false;
   const double* coeffs = nullptr;  // r_d x b_local (compact)
   int r_d = 0;
@@ -1792,7 +1873,7 @@ void norms_finish(ttg_ctx* c, Norms& nm, int64_t rows, bool produced) {
     prof_begin(c, "k_sum_vec", 8.0 * nm.b, 0.0);
     launch_k(c, ttg::k_sum_vec, 1, 256, 0, c->on2.as<double>(), (int)nm.b, c->scal.as<double>());
     post_launch(c);
-    allreduce_sum(c, c->scal.as<double>(), 1);
+    allreduce_sum(c, c->scal.as<double>(), 3);  // |Y|^2 and the shard-size check (global_obs)
   }
   nm.pending = false;
 }
@@ -1843,7 +1924,21 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       const bool big = o.deltas ? (dmult > 1e-12 * o.y_norm) : (dmult > 1e-12);
       run_svd = !big;
     }
-    if (run_svd) {
+    const long long Lg = L * c->world;
+    const bool tall = run_svd && a > kFastMax && (double)a > 2.0 * (double)Lg && !std::getenv("TTG_NO_TALL");
+    if (tall) {
+      if (nm.pending && src.S == nm.Y) norms_finish(c, nm, 0, false);
+      if (!norm_checked && !nm.pending) {
+        check_finite_norm(read_scalar(c, c->scal.as<double>()));
+        norm_checked = true;
+      }
+      const long long kmax = o.star ? o.n_sel_global * cpo : Lg;
+      EigResult er = tall_eig(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, o.star ? o.sel : nullptr, cpo,
+                              kmax, dsrc, dmult, out.accurate_modes, out.gram_only_unstable);
+      r_R = er.rank;
+      out.discarded_sq += er.tail_sq;
+      out.tall_modes++;
+    } else if (run_svd) {
       const uint8_t* sel = o.star ? o.sel : nullptr;
       const int64_t rows = src.Psi ? src.As * n_i : a;
       double* tsq = norms_tiles_for(c, nm, src.S, rows, L);
@@ -1872,11 +1967,18 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
           out.raw_fallbacks++;
         }
       }
-      if (needs_accurate(er) && accurate_supported((int)a, (int)r_old)) {
-        const double* X = materialise(c, src, n_i, c->matbuf);
-        er = accurate_eig(c, X, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, kmax, dsrc,
-                          dmult);
-        out.accurate_modes++;
+      if (needs_accurate(er)) {
+        if (accurate_supported((int)a, (int)r_old)) {
+          const double* X = materialise(c, src, n_i, c->matbuf);
+          er = accurate_eig(c, X, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, kmax, dsrc,
+                            dmult);
+          out.accurate_modes++;
+        } else {
+          out.gram_only_unstable++;  // surfaced in ttg_report; TTG_STRICT turns it into a NumericError
+          if (std::getenv("TTG_STRICT"))
+            fail(TTG_E_NUMERIC, "svd_trunc: threshold below the Gram eigen-solve's resolution on a " + std::to_string(a) +
+                                    "-row unfolding and no factor path applies");
+        }
       }
       r_R = er.rank;
       out.discarded_sq += er.tail_sq;
@@ -2174,6 +2276,12 @@ void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double
   allreduce_sum(c, c->stats.as<double>(), 9);
 }
 
+void fill_report_numerics(ttg_report* rep, const SweepOut& so) {
+  rep->accurate_modes = so.accurate_modes;
+  rep->raw_fallbacks = so.raw_fallbacks;
+  rep->gram_only_unstable = so.gram_only_unstable;
+}
+
 struct Timer {
   ttg_ctx* c;
   explicit Timer(ttg_ctx* cc) : c(cc) { CK(cudaEventRecord(c->ev0, c->stream)); }
@@ -2235,6 +2343,7 @@ void do_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const int64_t
   rep->batch_rel_error_estimate = (y_norm == 0.0) ? 0.0 : std::sqrt(so.discarded_sq) / y_norm;
   rep->guard_reorthogonalised = *guards_slot(c);  // fetched by the sweep, valid after read_scalar's sync
   rep->modes_updated = so.modes_updated;
+  fill_report_numerics(rep, so);
   rep->seconds = tm.stop();
 }
 
@@ -2333,6 +2442,7 @@ void do_star_update(ttg_ctx* c, ttg_tt* tt, const double* y, int where, const in
     coeffs = so.coeffs;
     r_d = so.r_d;
     rep->modes_updated = so.modes_updated;
+    fill_report_numerics(rep, so);
   }
   trace("star:sweep done");
   append_last_core(c, tt, coeffs, r_d, b);
@@ -2392,6 +2502,7 @@ ttg_tt* do_bootstrap(ttg_ctx* c, const double* y, int where, const int64_t* shap
     rep->n_ranks = d + 2;
     fill_report_ranks(rep->ranks_after, tt);
     for (int i = 0; i <= d + 1; ++i) rep->ranks_before[i] = 1;
+    fill_report_numerics(rep, so);
     rep->eps_target = eps * y_norm / std::sqrt((double)(ndim - 1));
     const double* src = c->coll ? c->coeffs_all.as<double>() : so.coeffs;
     const double kept_sq = sumsq_device(c, src, (long long)so.r_d * bg);  // tt_norm (tensor_train.cpp:383-386)
@@ -2492,7 +2603,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
         (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
         (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
-        (const void*)ttg::k_gram_reduce, (const void*)ttg::k_syev, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
+        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,
@@ -2500,18 +2611,22 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_syrk_ws16<6, 1>, (const void*)ttg::k_syrk_ws16<10, 1>, (const void*)ttg::k_syrk_ws16<5, 3>,
         (const void*)ttg::k_syrk_ws16<7, 3>, (const void*)ttg::k_syrk_ws16<14, 2>, (const void*)ttg::k_syrk_ws16<12, 3>, (const void*)ttg::k_coef_stats,
         (const void*)ttg::k_star_local, (const void*)ttg::k_star_mask, (const void*)ttg::k_mask_cols,
-        (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_gemm<false, false>,
-        (const void*)ttg::k_gemm<true, false>, (const void*)ttg::k_gemm<false, true>, (const void*)ttg::k_syrk<1>,
+        (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_dgemm<false, false, 64>,
+        (const void*)ttg::k_dgemm<true, false, 64>, (const void*)ttg::k_dgemm<false, true, 64>,
+        (const void*)ttg::k_dgemm<true, true, 64>, (const void*)ttg::k_dgemm<false, false, 128>,
+        (const void*)ttg::k_dgemm<true, false, 128>, (const void*)ttg::k_dgemm<false, true, 128>,
+        (const void*)ttg::k_dgemm<true, true, 128>, (const void*)ttg::k_dgemm_reduce, (const void*)ttg::k_transpose, (const void*)ttg::k_tall_u,
+        (const void*)ttg::k_syrk<1>,
         (const void*)ttg::k_syrk<2>, (const void*)ttg::k_syrk<3>, (const void*)ttg::k_syrk<5>,
         (const void*)ttg::k_syrk<8>, (const void*)ttg::k_syrk2<1>, (const void*)ttg::k_syrk2<2>,
-        (const void*)ttg::k_syrk2<3>, (const void*)ttg::k_gram_reduce2, (const void*)ttg::k_gram_reduce_s1, (const void*)ttg::k_gram_reduce_s2, (const void*)ttg::k_make_frags16,
+        (const void*)ttg::k_syrk2<3>, (const void*)ttg::k_gram_reduce_s1, (const void*)ttg::k_gram_reduce_s2, (const void*)ttg::k_make_frags16,
         (const void*)ttg::k_project_ws16<4, 1>, (const void*)ttg::k_project_ws16<4, 2>,
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>, (const void*)ttg::k_pcp};
     for (int nbk = 7; nbk <= kKpMaxNbk; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
     for (int nb = 1; nb <= 4; ++nb)
-      for (int t = 0; t <= 2; ++t) {
+      for (int t = 0; t <= kKcMaxTail; ++t) {
         CK(cudaFuncGetAttributes(&fa, kc_pick(4, nb, t)));
         CK(cudaFuncGetAttributes(&fa, kc_pick(8, nb, t)));
       }
@@ -2553,10 +2668,11 @@ int ttg_ctx_create_dist(int device, int rank, int world, const uint8_t nccl_id[1
     ctx_init(c, device);
     c->rank = rank;
     c->world = world;
-    // NCCL kernels interleave in the stream: PDL off unless TTG_NCCL_PDL is set
-    // (our kernels never trigger early, so the opt-in is safe by construction;
-    // kept opt-in until measured at N > 1)
-    c->pdl = c->pdl && std::getenv("TTG_NCCL_PDL") != nullptr;
+    // NCCL kernels interleave in the stream.  PDL stays on: our kernels never
+    // trigger early, so a kernel behind an NCCL kernel launches at its exit
+    // and every kernel's griddepcontrol.wait (tests/test_pdl_static.py) orders
+    // its reads after the collective's writes; TTG_NCCL_NO_PDL turns it off.
+    c->pdl = c->pdl && std::getenv("TTG_NCCL_NO_PDL") == nullptr;
     c->coll = true;
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
@@ -2599,8 +2715,6 @@ int ttg_ctx_create_hostcoll(int device, int rank, int world, ttg_host_allreduce_
 void ttg_ctx_destroy(ttg_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->blas) cublasDestroy(c->blas);
-  if (c->solver) cusolverDnDestroy(c->solver);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_eig) cudaFreeHost(c->h_eig);
   if (c->h_scal) cudaFreeHost(c->h_scal);

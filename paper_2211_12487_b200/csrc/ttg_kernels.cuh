@@ -1087,27 +1087,6 @@ __global__ void k_gram_reduce_s2(const double* __restrict__ tmp, int xs, int a, 
   }
 }
 
-// Fixed-order reduction of the per-CTA Gram partials into the full symmetric
-// a x a matrix G (column-major).
-__global__ void k_gram_reduce(const double* __restrict__ partials, int nx, int sbd, int a,
-                              double* __restrict__ G) {
-  griddep_wait();
-  long long n = (long long)a * a;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
-    int i = (int)(e % a), j = (int)(e / a);
-    int ii = i, jj = j;
-    if (jj > ii) { const int tmp = ii; ii = jj; jj = tmp; }  // lower-triangle source
-    const int I = ii / sbd, J = jj / sbd;
-    const int py = I * (I + 1) / 2 + J;
-    const double* src = partials + (long long)py * nx * sbd * sbd + (ii - I * sbd) + (long long)sbd * (jj - J * sbd);
-    double s = 0.0;
-    for (int x = 0; x < nx; ++x) s += src[(long long)x * sbd * sbd];
-    G[e] = s;
-  }
-}
-
-
 // ---------------------------------------------------------------------------
 // Accurate path (small delta): TSQR R-factor of the residual.  With
 // R^T = Q T (T a x a upper triangular), T^T T = R R^T but T carries the
@@ -1587,256 +1566,6 @@ __global__ void __launch_bounds__(kThreads) k_project_tma(const __grid_constant_
   }
 }
 
-// Projection out (r x L) = W^T X for short operands (a8 <= 64) with
-// 16 < r8 <= 32: 64-column tensor-map tiles, warp w = (column group cw = w % 4
-// of 16 columns = two DMMA n-blocks, k half kh = w / 4 = box parity).  Each
-// warp keeps the W^T fragments of its 8 k-steps for all MR <= 4 m-blocks in
-// registers (32 doubles) and reuses every fragment for both n-blocks; the two
-// k halves are summed through shared memory.  Same ring / barrier protocol and
-// output layout as k_project_tma.
-__global__ void __launch_bounds__(kThreads) k_project_w2(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
-  griddep_wait();
-  constexpr int TC = 64, BOX = 16 * TC;
-  extern __shared__ __align__(1024) double smem_raw[];
-  __shared__ __align__(8) uint64_t full[kProjStages];
-  __shared__ double red_ss[4];
-  double* smem = align1024(smem_raw);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int nst = p.nst;
-  const int nbox = (p.src.a + 15) >> 4;
-  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
-  const int stage = nbox * BOX;
-  double* stg_all = smem + nst * stage;  // 8 warps x 16 columns x r (r <= 32)
-  double* stg = stg_all + warp * 16 * 32;
-  const int cw = warp & 3, kh = warp >> 2;
-  double wreg[4 * 8];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int kb = 4 * (2 * (jj >> 2) + kh) + (jj & 3);
-      wreg[u * 8 + jj] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
-    }
-  const long long grid = gridDim.x;
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tm);
-    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-    for (int s = 0; s < nst - 1; ++s) {
-      const long long tl = blockIdx.x + s * grid;
-      if (tl < p.n_tiles) {
-        mbar_expect_tx(&full[s], (unsigned)nbox * BOX * 8u);
-        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + s * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[s]);
-      }
-    }
-  }
-  __syncthreads();
-  // swizzled B-fragment offsets for the two n-blocks (columns 16cw + 8n + g)
-  int osw[2][4];
-#pragma unroll
-  for (int n = 0; n < 2; ++n) {
-    const int c = 16 * cw + 8 * n + g;
-    const int hsw = (t >> 1) ^ (c & 7);
-#pragma unroll
-    for (int m = 0; m < 4; ++m) osw[n][m] = c * 16 + (t & 1) + (((m << 1) ^ hsw) << 1);
-  }
-  int it = 0;
-  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid, ++it) {
-    const int st = it % nst;
-    mbar_wait(&full[st], (unsigned)((it / nst) & 1));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const long long tl = tile + (nst - 1) * grid;
-      if (tl < p.n_tiles) {
-        const int sn = (it + nst - 1) % nst;
-        mbar_expect_tx(&full[sn], (unsigned)nbox * BOX * 8u);
-        for (int b = 0; b < nbox; ++b) tma_load_2d(smem + sn * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[sn]);
-      }
-    }
-    const double* T = smem + st * stage;
-    double q[4][2][2];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) q[u][0][0] = q[u][0][1] = q[u][1][0] = q[u][1][1] = 0.0;
-    double ss = 0.0;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {  // 4 k-steps (one box) at a time
-      const int b = 2 * half + kh;
-      double bv[2][4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool ok = 4 * b + j < KA;
-#pragma unroll
-        for (int n = 0; n < 2; ++n) bv[n][j] = ok ? T[b * BOX + osw[n][j]] : 0.0;
-      }
-      if (p.tsumsq) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) ss = fma(bv[0][j], bv[0][j], fma(bv[1][j], bv[1][j], ss));
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (u < MR) {
-            const double w = wreg[u * 8 + 4 * half + j];
-            dmma(q[u][0][0], q[u][0][1], w, bv[0][j]);
-            dmma(q[u][1][0], q[u][1][1], w, bv[1][j]);
-          }
-    }
-    // stage this warp's 16 x r partial block (column-major, ld r)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int row = u * 8 + g;
-      if (u < MR && row < p.r)
-#pragma unroll
-        for (int n = 0; n < 2; ++n) {
-          stg[row + p.r * (8 * n + 2 * t)] = q[u][n][0];
-          stg[row + p.r * (8 * n + 2 * t + 1)] = q[u][n][1];
-        }
-    }
-    if (p.tsumsq) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (kh == 1 && lane == 0) red_ss[cw] = ss;
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
-    if (kh == 0) {
-      const double* oth = stg_all + (warp + 4) * 16 * 32;
-      const long long colw = tile * TC + 16 * cw;
-      const int nval = (int)max(0LL, min(16LL, p.src.L - colw));
-      double* dst = p.out + colw * p.r;
-      const int n = nval * p.r;
-      for (int e = lane; e < n; e += 32) dst[e] = stg[e] + oth[e];
-      if (p.tsumsq && lane == 0) {
-        // two 8-column groups of the TC = 64 sums layout
-        const double tot = ss + red_ss[cw];
-        p.tsumsq[tile * kConsumerWarps + 2 * cw] = tot;
-        p.tsumsq[tile * kConsumerWarps + 2 * cw + 1] = 0.0;
-      }
-    }
-  }
-}
-
-// Projection out (r x L) = W^T X with mma.m16n8k16 on the transposed tile:
-// out^T (16 columns x 8 r-rows) += X^T (16 columns x 16 rows of a) W (16 x 8),
-// so r is padded to 8 only and one instruction does 4096 FMA.  64-column
-// tensor-map tiles (128-byte swizzle; the A fragment is the conflict-free
-// "4 rows x 8 columns" pattern twice); warp w: columns 16 (w % 4) .. +16,
-// boxes of parity w / 4 (the two k halves are summed through shared memory).
-// W fragments are the m8n8k4 U^T fragments (k_make_frags): the B fragment of
-// (box b, n-block nb) is UTf[(nb KA + 4b + i) 32 + lane], i = 0..3, staged in
-// shared memory.  r <= 32 (NB <= 4 n-blocks).  Output staged per warp (16 x r
-// block, contiguous in out) and stored coalesced; optional per-(tile, 8-column
-// group) input sums of squares.
-__global__ void __launch_bounds__(kThreads) k_project_m16(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
-  griddep_wait();
-  constexpr int TC = 64, BOX = 16 * TC;
-  extern __shared__ __align__(1024) double smem_raw[];
-  __shared__ __align__(8) uint64_t full[kProjStages];
-  __shared__ double red_ss[4];
-  double* smem = align1024(smem_raw);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int nst = p.nst;
-  const int nks = (p.src.a + 15) >> 4;
-  const int KA = p.a8 >> 2, NB = p.r8 >> 3;
-  const int stage = nks * BOX;
-  double* Wfs = smem + nst * stage;
-  const int nfr = NB * KA * 32;
-  double* stg_all = Wfs + nfr;  // 8 warps x 16 columns x r (r <= 32)
-  double* stg = stg_all + warp * 16 * 32;
-  const int cw = warp & 3, kh = warp >> 2;
-  for (int i = threadIdx.x; i < nfr; i += kThreads) Wfs[i] = p.WTf[i];
-  const long long grid = gridDim.x;
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tm);
-    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-    for (int s = 0; s < nst - 1; ++s) {
-      const long long tl = blockIdx.x + s * grid;
-      if (tl < p.n_tiles) {
-        mbar_expect_tx(&full[s], (unsigned)nks * BOX * 8u);
-        for (int b = 0; b < nks; ++b) tma_load_2d(smem + s * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[s]);
-      }
-    }
-  }
-  __syncthreads();
-  // A element i of a box: row 4(i>>1) + t, column 16cw + g + 8(i&1)
-  int osw[8];
-  {
-    const int hsw = (t >> 1) ^ g;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      osw[i] = (16 * cw + g + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
-  }
-  int it = 0;
-  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid, ++it) {
-    const int st = it % nst;
-    mbar_wait(&full[st], (unsigned)((it / nst) & 1));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const long long tl = tile + (nst - 1) * grid;
-      if (tl < p.n_tiles) {
-        const int sn = (it + nst - 1) % nst;
-        mbar_expect_tx(&full[sn], (unsigned)nks * BOX * 8u);
-        for (int b = 0; b < nks; ++b) tma_load_2d(smem + sn * stage + b * BOX, &tm, 16 * b, (int)(tl * TC), &full[sn]);
-      }
-    }
-    const double* T = smem + st * stage;
-    double acc[4][4];
-#pragma unroll
-    for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0;
-    double ss = 0.0;
-    for (int b = kh; b < nks; b += 2) {
-      double av[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = T[b * BOX + osw[i]];
-      if (p.tsumsq) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ss = fma(av[i], av[i], ss);
-      }
-#pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
-        if (nb < NB) {
-          double bw[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int kb = 4 * b + i;
-            bw[i] = kb < KA ? Wfs[(nb * KA + kb) * 32 + lane] : 0.0;
-          }
-          dmma16(acc[nb], av, bw);
-        }
-    }
-    // c[i] = out^T[column g + 8(i>>1)][row 8nb + 2t + (i&1)]  ->  stg[row + r * column]
-#pragma unroll
-    for (int nb = 0; nb < 4; ++nb)
-      if (nb < NB)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = 8 * nb + 2 * t + (i & 1);
-          if (row < p.r) stg[row + p.r * (g + 8 * (i >> 1))] = acc[nb][i];
-        }
-    if (p.tsumsq) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (kh == 1 && lane == 0) red_ss[cw] = ss;
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
-    if (kh == 0) {
-      const double* oth = stg_all + (warp + 4) * 16 * 32;
-      const long long colw = tile * TC + 16 * cw;
-      const int nval = (int)max(0LL, min(16LL, p.src.L - colw));
-      double* dst = p.out + colw * p.r;
-      const int n = nval * p.r;
-      for (int e = lane; e < n; e += 32) dst[e] = stg[e] + oth[e];
-      if (p.tsumsq && lane == 0) {
-        p.tsumsq[tile * kConsumerWarps + 2 * cw] = ss + red_ss[cw];
-        p.tsumsq[tile * kConsumerWarps + 2 * cw + 1] = 0.0;
-      }
-    }
-  }
-}
-
 // W (a x r, ld) -> m16n8k16 B fragments for the k-step-major projection
 // kernels: Wm[((b NB + nb) 4 + i) 32 + lane] = W[16b + t + 4i][8nb + g]
 // (lane = 4g + t), zero outside W; b < nks = ceil(a/16), nb < NB = r8/8.
@@ -2170,154 +1899,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_cons
 // shrink with a.  W^T fragments in registers (REGW: a8 <= 64, MR <= 2),
 // shared memory (frag_smem) or global (L1).  Outputs staged per warp (r <= 32)
 // and written coalesced; optional per-(tile, warp) input sums of squares.
-constexpr int kBoxStages = 16;
-template <int MRMAX, bool REGW>
-__global__ void __launch_bounds__(kSyrkThreads) k_project_box(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
-  griddep_wait();
-  extern __shared__ __align__(1024) double smem_raw[];
-  __shared__ __align__(8) uint64_t full[kBoxStages], empty[kBoxStages];
-  double* ring = align1024(smem_raw);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int nst = p.nst;
-  const int nbox = (p.src.a + 15) >> 4;
-  const int KA = p.a8 >> 2, MR = p.r8 >> 3;
-  const int nfr = MR * KA * 32;
-  double* Wfs = ring + nst * 1024;
-  double* stg_all = Wfs + (p.frag_smem ? nfr : 0);
-  const bool staged = p.r <= 32;
-  if (!REGW && p.frag_smem)
-    for (int i = threadIdx.x; i < nfr; i += blockDim.x) Wfs[i] = p.WTf[i];
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < nst; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const long long grid = gridDim.x;
-  if (warp == kConsumerWarps) {  // ---- producer ----
-    if (lane == 0) {
-      tma_prefetch_desc(&tm);
-      int it = 0;
-      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid)
-        for (int b = 0; b < nbox; ++b, ++it) {
-          const int s = it % nst;
-          if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
-          mbar_expect_tx(&full[s], 8192u);
-          tma_load_2d(ring + s * 1024, &tm, 16 * b, (int)(tile * kTC), &full[s]);
-        }
-    }
-    return;
-  }
-  // ---- consumers ----
-  constexpr int NS = MRMAX <= 4 ? 2 : 1;  // independent accumulator sets (k split)
-  double wreg[REGW ? 32 : 1];
-  if (REGW) {
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int kb = 0; kb < 16; ++kb)
-        wreg[u * 16 + kb] = (u < MR && kb < KA) ? p.WTf[(u * KA + kb) * 32 + lane] : 0.0;
-  }
-  const double* Wf = p.frag_smem ? Wfs : p.WTf;
-  double* stg = stg_all + warp * 8 * 32;
-  const int c0 = warp * 8;
-  const int hsw = (t >> 1) ^ g;
-  const int lbase = (c0 + g) * 16 + (t & 1);
-  int osw[4];
-#pragma unroll
-  for (int m = 0; m < 4; ++m) osw[m] = lbase + (((m << 1) ^ hsw) << 1);
-  int it = 0;
-  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
-    double q[MRMAX][NS][2];
-#pragma unroll
-    for (int u = 0; u < MRMAX; ++u)
-#pragma unroll
-      for (int x = 0; x < NS; ++x) q[u][x][0] = q[u][x][1] = 0.0;
-    double ss = 0.0;
-    if (REGW) {
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        if (b < nbox) {
-          const int s = it % nst;
-          mbar_wait(&full[s], (unsigned)((it / nst) & 1));
-          const double* T = ring + s * 1024;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int kb = 4 * b + j;
-            if (kb < KA) {
-              const double bv = T[osw[j]];
-              ss = fma(bv, bv, ss);
-              dmma(q[0][j & (NS - 1)][0], q[0][j & (NS - 1)][1], wreg[kb], bv);
-              if (MRMAX > 1 && MR > 1) dmma(q[1][j & (NS - 1)][0], q[1][j & (NS - 1)][1], wreg[16 + kb], bv);
-            }
-          }
-          __syncwarp();
-          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[s])) : "memory");
-          ++it;
-        }
-      }
-    } else {
-      for (int b = 0; b < nbox; ++b, ++it) {
-        const int s = it % nst;
-        mbar_wait(&full[s], (unsigned)((it / nst) & 1));
-        const double* T = ring + s * 1024;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int kb = 4 * b + j;
-          if (kb < KA) {
-            const double bv = T[osw[j]];
-            ss = fma(bv, bv, ss);
-#pragma unroll
-            for (int u = 0; u < MRMAX; ++u)
-              if (u < MR) dmma(q[u][j & (NS - 1)][0], q[u][j & (NS - 1)][1], Wf[(u * KA + kb) * 32 + lane], bv);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[s])) : "memory");
-      }
-    }
-    const long long colw = tile * kTC + c0;
-    const int nval = (int)max(0LL, min(8LL, p.src.L - colw));
-    const long long col0 = colw + 2 * t;
-    const bool ok0 = 2 * t < nval, ok1 = 2 * t + 1 < nval;
-    double* o0 = p.out + col0 * p.r;
-    double* o1 = o0 + p.r;
-#pragma unroll
-    for (int u = 0; u < MRMAX; ++u) {
-      const int row = u * 8 + g;
-      if (u < MR && row < p.r) {
-        double v0 = q[u][0][0], v1 = q[u][0][1];
-        if (NS > 1) {
-          v0 += q[u][NS - 1][0];
-          v1 += q[u][NS - 1][1];
-        }
-        if (staged) {
-          stg[row + p.r * (2 * t)] = v0;
-          stg[row + p.r * (2 * t + 1)] = v1;
-        } else {
-          if (ok0) o0[row] = v0;
-          if (ok1) o1[row] = v1;
-        }
-      }
-    }
-    if (staged) {
-      __syncwarp();
-      double* dst = p.out + colw * p.r;
-      const int n = nval * p.r;
-      for (int e = lane; e < n; e += 32) dst[e] = stg[e];
-      __syncwarp();
-    }
-    if (p.tsumsq) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) p.tsumsq[tile * kConsumerWarps + warp] = ss;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // SYRK over tensor-map tiles: C = sum over (selected) columns x x^T, x the
 // a rows of X (a <= 256).  A tile is kTC full-height columns, ceil(a/16) TMA
@@ -2331,7 +1912,7 @@ __global__ void __launch_bounds__(kSyrkThreads) k_project_box(const __grid_const
 // bank-conflict free (tools/probe: checked exhaustively).  Observation
 // selection skips whole tiles (requires cols_per_obs % kTC == 0).  Each CTA
 // writes its owned blocks into partials[blockIdx.x] (a8 x a8); parts own
-// disjoint blocks, so k_gram_reduce2 sums over blockIdx.x only.
+// disjoint blocks, so k_gram_reduce_s1/s2 sum over blockIdx.x only.
 // ---------------------------------------------------------------------------
 struct Syrk2Args {
   int a, a8, nbox, nst;
@@ -2479,7 +2060,7 @@ __global__ void __launch_bounds__(kSyrkThreads) k_syrk2(const __grid_constant__ 
 // (4 loads each) feeding two MMAs.  The k index of a step is permuted,
 // column(t, j) = 8(j>>1) + 2(j&1) + (t&1) + 4(t>>1), which makes every
 // fragment load bank-conflict free under the swizzle (checked exhaustively).
-// Per-CTA partials (a8 x a8, owned blocks) are summed by k_gram_reduce2.
+// Per-CTA partials (a8 x a8, owned blocks) are summed by k_gram_reduce_s1/s2.
 // Input sums of squares (tsumsq, 8 per 64-column tile) come from the B
 // fragments of the diagonal groups (p == mi cover every row once), reduced
 // across warps in shared memory behind a consumer-only named barrier.
@@ -2632,20 +2213,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_syrk_ws16(const __grid_const
   }
 }
 
-// G (a x a, symmetric) = sum over the nx CTA partials (lower triangle read)
-__global__ void k_gram_reduce2(const double* __restrict__ partials, int nx, int a8, int a, double* __restrict__ G) {
-  griddep_wait();
-  const long long n = (long long)a * a;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    int i = (int)(e % a), j = (int)(e / a);
-    if (j > i) { const int tmp = i; i = j; j = tmp; }
-    const double* src = partials + i + (long long)a8 * j;
-    double s = 0.0;
-    for (int x = 0; x < nx; ++x) s += src[(long long)x * a8 * a8];
-    G[e] = s;
-  }
-}
-
 // per-observation sums from per-(tile, warp) partials (tiles never straddle
 // observations): one block per observation, fixed assignment + fixed tree
 __global__ void k_tiles_to_obs(const double* __restrict__ ts, long long tiles_per_obs, int nobs,
@@ -2687,50 +2254,6 @@ __global__ void k_sum_vec(const double* __restrict__ v, int n, double* __restric
   if (threadIdx.x == 0) *total = s;
 }
 
-// ---------------------------------------------------------------------------
-// Generic path (any a): C = alpha op(A) op(B) + beta C, column-major, DFMA,
-// 32x32 smem tiles, one output per thread.  Fixed summation order, so results
-// are deterministic.  Used for unfoldings with a8 > 128 (and reconstruct).
-// grid = (ceil(n/32), ceil(m/32)), block = (32, 32).
-// ---------------------------------------------------------------------------
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(1024) k_gemm(const double* __restrict__ A, long long lda,
-                                               const double* __restrict__ B, long long ldb, double* C,
-                                               long long ldc, long long m, long long n, long long k,
-                                               double alpha, double beta) {
-  griddep_wait();
-  __shared__ double As[32][33];  // As[kk][i]
-  __shared__ double Bs[32][33];  // Bs[j][kk]
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const long long row0 = (long long)blockIdx.y * 32, col0 = (long long)blockIdx.x * 32;
-  double acc = 0.0;
-  for (long long k0 = 0; k0 < k; k0 += 32) {
-    if (!TA) {  // A[i + lda*kk]
-      long long i = row0 + tx, kk = k0 + ty;
-      As[ty][tx] = (i < m && kk < k) ? A[i + lda * kk] : 0.0;
-    } else {    // op(A)(i,kk) = A[kk + lda*i]
-      long long kk = k0 + tx, i = row0 + ty;
-      As[tx][ty] = (i < m && kk < k) ? A[kk + lda * i] : 0.0;
-    }
-    if (!TB) {  // B[kk + ldb*j]
-      long long kk = k0 + tx, j = col0 + ty;
-      Bs[ty][tx] = (kk < k && j < n) ? B[kk + ldb * j] : 0.0;
-    } else {    // op(B)(kk,j) = B[j + ldb*kk]
-      long long j = col0 + tx, kk = k0 + ty;
-      Bs[tx][ty] = (kk < k && j < n) ? B[j + ldb * kk] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int kk = 0; kk < 32; ++kk) acc = fma(As[kk][tx], Bs[ty][kk], acc);
-    __syncthreads();
-  }
-  long long i = row0 + tx, j = col0 + ty;
-  if (i < m && j < n) {
-    double v = alpha * acc;
-    if (beta != 0.0) v += beta * C[i + ldc * j];
-    C[i + ldc * j] = v;
-  }
-}
 
 // zero the columns of observations that are not selected
 __global__ void k_mask_cols(double* __restrict__ X, int a, long long L, const uint8_t* __restrict__ sel,

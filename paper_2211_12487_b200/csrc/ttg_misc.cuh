@@ -529,4 +529,75 @@ __global__ void k_star_mask(const double* __restrict__ errs, int b, double eps, 
     sel[o] = subselect ? (errs[o] > eps ? 1 : 0) : 1;
 }
 
+// ---- tall unfoldings (a > 2 L): the small side ----------------------------
+// The reference's own tall branch (truncated_svd.cpp:51-59) QR-reduces an
+// a x L residual with a > 2 L before its SVD; here the eigen-problem is solved
+// on the L x L side (R^T R, or the TSQR factor of R^T on the accurate path)
+// and the left singular vectors are recovered as u_j = R v_j / |R v_j|.
+
+// out (L x a) = X^T (X: a x L, column-major), 32 x 32 smem tiles
+__global__ void k_transpose(const double* __restrict__ X, int a, long long L, double* __restrict__ out) {
+  griddep_wait();
+  __shared__ double tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32;
+  const int r0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = r0 + threadIdx.x;
+    const long long c = c0 + j;
+    tile[j][threadIdx.x] = (r < a && c < L) ? X[r + (long long)a * c] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = r0 + j;
+    const long long c = c0 + threadIdx.x;
+    if (r < a && c < L) out[c + L * (long long)r] = tile[threadIdx.x][j];
+  }
+}
+
+// U_R column j (one CTA per kept direction): u = R v_j (R: a x L, V: L x rank,
+// ld L), normalised, sign rule (largest-|.| entry, first index, positive:
+// truncated_svd.cpp:16-25).
+__global__ void __launch_bounds__(256) k_tall_u(const double* __restrict__ R, int a, int L,
+                                                const double* __restrict__ V, double* __restrict__ U) {
+  griddep_wait();
+  __shared__ double red[8];
+  __shared__ int redi[8];
+  __shared__ double s_inv;
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* v = V + (long long)L * j;
+  double* u = U + (long long)a * j;
+  double nn = 0.0, best = -1.0;
+  int bi = a;
+  for (int i = tid; i < a; i += blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < L; ++l) s = fma(R[i + (long long)a * l], v[l], s);
+    u[i] = s;
+    nn = fma(s, s, nn);
+    if (fabs(s) > best) { best = fabs(s); bi = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    nn += __shfl_xor_sync(0xffffffffu, nn, o);
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if (lane == 0) { red[warp] = nn; redi[warp] = bi; }
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0, bb = -1.0;
+    int bidx = a;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      const int ix = redi[w];
+      const double vv = ix < a ? fabs(u[ix]) : -1.0;
+      if (vv > bb || (vv == bb && ix < bidx)) { bb = vv; bidx = ix; }
+    }
+    const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    s_inv = (bidx < a && u[bidx] < 0.0) ? -inv : inv;
+  }
+  __syncthreads();
+  const double f = s_inv;
+  for (int i = tid; i < a; i += blockDim.x) u[i] *= f;
+}
+
 }  // namespace ttg

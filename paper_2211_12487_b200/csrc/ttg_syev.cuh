@@ -34,6 +34,7 @@ struct SyevArgs {
   double* lam;            // out: computed eigenvalues, descending (first n_lam)
   double* zbuf;           // scratch: 32 x 6a (inverse-iteration vectors + LU factors)
   EigResult* res;
+  const double* tri;      // non-null: Ag already holds Q^T G Q's reflectors (k_sytrd_grid) and tri = [d | e | tau]
 };
 
 constexpr int kSyevThreads = 1024;
@@ -99,9 +100,18 @@ __global__ void __launch_bounds__(kSyevThreads) k_syev(SyevArgs p) {
   double* lam = w + a;        // a   top eigenvalues (descending)
 
   const long long t0 = clock64();
+  double trace = 0.0;
+  if (p.tri) {  // tridiagonalised by k_sytrd_grid (multi-CTA): reflectors in Ag, d / e / tau given
+    for (int i = tid; i < a; i += blockDim.x) {
+      d[i] = p.tri[i];
+      e[i] = p.tri[a + i];
+      tau[i] = p.tri[2 * a + i];
+    }
+    for (int i = 0; i < a; ++i) trace += p.G[i + (size_t)a * i];  // all threads, same order
+    __syncthreads();
+  } else {
   for (long long i = tid; i < (long long)a * a; i += blockDim.x) A[i] = p.G[i];
   __syncthreads();
-  double trace = 0.0;
   for (int i = 0; i < a; ++i) trace += A[i + (size_t)a * i];  // all threads, same order
 
   // ---- 1. tridiagonalisation --------------------------------------------
@@ -183,6 +193,7 @@ __global__ void __launch_bounds__(kSyevThreads) k_syev(SyevArgs p) {
     e[a - 1] = 0.0;
   }
   __syncthreads();
+  }  // phase 1
   double gl = 0.0, gu = 0.0, emax2 = 0.0;
   for (int i = 0; i < a; ++i) {  // Gershgorin bounds (all threads)
     double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < a ? fabs(e[i]) : 0.0);
@@ -1003,68 +1014,189 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
   }
 }
 
-// Rank rule, outputs and sign rule on a full eigen-decomposition of G
-// computed by cuSOLVER syevd (large a, where the one-CTA tridiagonal solver
-// is latency-bound): evals ascending, Q columns the eigenvectors (in place of
-// G's copy).  Same rule as k_syev: the smallest r <= kcap with
-// sqrt(trace(G) - sum_{j<r} lambda_j) <= delta ('>' keeps the smaller rank),
-// U_R = the top r eigenvectors with the largest-|.| entry (first index)
-// positive, lam = eigenvalues descending.  One CTA.
-__global__ void __launch_bounds__(1024) k_syev_select(const double* __restrict__ G, int a, const double* __restrict__ evals,
-                                                      const double* __restrict__ Q, const int* __restrict__ info,
-                                                      SyevArgs p) {
-  griddep_wait();
-  __shared__ double red[33];
-  __shared__ int s_rank;
-  __shared__ double s_tail, s_trace;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  double tp = 0.0;
-  for (int i = tid; i < a; i += blockDim.x) tp += G[i + (size_t)a * i];
-  const double trace = block_sum_all(tp, red);
-  const double delta = p.delta_src ? p.delta_mult * sqrt(*p.delta_src) : p.delta_mult;
-  const long long kcap = p.kmax < a ? p.kmax : a;
-  if (tid == 0) {
-    double pre = 0.0;
-    int found = (int)kcap;
-    for (int r = 0; r <= a; ++r) {
-      if (r <= kcap && !(sqrt(fmax(trace - pre, 0.0)) > delta)) { found = r; break; }
-      if (r < a) pre += evals[a - 1 - r];
+
+}  // namespace ttg
+
+namespace ttg {
+
+// ---------------------------------------------------------------------------
+// Multi-CTA Householder tridiagonalisation Q^T G Q = T for the large Grams
+// (a > ~256) that neither fit one CTA's shared memory nor keep few enough
+// directions for the block subspace path (replaces cuSOLVER syevd).  LAPACK
+// dsytd2 'L' numerics with dlatrd's lazy panel update, on P co-resident CTAs
+// (cooperative launch, one grid barrier per column):
+//   A  step j (panel column jj): every CTA rebuilds the updated column j,
+//      a_j = A[:, j] - V W[j,:]^T - W V[j,:]^T (q < jj), and its reflector
+//      (identical bytes on every CTA: same code, same order);
+//   B  its rows of p = (A - V W^T - W V^T) v (row i = column i: symmetric
+//      storage, contiguous reads), then the grid barrier;
+//   C  every CTA reads p, forms w = tau p - tau/2 (tau p^T v) v and writes its
+//      rows into the panel W (the latest v, w stay in shared memory for the
+//      next step, so no second barrier);
+//   D  panel end (nb columns): A_trailing -= V W^T + W V^T (both triangles),
+//      between two barriers.
+// Output: d, e, tau (tri = [d | e | tau]) and the reflectors' essential parts in
+// A's columns below the subdiagonal -- the layout k_syev's phases 2-3 consume.
+// ---------------------------------------------------------------------------
+constexpr int kTrdThreads = 512;
+constexpr int kTrdPanel = 16;
+
+struct TrdArgs {
+  double* A;        // a x a (copy of G), overwritten
+  int a;
+  double* V;        // a x kTrdPanel panel
+  double* W;        // a x kTrdPanel panel
+  double* pbuf;     // a
+  double* tri;      // 3a: d, e, tau
+  unsigned* bar;    // [count, generation], zeroed by the host
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(32);
     }
-    double pre2 = 0.0;
-    for (int r = 0; r < found; ++r) pre2 += evals[a - 1 - r];
-    s_rank = found;
-    s_tail = fmax(trace - pre2, 0.0);
-    s_trace = trace;
+    __threadfence();
   }
   __syncthreads();
-  const int rank = s_rank;
-  for (int j = tid; j < a; j += blockDim.x) p.lam[j] = evals[a - 1 - j];
-  if (tid == 0) {
-    p.res->rank = rank;
-    p.res->tail_sq = s_tail;
-    p.res->delta = delta;
-    p.res->converged = (*info == 0) ? 1 : 0;
-    p.res->sweeps = 0;
-    p.res->lam_max = evals[a - 1];
-    p.res->lam_min_kept = rank > 0 ? evals[a - rank] : 0.0;
-    p.res->t_phase[0] = p.res->t_phase[1] = p.res->t_phase[2] = 0;
-    p.res->t_phase[3] = a;
+}
+
+__global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
+  griddep_wait();  // launched cooperatively without PDL: a no-op, kept for the invariant
+  extern __shared__ __align__(16) double tsm[];
+  __shared__ double red[kTrdThreads / 32 + 1];
+  __shared__ double vtw[2 * kTrdPanel];  // W^T v, V^T v of the current step
+  const int a = p.a, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const unsigned P = gridDim.x;
+  double* A = p.A;
+  double* col = tsm;        // updated column j (rows j..a-1), then v (rows j+1..)
+  double* v = tsm + a;      // current v (rows 0..a-1, zero above j+1)
+  double* vp = v + a;       // previous step's v
+  double* wp = vp + a;      // previous step's w
+  double* pv = wp + a;      // p / w of the current step
+  const double* V = p.V;
+  const double* W = p.W;
+  for (int j0 = 0; j0 + 2 < a; j0 += kTrdPanel) {
+    const int jend = min(j0 + kTrdPanel, a - 2);  // columns j0 .. jend-1 in this panel
+    for (int j = j0; j < jend; ++j) {
+      const int jj = j - j0;
+      // ---- A: updated column j and its reflector (every CTA) ----
+      for (int i = j + tid; i < a; i += blockDim.x) {
+        double x = A[i + (size_t)a * j];
+        for (int q = 0; q < jj; ++q) {
+          const double vq = (q == jj - 1) ? vp[i] : V[i + (size_t)a * q];
+          const double wq = (q == jj - 1) ? wp[i] : W[i + (size_t)a * q];
+          const double vjq = (q == jj - 1) ? vp[j] : V[j + (size_t)a * q];
+          const double wjq = (q == jj - 1) ? wp[j] : W[j + (size_t)a * q];
+          x -= vq * wjq + wq * vjq;
+        }
+        col[i] = x;
+      }
+      __syncthreads();
+      double xs = 0.0;
+      for (int i = j + 2 + tid; i < a; i += blockDim.x) xs = fma(col[i], col[i], xs);
+      xs = block_sum_all(xs, red);
+      const double alpha = col[j + 1];
+      double tk = 0.0, beta = alpha;
+      if (xs != 0.0) {
+        beta = sqrt(alpha * alpha + xs);
+        if (alpha >= 0.0) beta = -beta;
+        tk = (beta - alpha) / beta;
+      }
+      const double sc = xs != 0.0 ? 1.0 / (alpha - beta) : 0.0;
+      // v: rows j+1.. (v[j+1] = 1); zero elsewhere
+      for (int i = tid; i < a; i += blockDim.x) v[i] = (i <= j) ? 0.0 : (i == j + 1 ? 1.0 : col[i] * sc);
+      if (blockIdx.x == 0 && tid == 0) {
+        p.tri[j] = col[j];
+        p.tri[a + j] = beta;
+        p.tri[2 * a + j] = tk;
+      }
+      __syncthreads();
+      // V[:, jj] = v: each CTA writes its own row slice (read back only after a barrier)
+      const int rows_per = (a + (int)P - 1) / (int)P;
+      const int r0 = (int)blockIdx.x * rows_per, r1 = min(a, r0 + rows_per);
+      for (int i = r0 + tid; i < r1; i += blockDim.x) p.V[i + (size_t)a * jj] = v[i];
+      // ---- B: W^T v, V^T v (q < jj), then this CTA's rows of p ----
+      for (int q = warp; q < 2 * jj; q += nw) {
+        const int qq = q % jj;
+        const bool isw = q < jj;
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < a; i += 32) {
+          const double m = (qq == jj - 1) ? (isw ? wp[i] : vp[i]) : (isw ? W : V)[i + (size_t)a * qq];
+          s = fma(m, v[i], s);
+        }
+        s = warp_sum(s);
+        if (lane == 0) vtw[q] = s;
+      }
+      __syncthreads();
+      for (int i = max(r0, j + 1) + warp; i < r1; i += nw) {
+        const double* ci = A + (size_t)a * i;
+        double s = 0.0;
+        for (int k = j + 1 + lane; k < a; k += 32) s = fma(ci[k], v[k], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+          for (int q = 0; q < jj; ++q) {
+            const double vq = (q == jj - 1) ? vp[i] : V[i + (size_t)a * q];
+            const double wq = (q == jj - 1) ? wp[i] : W[i + (size_t)a * q];
+            s -= vq * vtw[q] + wq * vtw[jj + q];
+          }
+          p.pbuf[i] = s;
+        }
+      }
+      grid_barrier(p.bar, P);
+      // every CTA has read column j (step A): store the reflector in it
+      if (blockIdx.x == 0)
+        for (int i = j + 2 + tid; i < a; i += blockDim.x) A[i + (size_t)a * j] = v[i];
+      // ---- C: w = tau p + alpha2 v (every CTA, full length) ----
+      double pvs = 0.0;
+      for (int i = j + 1 + tid; i < a; i += blockDim.x) {
+        const double w0 = tk * p.pbuf[i];
+        pv[i] = w0;
+        pvs = fma(w0, v[i], pvs);
+      }
+      pvs = block_sum_all(pvs, red);
+      const double al2 = -0.5 * tk * pvs;
+      for (int i = tid; i < a; i += blockDim.x) {
+        const double wi = (i <= j) ? 0.0 : fma(al2, v[i], pv[i]);
+        wp[i] = wi;
+        vp[i] = v[i];
+      }
+      __syncthreads();
+      for (int i = r0 + tid; i < r1; i += blockDim.x) p.W[i + (size_t)a * jj] = wp[i];
+      __syncthreads();
+    }
+    // ---- D: trailing update of both triangles, columns / rows >= jend ----
+    grid_barrier(p.bar, P);
+    const int np = jend - j0;
+    const int m = a - jend;
+    const long long tot = (long long)m * m;
+    for (long long e = blockIdx.x * (long long)blockDim.x + tid; e < tot; e += (long long)P * blockDim.x) {
+      const int i = jend + (int)(e % m), k = jend + (int)(e / m);
+      double x = A[i + (size_t)a * k];
+      for (int q = 0; q < np; ++q)
+        x -= V[i + (size_t)a * q] * W[k + (size_t)a * q] + W[i + (size_t)a * q] * V[k + (size_t)a * q];
+      A[i + (size_t)a * k] = x;
+    }
+    grid_barrier(p.bar, P);
   }
-  for (int j = warp; j < rank; j += nw) {
-    const double* z = Q + (size_t)(a - 1 - j) * a;
-    double best = -1.0;
-    int bi = a;
-    for (int i = lane; i < a; i += 32) {
-      const double vv = fabs(z[i]);
-      if (vv > best) { best = vv; bi = i; }
+  // last 2 x 2 block (k_syev's tail convention)
+  if (blockIdx.x == 0 && tid == 0) {
+    if (a >= 2) {
+      p.tri[a - 2] = A[(a - 2) + (size_t)a * (a - 2)];
+      p.tri[a + a - 2] = A[(a - 1) + (size_t)a * (a - 2)];
+      p.tri[2 * a + a - 2] = 0.0;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    const double sgn = (z[bi] < 0.0) ? -1.0 : 1.0;
-    for (int i = lane; i < a; i += 32) p.UR[(size_t)j * a + i] = sgn * z[i];
+    p.tri[a - 1] = A[(a - 1) + (size_t)a * (a - 1)];
+    p.tri[a + a - 1] = 0.0;
+    p.tri[2 * a + a - 1] = 0.0;
   }
 }
 

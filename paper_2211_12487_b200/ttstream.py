@@ -213,6 +213,9 @@ class UpdateReport:
     tolerance_clamped: bool = False
     guard_reorthogonalised: int = 0
     modes_updated: int = 0
+    accurate_modes: int = 0
+    raw_fallbacks: int = 0
+    gram_only_unstable: int = 0
 
     @staticmethod
     def _from(r: _lib.Report) -> "UpdateReport":
@@ -223,7 +226,8 @@ class UpdateReport:
             ranks_after=[int(r.ranks_after[i]) for i in range(n)],
             eps_target=r.eps_target, batch_rel_error_estimate=r.batch_rel_error_estimate,
             seconds=r.seconds, tolerance_clamped=bool(r.tolerance_clamped),
-            guard_reorthogonalised=r.guard_reorthogonalised, modes_updated=r.modes_updated)
+            guard_reorthogonalised=r.guard_reorthogonalised, modes_updated=r.modes_updated,
+            accurate_modes=r.accurate_modes, raw_fallbacks=r.raw_fallbacks, gram_only_unstable=r.gram_only_unstable)
 
 
 @dataclass

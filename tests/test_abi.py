@@ -56,9 +56,24 @@ def test_ctypes_binding_covers_header():
 def test_struct_layouts_match_header():
     from paper_2211_12487_b200 import _lib
 
-    # ttg_report: 3 int64 + 2 int32 + 2*(33 int64) + 3 double + 2 int32
-    assert ctypes.sizeof(_lib.Report) == 3 * 8 + 2 * 4 + 2 * 33 * 8 + 3 * 8 + 2 * 4
+    # ttg_report: 3 int64 + 2 int32 + 2*(33 int64) + 3 double + 5 int32 (+ tail padding to 8)
+    assert ctypes.sizeof(_lib.Report) == 3 * 8 + 2 * 4 + 2 * 33 * 8 + 3 * 8 + 5 * 4 + 4
     assert ctypes.sizeof(_lib.Heuristics) == 8 + 4 * 4
+    # and the C compiler agrees with the ctypes mirror, field by field
+    import subprocess
+    import tempfile
+
+    fields = [f for f, _ in _lib.Report._fields_]
+    prog = "#include <stdio.h>\n#include <stddef.h>\n#include \"ttg.h\"\nint main(void){printf(\"%zu\", sizeof(ttg_report));"
+    prog += "".join(f'printf(" %zu", offsetof(ttg_report, {f}));' for f in fields) + "return 0;}\n"
+    with tempfile.TemporaryDirectory() as td:
+        src, exe = os.path.join(td, "s.c"), os.path.join(td, "s")
+        with open(src, "w") as f:
+            f.write(prog)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", exe, src], check=True)
+        got = [int(v) for v in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(_lib.Report)
+    assert got[1:] == [getattr(_lib.Report, f).offset for f in fields]
 
 
 def test_heuristics_default_from_library(lib):

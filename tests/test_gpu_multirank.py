@@ -29,6 +29,23 @@ def _free_port():
     return p
 
 
+def _increment(s, k, algo):
+    """Full (unsharded) increment k.  "star_skew": the first half of every
+    update increment is re-sampled inside the current span (rejected by the
+    subselection) and the second half carries the drift (selected), so with two
+    ranks one shard contributes no selected observation at all and the other
+    all of them (per-rank |D| = 0 / b/2)."""
+    y = s.increment(k)
+    if algo == "star_skew" and k >= 2 and k % 2 == 0:
+        h = s.batch // 2
+        y = np.concatenate([s.increment(k - 1)[..., :h], y[..., h:]], axis=-1)
+    return np.asfortranarray(y)
+
+
+def _n_inc(algo):
+    return 1 if algo == "boot" else N_INC
+
+
 def _worker(rank, world, port, algo, q):
     import torch
     import torch.distributed as dist
@@ -55,8 +72,8 @@ def _worker(rank, world, port, algo, q):
         bl = s.batch // world
         reps = []
         tt = None
-        for k in range(N_INC):
-            y = np.asfortranarray(s.increment(k)[..., rank * bl:(rank + 1) * bl])
+        for k in range(_n_inc(algo)):
+            y = np.asfortranarray(_increment(s, k, algo)[..., rank * bl:(rank + 1) * bl])
             if k == 0:
                 tt, rep = tt_ice_bootstrap(y, s.eps, ctx=ctx)
             elif algo == "ice":
@@ -75,7 +92,8 @@ def _worker(rank, world, port, algo, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("algo,world", [("ice", 2), ("star", 2), ("star", 4)])
+@pytest.mark.parametrize("algo,world", [("ice", 2), ("star", 2), ("star", 4), ("star_skew", 2), ("boot", 2),
+                                        ("boot", 4)])
 def test_ranks_on_one_gpu_match_unsharded_oracle(algo, world):
     import torch
     import torch.multiprocessing as mp
@@ -98,7 +116,7 @@ def test_ranks_on_one_gpu_match_unsharded_oracle(algo, world):
     assert res[0] == "ok", res
     _, reps, cores, ortho, bounds = res
     s = Stream(3, seed=5, modes=(6,) * 4, batch=16, true_rank=5)
-    ys = [s.increment(k) for k in range(N_INC)]
+    ys = [_increment(s, k, algo) for k in range(_n_inc(algo))]
     tr, rr = REF.tt_ice_bootstrap(ys[0], s.eps)
     ref = [rr]
     for y in ys[1:]:
@@ -108,11 +126,60 @@ def test_ranks_on_one_gpu_match_unsharded_oracle(algo, world):
         assert ranks == list(r.ranks_after)
         assert used == r.obs_used
         assert estimates_agree(est, r.batch_rel_error_estimate, pythagoras=(algo != "ice" or r.increment_index == 0))
+    if algo == "star_skew":  # the skew really happened: half the batch drove the update
+        assert any(used == s.batch // 2 for _, used, _ in reps[1:])
     tg = O.TensorTrain([O.TTCore(np.asfortranarray(c)) for c in cores], ortho, bounds)
     compare_trains(tg, tr)
     compare_reconstructions(tg, tr, list(enumerate(ys)))
     for p in procs:
         assert p.exitcode == 0
+
+
+def _mismatch_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2211_12487_b200 import Context, DimensionError, tt_ice_bootstrap
+        from paper_2211_12487_b200.streams import Stream
+
+        ctx = Context.with_host_collectives(0, rank, world, lambda a: dist.all_reduce(torch.from_numpy(a)),
+                                            lambda b: b)
+        y = np.asfortranarray(Stream(3, seed=5, modes=(6,) * 4, batch=8 + 2 * rank, true_rank=5).increment(0))
+        try:
+            tt_ice_bootstrap(y, 0.01, ctx=ctx)
+            q.put((rank, "no error"))
+        except DimensionError as e:
+            q.put((rank, str(e)))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_unequal_shard_sizes_rejected_on_every_rank():
+    """Shard sizes ride on the |Y|^2 all-reduce (global_obs): unequal per-rank
+    batches raise DimensionError on EVERY rank before anything is mutated (no
+    rank continues into collectives the others skip)."""
+    import torch
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    port = _free_port()
+    procs = [ctxm.Process(target=_mismatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    assert set(got) == {0, 1}
+    for r in (0, 1):
+        assert "same batch shard size" in got[r], got
 
 
 @pytest.mark.parametrize("algo", ["ice", "star"])
