@@ -141,7 +141,8 @@ struct ttg_ctx {
   } pf[2];
   cudaStream_t copy = nullptr;
   int pf_next = 0, pf_inuse = -1;
-  DevBuf trd;  // k_sytrd_grid panels, p, [d | e | tau], barrier
+  DevBuf trd;  // k_sytrd_grid p, [d | e | tau], barrier
+  std::vector<int> mode_hint;  // rank kept per mode at the previous increment (eig block-attempt hint)
   std::string err;
   int64_t launches = 0;
   int num_sms = 148;
@@ -1047,7 +1048,11 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
 // ---- eigen-solve -------------------------------------------------------------
 // factor == 0: G is the residual Gram -> tridiagonal solver (k_syev).
 // factor == 1: G holds the TSQR factor T -> one-sided Jacobi on T^T (k_jacobi_eig).
-EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double delta_mult, int factor = 0) {
+// hint: the rank this mode kept at the previous increment (-1: unknown).  A
+// block attempt whose Gram does not fit shared memory costs ~40 L2 passes of
+// G when it fails, so it is skipped when the hint says the block is too small.
+EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double delta_mult, int factor = 0,
+              int hint = -1) {
   c->UR.ensure(sizeof(double) * (size_t)a * a);
   c->lam.ensure(sizeof(double) * a);
   c->eigres.ensure(sizeof(EigResult));
@@ -1079,6 +1084,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         if (smem_s <= kcap) {
           sa.in_smem = 1;
         } else {
+          if (hint >= K - 1) continue;  // G from L2 and the last solve kept more than this block can
           sa.in_smem = 0;
           smem_s = sub_vec;
         }
@@ -1115,21 +1121,24 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         // phases on the result (reflectors in W, tri = [d | e | tau])
         c->W.ensure(sizeof(double) * (size_t)a * a);
         CK(cudaMemcpyAsync(c->W.p, c->G.p, sizeof(double) * (size_t)a * a, cudaMemcpyDeviceToDevice, c->stream));
-        c->trd.ensure(sizeof(double) * ((size_t)2 * ttg::kTrdPanel * a + 4 * (size_t)a) + 64);
+        c->trd.ensure(sizeof(double) * 4 * (size_t)a + 64);
         ttg::TrdArgs ta{};
         ta.A = c->W.as<double>();
         ta.a = a;
-        ta.V = c->trd.as<double>();
-        ta.W = ta.V + (size_t)ttg::kTrdPanel * a;
-        ta.pbuf = ta.W + (size_t)ttg::kTrdPanel * a;
+        ta.pbuf = c->trd.as<double>();
         ta.tri = ta.pbuf + a;
         ta.bar = reinterpret_cast<unsigned*>(ta.tri + 3 * (size_t)a);
         CK(cudaMemsetAsync(ta.bar, 0, 2 * sizeof(unsigned), c->stream));
-        const size_t tsm = sizeof(double) * 5 * (size_t)a;
+        // panel width: the widest of 16 / 8 / 4 / 2 whose (3 + 2 nb) a doubles fit one CTA
+        const size_t tcap = dyn_smem_cap((const void*)ttg::k_sytrd_grid);
+        ta.nb = 16;
+        while (ta.nb > 2 && sizeof(double) * (3 + 2 * (size_t)ta.nb) * a > tcap) ta.nb /= 2;
+        const size_t tsm = sizeof(double) * (3 + 2 * (size_t)ta.nb) * a;
+        if (tsm > tcap) fail(TTG_E_RESOURCE, "eigen-solve of a " + std::to_string(a) + "-row Gram exceeds the device solver");
         const int occ = kernel_occupancy((const void*)ttg::k_sytrd_grid, ttg::k_sytrd_grid, ttg::kTrdThreads, tsm);
         if (occ < 1) fail(TTG_E_RESOURCE, "tridiagonalisation kernel does not fit on an SM");
-        const int want = std::getenv("TTG_TRD_CTAS") ? std::atoi(std::getenv("TTG_TRD_CTAS")) : 32;
-        const int nblk = std::max(1, std::min({want, c->num_sms * occ, (a + 31) / 32}));
+        const int want = std::getenv("TTG_TRD_CTAS") ? std::atoi(std::getenv("TTG_TRD_CTAS")) : c->num_sms;
+        const int nblk = std::max(1, std::min({want, c->num_sms * occ, (a + 3) / 4}));
         char nm[64];
         std::snprintf(nm, sizeof nm, "k_sytrd_grid[a=%d]", a);
         prof_begin(c, nm, 24.0 * a * a, 4.0 / 3.0 * a * a * a);
@@ -1158,6 +1167,16 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
       prof_begin(c, nm, 16.0 * a * a, args.tri ? 2.0 * a * a : 4.0 / 3.0 * a * a * a);
       launch_k(c, ttg::k_syev, 1, ttg::kSyevThreads, smem, args);
       post_launch(c);
+      if (args.tri) {  // back-transform of the kept vectors, one warp each, over the grid
+        const long long kcap = std::min<long long>(kmax, a);
+        const size_t bsm = sizeof(double) * ttg::kBtWarps * (size_t)a;
+        kernel_occupancy((const void*)ttg::k_syev_bt, ttg::k_syev_bt, ttg::kBtWarps * 32, bsm);
+        prof_begin(c, "k_syev_bt", 8.0 * a * a / 2, 4.0 * a * a / 2);
+        launch_k(c, ttg::k_syev_bt, (unsigned)std::max<long long>(1, (kcap + ttg::kBtWarps - 1) / ttg::kBtWarps),
+                 ttg::kBtWarps * 32, bsm, (const double*)c->W.as<double>(), a, (const double*)(args.tri + 2 * (size_t)a),
+                 (const ttg::EigResult*)c->eigres.as<EigResult>(), c->UR.as<double>());
+        post_launch(c);
+      }
     }
   } else {
     size_t need_smem = sizeof(double) * ((size_t)a * a + a) + sizeof(int) * a + 64;
@@ -1637,7 +1656,8 @@ struct NoColl {
 // thousands (configs[2] modes 6-7: a ~ 3000, L = 96 / 32) at the cost of an
 // L x L eigen-solve; the accurate path needs L <= 128, not a.
 EigResult tall_eig(ttg_ctx* c, const Src& src, int64_t n_i, const double* U, int r_old, const uint8_t* sel,
-                   long long cpo, long long kmax, const double* dsrc, double dmult, int& accurate, int& unstable) {
+                   long long cpo, long long kmax, const double* dsrc, double dmult, int hint, int& accurate,
+                   int& unstable) {
   const int64_t a = src.r * n_i;
   const long long L = src.Ls / n_i;
   const double* X = materialise(c, src, n_i, c->matbuf);
@@ -1665,7 +1685,7 @@ EigResult tall_eig(ttg_ctx* c, const Src& src, int64_t n_i, const double* U, int
   NoColl nc(c);  // every rank now holds the same Rg: local, identical solves
   c->G.ensure(sizeof(double) * (size_t)(Lg * Lg));
   gemm<true, false>(c, Rg, a, Rg, a, c->G.as<double>(), Lg, Lg, Lg, a, 1.0, 0.0);  // R^T R (exactly symmetric)
-  EigResult er = eig(c, (int)Lg, kmax, dsrc, dmult);
+  EigResult er = eig(c, (int)Lg, kmax, dsrc, dmult, 0, hint);
   if (needs_accurate(er)) {
     if (accurate_supported((int)Lg, 0)) {
       c->tallXt.ensure(sizeof(double) * (size_t)(a * Lg));
@@ -1933,11 +1953,13 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         norm_checked = true;
       }
       const long long kmax = o.star ? o.n_sel_global * cpo : Lg;
+      if ((int)c->mode_hint.size() < d) c->mode_hint.assign(d, -1);
       EigResult er = tall_eig(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, o.star ? o.sel : nullptr, cpo,
-                              kmax, dsrc, dmult, out.accurate_modes, out.gram_only_unstable);
+                              kmax, dsrc, dmult, c->mode_hint[i], out.accurate_modes, out.gram_only_unstable);
       r_R = er.rank;
       out.discarded_sq += er.tail_sq;
       out.tall_modes++;
+      c->mode_hint[i] = (int)r_R;
     } else if (run_svd) {
       const uint8_t* sel = o.star ? o.sel : nullptr;
       const int64_t rows = src.Psi ? src.As * n_i : a;
@@ -1955,7 +1977,8 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       }
       const long long kmax = o.star ? o.n_sel_global * cpo : L * c->world;
       trace("sweep:gram launched");
-      EigResult er = eig(c, (int)a, kmax, dsrc, dmult);
+      if ((int)c->mode_hint.size() < d) c->mode_hint.assign(d, -1);
+      EigResult er = eig(c, (int)a, kmax, dsrc, dmult, 0, c->mode_hint[i]);
       trace("sweep:eig done");
       if (raw && er.rank > 0 && r_old > 0) {  // no projector (empty basis): C is G exactly
         // raw-Gram cancellation costs ~eps*tr(C)/gap in the kept vectors: keep
@@ -1963,7 +1986,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         const double trC = c->h_scal[8];  // trace(C), fetched with the eigen result
         if (er.lam_min_kept < 1e-3 * trC) {
           gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, nullptr);
-          er = eig(c, (int)a, kmax, dsrc, dmult);
+          er = eig(c, (int)a, kmax, dsrc, dmult, 0, er.rank);
           out.raw_fallbacks++;
         }
       }
@@ -1982,6 +2005,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       }
       r_R = er.rank;
       out.discarded_sq += er.tail_sq;
+      c->mode_hint[i] = (int)r_R;
     }
     int64_t r_new;
     bool zero_next = false;
@@ -2206,21 +2230,20 @@ const double* interface_gram_compute(ttg_ctx* c, const ttg_tt* tt) {
     post_launch(c);
     return c->iface[0].as<double>();
   }
+  // large ranks: M_i = C_i^T (M_{i-1} C_i) per core on the DMMA GEMM, with C_i
+  // viewed as r_{i-1} x (n r_i) for the first product and as (r_{i-1} n) x r_i
+  // for the second (the same column-major buffer)
+  c->iface[0].ensure(sizeof(double) * rmax * rmax);
+  c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
   const double one = 1.0;
   CK(cudaMemcpyAsync(c->iface[0].p, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
   int f = 0;
   for (int i = 0; i < tt->d; ++i) {
-    const int rl = (int)tt->ranks[i], n = (int)tt->modes[i], rr = (int)tt->ranks[i + 1];
-    const long long t1 = (long long)rl * n * rr;
-    prof_begin(c, "k_iface", 8.0 * t1, 2.0 * t1 * rl);
-    launch_k(c, ttg::k_iface_step1, grid_for(t1, 256, 1024), 256, 0, c->iface[f].as<double>(),
-                                                                        tt->cores[i].as<double>(), rl, n, rr,
-                                                                        c->Mtmp.as<double>());
-    post_launch(c);
-    prof_begin(c, "k_iface", 8.0 * rr * rr, 2.0 * rr * rr * n * rl);
-    launch_k(c, ttg::k_iface_step2, grid_for((long long)rr * rr, 128, 1024), 128, 0, 
-        c->Mtmp.as<double>(), tt->cores[i].as<double>(), rl, n, rr, c->iface[f ^ 1].as<double>());
-    post_launch(c);
+    const long long rl = tt->ranks[i], n = tt->modes[i], rr = tt->ranks[i + 1];
+    const double* C = tt->cores[i].as<double>();
+    double* T = c->Mtmp.as<double>();
+    gemm<false, false>(c, c->iface[f].as<double>(), rl, C, rl, T, rl, rl, n * rr, rl, 1.0, 0.0);
+    gemm<true, false>(c, C, rl * n, T, rl * n, c->iface[f ^ 1].as<double>(), rr, rr, rr, rl * n, 1.0, 0.0);
     f ^= 1;
   }
   return c->iface[f].as<double>();
@@ -2603,11 +2626,11 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
         (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
         (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
-        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
+        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,
-        (const void*)ttg::k_iface_step1, (const void*)ttg::k_iface_step2, (const void*)ttg::k_iface_all, (const void*)ttg::k_build_q, (const void*)ttg::k_syrk_ws16<1, 1>, (const void*)ttg::k_syrk_ws16<3, 1>,
+        (const void*)ttg::k_iface_all, (const void*)ttg::k_build_q, (const void*)ttg::k_syrk_ws16<1, 1>, (const void*)ttg::k_syrk_ws16<3, 1>,
         (const void*)ttg::k_syrk_ws16<6, 1>, (const void*)ttg::k_syrk_ws16<10, 1>, (const void*)ttg::k_syrk_ws16<5, 3>,
         (const void*)ttg::k_syrk_ws16<7, 3>, (const void*)ttg::k_syrk_ws16<14, 2>, (const void*)ttg::k_syrk_ws16<12, 3>, (const void*)ttg::k_coef_stats,
         (const void*)ttg::k_star_local, (const void*)ttg::k_star_mask, (const void*)ttg::k_mask_cols,
@@ -2825,6 +2848,10 @@ int ttg_prefetch(ttg_ctx* c, const double* y, int64_t n) {
     const int i = c->pf_next;
     c->pf_next ^= 1;
     auto& s = c->pf[i];
+    // an older, never consumed copy of the same host buffer is stale now (the
+    // caller may have refilled it): only the newest prefetch may be consumed
+    auto& o = c->pf[i ^ 1];
+    if (o.valid && o.src == y && o.n == n) o.valid = false;
     if (s.used) CK(cudaStreamWaitEvent(c->copy, s.freed, 0));  // an earlier update may still read this slot
     s.buf.ensure(sizeof(double) * (size_t)std::max<int64_t>(n, 1), false, c->copy);
     CK(cudaMemcpyAsync(s.buf.p, y, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->copy));

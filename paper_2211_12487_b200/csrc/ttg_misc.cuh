@@ -98,37 +98,6 @@ __global__ void k_pad_core(const double* __restrict__ core, int r_old, int n, in
   }
 }
 
-// M_new = sum_j G_j^T M G_j  (G_j = core[:, j, :], r_l x r_r), two steps via scratch T.
-__global__ void k_iface_step1(const double* __restrict__ M, const double* __restrict__ core, int rl,
-                              int n, int rr, double* __restrict__ T) {
-  griddep_wait();
-  // T[p', j, q] = sum_p M[p', p] core[p, j, q]
-  long long tot = (long long)rl * n * rr;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
-       e += (long long)gridDim.x * blockDim.x) {
-    int pp = (int)(e % rl);
-    long long rest = e / rl;
-    double s = 0.0;
-    for (int p = 0; p < rl; ++p) s = fma(M[pp + (long long)rl * p], core[p + (long long)rl * rest], s);
-    T[e] = s;
-  }
-}
-__global__ void k_iface_step2(const double* __restrict__ T, const double* __restrict__ core, int rl,
-                              int n, int rr, double* __restrict__ Mn) {
-  griddep_wait();
-  // Mn[q, q'] = sum_{j, p'} core[p', j, q] T[p', j, q']
-  long long tot = (long long)rr * rr;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
-       e += (long long)gridDim.x * blockDim.x) {
-    int q = (int)(e % rr), q2 = (int)(e / rr);
-    double s = 0.0;
-    for (int j = 0; j < n; ++j)
-      for (int pp = 0; pp < rl; ++pp)
-        s = fma(core[pp + (long long)rl * (j + (long long)n * q)],
-                T[pp + (long long)rl * (j + (long long)n * q2)], s);
-    Mn[e] = s;
-  }
-}
 
 // The whole interface chain in one launch (one block, sequential over the
 // modes, steps separated by block barriers; intermediates in global/L2):

@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(kSyevThreads) k_syev(SyevArgs p) {
       }
     }
     __syncthreads();
-    if (j < rank) {
+    if (j < rank && p.tri) {  // multi-CTA back-transform and sign rule follow (k_syev_bt)
+      for (int i = lane; i < a; i += 32) p.UR[(size_t)j * a + i] = z[i];
+    } else if (j < rank) {
       // back-transform: u = H_0 ... H_{a-3} z ; H_k acts on rows k+1.. with v_k = [1; A[k+2.., k]]
       for (int k = a - 3; k >= 0; --k) {
         const double tk = tau[k];
@@ -1021,31 +1023,28 @@ namespace ttg {
 
 // ---------------------------------------------------------------------------
 // Multi-CTA Householder tridiagonalisation Q^T G Q = T for the large Grams
-// (a > ~256) that neither fit one CTA's shared memory nor keep few enough
+// (a > ~160) that do not fit one CTA's shared memory and keep too many
 // directions for the block subspace path (replaces cuSOLVER syevd).  LAPACK
 // dsytd2 'L' numerics with dlatrd's lazy panel update, on P co-resident CTAs
-// (cooperative launch, one grid barrier per column):
-//   A  step j (panel column jj): every CTA rebuilds the updated column j,
-//      a_j = A[:, j] - V W[j,:]^T - W V[j,:]^T (q < jj), and its reflector
-//      (identical bytes on every CTA: same code, same order);
-//   B  its rows of p = (A - V W^T - W V^T) v (row i = column i: symmetric
-//      storage, contiguous reads), then the grid barrier;
-//   C  every CTA reads p, forms w = tau p - tau/2 (tau p^T v) v and writes its
-//      rows into the panel W (the latest v, w stay in shared memory for the
-//      next step, so no second barrier);
-//   D  panel end (nb columns): A_trailing -= V W^T + W V^T (both triangles),
-//      between two barriers.
-// Output: d, e, tau (tri = [d | e | tau]) and the reflectors' essential parts in
-// A's columns below the subdiagonal -- the layout k_syev's phases 2-3 consume.
+// (cooperative launch, one grid barrier per column).  Every CTA holds the
+// whole current panel V, W (a x nb) in shared memory -- each computes every
+// v and w itself, from identical inputs in the same order, so the copies are
+// bitwise identical and no panel traffic crosses the grid:
+//   A  step j (panel column jj): the updated column
+//      a_j = A[:, j] - V W[j,:]^T - W V[j,:]^T (q < jj) and its reflector v;
+//   B  this CTA's rows of p = (A - V W^T - W V^T) v (row i = column i of the
+//      symmetric storage: contiguous reads), then the grid barrier;
+//   C  w = tau p - tau/2 (tau p^T v) v from the gathered p, appended to W;
+//   D  panel end: A_trailing -= V W^T + W V^T (both triangles), then a barrier.
+// Output: d, e, tau (tri = [d | e | tau]) and the reflectors' essential parts
+// in A's columns below the subdiagonal -- the layout of k_syev phases 2-3.
 // ---------------------------------------------------------------------------
 constexpr int kTrdThreads = 512;
-constexpr int kTrdPanel = 16;
 
 struct TrdArgs {
   double* A;        // a x a (copy of G), overwritten
   int a;
-  double* V;        // a x kTrdPanel panel
-  double* W;        // a x kTrdPanel panel
+  int nb;           // panel width (shared memory: (3 + 2 nb) a doubles)
   double* pbuf;     // a
   double* tri;      // 3a: d, e, tau
   unsigned* bar;    // [count, generation], zeroed by the host
@@ -1073,31 +1072,26 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
   griddep_wait();  // launched cooperatively without PDL: a no-op, kept for the invariant
   extern __shared__ __align__(16) double tsm[];
   __shared__ double red[kTrdThreads / 32 + 1];
-  __shared__ double vtw[2 * kTrdPanel];  // W^T v, V^T v of the current step
-  const int a = p.a, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ double vtw[2 * 64];
+  const int a = p.a, nb = p.nb, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const unsigned P = gridDim.x;
   double* A = p.A;
-  double* col = tsm;        // updated column j (rows j..a-1), then v (rows j+1..)
-  double* v = tsm + a;      // current v (rows 0..a-1, zero above j+1)
-  double* vp = v + a;       // previous step's v
-  double* wp = vp + a;      // previous step's w
-  double* pv = wp + a;      // p / w of the current step
-  const double* V = p.V;
-  const double* W = p.W;
-  for (int j0 = 0; j0 + 2 < a; j0 += kTrdPanel) {
-    const int jend = min(j0 + kTrdPanel, a - 2);  // columns j0 .. jend-1 in this panel
+  double* col = tsm;          // updated column j
+  double* v = col + a;        // reflector of step j (zero above j + 1)
+  double* pv = v + a;         // tau p of step j
+  double* Vs = pv + a;        // panel V (a x nb)
+  double* Ws = Vs + (size_t)a * nb;  // panel W (a x nb)
+  const int rows_per = (a + (int)P - 1) / (int)P;
+  const int r0 = (int)blockIdx.x * rows_per, r1 = min(a, r0 + rows_per);
+  for (int j0 = 0; j0 + 2 < a; j0 += nb) {
+    const int jend = min(j0 + nb, a - 2);  // columns j0 .. jend-1 in this panel
     for (int j = j0; j < jend; ++j) {
       const int jj = j - j0;
       // ---- A: updated column j and its reflector (every CTA) ----
       for (int i = j + tid; i < a; i += blockDim.x) {
         double x = A[i + (size_t)a * j];
-        for (int q = 0; q < jj; ++q) {
-          const double vq = (q == jj - 1) ? vp[i] : V[i + (size_t)a * q];
-          const double wq = (q == jj - 1) ? wp[i] : W[i + (size_t)a * q];
-          const double vjq = (q == jj - 1) ? vp[j] : V[j + (size_t)a * q];
-          const double wjq = (q == jj - 1) ? wp[j] : W[j + (size_t)a * q];
-          x -= vq * wjq + wq * vjq;
-        }
+        for (int q = 0; q < jj; ++q)
+          x -= Vs[i + (size_t)a * q] * Ws[j + (size_t)a * q] + Ws[i + (size_t)a * q] * Vs[j + (size_t)a * q];
         col[i] = x;
       }
       __syncthreads();
@@ -1112,7 +1106,6 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
         tk = (beta - alpha) / beta;
       }
       const double sc = xs != 0.0 ? 1.0 / (alpha - beta) : 0.0;
-      // v: rows j+1.. (v[j+1] = 1); zero elsewhere
       for (int i = tid; i < a; i += blockDim.x) v[i] = (i <= j) ? 0.0 : (i == j + 1 ? 1.0 : col[i] * sc);
       if (blockIdx.x == 0 && tid == 0) {
         p.tri[j] = col[j];
@@ -1120,19 +1113,11 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
         p.tri[2 * a + j] = tk;
       }
       __syncthreads();
-      // V[:, jj] = v: each CTA writes its own row slice (read back only after a barrier)
-      const int rows_per = (a + (int)P - 1) / (int)P;
-      const int r0 = (int)blockIdx.x * rows_per, r1 = min(a, r0 + rows_per);
-      for (int i = r0 + tid; i < r1; i += blockDim.x) p.V[i + (size_t)a * jj] = v[i];
       // ---- B: W^T v, V^T v (q < jj), then this CTA's rows of p ----
       for (int q = warp; q < 2 * jj; q += nw) {
-        const int qq = q % jj;
-        const bool isw = q < jj;
+        const double* m = (q < jj ? Ws : Vs) + (size_t)a * (q % jj);
         double s = 0.0;
-        for (int i = j + 1 + lane; i < a; i += 32) {
-          const double m = (qq == jj - 1) ? (isw ? wp[i] : vp[i]) : (isw ? W : V)[i + (size_t)a * qq];
-          s = fma(m, v[i], s);
-        }
+        for (int i = j + 1 + lane; i < a; i += 32) s = fma(m[i], v[i], s);
         s = warp_sum(s);
         if (lane == 0) vtw[q] = s;
       }
@@ -1143,11 +1128,7 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
         for (int k = j + 1 + lane; k < a; k += 32) s = fma(ci[k], v[k], s);
         s = warp_sum(s);
         if (lane == 0) {
-          for (int q = 0; q < jj; ++q) {
-            const double vq = (q == jj - 1) ? vp[i] : V[i + (size_t)a * q];
-            const double wq = (q == jj - 1) ? wp[i] : W[i + (size_t)a * q];
-            s -= vq * vtw[q] + wq * vtw[jj + q];
-          }
+          for (int q = 0; q < jj; ++q) s -= Vs[i + (size_t)a * q] * vtw[q] + Ws[i + (size_t)a * q] * vtw[jj + q];
           p.pbuf[i] = s;
         }
       }
@@ -1155,26 +1136,24 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
       // every CTA has read column j (step A): store the reflector in it
       if (blockIdx.x == 0)
         for (int i = j + 2 + tid; i < a; i += blockDim.x) A[i + (size_t)a * j] = v[i];
-      // ---- C: w = tau p + alpha2 v (every CTA, full length) ----
+      // ---- C: w = tau p + alpha2 v (every CTA, full length) -> panel ----
       double pvs = 0.0;
       for (int i = j + 1 + tid; i < a; i += blockDim.x) {
-        const double w0 = tk * p.pbuf[i];
+        const double w0 = tk * __ldcg(p.pbuf + i);
         pv[i] = w0;
         pvs = fma(w0, v[i], pvs);
       }
       pvs = block_sum_all(pvs, red);
       const double al2 = -0.5 * tk * pvs;
       for (int i = tid; i < a; i += blockDim.x) {
-        const double wi = (i <= j) ? 0.0 : fma(al2, v[i], pv[i]);
-        wp[i] = wi;
-        vp[i] = v[i];
+        Ws[i + (size_t)a * jj] = (i <= j) ? 0.0 : fma(al2, v[i], pv[i]);
+        Vs[i + (size_t)a * jj] = v[i];
       }
       __syncthreads();
-      for (int i = r0 + tid; i < r1; i += blockDim.x) p.W[i + (size_t)a * jj] = wp[i];
-      __syncthreads();
     }
-    // ---- D: trailing update of both triangles, columns / rows >= jend ----
-    grid_barrier(p.bar, P);
+    // ---- D: trailing update of both triangles, rows / columns >= jend ----
+    // (every CTA finished step B of the panel's last column at its barrier;
+    // nothing reads A between there and here)
     const int np = jend - j0;
     const int m = a - jend;
     const long long tot = (long long)m * m;
@@ -1182,7 +1161,7 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
       const int i = jend + (int)(e % m), k = jend + (int)(e / m);
       double x = A[i + (size_t)a * k];
       for (int q = 0; q < np; ++q)
-        x -= V[i + (size_t)a * q] * W[k + (size_t)a * q] + W[i + (size_t)a * q] * V[k + (size_t)a * q];
+        x -= Vs[i + (size_t)a * q] * Ws[k + (size_t)a * q] + Ws[i + (size_t)a * q] * Vs[k + (size_t)a * q];
       A[i + (size_t)a * k] = x;
     }
     grid_barrier(p.bar, P);
@@ -1198,6 +1177,50 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
     p.tri[a + a - 1] = 0.0;
     p.tri[2 * a + a - 1] = 0.0;
   }
+}
+
+// Back-transform of the kept eigenvectors of T (k_syev in tri mode leaves the
+// inverse-iteration vectors z in UR): u = H_0 ... H_{a-3} z with the reflectors
+// of k_sytrd_grid (v_k = [1; A[k+2.., k]]), then the sign rule (largest-|.|
+// entry, first index, positive: truncated_svd.cpp:16-25).  One warp per
+// vector, vectors spread over the grid; rank read from the eigen result.
+constexpr int kBtWarps = 4;
+__global__ void __launch_bounds__(kBtWarps * 32) k_syev_bt(const double* __restrict__ A, int a,
+                                                            const double* __restrict__ tau, const EigResult* res,
+                                                            double* __restrict__ UR) {
+  griddep_wait();
+  extern __shared__ __align__(16) double bsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x * kBtWarps + warp;
+  if (j >= res->rank) return;
+  double* z = bsm + (size_t)warp * a;
+  double* u = UR + (size_t)j * a;
+  for (int i = lane; i < a; i += 32) z[i] = u[i];
+  __syncwarp();
+  for (int k = a - 3; k >= 0; --k) {
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    const double* vk = A + (size_t)a * k;
+    double s = (lane == 0) ? z[k + 1] : 0.0;
+    for (int i = k + 2 + lane; i < a; i += 32) s = fma(vk[i], z[i], s);
+    s = warp_sum(s) * tk;
+    if (lane == 0) z[k + 1] -= s;
+    for (int i = k + 2 + lane; i < a; i += 32) z[i] -= s * vk[i];
+    __syncwarp();
+  }
+  double best = -1.0;
+  int bi = a;
+  for (int i = lane; i < a; i += 32) {
+    const double vv = fabs(z[i]);
+    if (vv > best) { best = vv; bi = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  const double sgn = (z[bi] < 0.0) ? -1.0 : 1.0;
+  for (int i = lane; i < a; i += 32) u[i] = sgn * z[i];
 }
 
 }  // namespace ttg

@@ -99,7 +99,7 @@ def test_fullsize_against_reference(ctx, name):
             tg, rg = tt_ice_update(tg, y, eps, shape=shape)
         else:
             tg, rg = tt_ice_star_update(tg, y, eps, shape=shape)
-        compare_reports(rg, _report(fx, k, shape[-1]), star=(algo != "ice"))
+        compare_reports(rg, _report(fx, k, shape[-1]), star=(algo != "ice"), n_elems=int(np.prod(shape)))
         b, e = tg.increment_range(k)
         err = rre(tg, y, b, e, shape=shape)
         worst["rre"] = max(worst["rre"], abs(err - float(fx["rre"][k])))

@@ -38,7 +38,7 @@ def run_stream(ctx, stream, n_inc, algo="ice", cfg=None, check_every=1, eps=None
             ocfg = O.HeuristicConfig(**vars(cfg)) if cfg else O.HeuristicConfig()
             tg, rg = tt_ice_star_update(tg, y, eps, cfg)
             tr, rr = REF.tt_ice_star_update(tr, y, eps, ocfg)
-        compare_reports(rg, rr, star=(algo != "ice"))
+        compare_reports(rg, rr, star=(algo != "ice"), n_elems=y.size)
         if k % check_every == 0 or k == n_inc - 1:
             compare_trains(tg, tr)
     gh = to_oracle(tg)
@@ -383,6 +383,25 @@ def test_prefetch_host_increments(ctx):
         assert np.array_equal(ca, cb)
 
 
+def test_prefetch_refilled_buffer_is_not_stale(ctx):
+    """ttg_prefetch of a buffer that is never consumed, then refilled and
+    prefetched again: the update must read the NEW contents (only the newest
+    prefetch of a host pointer may be consumed)."""
+    st = Stream(3, seed=6, modes=(4,) * 5, batch=8)
+    y0, y1, y2 = (np.asfortranarray(st.increment(k)) for k in range(3))
+    ta, _ = tt_ice_bootstrap(y0, st.eps, ctx=ctx)
+    tb, _ = tt_ice_bootstrap(y0, st.eps, ctx=ctx)
+    buf = np.asfortranarray(y1.copy())
+    ctx.prefetch(buf)           # slot A <- y1 (never consumed)
+    buf[...] = y2               # the caller refills the same host buffer
+    ctx.prefetch(buf)           # slot B <- y2; slot A must be invalidated
+    ta, ra = tt_ice_star_update(ta, buf, st.eps)
+    tb, rb = tt_ice_star_update(tb, y2, st.eps)
+    assert ra.ranks_after == rb.ranks_after
+    for ca, cb in zip(ta.cores(), tb.cores()):
+        assert np.array_equal(ca, cb)
+
+
 def test_device_io_ordered_against_torch_stream(ctx):
     """Device increments produced by torch and device results consumed by torch
     without any host synchronisation (ttg_ctx_wait_stream / ttg_ctx_join_stream):
@@ -400,11 +419,13 @@ def test_device_io_ordered_against_torch_stream(ctx):
     th.close()
     td = None
     for k, y in enumerate(ys):
-        dev = torch.from_numpy(np.ravel(y, order="F")).cuda()
+        src = torch.from_numpy(np.ravel(y, order="F")).cuda()
+        torch.cuda.synchronize()
+        dev = torch.zeros_like(src)  # the increment's bytes are written only by the queued copy below
         big = torch.randn(1 << 26, device="cuda", dtype=torch.float64)  # keeps torch's stream busy
         for _ in range(4):
             big.mul_(1.0000001)
-        dev.mul_(2.0).mul_(0.5)  # the last writes of the increment are queued behind the big kernels
+        dev.copy_(src)  # queued behind the big kernels: an update reading early sees zeros
         if k == 0:
             td, _ = tt_ice_bootstrap(dev, s.eps, ctx=ctx, shape=y.shape)
         else:
