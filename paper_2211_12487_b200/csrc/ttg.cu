@@ -1084,7 +1084,10 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         if (smem_s <= kcap) {
           sa.in_smem = 1;
         } else {
-          if (hint >= K - 1) continue;  // G from L2 and the last solve kept more than this block can
+          // G from L2: each failed iteration re-reads it, so only try when the
+          // last solve of this mode kept fewer directions than the block holds
+          // (and, above a = 512, only when that is known)
+          if (hint >= K - 1 || (a > 512 && hint < 0)) continue;
           sa.in_smem = 0;
           smem_s = sub_vec;
         }
@@ -1930,7 +1933,6 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     const long long L = src.Ls / n_i;
     const long long cpo = L / b;
     const bool was_unchanged = unchanged;
-    if (a > 4096) fail(TTG_E_RESOURCE, "unfolding rows a_i = " + std::to_string(a) + " exceed the device solver limit");
     const double* dsrc = o.deltas ? nullptr : o.delta_src;
     const double dmult = o.deltas ? o.deltas[i] : o.delta_mult;
     int64_t r_R = 0;
@@ -1945,7 +1947,13 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       run_svd = !big;
     }
     const long long Lg = L * c->world;
-    const bool tall = run_svd && a > kFastMax && (double)a > 2.0 * (double)Lg && !std::getenv("TTG_NO_TALL");
+    // tall: the reference's own QR branch (a > 2 L, truncated_svd.cpp:51-59), and
+    // any a x L residual too large for one CTA's shared memory whose L x L side
+    // is the smaller eigen-problem
+    const bool tall = run_svd && a > kFastMax && !std::getenv("TTG_NO_TALL") &&
+                      ((double)a > 2.0 * (double)Lg || (a > 256 && Lg < a));
+    if (run_svd && !tall && a > 4096)
+      fail(TTG_E_RESOURCE, "unfolding rows a_i = " + std::to_string(a) + " exceed the device solver limit");
     if (tall) {
       if (nm.pending && src.S == nm.Y) norms_finish(c, nm, 0, false);
       if (!norm_checked && !nm.pending) {
