@@ -150,7 +150,8 @@ struct ttg_ctx {
   // workspaces (grow-only)
   DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, UTt, Uf, Upad, scratch, eigres, on2, sumsq_part,
       scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2], tsq, psif, wcomb, psi[2],
-      spsi[2], scoeffs, matbuf, tmp, Craw, small[4], gcount, gemm_ws, tallR, tallRg, tallXt, UR2;
+      spsi[2], scoeffs, matbuf, tmp, Craw, small[4], gcount, gemm_ws, gemm_ws_side, iface_T, tallR, tallRg, tallXt,
+      UR2;
   std::vector<DevBuf> scur;       // TT-ICE* stats-chain intermediates (reused by the sweep)
   std::vector<bool> stat_has;
   ttg::EigResult* h_eig = nullptr;
@@ -440,9 +441,10 @@ void make_frags(ttg_ctx* c, const double* U, int a, int r, int ld, bool need_ut,
 // C = alpha op(A) op(B) + beta C (column-major) on the DMMA GEMM (ttg_gemm.cuh):
 // every plain GEMM of the sweep, small or large.  Few output tiles with a long
 // k (R^T R, append Grams) split k over grid z with a fixed-order reduction.
+// ws: split-k workspace (default c->gemm_ws; GEMMs on the side stream pass their own)
 template <bool TA, bool TB>
 void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
-          long long m, long long n, long long k, double alpha, double beta) {
+          long long m, long long n, long long k, double alpha, double beta, DevBuf* ws = nullptr) {
   if (m == 0 || n == 0) return;
   ttg::DgemmArgs a{A, lda, B, ldb, C, ldc, m, n, k, alpha, beta, 0, nullptr};
   const bool big = m > 64;
@@ -460,8 +462,9 @@ void gemm(ttg_ctx* c, const double* A, long long lda, const double* B, long long
   nz = (int)std::max<long long>(1, (k + a.kchunk - 1) / std::max<long long>(a.kchunk, 1));
   if (k == 0) a.kchunk = ttg::kGemmBK;
   if (nz > 1) {
-    c->gemm_ws.ensure(sizeof(double) * (size_t)nz * m * n);
-    a.ws = c->gemm_ws.as<double>();
+    DevBuf& w = ws ? *ws : c->gemm_ws;
+    w.ensure(sizeof(double) * (size_t)nz * m * n);
+    a.ws = w.as<double>();
   }
   auto kern = big ? ttg::k_dgemm<TA, TB, 128> : ttg::k_dgemm<TA, TB, 64>;
   const size_t smem = big ? ttg::dgemm_smem<128>() : ttg::dgemm_smem<64>();
@@ -1170,13 +1173,16 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
       prof_begin(c, nm, 16.0 * a * a, args.tri ? 2.0 * a * a : 4.0 / 3.0 * a * a * a);
       launch_k(c, ttg::k_syev, 1, ttg::kSyevThreads, smem, args);
       post_launch(c);
-      if (args.tri) {  // back-transform of the kept vectors, one warp each, over the grid
+      if (args.tri) {  // back-transform of the kept vectors, VB per CTA, over the grid
         const long long kcap = std::min<long long>(kmax, a);
-        const size_t bsm = sizeof(double) * ttg::kBtWarps * (size_t)a;
-        kernel_occupancy((const void*)ttg::k_syev_bt, ttg::k_syev_bt, ttg::kBtWarps * 32, bsm);
+        const bool wide = (size_t)8 * a * sizeof(double) <= (size_t)c->smem_optin - 4096;
+        const int vb = wide ? 8 : 4;
+        const size_t bsm = sizeof(double) * vb * (size_t)a;
+        auto kbt = wide ? ttg::k_syev_bt<8> : ttg::k_syev_bt<4>;
+        kernel_occupancy((const void*)kbt, kbt, ttg::kBtThreads, bsm);
         prof_begin(c, "k_syev_bt", 8.0 * a * a / 2, 4.0 * a * a / 2);
-        launch_k(c, ttg::k_syev_bt, (unsigned)std::max<long long>(1, (kcap + ttg::kBtWarps - 1) / ttg::kBtWarps),
-                 ttg::kBtWarps * 32, bsm, (const double*)c->W.as<double>(), a, (const double*)(args.tri + 2 * (size_t)a),
+        launch_k(c, kbt, (unsigned)std::max<long long>(1, (kcap + vb - 1) / vb), ttg::kBtThreads, bsm,
+                 (const double*)c->W.as<double>(), a, (const double*)(args.tri + 2 * (size_t)a),
                  (const ttg::EigResult*)c->eigres.as<EigResult>(), c->UR.as<double>());
         post_launch(c);
       }
@@ -1384,7 +1390,7 @@ bool project_ws16(ttg_ctx* c, const double* X, int a, long long L, const double*
 // DFMA tail rows of k_project_kc: r = 8 NB + T with T <= kKcMaxTail costs
 // NB + T/8 n-blocks of FP64 work instead of NB + 1 (r = 19..20 no longer pay
 // for 24 rows).
-constexpr int kKcMaxTail = 4;
+constexpr int kKcMaxTail = 3;  // measured: T = 4 (r = 20) runs slower than padding to NB + 1
 template <int NCW, int NB, int T>
 void* kc_kernel() {
   return (void*)ttg::k_project_kc<NCW, NB, T>;
@@ -2241,17 +2247,21 @@ const double* interface_gram_compute(ttg_ctx* c, const ttg_tt* tt) {
   // large ranks: M_i = C_i^T (M_{i-1} C_i) per core on the DMMA GEMM, with C_i
   // viewed as r_{i-1} x (n r_i) for the first product and as (r_{i-1} n) x r_i
   // for the second (the same column-major buffer)
+  // (may run on the side stream beside the statistics pass: its own buffers,
+  // grown by star_stats before the fork)
   c->iface[0].ensure(sizeof(double) * rmax * rmax);
-  c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
+  c->iface_T.ensure(sizeof(double) * rmax * nmax * rmax);
+  c->gemm_ws_side.ensure(sizeof(double) * 64 * rmax * rmax);
   const double one = 1.0;
   CK(cudaMemcpyAsync(c->iface[0].p, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
   int f = 0;
   for (int i = 0; i < tt->d; ++i) {
     const long long rl = tt->ranks[i], n = tt->modes[i], rr = tt->ranks[i + 1];
     const double* C = tt->cores[i].as<double>();
-    double* T = c->Mtmp.as<double>();
-    gemm<false, false>(c, c->iface[f].as<double>(), rl, C, rl, T, rl, rl, n * rr, rl, 1.0, 0.0);
-    gemm<true, false>(c, C, rl * n, T, rl * n, c->iface[f ^ 1].as<double>(), rr, rr, rr, rl * n, 1.0, 0.0);
+    double* T = c->iface_T.as<double>();
+    gemm<false, false>(c, c->iface[f].as<double>(), rl, C, rl, T, rl, rl, n * rr, rl, 1.0, 0.0, &c->gemm_ws_side);
+    gemm<true, false>(c, C, rl * n, T, rl * n, c->iface[f ^ 1].as<double>(), rr, rr, rr, rl * n, 1.0, 0.0,
+                      &c->gemm_ws_side);
     f ^= 1;
   }
   return c->iface[f].as<double>();
@@ -2273,6 +2283,8 @@ void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double
     c->iface[0].ensure(sizeof(double) * rmax * rmax);
     c->iface[1].ensure(sizeof(double) * rmax * rmax);
     c->Mtmp.ensure(sizeof(double) * rmax * nmax * rmax);
+    c->iface_T.ensure(sizeof(double) * rmax * nmax * rmax);
+    c->gemm_ws_side.ensure(sizeof(double) * 64 * rmax * rmax);
     CK(cudaEventRecord(c->ev_fork, c->stream));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     std::swap(c->stream, c->side);
@@ -2634,7 +2646,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
         (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
         (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
-        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
+        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt<4>, (const void*)ttg::k_syev_bt<8>, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,

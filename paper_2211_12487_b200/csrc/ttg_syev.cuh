@@ -1083,16 +1083,38 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
   double* Ws = Vs + (size_t)a * nb;  // panel W (a x nb)
   const int rows_per = (a + (int)P - 1) / (int)P;
   const int r0 = (int)blockIdx.x * rows_per, r1 = min(a, r0 + rows_per);
+  // A warp owns one row i_w of p when rows_per <= warps (the usual case): its
+  // row (= column i_w, symmetric storage) is cached in registers for a whole
+  // panel (the panel's updates are lazy; the column changes only at step D).
+  constexpr int QC = 32;
+  const int iw = r0 + warp;
+  const bool own = rows_per <= nw && iw < r1;
+  double creg[QC];
+  constexpr int QA = 8;  // column j + 1 prefetched for step A (a <= 8 * kTrdThreads)
+  double pre[QA];
+  bool have_pre = false;
   for (int j0 = 0; j0 + 2 < a; j0 += nb) {
     const int jend = min(j0 + nb, a - 2);  // columns j0 .. jend-1 in this panel
+    const bool cached = own && a - (j0 + 1) <= 32 * QC;
+    if (cached) {
+#pragma unroll
+      for (int q = 0; q < QC; ++q) {
+        const int k = j0 + 1 + lane + 32 * q;
+        creg[q] = k < a ? A[k + (size_t)a * iw] : 0.0;
+      }
+    }
     for (int j = j0; j < jend; ++j) {
       const int jj = j - j0;
       // ---- A: updated column j and its reflector (every CTA) ----
-      for (int i = j + tid; i < a; i += blockDim.x) {
-        double x = A[i + (size_t)a * j];
-        for (int q = 0; q < jj; ++q)
-          x -= Vs[i + (size_t)a * q] * Ws[j + (size_t)a * q] + Ws[i + (size_t)a * q] * Vs[j + (size_t)a * q];
-        col[i] = x;
+#pragma unroll
+      for (int q = 0; q < QA; ++q) {
+        const int i = j + tid + q * (int)blockDim.x;
+        if (i < a) {
+          double x = have_pre ? pre[q] : A[i + (size_t)a * j];
+          for (int qq = 0; qq < jj; ++qq)
+            x -= Vs[i + (size_t)a * qq] * Ws[j + (size_t)a * qq] + Ws[i + (size_t)a * qq] * Vs[j + (size_t)a * qq];
+          col[i] = x;
+        }
       }
       __syncthreads();
       double xs = 0.0;
@@ -1122,17 +1144,42 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
         if (lane == 0) vtw[q] = s;
       }
       __syncthreads();
-      for (int i = max(r0, j + 1) + warp; i < r1; i += nw) {
-        const double* ci = A + (size_t)a * i;
-        double s = 0.0;
-        for (int k = j + 1 + lane; k < a; k += 32) s = fma(ci[k], v[k], s);
-        s = warp_sum(s);
-        if (lane == 0) {
-          for (int q = 0; q < jj; ++q) s -= Vs[i + (size_t)a * q] * vtw[q] + Ws[i + (size_t)a * q] * vtw[jj + q];
-          p.pbuf[i] = s;
+      if (cached) {
+        if (iw >= j + 1) {
+          double s = 0.0;  // v is zero above row j + 1, so the cached rows <= j drop out
+#pragma unroll
+          for (int q = 0; q < QC; ++q) {
+            const int k = j0 + 1 + lane + 32 * q;
+            if (k < a) s = fma(creg[q], v[k], s);
+          }
+          s = warp_sum(s);
+          if (lane == 0) {
+            for (int q = 0; q < jj; ++q) s -= Vs[iw + (size_t)a * q] * vtw[q] + Ws[iw + (size_t)a * q] * vtw[jj + q];
+            p.pbuf[iw] = s;
+          }
+        }
+      } else {
+        for (int i = max(r0, j + 1) + warp; i < r1; i += nw) {
+          const double* ci = A + (size_t)a * i;
+          double s = 0.0;
+          for (int k = j + 1 + lane; k < a; k += 32) s = fma(ci[k], v[k], s);
+          s = warp_sum(s);
+          if (lane == 0) {
+            for (int q = 0; q < jj; ++q) s -= Vs[i + (size_t)a * q] * vtw[q] + Ws[i + (size_t)a * q] * vtw[jj + q];
+            p.pbuf[i] = s;
+          }
         }
       }
       grid_barrier(p.bar, P);
+      // prefetch column j + 1 for the next step A (unchanged until step D)
+      have_pre = j + 1 < jend && a <= QA * (int)blockDim.x;
+      if (have_pre) {
+#pragma unroll
+        for (int q = 0; q < QA; ++q) {
+          const int i = j + 1 + tid + q * (int)blockDim.x;
+          pre[q] = i < a ? A[i + (size_t)a * (j + 1)] : 0.0;
+        }
+      }
       // every CTA has read column j (step A): store the reflector in it
       if (blockIdx.x == 0)
         for (int i = j + 2 + tid; i < a; i += blockDim.x) A[i + (size_t)a * j] = v[i];
@@ -1165,6 +1212,7 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
       A[i + (size_t)a * k] = x;
     }
     grid_barrier(p.bar, P);
+    have_pre = false;
   }
   // last 2 x 2 block (k_syev's tail convention)
   if (blockIdx.x == 0 && tid == 0) {
@@ -1182,45 +1230,106 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd_grid(TrdArgs p) {
 // Back-transform of the kept eigenvectors of T (k_syev in tri mode leaves the
 // inverse-iteration vectors z in UR): u = H_0 ... H_{a-3} z with the reflectors
 // of k_sytrd_grid (v_k = [1; A[k+2.., k]]), then the sign rule (largest-|.|
-// entry, first index, positive: truncated_svd.cpp:16-25).  One warp per
-// vector, vectors spread over the grid; rank read from the eigen result.
-constexpr int kBtWarps = 4;
-__global__ void __launch_bounds__(kBtWarps * 32) k_syev_bt(const double* __restrict__ A, int a,
-                                                            const double* __restrict__ tau, const EigResult* res,
-                                                            double* __restrict__ UR) {
+// entry, first index, positive: truncated_svd.cpp:16-25).  One CTA applies
+// every reflector to VB vectors at once (each reflector read from L2 once per
+// VB vectors, the next one prefetched into registers while the current dot
+// products reduce); the rank is read from the eigen result.
+constexpr int kBtThreads = 256;
+template <int VB>
+__global__ void __launch_bounds__(kBtThreads) k_syev_bt(const double* __restrict__ A, int a,
+                                                         const double* __restrict__ tau, const EigResult* res,
+                                                         double* __restrict__ UR) {
   griddep_wait();
   extern __shared__ __align__(16) double bsm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int j = blockIdx.x * kBtWarps + warp;
-  if (j >= res->rank) return;
-  double* z = bsm + (size_t)warp * a;
-  double* u = UR + (size_t)j * a;
-  for (int i = lane; i < a; i += 32) z[i] = u[i];
-  __syncwarp();
+  __shared__ double red[VB][kBtThreads / 32];
+  __shared__ double sv[VB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kBtThreads / 32;
+  const int rank = res->rank;
+  const int j0 = blockIdx.x * VB;
+  if (j0 >= rank) return;
+  const int nv = min(VB, rank - j0);
+  double* z = bsm;  // VB x a
+  for (int v = 0; v < nv; ++v)
+    for (int i = tid; i < a; i += kBtThreads) z[(size_t)v * a + i] = UR[(size_t)(j0 + v) * a + i];
+  __syncthreads();
+  constexpr int PR = 16;  // prefetched reflector entries per thread (a <= 16 * 256 + 2)
+  double cur[PR];
+  auto fetch = [&](int k, double (&dst)[PR]) {
+#pragma unroll
+    for (int q = 0; q < PR; ++q) {
+      const int i = k + 2 + tid + q * kBtThreads;
+      dst[q] = (k >= 0 && i < a) ? A[(size_t)a * k + i] : 0.0;
+    }
+  };
+  fetch(a - 3, cur);
   for (int k = a - 3; k >= 0; --k) {
+    double nxt[PR];
+    fetch(k - 1, nxt);  // next reflector in flight while this one reduces
     const double tk = tau[k];
-    if (tk == 0.0) continue;
-    const double* vk = A + (size_t)a * k;
-    double s = (lane == 0) ? z[k + 1] : 0.0;
-    for (int i = k + 2 + lane; i < a; i += 32) s = fma(vk[i], z[i], s);
-    s = warp_sum(s) * tk;
-    if (lane == 0) z[k + 1] -= s;
-    for (int i = k + 2 + lane; i < a; i += 32) z[i] -= s * vk[i];
-    __syncwarp();
+    if (tk != 0.0) {
+      double s[VB];
+#pragma unroll
+      for (int v = 0; v < VB; ++v) {
+        s[v] = 0.0;
+        if (v < nv) {
+          const double* zv = z + (size_t)v * a;
+#pragma unroll
+          for (int q = 0; q < PR; ++q) {
+            const int i = k + 2 + tid + q * kBtThreads;
+            if (i < a) s[v] = fma(cur[q], zv[i], s[v]);
+          }
+          if (tid == 0) s[v] += zv[k + 1];
+        }
+        s[v] = warp_sum(s[v]);
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int v = 0; v < VB; ++v) red[v][warp] = s[v];
+      __syncthreads();
+      if (tid < VB) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t += red[tid][w];
+        sv[tid] = t * tk;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int v = 0; v < VB; ++v) {
+        if (v < nv) {
+          double* zv = z + (size_t)v * a;
+          const double f = sv[v];
+#pragma unroll
+          for (int q = 0; q < PR; ++q) {
+            const int i = k + 2 + tid + q * kBtThreads;
+            if (i < a) zv[i] -= f * cur[q];
+          }
+          if (tid == 0) zv[k + 1] -= f;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < PR; ++q) cur[q] = nxt[q];
   }
-  double best = -1.0;
-  int bi = a;
-  for (int i = lane; i < a; i += 32) {
-    const double vv = fabs(z[i]);
-    if (vv > best) { best = vv; bi = i; }
+  // sign rule per vector, one warp each
+  for (int v = warp; v < nv; v += NW) {
+    const double* zv = z + (size_t)v * a;
+    double best = -1.0;
+    int bi = a;
+    for (int i = lane; i < a; i += 32) {
+      const double vv = fabs(zv[i]);
+      if (vv > best) { best = vv; bi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double sgn = (zv[bi] < 0.0) ? -1.0 : 1.0;
+    double* u = UR + (size_t)(j0 + v) * a;
+    for (int i = lane; i < a; i += 32) u[i] = sgn * zv[i];
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-  }
-  const double sgn = (z[bi] < 0.0) ? -1.0 : 1.0;
-  for (int i = lane; i < a; i += 32) u[i] = sgn * z[i];
 }
 
 }  // namespace ttg
