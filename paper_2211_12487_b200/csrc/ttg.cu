@@ -1077,12 +1077,16 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     bool done = false;
     if (!std::getenv("TTG_FULL_EIG")) {
       // block of 4 first (the common case keeps 1-2 directions), then 8
-      for (int K : {4, 8}) {
+      // a mode that kept at most one direction last time starts with a block of 2
+      // (2 x 2 Rayleigh-Ritz: one rotation; CholQR of two columns)
+      const std::vector<int> blocks = (hint == 0 || hint == 1) ? std::vector<int>{2, 4, 8} : std::vector<int>{4, 8};
+      for (int K : blocks) {
         if (done || a >= kFastSkip) break;  // very large a: straight to the full decomposition
         const size_t sub_vec = sizeof(double) * (size_t)2 * a * K;
         size_t smem_s = sizeof(double) * (size_t)a * a + sub_vec;
         ttg::SyevArgs sa = args;
-        const size_t kcap = dyn_smem_cap(K == 4 ? (const void*)ttg::k_syev_top<4> : (const void*)ttg::k_syev_top<8>);
+        auto kern = K == 2 ? ttg::k_syev_top<2> : K == 4 ? ttg::k_syev_top<4> : ttg::k_syev_top<8>;
+        const size_t kcap = dyn_smem_cap((const void*)kern);
         if (sub_vec > kcap) break;  // even the block vectors do not fit: full solver
         if (smem_s <= kcap) {
           sa.in_smem = 1;
@@ -1094,7 +1098,6 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
           sa.in_smem = 0;
           smem_s = sub_vec;
         }
-        auto kern = K == 4 ? ttg::k_syev_top<4> : ttg::k_syev_top<8>;
         kernel_occupancy((const void*)kern, kern, ttg::kSubThreads, smem_s);
         char nm[64];
         std::snprintf(nm, sizeof nm, "k_syev_top[a=%d]", a);
@@ -1506,10 +1509,77 @@ bool project_kc(ttg_ctx* c, const double* X, int a, long long L, const double* W
   return true;
 }
 
+// High-rank projection (34 < r <= 128, even a): k_project_ws, W^T fragments
+// streamed through the ring with the X boxes.  False when it does not apply.
+template <int NCW, int NB>
+void* ws_kernel() {
+  return (void*)ttg::k_project_ws<NCW, NB>;
+}
+template <int NCW, int NB>
+void* ws_pick_t(int nb) {
+  if constexpr (NB > 16) {
+    return nullptr;
+  } else {
+    return nb == NB ? ws_kernel<NCW, NB>() : ws_pick_t<NCW, NB + 1>(nb);
+  }
+}
+void* ws_pick(int ncw, int nb) { return ncw == 8 ? ws_pick_t<8, 5>(nb) : ws_pick_t<4, 5>(nb); }
+
+bool project_ws(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
+                double* tsq) {
+  if (std::getenv("TTG_NO_PWS") || (a & 1) || r <= 34 || r > 128) return false;
+  const int NB = (r + 7) / 8, nks = (a + 15) / 16;
+  const int ncw = nks > 4 ? 8 : 4, tc = 16 * ncw;
+  const size_t cap = (size_t)c->smem_optin - 2048;
+  const size_t box = sizeof(double) * 16 * tc, wch = sizeof(double) * 128 * NB;
+  int kc = 0, nst = 0;
+  for (int kcw : {2, 4, 1}) {  // deepest ring with >= 3 stages, else >= 2
+    const int k_ = std::min(kcw, nks);
+    const int n_ = (int)std::min<size_t>(ttg::kProjStages, cap / (k_ * (box + wch)));
+    if (n_ >= 3 || (n_ >= 2 && kc == 0)) {
+      kc = k_;
+      nst = n_;
+      if (n_ >= 3) break;
+    }
+  }
+  if (kc == 0) return false;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, X, a, L, tc)) return false;
+  const size_t nfr = (size_t)nks * NB * 128;
+  c->UTf.ensure(sizeof(double) * nfr);
+  prof_begin(c, "k_make_frags16", 8.0 * nfr, 0.0);
+  launch_k(c, ttg::k_make_frags16, grid_for((long long)nfr, 256, 512), 256, 0, W, a, r, ldw, nks, NB,
+           c->UTf.as<double>());
+  post_launch(c);
+  ttg::ProjArgs args{};
+  args.src = ttg::TileSrc{X, a, L, nullptr, 1};
+  args.a8 = ttg::round_up(a, 8);
+  args.WTf = c->UTf.as<double>();
+  args.r = r;
+  args.r8 = 8 * NB;
+  args.out = out;
+  args.tsumsq = tsq;
+  args.n_tiles = (L + tc - 1) / tc;
+  args.nst = nst;
+  args.kc = kc;
+  const size_t smem = 1024 + (size_t)nst * kc * (box + wch);
+  auto kern = reinterpret_cast<void (*)(const CUtensorMap, ttg::ProjArgs)>(ws_pick(ncw, NB));
+  const int threads = (ncw + 1) * 32;
+  const int occ = std::max(kernel_occupancy((const void*)kern, kern, threads, smem), 1);
+  const int gx = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, args.n_tiles));
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_project[a=%d,r=%d]", a, r);
+  prof_begin(c, nm, 8.0 * ((double)a + r) * L, 2.0 * a * r * (double)L);
+  launch_k(c, kern, gx, threads, smem, tm, args);
+  post_launch(c);
+  return true;
+}
+
 bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
              double* tsq = nullptr) {
   const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
   if (project_kc(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;
+  if (project_ws(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;
   if (a8 > kFastMax1 || r8 > kFastMax) {
     gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
     return false;
@@ -2307,10 +2377,20 @@ void star_stats(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, double
   c->errs.ensure(sizeof(double) * b);
   c->rn2.ensure(sizeof(double) * b);
   c->stats.ensure(sizeof(ttg::StarStats));
-  prof_begin(c, "k_coef_stats", 8.0 * r * b, 2.0 * r * r * b);
-  launch_k(c, ttg::k_coef_stats, grid_for(32 * b, 256, 1024), 256, 0, coeffs, r, (int)b, M, c->cn2.as<double>(),
-                                                                   c->cmc.as<double>());
-  post_launch(c);
+  if (r > 64) {  // c^T M c through T = M C on the DMMA GEMM
+    c->small[2].ensure(sizeof(double) * (size_t)r * b);
+    double* T = c->small[2].as<double>();
+    gemm<false, false>(c, M, r, coeffs, r, T, r, r, b, r, 1.0, 0.0);
+    prof_begin(c, "k_coef_stats", 16.0 * r * b, 4.0 * r * b);
+    launch_k(c, ttg::k_coef_dots, grid_for(32 * b, 256, 1024), 256, 0, coeffs, (const double*)T, r, (int)b,
+             c->cn2.as<double>(), c->cmc.as<double>());
+    post_launch(c);
+  } else {
+    prof_begin(c, "k_coef_stats", 8.0 * r * b, 2.0 * r * r * b);
+    launch_k(c, ttg::k_coef_stats, grid_for(32 * b, 256, 1024), 256, 0, coeffs, r, (int)b, M, c->cn2.as<double>(),
+                                                                     c->cmc.as<double>());
+    post_launch(c);
+  }
   prof_begin(c, "k_star_local", 32.0 * b, 10.0 * b);
   launch_k(c, ttg::k_star_local, 1, 256, 0, c->on2.as<double>(), c->cn2.as<double>(), c->cmc.as<double>(),
                                              (int)b, eps, c->errs.as<double>(), c->rn2.as<double>(),
@@ -2646,13 +2726,13 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
         (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
         (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
-        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt<4>, (const void*)ttg::k_syev_bt<8>, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
+        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt<4>, (const void*)ttg::k_syev_bt<8>, (const void*)ttg::k_syev_top<2>, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,
         (const void*)ttg::k_iface_all, (const void*)ttg::k_build_q, (const void*)ttg::k_syrk_ws16<1, 1>, (const void*)ttg::k_syrk_ws16<3, 1>,
         (const void*)ttg::k_syrk_ws16<6, 1>, (const void*)ttg::k_syrk_ws16<10, 1>, (const void*)ttg::k_syrk_ws16<5, 3>,
-        (const void*)ttg::k_syrk_ws16<7, 3>, (const void*)ttg::k_syrk_ws16<14, 2>, (const void*)ttg::k_syrk_ws16<12, 3>, (const void*)ttg::k_coef_stats,
+        (const void*)ttg::k_syrk_ws16<7, 3>, (const void*)ttg::k_syrk_ws16<14, 2>, (const void*)ttg::k_syrk_ws16<12, 3>, (const void*)ttg::k_coef_stats, (const void*)ttg::k_coef_dots,
         (const void*)ttg::k_star_local, (const void*)ttg::k_star_mask, (const void*)ttg::k_mask_cols,
         (const void*)ttg::k_merge_rows, (const void*)ttg::k_kron_eye, (const void*)ttg::k_dgemm<false, false, 64>,
         (const void*)ttg::k_dgemm<true, false, 64>, (const void*)ttg::k_dgemm<false, true, 64>,
@@ -2668,6 +2748,10 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
         (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>, (const void*)ttg::k_pcp};
     for (int nbk = 7; nbk <= kKpMaxNbk; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
+    for (int nb = 5; nb <= 16; ++nb) {
+      CK(cudaFuncGetAttributes(&fa, ws_pick(4, nb)));
+      CK(cudaFuncGetAttributes(&fa, ws_pick(8, nb)));
+    }
     for (int nb = 1; nb <= 4; ++nb)
       for (int t = 0; t <= kKcMaxTail; ++t) {
         CK(cudaFuncGetAttributes(&fa, kc_pick(4, nb, t)));

@@ -1891,6 +1891,137 @@ __global__ void __launch_bounds__((NCW + 1) * 32) k_project_kc(const __grid_cons
   }
 }
 
+// High-rank projection out (r x L) = W^T X, 34 < r <= 128 (the companion
+// sweep's R = 64 / 128 chains, tt_project tensor_train.cpp:195-226): the
+// k_project_kc pipeline with the W fragments STREAMED through the ring next to
+// the X boxes (a x r fragments no longer fit shared memory: 256 KB at a = 512,
+// r = 64).  Each stage carries kc X boxes (TMA tensor map, 128-byte swizzle)
+// plus the same kc k-steps of W^T fragments (one bulk copy from the
+// k_make_frags16 layout, L2-resident); consumer warp w keeps the NB = r8/8
+// n-block accumulators of its 16 columns in registers across the chunks and
+// stores them straight from registers (the output is r/a of the input).
+template <int NCW, int NB>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) k_project_ws(const __grid_constant__ CUtensorMap tm, ProjArgs p) {
+  griddep_wait();
+  constexpr int TC = 16 * NCW, BOX = 16 * TC, WCH = NB * 128;
+  extern __shared__ __align__(1024) double smem_raw[];
+  __shared__ __align__(8) uint64_t full[kProjStages], empty[kProjStages];
+  double* smem = align1024(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nst = p.nst, kc = p.kc;
+  const int nks = (p.src.a + 15) >> 4;
+  const int nch = (nks + kc - 1) / kc;
+  const int stage = kc * (BOX + WCH);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long grid = gridDim.x;
+  if (warp == NCW) {  // ---- producer ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      int it = 0, s = 0;
+      for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+        for (int ch = 0; ch < nch; ++ch, ++it) {
+          if (it >= nst) mbar_wait(&empty[s], (unsigned)(((it / nst) - 1) & 1));
+          const int b0 = ch * kc, nb = min(kc, nks - b0);
+          mbar_expect_tx(&full[s], (unsigned)nb * (BOX + WCH) * 8u);
+          double* st = smem + s * stage;
+          for (int b = 0; b < nb; ++b) tma_load_2d(st + b * BOX, &tm, 16 * (b0 + b), (int)(tile * TC), &full[s]);
+          bulk_g2s(st + kc * BOX, p.WTf + (size_t)b0 * WCH, (unsigned)nb * WCH * 8u, &full[s]);
+          if (++s == nst) s = 0;
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers (fragment addressing as k_project_kc) ----
+  const int pg = ((g & 3) << 1) | (g >> 2);
+  int osw[8];
+  {
+    const int hsw = (t >> 1) ^ pg;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) osw[i] = (16 * warp + pg + 8 * (i & 1)) * 16 + (t & 1) + (((2 * (i >> 1)) ^ hsw) << 1);
+  }
+  const bool want_ss = p.tsumsq != nullptr;
+  int st = 0;
+  unsigned ph = 0;
+  for (long long tile = blockIdx.x; tile < p.n_tiles; tile += grid) {
+    double acc[NB][4];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0;
+    double ss0 = 0.0, ss1 = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+      mbar_wait(&full[st], ph);
+      const double* ab = smem + st * stage;
+      const double* wb = ab + kc * BOX + lane;
+      const int b0 = ch * kc, nb_ch = min(kc, nks - b0);
+      for (int bb = 0; bb < nb_ch; ++bb, ab += BOX, wb += WCH) {
+        double av[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = ab[osw[i]];
+        if (want_ss) {
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            ss0 = fma(av[i], av[i], ss0);
+            ss1 = fma(av[i + 1], av[i + 1], ss1);
+          }
+        }
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          double bw[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) bw[i] = wb[(nb * 4 + i) * 32];
+          dmma16(acc[nb], av, bw);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[st])) : "memory");
+      if (++st == nst) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+    // acc[nb][i]: tile column pg + 8 (i >> 1) of the warp, output row 8 nb + 2 t + (i & 1)
+    const long long colw = tile * TC + 16 * warp;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const long long col = colw + pg + 8 * h;
+      if (col < p.src.L) {
+        double* dst = p.out + col * p.r;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          const int row = 8 * nb + 2 * t;
+          if (row + 1 < p.r && !(p.r & 1)) {
+            *reinterpret_cast<double2*>(dst + row) = make_double2(acc[nb][2 * h], acc[nb][2 * h + 1]);
+          } else {
+            if (row < p.r) dst[row] = acc[nb][2 * h];
+            if (row + 1 < p.r) dst[row + 1] = acc[nb][2 * h + 1];
+          }
+        }
+      }
+    }
+    if (want_ss) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ss0 += __shfl_xor_sync(0xffffffffu, ss0, o);
+        ss1 += __shfl_xor_sync(0xffffffffu, ss1, o);
+      }
+      if (lane == 0) {
+        const long long c64 = colw >> 6;
+        const int grp = (int)((colw & 63) >> 3);
+        p.tsumsq[c64 * kConsumerWarps + grp] = ss0;
+        p.tsumsq[c64 * kConsumerWarps + grp + 1] = ss1;
+      }
+    }
+  }
+}
+
 // Projection out (r x L) = W^T X over a ring of single TMA boxes (16 rows x
 // 64 columns = 8 KB, 128-byte swizzle): warp 8 lane 0 is the producer (full /
 // empty mbarriers per stage), warps 0..7 consume.  A column tile of any height

@@ -234,6 +234,31 @@ __global__ void k_coef_stats(const double* __restrict__ C, int r, int b, const d
   }
 }
 
+// Large r: cn2 / cmc from T = M C computed by the DMMA GEMM (r^2 b flops on the
+// tensor pipe instead of one warp's DFMA chain per observation).
+__global__ void k_coef_dots(const double* __restrict__ C, const double* __restrict__ T, int r, int b,
+                            double* __restrict__ cn2, double* __restrict__ cmc) {
+  griddep_wait();
+  const int lane = threadIdx.x & 31;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < b; o += nwarp) {
+    const double* c = C + (long long)r * o;
+    const double* t = T + (long long)r * o;
+    double s = 0.0, m = 0.0;
+    for (int i = lane; i < r; i += 32) {
+      const double ci = __ldg(c + i);
+      s = fma(ci, ci, s);
+      m = fma(ci, __ldg(t + i), m);
+    }
+    s = warp_sum(s);
+    m = warp_sum(m);
+    if (lane == 0) {
+      cn2[o] = s;
+      cmc[o] = m;
+    }
+  }
+}
+
 // TT-ICE* per-observation errors and the partial sums the decision needs
 // (tt_ice_star.cpp:22-65, 90-100, 121-158).  Single thread, observation order
 // = the reference's loop order.  sums[] layout:

@@ -788,9 +788,10 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
   griddep_wait();
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[64];
-  __shared__ double H[K * K], Wv[K * K], theta[K], resn[K];
-  __shared__ double Sq[K * K], Rq[2 * K], Wt[72];
-  __shared__ double zpart[128 * K];  // second-half partial sums of Z = G X (a <= 128)
+  __shared__ double H[(K < 4 ? 4 : K) * (K < 4 ? 4 : K)], Wv[(K < 4 ? 4 : K) * (K < 4 ? 4 : K)], theta[K < 4 ? 4 : K],
+      resn[K < 4 ? 4 : K];
+  constexpr int KS = K < 4 ? 4 : K;  // block_cholqr2_4 / thread_sym_eig4 work on 4 x 4 scratch
+  __shared__ double Sq[KS * KS], Rq[2 * KS], Wt[72];
   __shared__ int s_state, s_rank;
   __shared__ double s_tail;
   const long long t0 = clock64();
@@ -849,45 +850,37 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
   int it = 0;
   for (; it < kSubIters; ++it) {
     long long tq0 = clock64();
-    // Z = G X: one thread per row i (G[i + a*j] over consecutive i is
-    // conflict-free, X[j + a*c] is a broadcast), K independent chains
+    // Z = G X on DMMA m8n8k4: warp task = one 8-row block of Z (all K <= 8
+    // columns at once, X padded to 8 columns by predicated zeros); two
+    // accumulator chains over the even / odd k-steps.  G in shared memory or
+    // L2 (a lane reads G[i0 + g][k0 + t]: 8 contiguous rows x 4 columns).
     {
-      // a <= 128: two threads per row (j halves; the second half's partial
-      // sums go through zpart), else one thread per row; two interleaved
-      // partial sums per column, loads batched
-      const int tpr = (2 * a <= (int)blockDim.x) ? 2 : 1;
-      const int jh = tpr == 2 ? (a + 1) / 2 : a;
-      for (int w = tid; w < a * tpr; w += blockDim.x) {
-        const int i = w % a, part = w / a;
-        const int j0 = part * jh, j1 = part ? a : jh;
-        double acc[K], acc2[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = acc2[c] = 0.0;
-        int j = j0;
-#pragma unroll 4
-        for (; j + 1 < j1; j += 2) {
-          const double g0 = G[i + (size_t)a * j], g1 = G[i + (size_t)a * (j + 1)];
-#pragma unroll
-          for (int c = 0; c < K; ++c)
-            if (c < k) {
-              acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
-              acc2[c] = fma(g1, X[j + 1 + (size_t)a * c], acc2[c]);
-            }
+      const int g = lane >> 2, t = lane & 3;
+      const int nrb = (a + 7) >> 3;
+      for (int rb = warp; rb < nrb; rb += nw) {
+        const int i = rb * 8 + g;
+        double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+        int k0 = 0;
+        for (; k0 + 8 <= a; k0 += 8) {
+          const double ga = i < a ? G[i + (size_t)a * (k0 + t)] : 0.0;
+          const double gb = i < a ? G[i + (size_t)a * (k0 + 4 + t)] : 0.0;
+          const double xa = g < k ? X[(k0 + t) + (size_t)a * g] : 0.0;
+          const double xb = g < k ? X[(k0 + 4 + t) + (size_t)a * g] : 0.0;
+          dmma(c0, c1, ga, xa);
+          dmma(e0, e1, gb, xb);
         }
-        if (j < j1) {
-          const double g0 = G[i + (size_t)a * j];
-#pragma unroll
-          for (int c = 0; c < K; ++c)
-            if (c < k) acc[c] = fma(g0, X[j + (size_t)a * c], acc[c]);
+        for (; k0 < a; k0 += 4) {
+          const bool kv = k0 + t < a;
+          const double ga = (i < a && kv) ? G[i + (size_t)a * (k0 + t)] : 0.0;
+          const double xa = (g < k && kv) ? X[(k0 + t) + (size_t)a * g] : 0.0;
+          dmma(c0, c1, ga, xa);
         }
-        double* dst = part ? zpart : Z;
-#pragma unroll
-        for (int c = 0; c < K; ++c)
-          if (c < k) dst[i + (size_t)a * c] = acc[c] + acc2[c];
-      }
-      if (tpr == 2) {
-        __syncthreads();
-        for (int e = tid; e < a * k; e += blockDim.x) Z[e] += zpart[e];
+        c0 += e0;
+        c1 += e1;
+        if (i < a) {
+          if (2 * t < k) Z[i + (size_t)a * (2 * t)] = c0;
+          if (2 * t + 1 < k) Z[i + (size_t)a * (2 * t + 1)] = c1;
+        }
       }
     }
     __syncthreads();
@@ -902,7 +895,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
     }
     __syncthreads();
     long long tq2 = clock64();
-    if constexpr (K == 4) {
+    if constexpr (K <= 4) {
       if (tid == 0) jac_sweeps += thread_sym_eig4(H, k, theta, Wv);
     } else if (warp == 0) {
       const int nsw = warp_sym_eig<K>(H, k, theta, Wv, Wt);
@@ -969,7 +962,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
       X[e] = s;
     }
     __syncthreads();
-    if constexpr (K == 4) block_cholqr2_4(X, a, k, Sq, Rq);
+    if constexpr (K <= 4) block_cholqr2_4(X, a, k, Sq, Rq);
     else block_cholqr2<K>(X, Z, a, k, Sq, Rq);
   }
   const int rank = s_rank;
