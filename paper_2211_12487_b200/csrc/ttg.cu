@@ -142,7 +142,6 @@ struct ttg_ctx {
   cudaStream_t copy = nullptr;
   int pf_next = 0, pf_inuse = -1;
   DevBuf trd;  // k_sytrd_grid p, [d | e | tau], barrier
-  std::vector<int> mode_hint;  // rank kept per mode at the previous increment (eig block-attempt hint)
   std::string err;
   int64_t launches = 0;
   int num_sms = 148;
@@ -193,6 +192,9 @@ struct ttg_tt {
   int64_t rc = 0, oc = 0, n_obs = 0;
   int64_t ortho_count = 0;
   std::vector<int64_t> bounds;
+  // rank kept per mode at the previous update of THIS train (eig block-attempt
+  // hint; per train, so a train's results never depend on other trains' history)
+  std::vector<int> mode_hint;
   uint64_t gen = next_gen();  // bumped whenever the cores may change (caches keyed on it)
   static uint64_t next_gen() {
     static std::atomic<uint64_t> g{0};
@@ -1022,6 +1024,17 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
     post_launch(c);
     return did;
   }
+  const size_t pcp_l2 = sizeof(double) * ttg::pcp_l2_smem_doubles((int)a, r_old);
+  if (!s.Psi && r_old <= 32 && ttg::round_up((int)a, 8) <= 256 && pcp_l2 + 1024 <= (size_t)c->smem_optin &&
+      !std::getenv("TTG_NO_PCP")) {
+    // one CTA, C from L2: G = P C P in place, trace(C) for the guard
+    kernel_occupancy((const void*)ttg::k_pcp_l2, ttg::k_pcp_l2, ttg::kPcpThreads, pcp_l2);
+    prof_begin(c, "k_pcp", 24.0 * a * a, 4.0 * a * a * std::max(r_old, 1));
+    launch_k(c, ttg::k_pcp_l2, 1, ttg::kPcpThreads, pcp_l2, c->G.as<double>(), (int)a, U, r_old,
+             c->scal.as<double>() + 4);
+    post_launch(c);
+    return did;
+  }
   c->Craw.ensure(sizeof(double) * (size_t)(rows * rows));
   CK(cudaMemcpyAsync(c->Craw.p, c->G.p, sizeof(double) * rows * rows, cudaMemcpyDeviceToDevice, c->stream));
   // G = Q^T C Q with Q = K P (one element-wise kernel, two GEMMs): the same
@@ -1094,7 +1107,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
           // G from L2: each failed iteration re-reads it, so only try when the
           // last solve of this mode kept fewer directions than the block holds
           // (and, above a = 512, only when that is known)
-          if (hint >= K - 1 || (a > 512 && hint < 0)) continue;
+          if (hint >= K || (a > 512 && hint < 0)) continue;  // a block of K certifies rank <= K - 1
           sa.in_smem = 0;
           smem_s = sub_vec;
         }
@@ -1523,11 +1536,11 @@ void* ws_pick_t(int nb) {
     return nb == NB ? ws_kernel<NCW, NB>() : ws_pick_t<NCW, NB + 1>(nb);
   }
 }
-void* ws_pick(int ncw, int nb) { return ncw == 8 ? ws_pick_t<8, 5>(nb) : ws_pick_t<4, 5>(nb); }
+void* ws_pick(int ncw, int nb) { return ncw == 8 ? ws_pick_t<8, 2>(nb) : ws_pick_t<4, 2>(nb); }
 
 bool project_ws(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
                 double* tsq) {
-  if (std::getenv("TTG_NO_PWS") || (a & 1) || r <= 34 || r > 128) return false;
+  if (std::getenv("TTG_NO_PWS") || (a & 1) || r <= 8 || r > 128) return false;
   const int NB = (r + 7) / 8, nks = (a + 15) / 16;
   const int ncw = nks > 4 ? 8 : 4, tc = 16 * ncw;
   const size_t cap = (size_t)c->smem_optin - 2048;
@@ -1578,8 +1591,11 @@ bool project_ws(ttg_ctx* c, const double* X, int a, long long L, const double* W
 bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
              double* tsq = nullptr) {
   const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
+  // (TTG_PWS_LOW: streamed-W kernel also for 8 < r <= 34, for measurements)
+  if (std::getenv("TTG_PWS_LOW") && r > 8 && a > 256 && project_ws(c, X, a, L, W, r, ldw, out, tsq))
+    return tsq != nullptr;
   if (project_kc(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;
-  if (project_ws(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;
+  if (r > 34 && project_ws(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;
   if (a8 > kFastMax1 || r8 > kFastMax) {
     gemm<true, false>(c, W, ldw, X, a, out, r, r, L, a, 1.0, 0.0);
     return false;
@@ -2037,13 +2053,13 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         norm_checked = true;
       }
       const long long kmax = o.star ? o.n_sel_global * cpo : Lg;
-      if ((int)c->mode_hint.size() < d) c->mode_hint.assign(d, -1);
+      if ((int)tt->mode_hint.size() < d) tt->mode_hint.assign(d, -1);
       EigResult er = tall_eig(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, o.star ? o.sel : nullptr, cpo,
-                              kmax, dsrc, dmult, c->mode_hint[i], out.accurate_modes, out.gram_only_unstable);
+                              kmax, dsrc, dmult, tt->mode_hint[i], out.accurate_modes, out.gram_only_unstable);
       r_R = er.rank;
       out.discarded_sq += er.tail_sq;
       out.tall_modes++;
-      c->mode_hint[i] = (int)r_R;
+      tt->mode_hint[i] = (int)r_R;
     } else if (run_svd) {
       const uint8_t* sel = o.star ? o.sel : nullptr;
       const int64_t rows = src.Psi ? src.As * n_i : a;
@@ -2061,8 +2077,8 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       }
       const long long kmax = o.star ? o.n_sel_global * cpo : L * c->world;
       trace("sweep:gram launched");
-      if ((int)c->mode_hint.size() < d) c->mode_hint.assign(d, -1);
-      EigResult er = eig(c, (int)a, kmax, dsrc, dmult, 0, c->mode_hint[i]);
+      if ((int)tt->mode_hint.size() < d) tt->mode_hint.assign(d, -1);
+      EigResult er = eig(c, (int)a, kmax, dsrc, dmult, 0, tt->mode_hint[i]);
       trace("sweep:eig done");
       if (raw && er.rank > 0 && r_old > 0) {  // no projector (empty basis): C is G exactly
         // raw-Gram cancellation costs ~eps*tr(C)/gap in the kept vectors: keep
@@ -2089,7 +2105,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       }
       r_R = er.rank;
       out.discarded_sq += er.tail_sq;
-      c->mode_hint[i] = (int)r_R;
+      tt->mode_hint[i] = (int)r_R;
     }
     int64_t r_new;
     bool zero_next = false;
@@ -2746,9 +2762,9 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_project_ws16<4, 1>, (const void*)ttg::k_project_ws16<4, 2>,
         (const void*)ttg::k_project_ws16<4, 3>, (const void*)ttg::k_project_ws16<4, 4>, (const void*)ttg::k_project_tma<true, 64>, (const void*)ttg::k_project_tma<false, 64>,
         (const void*)ttg::k_project_tma<true, 32>, (const void*)ttg::k_project_tma<false, 32>,
-        (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>, (const void*)ttg::k_pcp};
+        (const void*)ttg::k_sum_vec, (const void*)ttg::k_make_tail, (const void*)ttg::k_syrk_kx<8>, (const void*)ttg::k_pcp, (const void*)ttg::k_pcp_l2};
     for (int nbk = 7; nbk <= kKpMaxNbk; ++nbk) CK(cudaFuncGetAttributes(&fa, kp_pick(nbk)));
-    for (int nb = 5; nb <= 16; ++nb) {
+    for (int nb = 2; nb <= 16; ++nb) {
       CK(cudaFuncGetAttributes(&fa, ws_pick(4, nb)));
       CK(cudaFuncGetAttributes(&fa, ws_pick(8, nb)));
     }

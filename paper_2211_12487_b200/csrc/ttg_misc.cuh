@@ -515,6 +515,113 @@ __global__ void __launch_bounds__(kPcpThreads) k_pcp(const double* C, int a, con
   }
 }
 
+// k_pcp for Grams that do not fit shared memory (a8 <= 256, r <= 32): C stays
+// in L2 (read as DMMA fragments for W = C U and once more for the output), U,
+// W, Y = W - U sym(M)/2 and M = U^T W in shared memory.  G = P C P written in
+// place of C (every read of C's upper triangle -- only in W = C U -- precedes
+// the first write; the output phase reads only lower blocks and writes each
+// element's mirror), trace(C) for the raw-Gram guard.  Replaces the 4-launch
+// k_build_q + 2 GEMMs + k_symmetrize_trace path for the mode-3..7 Grams of
+// configs[3] at bond ranks 17-32.
+__host__ __device__ constexpr size_t pcp_l2_smem_doubles(int a, int r) {
+  return (size_t)3 * pcp_ld((a + 7) & ~7) * (((r > 1 ? r : 1) + 7) & ~7) +
+         (size_t)(((r > 1 ? r : 1) + 7) & ~7) * (((r > 1 ? r : 1) + 7) & ~7);
+}
+__global__ void __launch_bounds__(kPcpThreads) k_pcp_l2(double* C, int a, const double* __restrict__ U, int r,
+                                                        double* __restrict__ tr) {
+  griddep_wait();
+  extern __shared__ double psm[];
+  const int a8 = (a + 7) & ~7, r8 = (r + 7) & ~7, ld = pcp_ld(a8);
+  double* Us = psm;                       // ld x r8
+  double* Ws = Us + (size_t)ld * r8;      // ld x r8
+  double* Ys = Ws + (size_t)ld * r8;      // ld x r8
+  double* Ms = Ys + (size_t)ld * r8;      // r8 x r8
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  for (int e = tid; e < ld * r8; e += nt) {
+    const int i = e % ld, k = e / ld;
+    Us[e] = (i < a && k < r) ? __ldg(U + i + (size_t)a * k) : 0.0;
+  }
+  if (tid < 32) {
+    double s = 0.0;
+    for (int i = tid; i < a; i += 32) s += C[i + (size_t)a * i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (tid == 0) *tr = s;
+  }
+  __syncthreads();
+  // W = C U: warp task = 8-row block; C fragments from L2
+  const int nbr = a8 / 8, nbc = r8 / 8;  // nbc <= 4
+  for (int ib = warp; ib < nbr; ib += nwarp) {
+    double acc[4][2];
+#pragma unroll
+    for (int jb = 0; jb < 4; ++jb) acc[jb][0] = acc[jb][1] = 0.0;
+    const int i = ib * 8 + g;
+#pragma unroll 4
+    for (int k0 = 0; k0 < a8; k0 += 4) {
+      const int kk = k0 + t;
+      const double av = (i < a && kk < a) ? C[i + (size_t)a * kk] : 0.0;
+#pragma unroll
+      for (int jb = 0; jb < 4; ++jb)
+        if (jb < nbc) dmma(acc[jb][0], acc[jb][1], av, Us[kk + (size_t)ld * (jb * 8 + g)]);
+    }
+#pragma unroll
+    for (int jb = 0; jb < 4; ++jb)
+      if (jb < nbc) {
+        Ws[i + (size_t)ld * (jb * 8 + 2 * t)] = acc[jb][0];
+        Ws[i + (size_t)ld * (jb * 8 + 2 * t + 1)] = acc[jb][1];
+      }
+  }
+  __syncthreads();
+  // M = U^T W
+  for (int blk = warp; blk < nbc * nbc; blk += nwarp) {
+    const int kb = blk % nbc, lb = blk / nbc;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll 2
+    for (int k0 = 0; k0 < a8; k0 += 4)
+      dmma(d0, d1, Us[(k0 + t) + (size_t)ld * (kb * 8 + g)], Ws[(k0 + t) + (size_t)ld * (lb * 8 + g)]);
+    Ms[kb * 8 + g + r8 * (lb * 8 + 2 * t)] = d0;
+    Ms[kb * 8 + g + r8 * (lb * 8 + 2 * t + 1)] = d1;
+  }
+  __syncthreads();
+  // Y = W - U sym(M) / 2 (padded rows / columns zero)
+  for (int w = tid; w < ld * r8; w += nt) {
+    const int i = w % ld, l = w / ld;
+    double y = 0.0;
+    if (i < a && l < r) {
+      double s = 0.0;
+      for (int k = 0; k < r; ++k) s = fma(Us[i + ld * k], 0.5 * (Ms[k + r8 * l] + Ms[l + r8 * k]), s);
+      y = Ws[i + ld * l] - 0.5 * s;
+    }
+    Ys[w] = y;
+  }
+  __syncthreads();
+  // lower 8 x 8 blocks of G = C - [U Y][Y U]^T, mirrored
+  const int nlow = nbr * (nbr + 1) / 2;
+  for (int blk = warp; blk < nlow; blk += nwarp) {
+    int ib = 0;
+    while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
+    const int jb = blk - ib * (ib + 1) / 2;
+    double d0 = 0.0, d1 = 0.0;
+    const int i = ib * 8 + g, jrow = jb * 8 + g;
+#pragma unroll 2
+    for (int k0 = 0; k0 < r8; k0 += 4) dmma(d0, d1, Us[i + (size_t)ld * (k0 + t)], Ys[jrow + (size_t)ld * (k0 + t)]);
+#pragma unroll 2
+    for (int k0 = 0; k0 < r8; k0 += 4) dmma(d0, d1, Ys[i + (size_t)ld * (k0 + t)], Us[jrow + (size_t)ld * (k0 + t)]);
+    const double dv[2] = {d0, d1};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = jb * 8 + 2 * t + h;
+      if (i < a && j < a && (ib != jb || i >= j)) {
+        const double gv = C[i + (size_t)a * j] - dv[h];
+        C[i + (size_t)a * j] = gv;
+        C[j + (size_t)a * i] = gv;
+      }
+    }
+  }
+}
+
 // selection mask (err > eps, or all when subselect is off)
 __global__ void k_star_mask(const double* __restrict__ errs, int b, double eps, int subselect,
                             uint8_t* __restrict__ sel) {

@@ -861,6 +861,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
         const int i = rb * 8 + g;
         double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
         int k0 = 0;
+#pragma unroll 4
         for (; k0 + 8 <= a; k0 += 8) {
           const double ga = i < a ? G[i + (size_t)a * (k0 + t)] : 0.0;
           const double gb = i < a ? G[i + (size_t)a * (k0 + 4 + t)] : 0.0;
