@@ -1025,8 +1025,10 @@ bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_ol
     return did;
   }
   const size_t pcp_l2 = sizeof(double) * ttg::pcp_l2_smem_doubles((int)a, r_old);
-  if (!s.Psi && r_old <= 32 && ttg::round_up((int)a, 8) <= 256 && pcp_l2 + 1024 <= (size_t)c->smem_optin &&
-      !std::getenv("TTG_NO_PCP")) {
+  // (measured: one CTA streaming C from L2 twice is latency-bound, 88 us at a = 176,
+  // vs ~35 us for the multi-CTA path below: opt-in only)
+  if (std::getenv("TTG_PCP_L2") && !s.Psi && r_old <= 32 && ttg::round_up((int)a, 8) <= 256 &&
+      pcp_l2 + 1024 <= (size_t)c->smem_optin && !std::getenv("TTG_NO_PCP")) {
     // one CTA, C from L2: G = P C P in place, trace(C) for the guard
     kernel_occupancy((const void*)ttg::k_pcp_l2, ttg::k_pcp_l2, ttg::kPcpThreads, pcp_l2);
     prof_begin(c, "k_pcp", 24.0 * a * a, 4.0 * a * a * std::max(r_old, 1));
@@ -1101,8 +1103,12 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         auto kern = K == 2 ? ttg::k_syev_top<2> : K == 4 ? ttg::k_syev_top<4> : ttg::k_syev_top<8>;
         const size_t kcap = dyn_smem_cap((const void*)kern);
         if (sub_vec > kcap) break;  // even the block vectors do not fit: full solver
+        const size_t packed_s = sizeof(double) * ((((size_t)a * (a + 1) / 2) + 1) & ~(size_t)1) + sub_vec;
         if (smem_s <= kcap) {
           sa.in_smem = 1;
+        } else if (packed_s <= kcap) {  // the lower triangle fits: G stays on chip
+          sa.in_smem = 2;
+          smem_s = packed_s;
         } else {
           // G from L2: each failed iteration re-reads it, so only try when the
           // last solve of this mode kept fewer directions than the block holds
@@ -1591,8 +1597,11 @@ bool project_ws(ttg_ctx* c, const double* X, int a, long long L, const double* W
 bool project(ttg_ctx* c, const double* X, int a, long long L, const double* W, int r, int ldw, double* out,
              double* tsq = nullptr) {
   const int a8 = ttg::round_up(a, 8), r8 = ttg::round_up(r, 8);
-  // (TTG_PWS_LOW: streamed-W kernel also for 8 < r <= 34, for measurements)
-  if (std::getenv("TTG_PWS_LOW") && r > 8 && a > 256 && project_ws(c, X, a, L, W, r, ldw, out, tsq))
+  // tall sources (the a = 512 statistics pass) with r >= 20 (NB >= 3 n-blocks):
+  // the streamed-W ring is measured faster than resident fragments, whose
+  // 98 KB at NB = 3 leave room for only 3 x 32 KB stages (r = 24: 0.80 vs
+  // 0.84 ms per 4.29 GB; r = 32: 1.03 vs 1.09 ms)
+  if (!std::getenv("TTG_NO_PWS_MID") && r >= 20 && a >= 256 && project_ws(c, X, a, L, W, r, ldw, out, tsq))
     return tsq != nullptr;
   if (project_kc(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;
   if (r > 34 && project_ws(c, X, a, L, W, r, ldw, out, tsq)) return tsq != nullptr;

@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
                                                      const double* __restrict__ X, long long ldx,
                                                      double* __restrict__ part) {
   griddep_wait();
-  __shared__ double cs[kRreObsChunk * RMAX];
+  __shared__ __align__(16) double cs[kRreObsChunk * RMAX];
   __shared__ double red[2][8];
   double dsum = 0.0, xsum = 0.0;
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -40,12 +40,16 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
     __syncthreads();
     if (live) {
       for (int o = 0; o < mo; ++o) {
-        const double* co = cs + o * RMAX;
+        // coefficients as broadcast 16-byte shared loads: one LDS per two FMAs
+        // (one LDS.64 per FMA made the kernel shared-memory-issue bound at
+        // ~54 % of HBM)
+        const double2* co = reinterpret_cast<const double2*>(cs + o * RMAX);
         double dot0 = 0.0, dot1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < RMAX; k += 2) {
-          dot0 = fma(phi[k], co[k], dot0);
-          dot1 = fma(phi[k + 1], co[k + 1], dot1);
+        for (int k = 0; k < RMAX / 2; ++k) {
+          const double2 cc = co[k];
+          dot0 = fma(phi[2 * k], cc.x, dot0);
+          dot1 = fma(phi[2 * k + 1], cc.y, dot1);
         }
         const double x = X[s + ldx * (o0 + o)];
         const double df = x - (dot0 + dot1);

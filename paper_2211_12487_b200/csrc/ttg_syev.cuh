@@ -798,10 +798,27 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
   const int a = p.a;
   const int k = a < K ? a : K;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // in_smem: 1 = G in shared memory, 2 = its lower triangle packed in shared
+  // memory (a <= ~220: the full square does not fit, the triangle does),
+  // 0 = G read from L2
+  const bool packed = p.in_smem == 2;
+  const size_t gsz = packed ? (((size_t)a * (a + 1) / 2 + 1) & ~(size_t)1) : (size_t)a * a;
   double* G = p.in_smem ? sm : const_cast<double*>(p.G);
-  double* X = p.in_smem ? sm + (size_t)a * a : sm;
+  double* X = p.in_smem ? sm + gsz : sm;
   double* Z = X + (size_t)a * K;
-  if (p.in_smem) {  // a*a is even or odd: copy pairs, then the odd tail
+  auto gat = [&](int i, int j) -> double {  // G[i][j]
+    if (packed) {
+      const int hi = i > j ? i : j, lo = i > j ? j : i;
+      return G[(size_t)hi * (hi + 1) / 2 + lo];
+    }
+    return G[i + (size_t)a * j];
+  };
+  if (packed) {
+    for (long long e = tid; e < (long long)a * a; e += blockDim.x) {
+      const int i = (int)(e % a), j = (int)(e / a);
+      if (i >= j) G[(size_t)i * (i + 1) / 2 + j] = __ldg(p.G + e);
+    }
+  } else if (p.in_smem) {  // a*a is even or odd: copy pairs, then the odd tail
     const long long n = (long long)a * a, n2 = n >> 1;
     const double2* src = reinterpret_cast<const double2*>(p.G);
     double2* dst = reinterpret_cast<double2*>(G);
@@ -821,7 +838,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
     const double vi = (double)(h >> 11) * (1.0 / 9007199254740992.0) - 0.5;
     Z[i] = vi;
     vpart = fma(vi, vi, vpart);
-    gpart += G[i + (size_t)a * i];
+    gpart += gat(i, i);
   }
   const double vv = block_sum_all(vpart, red);
   __syncthreads();
@@ -863,8 +880,8 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
         int k0 = 0;
 #pragma unroll 4
         for (; k0 + 8 <= a; k0 += 8) {
-          const double ga = i < a ? G[i + (size_t)a * (k0 + t)] : 0.0;
-          const double gb = i < a ? G[i + (size_t)a * (k0 + 4 + t)] : 0.0;
+          const double ga = i < a ? gat(i, k0 + t) : 0.0;
+          const double gb = i < a ? gat(i, k0 + 4 + t) : 0.0;
           const double xa = g < k ? X[(k0 + t) + (size_t)a * g] : 0.0;
           const double xb = g < k ? X[(k0 + 4 + t) + (size_t)a * g] : 0.0;
           dmma(c0, c1, ga, xa);
@@ -872,7 +889,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) k_syev_top(SyevArgs p) {
         }
         for (; k0 < a; k0 += 4) {
           const bool kv = k0 + t < a;
-          const double ga = (i < a && kv) ? G[i + (size_t)a * (k0 + t)] : 0.0;
+          const double ga = (i < a && kv) ? gat(i, k0 + t) : 0.0;
           const double xa = (g < k && kv) ? X[(k0 + t) + (size_t)a * g] : 0.0;
           dmma(c0, c1, ga, xa);
         }
