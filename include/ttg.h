@@ -148,6 +148,12 @@ int ttg_ctx_reserve(ttg_ctx* ctx, int64_t bytes);
 /* Host<->device bytes moved by the context (H2D of host increments, D2H of
  * scalars/decisions). */
 int ttg_ctx_io_bytes(const ttg_ctx* ctx, int64_t* h2d, int64_t* d2h);
+/* Speculative sweeps (one host read per update instead of one per mode; no
+ * reference counterpart -- the reference's loop tt_ice.cpp:71-117 is host code):
+ * `sweeps` = update sweeps that sized launches from the previous update's ranks,
+ * `redone` = those a device-side check rejected and that were repeated with a
+ * host read per mode.  Results are identical either way. */
+int ttg_ctx_spec_stats(const ttg_ctx* ctx, int64_t* sweeps, int64_t* redone);
 /* Start copying a host increment (n doubles, ideally page-locked) to the
  * device on the context's copy stream, into one of two staging slots; the next
  * update / projection call given the same host pointer and size (where =

@@ -77,6 +77,7 @@ SIGNATURES = [
     ("ttg_ctx_num_kernel_stats", ctypes.c_int, [_P]),
     ("ttg_ctx_kernel_stat", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, _I64P, _DP, _DP, _DP]),
     ("ttg_ctx_io_bytes", ctypes.c_int, [_P, _I64P, _I64P]),
+    ("ttg_ctx_spec_stats", ctypes.c_int, [_P, _I64P, _I64P]),
     ("ttg_ctx_reserve", ctypes.c_int, [_P, ctypes.c_int64]),
     ("ttg_prefetch", ctypes.c_int, [_P, _DP, ctypes.c_int64]),
     ("ttg_tt_upload", ctypes.c_int, [_P, ctypes.c_int, _I64P, _I64P, _I64P, ctypes.POINTER(_DP), ctypes.c_int64,

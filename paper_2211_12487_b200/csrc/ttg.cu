@@ -6,11 +6,19 @@
 //   tt_ice_star_update             tt_ice_star.cpp:171-303
 //   tt_svd (bootstrap)             tt_svd.cpp:9-66
 // as a sequence of device passes over the increment:
-//   norms      per-observation |y_o|^2 and |Y|^2            (k_sumsq_obs)
-//   gram       residual Gram of cur_i vs U_pad (DMMA)        (k_gram_resid + k_gram_reduce)
-//   eig        one-sided Jacobi, rank rule, sign rule        (k_jacobi_eig)
-//   append     [U_pad U_R] with the 1e-10 guard              (k_append)
-//   project    cur_{i+1} = reshape(U_new^T cur_i) (DMMA)     (k_project)
+//   norms      per-observation |y_o|^2 and |Y|^2, fused into the first kernel that
+//              streams Y (k_tiles_to_obs; k_sumsq_obs when tiles straddle observations)
+//   gram       raw Gram C of the unfolding on DMMA (k_syrk_kx / k_syrk_kp / k_syrk2 +
+//              k_gram_reduce); the residual Gram P C P is never streamed from HBM
+//   decide     rank rule + kept directions + appended core in one launch (k_decide,
+//              ttg_decide.cuh); fallbacks: explicit P C P (k_pcp / k_build_q + GEMMs) ->
+//              k_syev_top / k_syev (+ k_sytrd_grid, k_syev_bt), explicit residual
+//              (k_gram_resid), TSQR factor + k_jacobi_eig, tall side (k_tall_u), k_append
+//   project    cur_{i+1} = reshape(U_new^T cur_i) (k_project_kc / k_project_ws, TMA + DMMA)
+//   pad        next core zero-padded to the new left rank (k_pad_core)
+// An update sweep is speculative (sweep()): launches after a k_decide mode are sized
+// with the rank that mode kept at the previous update, the kernel flags any
+// disagreement, and the host reads flag + per-mode results once per update.
 // Multi-GPU: the batch (observation) axis is sharded; the a_i x a_i Grams and
 // a handful of scalars are all-reduced and the coefficient columns
 // all-gathered with NCCL; every rank then runs the same deterministic eigen
@@ -41,6 +49,7 @@
 #include "ttg_syev.cuh"
 #include "ttg_io.cuh"
 #include "ttg_gemm.cuh"
+#include "ttg_decide.cuh"
 
 namespace {
 
@@ -150,10 +159,13 @@ struct ttg_ctx {
   DevBuf ystage, cur[2], partials, G, W, UR, lam, UTf, UTt, Uf, Upad, scratch, eigres, on2, sumsq_part,
       scal, coeffs, coeffs_all, cn2, cmc, errs, rn2, sel, stats, M, Mtmp, iface[2], tsq, psif, wcomb, psi[2],
       spsi[2], scoeffs, matbuf, tmp, Craw, small[4], gcount, gemm_ws, gemm_ws_side, iface_T, tallR, tallRg, tallXt,
-      UR2;
+      UR2, specflag, eiglog;
+  std::vector<DevBuf> corebak;    // speculative sweeps: the cores a sweep replaces, kept until it is verified
   std::vector<DevBuf> scur;       // TT-ICE* stats-chain intermediates (reused by the sweep)
   std::vector<bool> stat_has;
   ttg::EigResult* h_eig = nullptr;
+  ttg::EigResult* h_eiglog = nullptr;  // pinned: per-mode results of a speculative sweep + its flag
+  int64_t spec_sweeps = 0, spec_redone = 0;
   double* h_scal = nullptr;
   ttg::StarStats* h_stats = nullptr;
   // per-kernel accounting (launches, algorithmic bytes/flops always; event
@@ -195,6 +207,8 @@ struct ttg_tt {
   // rank kept per mode at the previous update of THIS train (eig block-attempt
   // hint; per train, so a train's results never depend on other trains' history)
   std::vector<int> mode_hint;
+  // speculative sweeps (ttg.cu sweep()): sweeps to sit out after a rejected guess, and its growth
+  int spec_wait = 0, spec_hold = 0;
   uint64_t gen = next_gen();  // bumped whenever the cores may change (caches keyed on it)
   static uint64_t next_gen() {
     static std::atomic<uint64_t> g{0};
@@ -1005,11 +1019,17 @@ bool syrk(ttg_ctx* c, const double* X, int a, long long L, const uint8_t* sel, l
 // The streaming kernel is then a plain SYRK of the source columns (no
 // residual, no pre-projection); the rest is (a x a)-sized.  trace(C) is left
 // in c->scal[4] for the accuracy guard (see sweep()).
+bool pcp_from_c(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, bool did);
 bool gram_raw_src(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, const uint8_t* sel,
                   long long cpo, double sel_frac, double* tsq) {
-  const int64_t rows = s.Psi ? s.As * n : s.r * n, a = s.r * n;
+  const int64_t rows = s.Psi ? s.As * n : s.r * n;
   const long long L = s.Ls / n;
   const bool did = syrk(c, s.S, (int)rows, L, sel, cpo, sel_frac, tsq);  // C -> c->G (rows x rows)
+  return pcp_from_c(c, s, n, U, r_old, did);
+}
+// c->G: raw Gram C of the source (rows x rows) -> residual Gram P K C K^T P (a x a)
+bool pcp_from_c(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old, bool did) {
+  const int64_t rows = s.Psi ? s.As * n : s.r * n, a = s.r * n;
   c->scal.ensure(sizeof(double) * 16);
   const size_t pcp_smem = sizeof(double) * ttg::pcp_smem_doubles((int)a, r_old);
   // (Y = W - U M / 2 keeps <= 8 elements per thread in registers: a r <= 4096;
@@ -1342,6 +1362,74 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
   launch_k(c, ttg::k_append, 1, 1024, 0, args);
   post_launch(c);
   return 0;  // the guard count is read once per update (guards_read), not per mode
+}
+
+// ---- one-launch mode decision (ttg_decide.cuh) -----------------------------------
+// Applies when the unfolding is read directly (no pending pre-projection), the
+// old basis is small and the previous update of this mode kept few directions.
+int decide_block(int hint) { return hint <= 1 ? 2 : 4; }
+bool decide_applies(const ttg_ctx* c, bool has_psi, int64_t a, int64_t r_old, int hint) {
+  if (std::getenv("TTG_NO_DECIDE") || has_psi || hint < 0 || hint > 3) return false;
+  const int K = decide_block(hint);
+  if (r_old < 1 || r_old > ttg::kDecMaxR || a > ttg::kDecMaxA || a - r_old < K) return false;
+  const void* kern = K == 2 ? (const void*)ttg::k_decide<2> : (const void*)ttg::k_decide<4>;
+  return sizeof(double) * ttg::dec_smem_doubles((int)a, (int)r_old, K) <= dyn_smem_cap(kern);
+}
+// C in c->G (a x a raw Gram), old basis Upad (a x r_old) -> rank, U_R (c->UR) and the
+// appended core in `out` (capacity a x (r_old + K - 1)); result in c->eigres, trace(C) in c->scal[4]
+void decide_launch(ttg_ctx* c, int a, int r_old, const double* Upad, double* out, long long kmax, const double* dsrc,
+                   double dmult, int hint, int expect, int* spec_flag, EigResult* log) {
+  const int K = decide_block(hint);
+  c->UR.ensure(sizeof(double) * (size_t)a * a);
+  c->lam.ensure(sizeof(double) * a);
+  c->eigres.ensure(sizeof(EigResult));
+  c->scal.ensure(sizeof(double) * 16);
+  ttg::DecideArgs da{};
+  da.C = c->G.as<double>();
+  da.a = a;
+  da.U = Upad;
+  da.r = r_old;
+  da.kmax = kmax;
+  da.delta_src = dsrc;
+  da.delta_mult = dmult;
+  da.UR = c->UR.as<double>();
+  da.lam = c->lam.as<double>();
+  da.out = out;
+  da.res = c->eigres.as<EigResult>();
+  da.trC = c->scal.as<double>() + 4;
+  da.guard_count = c->gcount.as<int>();
+  da.ldb = ttg::dec_ldb(a);
+  // k-range parts per 8-row block: the split that wastes the fewest of the 16 warps' rounds
+  const int nrb = (a + 7) / 8, nw = ttg::kDecThreads / 32;
+  int best = 1;
+  double best_cost = 1e300;
+  for (int ks = 1; ks <= ttg::kDecMaxSplit; ++ks) {
+    const double cost = (double)((nrb * ks + nw - 1) / nw) / ks;
+    if (cost < best_cost - 1e-9) { best_cost = cost; best = ks; }
+  }
+  da.ksplit = best;
+  da.expect = expect;
+  da.spec_flag = spec_flag;
+  da.log = log;
+  const size_t smem = sizeof(double) * ttg::dec_smem_doubles(a, r_old, K);
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "k_decide[a=%d]", a);
+  prof_begin(c, nm, 8.0 * a * a * 3, 2.0 * a * a * (r_old + 3.0 * K));
+  if (K == 2) {
+    kernel_occupancy((const void*)ttg::k_decide<2>, ttg::k_decide<2>, ttg::kDecThreads, smem);
+    launch_k(c, ttg::k_decide<2>, 1, ttg::kDecThreads, smem, da);
+  } else {
+    kernel_occupancy((const void*)ttg::k_decide<4>, ttg::k_decide<4>, ttg::kDecThreads, smem);
+    launch_k(c, ttg::k_decide<4>, 1, ttg::kDecThreads, smem, da);
+  }
+  post_launch(c);
+}
+EigResult eig_fetch(ttg_ctx* c) {
+  c->d2h += sizeof(EigResult) + sizeof(double);
+  CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_scal + 8, c->scal.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return *c->h_eig;
 }
 
 // Guard count of the last sweep: copied to the pinned slot after the sweep and
@@ -1947,6 +2035,7 @@ struct SweepOpts {
   double y_norm = 0.0;                // known only for the per-mode-delta API
   bool need_norms = false;            // fuse |y_o|^2 into the first pass over Y
   bool reuse_stats = false;           // TT-ICE*: intermediates of the stats chain are valid
+  bool speculate = true;              // size the launches after a k_decide mode with the rank hint, verify once
 };
 
 struct SweepOut {
@@ -2013,14 +2102,79 @@ bool can_fuse(const Src& s, int64_t n_i, int64_t r_new, int64_t n_next, int64_t 
          ttg::round_up((int)std::max<int64_t>(r_old_next, 1), 8) <= kFastMax;
 }
 
+// What a speculative sweep needs to be undone (owned by sweep(), filled by sweep_impl())
+struct SpecState {
+  bool any_spec = false;
+  std::vector<char> swapped;
+  std::vector<int64_t> old_ranks;
+  std::vector<int> hints_before;
+};
+struct SpecRejected {};
+
+SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm, SpecState& st);
+
 SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm) {
+  SpecState st;
+  auto undo = [&] {
+    c->spec_redone++;
+    for (size_t i = 0; i < st.swapped.size(); ++i)
+      if (st.swapped[i]) std::swap(tt->cores[i], c->corebak[i]);
+    tt->ranks = st.old_ranks;
+    tt->mode_hint = st.hints_before;
+    tt->spec_hold = std::min(8, 2 * tt->spec_hold + 1);
+  };
+  try {
+    SweepOut out = sweep_impl(c, tt, Y, b, o, nm, st);
+    if (st.any_spec) tt->spec_hold = 0;
+    return out;
+  } catch (const SpecRejected&) {
+    undo();
+  } catch (const TtgError&) {
+    // launches sized by a wrong guess may fail on their own (a solver that does
+    // not converge on garbage): only a failure of the synchronous sweep counts
+    if (!st.any_spec) throw;
+    undo();
+  }
+  tt->spec_wait = tt->spec_hold;
+  SweepOpts o2 = o;
+  o2.speculate = false;
+  SpecState st2;
+  return sweep_impl(c, tt, Y, b, o2, nm, st2);
+}
+
+SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm, SpecState& st) {
   SweepOut out;
   tt->gen = ttg_tt::next_gen();  // the sweep rewrites the cores
   c->gcount.ensure(sizeof(int));
   CK(cudaMemsetAsync(c->gcount.p, 0, sizeof(int), c->stream));
+  // Speculative sweep: a mode solved by k_decide does not wait for its rank --
+  // the host sizes the following launches with the rank this mode kept at the
+  // previous update, the kernel flags any disagreement, and flag + per-mode
+  // results are read once at the end.  A flagged sweep is undone (the replaced
+  // cores are kept aside until then) and repeated with a host read per mode.
+  // A train whose last guesses were rejected sits out a growing number of sweeps
+  // (1, 3, 7, 8 ...): alternating rank patterns must not pay for two sweeps every time.
+  bool spec_on = o.speculate && !o.bootstrap && !std::getenv("TTG_NO_SPEC");
+  if (spec_on && tt->spec_wait > 0) {
+    --tt->spec_wait;
+    spec_on = false;
+  }
+  std::vector<char> spec_mode(tt->d, 0);
+  std::vector<char>& swapped = st.swapped;
+  swapped.assign(tt->d, 0);
+  std::vector<double> tails(tt->d, 0.0);
+  st.hints_before = tt->mode_hint;
+  bool& any_spec = st.any_spec;
+  if (spec_on) {
+    c->specflag.ensure(sizeof(int));
+    c->eiglog.ensure(sizeof(EigResult) * (TTG_MAX_CORES + 1));
+    CK(cudaMemsetAsync(c->specflag.p, 0, sizeof(int), c->stream));
+    if ((int)c->corebak.size() < tt->d) c->corebak.resize(tt->d);
+  }
   const int d = tt->d;
   const int64_t S = prod(tt->modes);
   std::vector<int64_t> old_ranks = tt->ranks;
+  st.old_ranks = old_ranks;
   Src src{Y, 1, S * b, nullptr, 1};
   int flip = 0, pf = 0;
   bool unchanged = true;
@@ -2038,6 +2192,8 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     const double dmult = o.deltas ? o.deltas[i] : o.delta_mult;
     int64_t r_R = 0;
     bool run_svd = true;
+    bool decided = false;  // k_decide solved the mode and wrote the appended core
+    bool speculated = false;  // ... and the host did not wait for it (verified at the end of the sweep)
     if (o.star) {
       run_svd = (double)r_old / (double)a < o.tau;  // occupancy on the padded core, tt_ice_star.cpp:246-248
     } else if (!o.bootstrap && r_old == a) {
@@ -2066,7 +2222,7 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       EigResult er = tall_eig(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, o.star ? o.sel : nullptr, cpo,
                               kmax, dsrc, dmult, tt->mode_hint[i], out.accurate_modes, out.gram_only_unstable);
       r_R = er.rank;
-      out.discarded_sq += er.tail_sq;
+      tails[i] = er.tail_sq;
       out.tall_modes++;
       tt->mode_hint[i] = (int)r_R;
     } else if (run_svd) {
@@ -2077,8 +2233,14 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       // raw Gram (SYRK + small-side projector) for every source; the explicit
       // residual kernel is the accuracy fallback below
       const bool raw = !std::getenv("TTG_NO_RAW_GRAM") && (src.Psi || ttg::round_up((int)a, 8) > 0);
-      const bool did = raw ? gram_raw_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq)
-                           : gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq);
+      if ((int)tt->mode_hint.size() < d) tt->mode_hint.assign(d, -1);
+      const int hint = tt->mode_hint[i];
+      // one launch for P C P, the eigen-solve and the append (ttg_decide.cuh)
+      const bool dec = raw && !o.bootstrap && !(a & 1) && decide_applies(c, src.Psi != nullptr, a, r_old, hint);
+      bool did;
+      if (dec) did = syrk(c, src.S, (int)a, L, sel, cpo, sel_frac, tsq);  // C -> c->G
+      else did = raw ? gram_raw_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq)
+                     : gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq);
       if (tsq) norms_finish(c, nm, rows, did);
       if (!norm_checked && !nm.pending) {  // reject non-finite input before anything is mutated
         check_finite_norm(read_scalar(c, c->scal.as<double>()));
@@ -2086,10 +2248,45 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       }
       const long long kmax = o.star ? o.n_sel_global * cpo : L * c->world;
       trace("sweep:gram launched");
-      if ((int)tt->mode_hint.size() < d) tt->mode_hint.assign(d, -1);
-      EigResult er = eig(c, (int)a, kmax, dsrc, dmult, 0, tt->mode_hint[i]);
+      EigResult er;
+      if (dec) {
+        const bool alias = (Upad == tt->cores[i].p);
+        if (spec_on && !alias) {  // the sweep replaces this core: keep the old one until verified
+          std::swap(tt->cores[i], c->corebak[i]);
+          swapped[i] = 1;
+        }
+        tt->cores[i].ensure(sizeof(double) * (size_t)a * (r_old + decide_block(hint) - 1), /*keep=*/alias, c->stream);
+        if (alias) Upad = tt->cores[i].as<double>();
+        decide_launch(c, (int)a, (int)r_old, Upad, tt->cores[i].as<double>(), kmax, dsrc, dmult, hint,
+                      spec_on ? hint : -1, c->specflag.as<int>(), spec_on ? c->eiglog.as<EigResult>() + i : nullptr);
+        if (spec_on) {
+          er = EigResult{};
+          er.rank = hint;
+          er.converged = 1;
+          spec_mode[i] = 1;
+          any_spec = true;
+          speculated = true;
+        } else {
+          er = eig_fetch(c);
+        }
+        if (std::getenv("TTG_DEBUG"))
+          std::fprintf(stderr, "[ttg] decide a=%d r=%d K=%d conv=%d iters=%d rank=%d lam_max=%.3e tail=%.3e dev=%.2e\n", (int)a,
+                       (int)r_old, decide_block(hint), er.converged, er.sweeps, er.rank, er.lam_max, er.tail_sq, er.dev);
+        if (std::getenv("TTG_DEBUG"))
+          std::fprintf(stderr, "[ttg] decide cycles init=%lld pass1=%lld tgram=%lld zupd=%lld hs+rr=%lld rows+dec=%lld pass=%lld final=%lld\n",
+                       er.t_phase[0] & 0xffffffffll, er.t_phase[0] >> 32, er.t_phase[1] & 0xffffffffll, er.t_phase[1] >> 32,
+                       er.t_phase[2] & 0xffffffffll, er.t_phase[2] >> 32, er.t_phase[3] & 0xffffffffll, er.t_phase[3] >> 32);
+        if (er.converged) {
+          decided = true;
+        } else {  // more directions than the block holds: the explicit chain from the same C
+          pcp_from_c(c, src, n_i, Upad, (int)r_old, did);
+          er = eig(c, (int)a, kmax, dsrc, dmult, 0, std::max(hint, decide_block(hint)));
+        }
+      } else {
+        er = eig(c, (int)a, kmax, dsrc, dmult, 0, hint);
+      }
       trace("sweep:eig done");
-      if (raw && er.rank > 0 && r_old > 0) {  // no projector (empty basis): C is G exactly
+      if (!speculated && raw && er.rank > 0 && r_old > 0) {  // no projector (empty basis): C is G exactly
         // raw-Gram cancellation costs ~eps*tr(C)/gap in the kept vectors: keep
         // it only for directions carrying >= 1e-3 of the source energy
         const double trC = c->h_scal[8];  // trace(C), fetched with the eigen result
@@ -2097,14 +2294,16 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
           gram_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, nullptr);
           er = eig(c, (int)a, kmax, dsrc, dmult, 0, er.rank);
           out.raw_fallbacks++;
+          decided = false;
         }
       }
-      if (needs_accurate(er)) {
+      if (!speculated && needs_accurate(er)) {
         if (accurate_supported((int)a, (int)r_old)) {
           const double* X = materialise(c, src, n_i, c->matbuf);
           er = accurate_eig(c, X, (int)a, L, r_old > 0 ? Upad : nullptr, (int)r_old, (int)a, sel, cpo, kmax, dsrc,
                             dmult);
           out.accurate_modes++;
+          decided = false;
         } else {
           out.gram_only_unstable++;  // surfaced in ttg_report; TTG_STRICT turns it into a NumericError
           if (std::getenv("TTG_STRICT"))
@@ -2113,8 +2312,13 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
         }
       }
       r_R = er.rank;
-      out.discarded_sq += er.tail_sq;
+      tails[i] = er.tail_sq;
       tt->mode_hint[i] = (int)r_R;
+      if (decided && er.guard == 2) decided = false;  // Gram-deviation guard fired: k_append's correction
+    }
+    if (spec_on && !swapped[i] && Upad != tt->cores[i].p) {  // this mode's core is about to be replaced
+      std::swap(tt->cores[i], c->corebak[i]);
+      swapped[i] = 1;
     }
     int64_t r_new;
     bool zero_next = false;
@@ -2138,7 +2342,9 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
       const bool alias = (Upad == tt->cores[i].p);
       tt->cores[i].ensure(sizeof(double) * (size_t)a * r_new, /*keep=*/alias, c->stream);
       if (alias) Upad = tt->cores[i].as<double>();  // keep aliasing valid after growth
-      out.guards += append(c, Upad, (int)a, (int)r_old, (int)r_R, tt->cores[i].as<double>());
+      // (k_decide already wrote [U_pad U_R] unless its Gram-deviation guard fired)
+      if (!decided)
+        out.guards += append(c, Upad, (int)a, (int)r_old, (int)r_R, tt->cores[i].as<double>());
       out.cores_changed = true;
       out.modes_updated++;
       unchanged = false;
@@ -2222,6 +2428,19 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     trace("sweep:mode advanced");
   }
   guards_fetch(c);
+  if (any_spec) {
+    c->spec_sweeps++;
+    c->d2h += sizeof(EigResult) * d + sizeof(int);
+    CK(cudaMemcpyAsync(c->h_eiglog, c->eiglog.p, sizeof(EigResult) * d, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_eiglog + TTG_MAX_CORES, c->specflag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int flag = *reinterpret_cast<const int*>(c->h_eiglog + TTG_MAX_CORES);
+    if (std::getenv("TTG_DEBUG")) std::fprintf(stderr, "[ttg] speculative sweep: flag=%d\n", flag);
+    if (flag) throw SpecRejected{};  // sweep() undoes it and repeats with a host read per mode
+    for (int i = 0; i < d; ++i)
+      if (spec_mode[i]) tails[i] = c->h_eiglog[i].tail_sq;
+  }
+  for (int i = 0; i < d; ++i) out.discarded_sq += tails[i];
   return out;
 }
 
@@ -2751,7 +2970,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
         (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
         (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
-        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt<4>, (const void*)ttg::k_syev_bt<8>, (const void*)ttg::k_syev_top<2>, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>,
+        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt<4>, (const void*)ttg::k_syev_bt<8>, (const void*)ttg::k_syev_top<2>, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>, (const void*)ttg::k_decide<2>, (const void*)ttg::k_decide<4>,
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,
@@ -2785,6 +3004,7 @@ static int ctx_init(ttg_ctx* c, int device) {
     for (const void* k : ks) CK(cudaFuncGetAttributes(&fa, k));
   }
   CK(cudaMallocHost((void**)&c->h_eig, sizeof(ttg::EigResult)));
+  CK(cudaMallocHost((void**)&c->h_eiglog, sizeof(ttg::EigResult) * (TTG_MAX_CORES + 1)));
   CK(cudaMallocHost((void**)&c->h_scal, sizeof(double) * 16));
   CK(cudaMallocHost((void**)&c->h_stats, sizeof(ttg::StarStats)));
   return 0;
@@ -2869,6 +3089,7 @@ void ttg_ctx_destroy(ttg_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_eig) cudaFreeHost(c->h_eig);
+  if (c->h_eiglog) cudaFreeHost(c->h_eiglog);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -2968,6 +3189,13 @@ int ttg_ctx_io_bytes(const ttg_ctx* c, int64_t* h2d, int64_t* d2h) {
   if (!c) return TTG_E_ARGUMENT;
   if (h2d) *h2d = c->h2d;
   if (d2h) *d2h = c->d2h;
+  return TTG_OK;
+}
+
+int ttg_ctx_spec_stats(const ttg_ctx* c, int64_t* sweeps, int64_t* redone) {
+  if (!c) return TTG_E_ARGUMENT;
+  if (sweeps) *sweeps = c->spec_sweeps;
+  if (redone) *redone = c->spec_redone;
   return TTG_OK;
 }
 

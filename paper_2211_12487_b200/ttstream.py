@@ -159,6 +159,12 @@ class Context:
         _check(_lib.load().ttg_ctx_io_bytes(self._h, ctypes.byref(h), ctypes.byref(d)), self)
         return h.value, d.value
 
+    def spec_stats(self):
+        """(speculative sweeps, of which repeated synchronously) -- ttg_ctx_spec_stats."""
+        s, r = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.load().ttg_ctx_spec_stats(self._h, ctypes.byref(s), ctypes.byref(r)), self)
+        return s.value, r.value
+
     def prefetch(self, y: np.ndarray) -> None:
         """include/ttg.h ttg_prefetch: start the H2D copy of host increment ``y``
         (float64, first-index-fastest, ideally pinned) on the copy stream; the

@@ -246,6 +246,49 @@ def test_determinism_bitwise(ctx):
         assert np.array_equal(a, b)
 
 
+def _run_spec_stream(ctx, algo, speculate, monkeypatch):
+    """cfg3-type stream at 4^6: ranks grow on even increments, so the previous
+    update's ranks are sometimes right (verified sweep) and sometimes wrong
+    (flagged, undone, repeated)."""
+    if speculate:
+        monkeypatch.delenv("TTG_NO_SPEC", raising=False)
+    else:
+        monkeypatch.setenv("TTG_NO_SPEC", "1")
+    s = Stream(3, seed=5, modes=(4,) * 6, batch=24, true_rank=6)
+    tg, _ = tt_ice_bootstrap(s.increment(0), s.eps, ctx=ctx)
+    reps = []
+    for k in range(1, 12):
+        upd = tt_ice_update if algo == "ice" else tt_ice_star_update
+        tg, rep = upd(tg, s.increment(k), s.eps)
+        reps.append((tuple(rep.ranks_after), rep.obs_used, rep.batch_rel_error_estimate, rep.modes_updated))
+    return [c.copy() for c in tg.cores()], reps
+
+
+@pytest.mark.parametrize("algo", ["ice", "star"])
+def test_speculative_sweep_is_bitwise_the_synchronous_sweep(ctx, algo, monkeypatch):
+    """A sweep that sizes its launches from the previous update's ranks and
+    verifies once (ttg.cu sweep(), ttg_ctx_spec_stats) must produce the same
+    bytes as the sweep that reads every mode's rank on the host -- both when
+    the guess holds and when it is rejected and the sweep repeated."""
+    s0, r0 = ctx.spec_stats()
+    cores_spec, reps_spec = _run_spec_stream(ctx, algo, True, monkeypatch)
+    s1, r1 = ctx.spec_stats()
+    cores_sync, reps_sync = _run_spec_stream(ctx, algo, False, monkeypatch)
+    s2, r2 = ctx.spec_stats()
+    assert s1 > s0, "no sweep speculated"
+    if algo == "ice":
+        # TT-ICE sweeps every increment and this stream's ranks alternate 1, 0, 1, 0: every guess is
+        # wrong (the train then sits out 1, 3, 7 ... sweeps): the undo-and-repeat path
+        assert r1 > r0, "no speculative sweep was rejected: the rollback path is untested by this stream"
+    else:
+        # TT-ICE* skips the in-span increments, so the ranks of the previous update hold: the verified path
+        assert r1 - r0 < s1 - s0, "every speculative sweep was rejected"
+    assert (s2, r2) == (s1, r1), "TTG_NO_SPEC=1 still speculated"
+    assert reps_spec == reps_sync
+    for a, b in zip(cores_spec, cores_sync):
+        assert a.shape == b.shape and np.array_equal(a, b)
+
+
 def test_theorem_3_3_no_regression(ctx):
     """Earlier increments' reconstructions are unchanged (1e-12)."""
     s = Stream(3, seed=11, modes=(4,) * 5, batch=5, true_rank=4)
