@@ -39,10 +39,36 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
     }
     __syncthreads();
     if (live) {
-      for (int o = 0; o < mo; ++o) {
-        // coefficients as broadcast 16-byte shared loads: one LDS per two FMAs
-        // (one LDS.64 per FMA made the kernel shared-memory-issue bound at
-        // ~54 % of HBM)
+      // four observations per round: their X loads are issued together (one
+      // 8-byte load in flight per thread kept the kernel at ~54 % of HBM: too
+      // few bytes in flight per SM), and the coefficients come as broadcast
+      // 16-byte shared loads, one LDS per two FMAs
+      const double* xp = X + s + ldx * (long long)o0;
+      int o = 0;
+      for (; o + 4 <= mo; o += 4) {
+        double x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = __ldcs(xp + ldx * (o + q));
+        double d0[4], d1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) d0[q] = d1[q] = 0.0;
+#pragma unroll
+        for (int k = 0; k < RMAX / 2; ++k) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 cc = reinterpret_cast<const double2*>(cs + (o + q) * RMAX)[k];
+            d0[q] = fma(phi[2 * k], cc.x, d0[q]);
+            d1[q] = fma(phi[2 * k + 1], cc.y, d1[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double df = x[q] - (d0[q] + d1[q]);
+          dsum = fma(df, df, dsum);
+          xsum = fma(x[q], x[q], xsum);
+        }
+      }
+      for (; o < mo; ++o) {
         const double2* co = reinterpret_cast<const double2*>(cs + o * RMAX);
         double dot0 = 0.0, dot1 = 0.0;
 #pragma unroll
@@ -51,7 +77,7 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
           dot0 = fma(phi[2 * k], cc.x, dot0);
           dot1 = fma(phi[2 * k + 1], cc.y, dot1);
         }
-        const double x = X[s + ldx * (o0 + o)];
+        const double x = __ldcs(xp + ldx * o);
         const double df = x - (dot0 + dot1);
         dsum = fma(df, df, dsum);
         xsum = fma(x, x, xsum);
