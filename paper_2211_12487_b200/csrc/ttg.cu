@@ -1399,14 +1399,7 @@ void decide_launch(ttg_ctx* c, int a, int r_old, const double* Upad, double* out
   da.trC = c->scal.as<double>() + 4;
   da.guard_count = c->gcount.as<int>();
   da.ldb = ttg::dec_ldb(a);
-  // k-range parts per 8-row block: the split that wastes the fewest of the 16 warps' rounds
-  const int nrb = (a + 7) / 8, nw = ttg::kDecThreads / 32;
-  int best = 1;
-  double best_cost = 1e300;
-  for (int ks = 1; ks <= ttg::kDecMaxSplit; ++ks) {
-    const double cost = (double)((nrb * ks + nw - 1) / nw) / ks;
-    if (cost < best_cost - 1e-9) { best_cost = cost; best = ks; }
-  }
+  const int best = (a + 63) / 64;  // k-range parts per 8-row block (dec_pass: 64 columns of C per task)
   da.ksplit = best;
   da.expect = expect;
   da.spec_flag = spec_flag;

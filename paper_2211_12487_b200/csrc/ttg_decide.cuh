@@ -56,14 +56,19 @@ struct DecideArgs {
   double* trC;  // trace(C) for the host's raw-Gram guard
   int* guard_count;
   int ldb;      // smem leading dimension: >= round_up(a, 4), = 4 mod 16
-  int ksplit;   // k-range parts per 8-row block (tasks = blocks x parts over 16 warps)
+  int ksplit;   // k-range parts per 8-row block: ceil(a / 64) (dec_pass: 16 k-steps per task)
   int expect;   // speculative sweeps: assumed rank (-1: none)
   int* spec_flag;
   EigResult* log;  // per-mode copy of *res (read once per update), may be null
 };
 
-// (>= a + 32: the rolled chunk loop reads up to 7 k-steps of B rows past the range; they are zero)
-__host__ __device__ inline int dec_ldb(int a) { return (a + 31 + 15) / 16 * 16 + 4; }
+// (>= round_up(a, 64): the last k-range of a pass reads B rows up to there; rows >= a are zero)
+__host__ __device__ inline int dec_ldb(int a) { return (a + 63) / 64 * 64 + 4; }
+// The warp index as a warp-uniform value (lane 0's, broadcast): loops and
+// branches on it are then compiled as uniform, and the mma.sync inside them are
+// not each preceded by a WARPSYNC (which had serialised every DMMA of this kernel
+// behind its operand load).
+__device__ __forceinline__ int dec_warp() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
 __host__ __device__ inline int dec_bcols(int r, int K) {
   const int nbt = (r + K + 7) / 8;
   return nbt * 8 > r + 8 ? nbt * 8 : r + 8;
@@ -76,50 +81,41 @@ inline size_t dec_smem_doubles(int a, int r, int K) {
 // acc = C[rows of task] * B[:, col0 .. col0 + 8 nbt) over the task's k range.
 // Columns < r_tr feed the task's trace partial sum_i U[i][n] (C U)[i][n];
 // columns [xoff, xoff + K) are stored as the task's k-range partial of Y = C X
-// (Yp[ks], summed in order by the consumers).  The kernel runs once on one SM,
-// so its instruction footprint matters as much as its data: one rolled chunk
-// loop (8 k-steps, the next chunk's loads in flight), not inlined, nbt <= NBMAX
-// blocks by predicate.
+// (Yp[ks], summed in order by the consumers).  A task is one 8-row block x
+// kDecTaskK k-steps (64 columns of C), always full length: the A-fragment loads
+// of the last, partial range are clamped into the matrix and meet the zero
+// rows of the padded B operand, so the body carries no bounds predicates --
+// all loads of a task are in flight before its first DMMA.
+constexpr int kDecTaskK = 16;
 template <int NBMAX>
-__device__ __noinline__ void dec_pass(const double* __restrict__ C, int a, const double* Bs, int ldb, int col0, int nbt,
+__device__ __noinline__ void dec_pass(const double* __restrict__ C, int a, const double* Bs, int ldb, int col0,
                                       int r_tr, int xoff, int K, int ksplit, double* Yp, double* trpart) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = dec_warp(), nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int nrb = (a + 7) >> 3, nk = (a + 3) >> 2;
+  const int nrb = (a + 7) >> 3;
   const int ntask = nrb * ksplit;
 #pragma unroll 1
   for (int task = warp; task < ntask; task += nw) {
     const int rb = task / ksplit, ks = task - rb * ksplit;
-    const int k_lo = nk * ks / ksplit, k_hi = nk * (ks + 1) / ksplit;
     const int i = rb * 8 + g;
     const bool iv = i < a;
-    const double* crow = C + (size_t)a * (iv ? i : 0) + t;  // C symmetric: row i read as column i
+    const double* crow = C + (size_t)a * (iv ? i : a - 1);  // C symmetric: row i read as column i
+    const int k0 = ks * kDecTaskK * 4 + t;
+    double av[kDecTaskK];
+#pragma unroll
+    for (int u = 0; u < kDecTaskK; ++u) {
+      const int kk = k0 + 4 * u;
+      av[u] = __ldg(crow + (kk < a ? kk : a - 1));
+    }
     double acc[NBMAX][2];
 #pragma unroll
     for (int nb = 0; nb < NBMAX; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
-    double av[8], an[8];
+    const double* bp = Bs + k0 + (size_t)ldb * (col0 + g);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int kk = (k_lo + u) * 4;
-      av[u] = (iv && k_lo + u < k_hi && kk + t < a) ? __ldg(crow + kk) : 0.0;
-    }
-#pragma unroll 1
-    for (int kc = k_lo; kc < k_hi; kc += 8) {
+    for (int u = 0; u < kDecTaskK; ++u) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int kk = (kc + 8 + u) * 4;
-        an[u] = (iv && kc + 8 + u < k_hi && kk + t < a) ? __ldg(crow + kk) : 0.0;
-      }
-      const double* bp = Bs + kc * 4 + t + (size_t)ldb * (col0 + g);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        // (k-steps past k_hi multiply zeros: av = 0 there and the B rows stay inside the padded operand)
-#pragma unroll
-        for (int nb = 0; nb < NBMAX; ++nb)
-          if (nb < nbt) dmma(acc[nb][0], acc[nb][1], av[u], bp[4 * u + (size_t)ldb * 8 * nb]);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) av[u] = an[u];
+      for (int nb = 0; nb < NBMAX; ++nb)
+        dmma(acc[nb][0], acc[nb][1], av[u], bp[4 * u + (size_t)ldb * 8 * nb]);
     }
     double trp = 0.0;
 #pragma unroll
@@ -128,7 +124,7 @@ __device__ __noinline__ void dec_pass(const double* __restrict__ C, int a, const
       for (int h = 0; h < 2; ++h) {
         const int n = col0 + nb * 8 + 2 * t + h;
         const double v = acc[nb][h];
-        if (nb < nbt && iv) {
+        if (iv) {
           if (n < r_tr) trp = fma(v, Bs[i + (size_t)ldb * n], trp);
           else if (n >= xoff && n < xoff + K) Yp[(size_t)ldb * (ks * K + (n - xoff)) + i] = v;
         }
@@ -148,7 +144,7 @@ struct DecGramTask {
   int mb, k_lo, k_hi;  // k_hi <= k_lo: no task for this warp
 };
 __device__ __forceinline__ DecGramTask dec_gram_task(int nm, int a, int& kparts) {
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int warp = dec_warp(), nw = blockDim.x >> 5;
   const int nmb = (nm + 7) >> 3, nk = (a + 3) >> 2;
   kparts = nw / nmb;
   kparts = kparts < 1 ? 1 : (kparts > 8 ? 8 : kparts);
@@ -166,7 +162,7 @@ __device__ __forceinline__ DecGramTask dec_gram_task(int nm, int a, int& kparts)
 __device__ __noinline__ void dec_gram(const DecGramTask tk, const double* smbase, const int* aoff, int nm,
                                          const double* B, int ldb, int K, int nsum, int bstride, double* Qp) {
   if (tk.k_hi <= tk.k_lo) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = dec_warp();
   const int g = lane >> 2, t = lane & 3;
   const int m = tk.mb * 8 + g;
   const bool mv = m < nm, bv = g < K;
@@ -271,7 +267,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
   __shared__ int s_rk, s_reorth;
   __shared__ double s_dev;
   const int a = p.a, r = p.r, ldb = p.ldb;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = dec_warp(), nw = blockDim.x >> 5;
   const int bcols = dec_bcols(r, K);
   const int ksplit = p.ksplit;
   double* Bs = sm;                                     // [U | X | 0]
@@ -522,7 +518,13 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
     }
     // Y = C X (k-range partials); the first pass also carries C U for the trace
     if (boot) {
-      dec_pass<5>(p.C, a, Bs, ldb, 0, (r + K + 7) >> 3, r, r, K, ksplit, Yp, trpart);
+      switch ((r + K + 7) >> 3) {  // (one instantiation runs; the others cost no instruction fetch)
+        case 1: dec_pass<1>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
+        case 2: dec_pass<2>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
+        case 3: dec_pass<3>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
+        case 4: dec_pass<4>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
+        default: dec_pass<5>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
+      }
       __syncthreads();
       // trace(G) = trace(C) - trace(U^T C U), partials in task order
       const int ntask = ((a + 7) >> 3) * ksplit;
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
       if (!(sqrt(trace) > delta) || kcap == 0) state = 1;  // everything fits under delta: rank 0
       DEC_T(1)
     } else {
-      dec_pass<1>(p.C, a, Bs, ldb, r, 1, 0, r, K, ksplit, Yp, nullptr);
+      dec_pass<1>(p.C, a, Bs, ldb, r, 0, r, K, ksplit, Yp, nullptr);
       __syncthreads();
       DEC_T(6)
     }
