@@ -166,6 +166,7 @@ struct ttg_ctx {
   ttg::EigResult* h_eig = nullptr;
   ttg::EigResult* h_eiglog = nullptr;  // pinned: per-mode results of a speculative sweep + its flag
   int64_t spec_sweeps = 0, spec_redone = 0;
+  bool spec_active = false;  // a speculative sweep has k_decide modes in flight (fetch_eig_result polls their flag)
   double* h_scal = nullptr;
   ttg::StarStats* h_stats = nullptr;
   // per-kernel accounting (launches, algorithmic bytes/flops always; event
@@ -209,6 +210,8 @@ struct ttg_tt {
   std::vector<int> mode_hint;
   // speculative sweeps (ttg.cu sweep()): sweeps to sit out after a rejected guess, and its growth
   int spec_wait = 0, spec_hold = 0;
+  std::vector<int> hint_prev;  // mode_hint after the sweep before the last one
+  int hint_repeats = 0;        // consecutive sweeps whose per-mode ranks repeated
   uint64_t gen = next_gen();  // bumped whenever the cores may change (caches keyed on it)
   static uint64_t next_gen() {
     static std::atomic<uint64_t> g{0};
@@ -1083,6 +1086,24 @@ bool pcp_from_c(ttg_ctx* c, const Src& s, int64_t n, const double* U, int r_old,
   return did;
 }
 
+// Thrown inside a speculative sweep (sweep()) once the device flag says a guess was wrong.
+struct SpecRejected {};
+
+// Eigen result + trace(C) to the host (one stream synchronisation).  Inside a
+// speculative sweep the flag of the earlier k_decide modes rides along: a mode
+// that reads its result on the host must not go on to its fallback solvers on
+// operands a wrong guess has turned into garbage.
+void fetch_eig_result(ttg_ctx* c) {
+  c->d2h += sizeof(EigResult) + sizeof(double);
+  CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_scal + 8, c->scal.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  int* hflag = reinterpret_cast<int*>(c->h_eiglog + TTG_MAX_CORES);
+  if (c->spec_active)
+    CK(cudaMemcpyAsync(hflag, c->specflag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->spec_active && *hflag) throw SpecRejected{};
+}
+
 // ---- eigen-solve -------------------------------------------------------------
 // factor == 0: G is the residual Gram -> tridiagonal solver (k_syev).
 // factor == 1: G holds the TSQR factor T -> one-sided Jacobi on T^T (k_jacobi_eig).
@@ -1143,10 +1164,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
         prof_begin(c, nm, 16.0 * a * a, 2.0 * a * a * K);
         launch_k(c, kern, 1, ttg::kSubThreads, smem_s, sa);
         post_launch(c);
-        c->d2h += sizeof(EigResult) + sizeof(double);
-        CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(c->h_scal + 8, c->scal.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        fetch_eig_result(c);
         done = c->h_eig->converged != 0;
         if (std::getenv("TTG_DEBUG"))
           std::fprintf(stderr, "[ttg] eig_top K=%d a=%d conv=%d iters=%d rank=%d jac=%lld cycles copy=%lld init=%lld qr=%lld iter=%lld gx=%lld h=%lld eig=%lld res=%lld\n",
@@ -1260,10 +1278,7 @@ EigResult eig(ttg_ctx* c, int a, long long kmax, const double* delta_src, double
     post_launch(c);
   }
   if (!fast_done) {
-    c->d2h += sizeof(EigResult) + sizeof(double);
-    CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->h_scal + 8, c->scal.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    fetch_eig_result(c);
   }
   EigResult r = *c->h_eig;
   if (std::getenv("TTG_DEBUG"))
@@ -1418,10 +1433,7 @@ void decide_launch(ttg_ctx* c, int a, int r_old, const double* Upad, double* out
   post_launch(c);
 }
 EigResult eig_fetch(ttg_ctx* c) {
-  c->d2h += sizeof(EigResult) + sizeof(double);
-  CK(cudaMemcpyAsync(c->h_eig, c->eigres.p, sizeof(EigResult), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->h_scal + 8, c->scal.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  fetch_eig_result(c);
   return *c->h_eig;
 }
 
@@ -2102,9 +2114,16 @@ struct SpecState {
   std::vector<int64_t> old_ranks;
   std::vector<int> hints_before;
 };
-struct SpecRejected {};
-
 SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm, SpecState& st);
+
+// Guesses are only worth making for a train whose per-mode ranks repeat: a wrong
+// guess costs a second sweep.  hint_repeats counts the consecutive sweeps that
+// kept the same number of directions in every mode as the sweep before.
+void note_ranks(ttg_tt* tt) {
+  if (tt->mode_hint == tt->hint_prev && !tt->mode_hint.empty()) ++tt->hint_repeats;
+  else tt->hint_repeats = 0;
+  tt->hint_prev = tt->mode_hint;
+}
 
 SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm) {
   SpecState st;
@@ -2118,11 +2137,15 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
   };
   try {
     SweepOut out = sweep_impl(c, tt, Y, b, o, nm, st);
-    if (st.any_spec) tt->spec_hold = 0;
+    c->spec_active = false;
+    if (st.any_spec && tt->spec_hold > 0) --tt->spec_hold;  // (trust returns one verified sweep at a time)
+    note_ranks(tt);
     return out;
   } catch (const SpecRejected&) {
+    c->spec_active = false;
     undo();
   } catch (const TtgError&) {
+    c->spec_active = false;
     // launches sized by a wrong guess may fail on their own (a solver that does
     // not converge on garbage): only a failure of the synchronous sweep counts
     if (!st.any_spec) throw;
@@ -2132,7 +2155,9 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
   SweepOpts o2 = o;
   o2.speculate = false;
   SpecState st2;
-  return sweep_impl(c, tt, Y, b, o2, nm, st2);
+  SweepOut out = sweep_impl(c, tt, Y, b, o2, nm, st2);
+  note_ranks(tt);
+  return out;
 }
 
 SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOpts& o, Norms& nm, SpecState& st) {
@@ -2148,6 +2173,7 @@ SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const Sw
   // A train whose last guesses were rejected sits out a growing number of sweeps
   // (1, 3, 7, 8 ...): alternating rank patterns must not pay for two sweeps every time.
   bool spec_on = o.speculate && !o.bootstrap && !std::getenv("TTG_NO_SPEC");
+  if (spec_on && tt->hint_repeats < 1) spec_on = false;  // the last two sweeps did not agree: no guess
   if (spec_on && tt->spec_wait > 0) {
     --tt->spec_wait;
     spec_on = false;
@@ -2258,6 +2284,7 @@ SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const Sw
           er.converged = 1;
           spec_mode[i] = 1;
           any_spec = true;
+          c->spec_active = true;
           speculated = true;
         } else {
           er = eig_fetch(c);
@@ -2463,6 +2490,64 @@ bool can_fuse_proj(const ttg_ctx* c, const Src& s, int64_t n_i, int64_t r_i, int
 // Projection of Y through the train's current cores (projection-only fusion
 // plan, can_fuse_proj).  cache=true keeps the materialised intermediates (c->scur) and the
 // coefficients (c->scoeffs) for reuse by a following TT-ICE* sweep.
+// The last modes of a chain in one launch (k_project_tail) once an observation's
+// unfolding fits shared memory: returns the coefficient block, or null when the
+// tail does not qualify at mode i (the per-mode kernels then carry on).
+const double* project_tail(ttg_ctx* c, const ttg_tt* tt, const Src& src, int i, int64_t b, bool cache) {
+  const int d = tt->d, nm = d - i;
+  if (std::getenv("TTG_NO_TAIL") || src.Psi || nm < 2 || nm > ttg::kTailMaxModes || b <= 0) return nullptr;
+  ttg::TailArgs ta{};
+  ta.X = src.S;
+  ta.nm = nm;
+  long long cols = src.Ls / tt->modes[i] / b, rl = src.r;
+  if (cols * b * tt->modes[i] != src.Ls) return nullptr;
+  double fma_per_obs = 0.0;
+  long long obuf = 1;
+  for (int t = 0; t < nm; ++t) {
+    const long long n = tt->modes[i + t], rr = tt->ranks[i + t + 1];
+    if (t > 0) {
+      if (cols % n) return nullptr;
+      cols /= n;
+    }
+    if (rl * n > INT32_MAX || rr * cols > INT32_MAX) return nullptr;
+    ta.core[t] = tt->cores[i + t].as<double>();
+    ta.rows[t] = (int)(rl * n);
+    ta.rr[t] = (int)rr;
+    ta.cols[t] = (int)cols;
+    fma_per_obs += (double)rl * n * rr * cols;
+    obuf = std::max(obuf, rr * cols);
+    rl = rr;
+  }
+  if (ta.cols[nm - 1] != 1 || fma_per_obs > 2e6) return nullptr;
+  obuf = (obuf + 1) & ~1ll;
+  ta.obuf = (int)obuf;
+  long long ucap = 1;
+  for (int t = 0; t < nm; ++t) ucap = std::max(ucap, (long long)ttg::tail_ld(ta.rows[t]) * ta.rr[t]);
+  const size_t smem = sizeof(double) * ((size_t)ttg::tail_ld(ta.rows[0]) * ta.cols[0] + 2 * (size_t)obuf + (size_t)ucap + 8);
+  if (smem > dyn_smem_cap((const void*)ttg::k_project_tail)) return nullptr;
+  for (int t = 0; t < nm; ++t) {
+    const size_t bytes = sizeof(double) * (size_t)std::max<long long>((long long)ta.rr[t] * ta.cols[t] * b, 1);
+    if (t + 1 < nm) {
+      if (cache) {
+        c->scur[i + t + 1].ensure(bytes);
+        ta.out[t] = c->scur[i + t + 1].as<double>();
+        c->stat_has[i + t + 1] = true;
+      } else {
+        ta.out[t] = nullptr;
+      }
+    } else {
+      DevBuf& dst = cache ? c->scoeffs : c->coeffs;
+      dst.ensure(bytes);
+      ta.out[t] = dst.as<double>();
+    }
+  }
+  kernel_occupancy((const void*)ttg::k_project_tail, ttg::k_project_tail, ttg::kTailThreads, smem);
+  prof_begin(c, "k_project_tail", 8.0 * ta.rows[0] * ta.cols[0] * b, 2.0 * fma_per_obs * b);
+  launch_k(c, ttg::k_project_tail, (unsigned)b, ttg::kTailThreads, smem, ta);
+  post_launch(c);
+  return ta.out[nm - 1];
+}
+
 const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64_t b, bool cache, Norms& nm) {
   const int d = tt->d;
   const int64_t S = prod(tt->modes);
@@ -2478,6 +2563,8 @@ const double* project_chain(ttg_ctx* c, const ttg_tt* tt, const double* Y, int64
     const int64_t r = tt->ranks[i + 1];
     const double* Ui = tt->cores[i].as<double>();
     const int64_t rows = src.Psi ? src.As * n_i : src.r * n_i;
+    if (!(nm.pending && src.S == nm.Y))
+      if (const double* cf = project_tail(c, tt, src, i, b, cache)) return cf;
     if (i + 1 < d) {
       const int64_t n_next = tt->modes[i + 1];
       const int64_t rr = tt->ranks[i + 2];
@@ -2963,7 +3050,7 @@ static int ctx_init(ttg_ctx* c, int device) {
         (const void*)ttg::k_gram_resid<2, 4, true, true>, (const void*)ttg::k_gram_resid<3, 6, true, true>,
         (const void*)ttg::k_gram_resid<4, 8, true, true>, (const void*)ttg::k_project<true, true>,
         (const void*)ttg::k_project<true, false>, (const void*)ttg::k_project<false, false>,
-        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt<4>, (const void*)ttg::k_syev_bt<8>, (const void*)ttg::k_syev_top<2>, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>, (const void*)ttg::k_decide<2>, (const void*)ttg::k_decide<4>,
+        (const void*)ttg::k_syev, (const void*)ttg::k_sytrd_grid, (const void*)ttg::k_syev_bt<4>, (const void*)ttg::k_syev_bt<8>, (const void*)ttg::k_syev_top<2>, (const void*)ttg::k_syev_top<4>, (const void*)ttg::k_syev_top<8>, (const void*)ttg::k_decide<2>, (const void*)ttg::k_decide<4>, (const void*)ttg::k_project_tail,
         (const void*)ttg::k_jacobi_eig, (const void*)ttg::k_append, (const void*)ttg::k_tsqr_local,
         (const void*)ttg::k_tsqr_combine, (const void*)ttg::k_make_frags, (const void*)ttg::k_sumsq_obs,
         (const void*)ttg::k_sumsq_finalize, (const void*)ttg::k_tiles_to_obs, (const void*)ttg::k_pad_core,

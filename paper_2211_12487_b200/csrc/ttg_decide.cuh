@@ -260,6 +260,8 @@ __device__ __noinline__ double dec_chol_transform(const double* S, const double*
 template <int K>
 __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
   griddep_wait();
+  // an earlier mode of this speculative sweep already disagreed: its operands are garbage
+  if (p.expect >= 0 && *reinterpret_cast<volatile int*>(p.spec_flag) != 0) return;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[64], resp[16 * 4], trpart[32 * kDecMaxSplit];
   __shared__ double Qs[32 * 8], Ms[16], Wvs[16], Hs[16], Ss[16], thetas[4];

@@ -701,4 +701,91 @@ __global__ void __launch_bounds__(256) k_tall_u(const double* __restrict__ R, in
   for (int i = tid; i < a; i += blockDim.x) u[i] *= f;
 }
 
+// ---------------------------------------------------------------------------
+// The last modes of a projection chain (tt_project, tensor_train.cpp:195-226) in
+// ONE launch.  Once an observation's unfolding fits shared memory (cfg3: from
+// mode 5 on, 192 x 64 doubles), each remaining mode is a handful of
+// microseconds of arithmetic behind a launch of its own; here one CTA owns one
+// observation and walks the modes in place: stage t computes
+// core_t^T (rows_t x cols_t block) -> rr_t x cols_t, which, read as
+// (rr_t n_{t+1}) x (cols_t / n_{t+1}), is the next stage's input (the same flat
+// buffer, first index fastest).  Intermediate unfoldings are also written to
+// global memory when the caller keeps them (TT-ICE* reuses the statistics
+// chain's intermediates in the sweep).  Plain DFMA, fixed summation order.
+// ---------------------------------------------------------------------------
+constexpr int kTailMaxModes = 6;
+constexpr int kTailThreads = 512;
+struct TailArgs {
+  const double* X;  // rows[0] x (cols[0] * b), observation slowest
+  int nm;
+  const double* core[kTailMaxModes];  // (rows[t]) x rr[t], ld rows[t]
+  int rows[kTailMaxModes], rr[kTailMaxModes], cols[kTailMaxModes];
+  double* out[kTailMaxModes];  // rr[t] x (cols[t] * b) or null (the last one is the coefficient block)
+  int obuf;                    // doubles of one ping-pong output buffer (max rr[t] cols[t])
+};
+__host__ __device__ inline int tail_ld(int rows) { return (rows + 3 + 15) / 16 * 16 + 4; }  // >= rows + 3, = 4 mod 16
+__global__ void __launch_bounds__(kTailThreads) k_project_tail(TailArgs p) {
+  griddep_wait();
+  extern __shared__ __align__(16) double sm[];
+  const long long o = blockIdx.x;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform: no WARPSYNC per DMMA
+  const int g = lane >> 2, tq = lane & 3;
+  // shared memory: the observation's block and the current core with leading
+  // dimensions = 4 (mod 16) (the m8n8k4 fragment loads of a half-warp then hit
+  // 16 distinct banks) and zero rows up to a multiple of 4; two ping-pong
+  // output buffers (flat: the next stage reads them with its own row count)
+  const int rows0 = p.rows[0], cols0 = p.cols[0], ld0 = tail_ld(rows0);
+  double* xin = sm;
+  double* dstb[2] = {sm + (size_t)ld0 * cols0, nullptr};
+  dstb[1] = dstb[0] + p.obuf;
+  double* Us = dstb[1] + p.obuf;
+  {
+    const double* x = p.X + o * (long long)rows0 * cols0;
+    // (cp.async: every copy of the block is in flight before the first wait)
+    for (int c = warp; c < cols0; c += nw)
+      for (int k = lane; k < ld0; k += 32)
+        cp_async8(xin + k + (size_t)ld0 * c, x + (k < rows0 ? k : 0) + (size_t)rows0 * c, k < rows0);
+  }
+  const double* src = xin;
+  int lds = ld0;
+  for (int t = 0; t < p.nm; ++t) {
+    const int rows = p.rows[t], rr = p.rr[t], cols = p.cols[t], ldu = tail_ld(rows);
+    const double* __restrict__ U = p.core[t];
+    for (int j = warp; j < rr; j += nw)
+      for (int k = lane; k < ldu; k += 32)
+        cp_async8(Us + k + (size_t)ldu * j, U + (k < rows ? k : 0) + (size_t)rows * j, k < rows);
+    cp_async_commit();
+    cp_async_wait_0();
+    __syncthreads();
+    double* dst = dstb[t & 1];
+    double* gl = p.out[t] ? p.out[t] + o * (long long)rr * cols : nullptr;
+    // out (rr x cols) = U^T src on DMMA: one 8 x 8 block per warp task
+    const int nmb = (rr + 7) >> 3, nnb = (cols + 7) >> 3, nk = (rows + 3) >> 2;
+    for (int task = warp; task < nmb * nnb; task += nw) {
+      const int mb = task % nmb, nb = task / nmb;
+      const int m = mb * 8 + g, n = nb * 8 + g;
+      const double* ap = Us + (size_t)ldu * (m < rr ? m : rr - 1) + tq;       // A[m][k] = U[k][m]
+      const double* bp = src + (size_t)lds * (n < cols ? n : cols - 1) + tq;  // B[k][n] = src[k][n]
+      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+      int ks = 0;
+      for (; ks + 1 < nk; ks += 2) {
+        dmma(c0, c1, ap[4 * ks], bp[4 * ks]);
+        dmma(e0, e1, ap[4 * ks + 4], 4 * ks + 4 + tq < rows ? bp[4 * ks + 4] : 0.0);
+      }
+      if (ks < nk) dmma(c0, c1, ap[4 * ks], 4 * ks + tq < rows ? bp[4 * ks] : 0.0);
+      c0 += e0;
+      c1 += e1;
+      const int jo = mb * 8 + g, co = nb * 8 + 2 * tq;  // C[m = g][n = 2 tq, 2 tq + 1]
+      if (jo < rr) {
+        if (co < cols) { dst[jo + (size_t)rr * co] = c0; if (gl) gl[jo + (size_t)rr * co] = c0; }
+        if (co + 1 < cols) { dst[jo + (size_t)rr * (co + 1)] = c1; if (gl) gl[jo + (size_t)rr * (co + 1)] = c1; }
+      }
+    }
+    __syncthreads();
+    src = dst;  // rr x cols, read by the next stage as (rr n) x (cols / n): the same flat buffer
+    lds = t + 1 < p.nm ? p.rows[t + 1] : 1;
+  }
+}
+
 }  // namespace ttg
