@@ -361,6 +361,41 @@ def test_project_fixed_cores_high_rank(ctx, R):
     assert np.linalg.norm(cg - cr) <= TOL * np.linalg.norm(cr)
 
 
+@pytest.mark.parametrize("modes,ranks,b", [
+    ((5, 3, 7, 2, 3), (3, 5, 4, 3, 2), 3),        # odd row counts (rows % 4 != 0), odd column counts
+    ((6, 4, 3, 5, 2, 2, 3), (4, 6, 5, 7, 3, 2, 2), 5),  # six modes in the tail
+    ((9, 8, 8, 8), (7, 19, 23, 11), 17),          # ranks 17-23 (r8 padding), 64-column blocks
+    ((2, 2, 2), (2, 3, 1), 1),                    # tiny: the whole chain after the first mode
+])
+def test_project_chain_tail_shapes(ctx, modes, ranks, b, monkeypatch):
+    """The last modes of tt_project in one launch (k_project_tail, tensor_train.cpp:195-226):
+    shapes the m8n8k4 tiling has to pad or clamp, against the reference and against the
+    per-mode kernels (TTG_NO_TAIL=1), coefficients within 1e-10 relative."""
+    rng = np.random.default_rng(1000 + len(modes))
+    r = [1] + list(ranks)
+    cores = []
+    for i, n in enumerate(modes):
+        assert r[i] * n >= r[i + 1]
+        q, _ = np.linalg.qr(rng.standard_normal((r[i] * n, r[i + 1])))
+        cores.append(np.reshape(q, (r[i], n, r[i + 1]), order="F"))
+    cores.append(np.reshape(rng.standard_normal((r[-1], 1)), (r[-1], 1, 1), order="F"))
+    tg = TensorTrain.upload(cores, ortho_count=len(modes), batch_boundaries=[1], ctx=ctx)
+    tr = O.TensorTrain([O.TTCore(np.asfortranarray(c)) for c in cores], len(modes), [1])
+    y = np.asfortranarray(rng.standard_normal(tuple(modes) + (b,)))
+    cr = REF.tt_project(tr, y)
+    launches0 = ctx.launch_count
+    cg = tt_project(tg, y)
+    n_tail = ctx.launch_count - launches0
+    monkeypatch.setenv("TTG_NO_TAIL", "1")
+    launches0 = ctx.launch_count
+    cm = tt_project(tg, y)
+    n_modes = ctx.launch_count - launches0
+    assert n_tail < n_modes, "k_project_tail did not take over the tail of this chain"
+    assert cg.shape == cr.shape
+    assert np.linalg.norm(cg - cr) <= TOL * np.linalg.norm(cr)
+    assert np.linalg.norm(cg - cm) <= TOL * np.linalg.norm(cr)
+
+
 def test_bootstrap_tall_unfolding_full_solver(ctx):
     """a = 2048 rows: the block-8 subspace vectors no longer fit shared memory
     (2 a 8 doubles > the opt-in limit), so the solver goes straight from the
