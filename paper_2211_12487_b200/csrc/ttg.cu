@@ -2296,6 +2296,16 @@ SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const Sw
           std::fprintf(stderr, "[ttg] decide cycles init=%lld pass1=%lld tgram=%lld zupd=%lld hs+rr=%lld rows+dec=%lld pass=%lld final=%lld\n",
                        er.t_phase[0] & 0xffffffffll, er.t_phase[0] >> 32, er.t_phase[1] & 0xffffffffll, er.t_phase[1] >> 32,
                        er.t_phase[2] & 0xffffffffll, er.t_phase[2] >> 32, er.t_phase[3] & 0xffffffffll, er.t_phase[3] >> 32);
+        if (!er.converged && er.sweeps < ttg::kDecIters && decide_block(hint) == 2 && decide_applies(c, false, a, r_old, 2)) {
+          // more directions than a block of 2 holds (not: no convergence): a block of 4 from the same C before the
+          // explicit chain (whose block attempts re-read the a x a Gram from L2 per iteration)
+          const bool alias4 = (Upad == tt->cores[i].p);
+          tt->cores[i].ensure(sizeof(double) * (size_t)a * (r_old + 3), /*keep=*/alias4, c->stream);
+          if (alias4) Upad = tt->cores[i].as<double>();
+          decide_launch(c, (int)a, (int)r_old, Upad, tt->cores[i].as<double>(), kmax, dsrc, dmult, 2, -1,
+                        c->specflag.as<int>(), nullptr);
+          er = eig_fetch(c);
+        }
         if (er.converged) {
           decided = true;
         } else {  // more directions than the block holds: the explicit chain from the same C

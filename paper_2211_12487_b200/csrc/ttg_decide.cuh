@@ -1,7 +1,7 @@
 // ttg_decide.cuh — one launch per mode for the common case of the update sweep:
 // "old basis U (a x r), raw Gram C of the unfolding, a few new directions".
 //
-// Replaces, for a <= 256 and r <= 32, the chain
+// Replaces, for a <= 320 and r <= 40, the chain
 //   k_pcp | (k_build_q, 2 x k_dgemm, k_symmetrize_trace)  ->  k_syev_top  ->  k_append
 // (svd_trunc truncated_svd.cpp:29-94 on the residual of tt_ice.cpp:34-41, then
 // append_directions update_common.hpp:19-36) by ONE single-CTA kernel that never
@@ -36,10 +36,10 @@
 namespace ttg {
 
 constexpr int kDecThreads = 512;
-constexpr int kDecMaxA = 256;
-constexpr int kDecMaxR = 32;
-constexpr int kDecIters = 24;
-constexpr int kDecMaxSplit = 4;
+constexpr int kDecMaxA = 320;
+constexpr int kDecMaxR = 40;
+constexpr int kDecIters = 10;  // a spectrum without a gap below the kept directions belongs to the full solver
+constexpr int kDecMaxSplit = 5;  // ceil(kDecMaxA / 64)
 
 struct DecideArgs {
   const double* C;  // a x a raw Gram (symmetric, both triangles), global
@@ -263,9 +263,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
   // an earlier mode of this speculative sweep already disagreed: its operands are garbage
   if (p.expect >= 0 && *reinterpret_cast<volatile int*>(p.spec_flag) != 0) return;
   extern __shared__ __align__(16) double sm[];
-  __shared__ double red[64], resp[16 * 4], trpart[32 * kDecMaxSplit];
-  __shared__ double Qs[32 * 8], Ms[16], Wvs[16], Hs[16], Ss[16], thetas[4];
-  __shared__ int aoff[48];
+  __shared__ double red[64], resp[16 * 4], trpart[(kDecMaxA / 8) * kDecMaxSplit];
+  __shared__ double Qs[48 * 8], Ms[16], Wvs[16], Hs[16], Ss[16], thetas[4];
+  __shared__ int aoff[64];
   __shared__ int s_rk, s_reorth;
   __shared__ double s_dev;
   const int a = p.a, r = p.r, ldb = p.ldb;
@@ -295,12 +295,12 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
     const double* src = p.U + (size_t)a * (j < r ? j : 0);
     for (int i = lane; i < ldb; i += 32) col[i] = (j < r && i < a) ? __ldg(src + i) : 0.0;
   }
-  // (m < 32: the columns of U; 32 + m: [X | Z]; 40 + m: XW)
-  for (int m = tid; m < 48; m += blockDim.x)
-    aoff[m] = m < 32 ? ldb * (m < r ? m : 0)
-            : m < 32 + K ? (int)(X - sm) + ldb * (m - 32)
-            : m < 32 + 2 * K ? (int)(Zs - sm) + ldb * (m - 32 - K)
-            : m >= 40 && m < 40 + K ? (int)(XW - sm) + ldb * (m - 40) : 0;
+  // (m < 48: the columns of U; 48 + m: [X | Z]; 56 + m: XW)
+  for (int m = tid; m < 64; m += blockDim.x)
+    aoff[m] = m < 48 ? ldb * (m < r ? m : 0)
+            : m < 48 + K ? (int)(X - sm) + ldb * (m - 48)
+            : m < 48 + 2 * K ? (int)(Zs - sm) + ldb * (m - 48 - K)
+            : m >= 56 && m < 56 + K ? (int)(XW - sm) + ldb * (m - 56) : 0;
   double tpart = 0.0;
   for (int i = tid; i < a; i += blockDim.x) tpart += __ldg(p.C + i + (size_t)a * i);
   const double trC = block_sum_all(tpart, red);
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
     __syncthreads();
     DEC_T(3)
     // [X | Z]^T Z: H = X^T Z, S = Z^T Z in one DMMA reduction
-    dec_gram(tkXZ, sm, aoff + 32, 2 * K, Zs, ldb, K, 1, 0, Qp);
+    dec_gram(tkXZ, sm, aoff + 48, 2 * K, Zs, ldb, K, 1, 0, Qp);
     __syncthreads();
     if (warp == 0) {
       dec_gram_sum(Qp, 2 * K, K, kpXZ, Qs, lane, 32);
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
     DEC_T(5)
     if (state) { ++it; break; }
     if (s_reorth) {  // ill-conditioned single pass (boot / early rounds): CholQR again
-      dec_gram(tkX, sm, aoff + 32, K, X, ldb, K, 1, 0, Qp);
+      dec_gram(tkX, sm, aoff + 48, K, X, ldb, K, 1, 0, Qp);
       __syncthreads();
       if (warp == 0) {
         dec_gram_sum(Qp, K, K, kpX, Qs, lane, 32);
@@ -525,7 +525,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
         case 2: dec_pass<2>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
         case 3: dec_pass<3>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
         case 4: dec_pass<4>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
-        default: dec_pass<5>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
+        case 5: dec_pass<5>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
+        default: dec_pass<6>(p.C, a, Bs, ldb, 0, r, r, K, ksplit, Yp, trpart); break;
       }
       __syncthreads();
       // trace(G) = trace(C) - trace(U^T C U), partials in task order
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
       __syncthreads();
       dec_gram_sum(Qp, r, K, kpU, Qs, tid, blockDim.x);
       __syncthreads();
-      dec_gram(tkX, sm, aoff + 40, K, XW, ldb, K, 1, 0, Qp);
+      dec_gram(tkX, sm, aoff + 56, K, XW, ldb, K, 1, 0, Qp);
       __syncthreads();
       if (tid == 0) {
         double dev = dev_old;
