@@ -413,8 +413,10 @@ void allgather(ttg_ctx* c, const double* send, double* recv, size_t n) {
 // ---- norms ---------------------------------------------------------------
 // per-observation |y_o|^2 -> c->on2 (b), total -> c->scal[0] (global)
 void obs_norms(ttg_ctx* c, const double* Y, long long S, int b) {
-  int nchunk = (int)std::max<long long>(1, std::min<long long>((S + 65535) / 65536,
-                                                                (long long)c->num_sms * 8 / std::max(1, b) + 1));
+  // (16 K doubles per CTA at most, and enough CTAs to fill the device several times over:
+  // with 64 K-double chunks a 100-observation batch of 0.8 MB slabs ran on 200 CTAs at 2.4 TB/s)
+  int nchunk = (int)std::max<long long>(1, std::min<long long>((S + 16383) / 16384,
+                                                                (long long)c->num_sms * 16 / std::max(1, b) + 1));
   c->sumsq_part.ensure(sizeof(double) * (size_t)nchunk * b);
   c->on2.ensure(sizeof(double) * b);
   c->scal.ensure(sizeof(double) * 16);
@@ -2174,6 +2176,17 @@ SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const Sw
   // (1, 3, 7, 8 ...): alternating rank patterns must not pay for two sweeps every time.
   bool spec_on = o.speculate && !o.bootstrap && !std::getenv("TTG_NO_SPEC");
   if (spec_on && tt->hint_repeats < 1) spec_on = false;  // the last two sweeps did not agree: no guess
+  if (spec_on) {
+    // a guess saves one host read per k_decide mode and risks a second sweep: only
+    // when (nearly) every mode of the train is one (judged on the current ranks)
+    int eligible = 0;
+    for (int i = 0; i < tt->d; ++i) {
+      const int hint = i < (int)tt->mode_hint.size() ? tt->mode_hint[i] : -1;
+      const int64_t a = tt->ranks[i] * tt->modes[i];
+      if (!(a & 1) && decide_applies(c, false, a, tt->ranks[i + 1], hint)) ++eligible;
+    }
+    if (eligible + 2 < tt->d) spec_on = false;
+  }
   if (spec_on && tt->spec_wait > 0) {
     --tt->spec_wait;
     spec_on = false;

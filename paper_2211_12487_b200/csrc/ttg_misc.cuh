@@ -55,11 +55,26 @@ __global__ void k_sumsq_obs(const double* __restrict__ Y, long long S, int nchun
   if ((((uintptr_t)(y + b)) & 15) == 0) {
     long long n2 = (e - b) / 2;
     const double2* y2 = reinterpret_cast<const double2*>(y + b);
-    for (long long i = threadIdx.x; i < n2; i += blockDim.x) {
+    // four independent loads and accumulators per thread and round (fixed order)
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    long long i = threadIdx.x;
+    for (; i + 3 * (long long)blockDim.x < n2; i += 4 * (long long)blockDim.x) {
+      const double2 v0 = y2[i], v1 = y2[i + blockDim.x], v2 = y2[i + 2 * blockDim.x], v3 = y2[i + 3 * blockDim.x];
+      s = fma(v0.x, v0.x, s);
+      s = fma(v0.y, v0.y, s);
+      s1 = fma(v1.x, v1.x, s1);
+      s1 = fma(v1.y, v1.y, s1);
+      s2 = fma(v2.x, v2.x, s2);
+      s2 = fma(v2.y, v2.y, s2);
+      s3 = fma(v3.x, v3.x, s3);
+      s3 = fma(v3.y, v3.y, s3);
+    }
+    for (; i < n2; i += blockDim.x) {
       double2 v = y2[i];
       s = fma(v.x, v.x, s);
       s = fma(v.y, v.y, s);
     }
+    s = (s + s1) + (s2 + s3);
     for (long long i = b + 2 * n2 + threadIdx.x; i < e; i += blockDim.x) s = fma(y[i], y[i], s);
   } else {
     for (long long i = b + threadIdx.x; i < e; i += blockDim.x) s = fma(y[i], y[i], s);
