@@ -340,7 +340,7 @@ def test_upload_roundtrip_and_update(ctx):
 def test_project_fixed_cores_high_rank(ctx, R):
     """tt_project through pre-built orthonormal cores with bond ranks up to 128
     (BASELINE configs[4] companion sweep shapes at batch 2): the r > 34 paths
-    (k_project_tma, fused plain GEMMs on cuBLAS, the fusion cost model)
+    (k_project_ws with streamed W fragments, the DMMA GEMM, the fusion cost model)
     against the oracle, coefficients within 1e-10 relative."""
     modes, b = (8,) * 7, 2
     rng = np.random.default_rng(100 + R)
@@ -415,8 +415,9 @@ def test_bootstrap_tall_unfolding_full_solver(ctx):
 def test_update_large_append_guard_path(ctx):
     """a = 2048 rows, r_old ~ 150 kept directions + ~20 new ones: the appended
     block [U_pad U_R] has a r_new^2 >= 5e7, so its Gram guard runs through
-    cuBLAS DSYRK + the grid deviation reduction (k_gram_dev) and the
-    eigen-solve through cuSOLVER; TT-ICE against the oracle."""
+    the DMMA GEMM + the grid deviation reduction (k_gram_dev) and the
+    eigen-solve through the multi-CTA tridiagonalisation (k_sytrd_grid);
+    TT-ICE against the reference."""
     rng = np.random.default_rng(11)
     basis = np.linalg.qr(rng.standard_normal((2048, 190)))[0]
     spec = np.logspace(0, -1.5, 190)[:, None]
