@@ -25,11 +25,11 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
   __shared__ __align__(16) double cs[kRreObsChunk * RMAX];
   __shared__ double red[2][8];
   double dsum = 0.0, xsum = 0.0;
-  // Persistent blocks: the coefficients of an observation chunk are staged once
-  // per block and reused over all of the block's 256-row tiles (one tile per
-  // block made the block's life ~1 us of streaming behind ~1.5 us of staging
-  // and Phi-row latency).
-  const long long ntiles = (S + blockDim.x - 1) / blockDim.x;
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool live = s < S;
+  double phi[RMAX];
+#pragma unroll
+  for (int k = 0; k < RMAX; ++k) phi[k] = (live && k < r) ? Phi[s + S * k] : 0.0;
   for (int o0 = 0; o0 < m; o0 += kRreObsChunk) {
     const int mo = min(kRreObsChunk, m - o0);
     __syncthreads();
@@ -38,12 +38,6 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
       cs[e] = k < r ? C[k + ldc * (o0 + o)] : 0.0;
     }
     __syncthreads();
-   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long s = tile * (long long)blockDim.x + threadIdx.x;
-    const bool live = s < S;
-    double phi[RMAX];
-#pragma unroll
-    for (int k = 0; k < RMAX; ++k) phi[k] = (live && k < r) ? Phi[s + S * k] : 0.0;
     if (live) {
       // four observations per round: their X loads are issued together (one
       // 8-byte load in flight per thread kept the kernel at ~54 % of HBM: too
@@ -89,7 +83,6 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
         xsum = fma(x, x, xsum);
       }
     }
-   }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
