@@ -4,6 +4,7 @@
 // checkpoint is loaded.
 #pragma once
 #include "ttg_pdl.cuh"
+#include "ttg_kernels.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -103,6 +104,94 @@ __global__ void __launch_bounds__(256) k_rre_partial(const double* __restrict__ 
     }
     part[2 * blockIdx.x] = a;
     part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// The same partial sums on the FP64 tensor pipe (r <= 32).  The DFMA kernel
+// above issues one shared-memory load per two FMAs and its ncu capture shows
+// it waiting on exactly those (short scoreboard 5.5, LSU pipe 44 % busy, 57 %
+// of HBM).  Here a warp owns 32 rows (four m8n8k4 row blocks, its Phi
+// fragments in registers for the whole chunk) and walks the observations
+// eight at a time: 16 DMMAs per 4 coefficient loads, the eight X loads of a
+// lane in flight together.  Coefficients sit in shared memory with a stride
+// = 4 (mod 16), so a half-warp's fragment load hits 16 distinct banks.
+template <int RMAX>
+__global__ void __launch_bounds__(256) k_rre_dmma(const double* __restrict__ Phi, long long S, int r,
+                                                  const double* __restrict__ C, long long ldc, int m,
+                                                  const double* __restrict__ X, long long ldx,
+                                                  double* __restrict__ part) {
+  griddep_wait();
+  constexpr int NJ = RMAX / 4, LDC_S = RMAX + 4;
+  __shared__ __align__(16) double cs[kRreObsChunk * LDC_S];
+  __shared__ double red[2][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long long s_base = blockIdx.x * (long long)blockDim.x + warp * 32;
+  double a[4][NJ];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const long long s = s_base + 8 * q + g;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) a[q][j] = (s < S && 4 * j + t < r) ? Phi[s + S * (4 * j + t)] : 0.0;
+  }
+  double dsum = 0.0, xsum = 0.0;
+  for (int o0 = 0; o0 < m; o0 += kRreObsChunk) {
+    const int mo = min(kRreObsChunk, m - o0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kRreObsChunk * RMAX; e += blockDim.x) {
+      const int o = e / RMAX, k = e - o * RMAX;
+      cs[o * LDC_S + k] = (o < mo && k < r) ? C[k + ldc * (o0 + o)] : 0.0;
+    }
+    __syncthreads();
+    for (int og = 0; og < mo; og += 8) {
+      double x[4][2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const long long s = s_base + 8 * q + g;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int o = og + 2 * t + h;
+          x[q][h] = (s < S && o < mo) ? __ldcs(X + s + ldx * (long long)(o0 + o)) : 0.0;
+        }
+      }
+      double b[NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[j] = cs[(og + g) * LDC_S + 4 * j + t];
+      double acc[4][2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma(acc[q][0], acc[q][1], a[q][j], b[j]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double df = x[q][h] - acc[q][h];  // (masked entries: x = 0 and Phi row or coefficient column = 0)
+          dsum = fma(df, df, dsum);
+          xsum = fma(x[q][h], x[q][h], xsum);
+        }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = dsum;
+    red[1][warp] = xsum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0, v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      u += red[0][w];
+      v += red[1][w];
+    }
+    part[2 * blockIdx.x] = u;
+    part[2 * blockIdx.x + 1] = v;
   }
 }
 
