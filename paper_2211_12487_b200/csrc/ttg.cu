@@ -2112,6 +2112,7 @@ bool can_fuse(const Src& s, int64_t n_i, int64_t r_new, int64_t n_next, int64_t 
 // What a speculative sweep needs to be undone (owned by sweep(), filled by sweep_impl())
 struct SpecState {
   bool any_spec = false;
+  bool spec_on = false;  // replaced cores were kept aside (the train can be handed back as it was)
   std::vector<char> swapped;
   std::vector<int64_t> old_ranks;
   std::vector<int> hints_before;
@@ -2150,7 +2151,16 @@ SweepOut sweep(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const SweepOp
     c->spec_active = false;
     // launches sized by a wrong guess may fail on their own (a solver that does
     // not converge on garbage): only a failure of the synchronous sweep counts
-    if (!st.any_spec) throw;
+    if (!st.any_spec) {
+      // a genuine failure: hand the kept-aside cores back before it propagates
+      for (size_t i = 0; i < st.swapped.size(); ++i)
+        if (st.swapped[i]) std::swap(tt->cores[i], c->corebak[i]);
+      if (st.spec_on && !st.old_ranks.empty()) {
+        tt->ranks = st.old_ranks;
+        tt->mode_hint = st.hints_before;
+      }
+      throw;
+    }
     undo();
   }
   tt->spec_wait = tt->spec_hold;
@@ -2191,6 +2201,7 @@ SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const Sw
     --tt->spec_wait;
     spec_on = false;
   }
+  st.spec_on = spec_on;
   std::vector<char> spec_mode(tt->d, 0);
   std::vector<char>& swapped = st.swapped;
   swapped.assign(tt->d, 0);
