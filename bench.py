@@ -404,6 +404,11 @@ def our_arm(args):
                                     "ms/step with events vs the headline region without them)",
                      "algorithmic_bytes_per_launch": dom["bytes"] / dom["launches"],
                      "algorithmic_flops_per_launch": dom["flops"] / dom["launches"]})
+        if dom["name"].startswith("k_project[a=512"):
+            # the algorithmic flops put this family on the HBM side of the ridge, but it issues the
+            # rank padded to a multiple of 8 (r = 20..24: 25.8 GF = 0.70 ms at 37 TF/s per launch)
+            roof["note"] = ("co-bound: ncu at the bench's clocks shows the FP64 tensor pipe 82 % busy and DRAM "
+                            "traffic 1.00x algorithmic (profiles/r02_stats_ws_r20_full.md, r02_stats_ws_r24_full.md)")
         # kernel-level step roofline: sum over the LAUNCHED kernels of
         # max(bytes/BW, flops/peak) with each kernel's own traffic (how close
         # each launch runs to its own bound; the SURVEY per-increment
