@@ -1656,6 +1656,11 @@ bool project_ws(ttg_ctx* c, const double* X, int a, long long L, const double* W
       if (n_ >= 3) break;
     }
   }
+  if (const char* e = std::getenv("TTG_PWS_KC")) {  // tuning override: k16-steps per stage
+    const int k_ = std::max(1, std::min(std::atoi(e), nks));
+    const int n_ = (int)std::min<size_t>(ttg::kProjStages, cap / (k_ * (box + wch)));
+    if (n_ >= 2) { kc = k_; nst = n_; }
+  }
   if (kc == 0) return false;
   CUtensorMap tm;
   if (!make_tmap(&tm, X, a, L, tc)) return false;
