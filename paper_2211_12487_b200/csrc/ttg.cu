@@ -210,6 +210,7 @@ struct ttg_tt {
   std::vector<int> mode_hint;
   // speculative sweeps (ttg.cu sweep()): sweeps to sit out after a rejected guess, and its growth
   int spec_wait = 0, spec_hold = 0;
+  std::vector<int> decide_off;  // per mode: sweeps for which k_decide is not tried (it did not converge last time)
   std::vector<int> hint_prev;  // mode_hint after the sweep before the last one
   int hint_repeats = 0;        // consecutive sweeps whose per-mode ranks repeated
   uint64_t gen = next_gen();  // bumped whenever the cores may change (caches keyed on it)
@@ -1386,7 +1387,9 @@ int append(ttg_ctx* c, const double* Upad, int a, int r_old, int r_R, double* ou
 // old basis is small and the previous update of this mode kept few directions.
 int decide_block(int hint) { return hint <= 1 ? 2 : 4; }
 bool decide_applies(const ttg_ctx* c, bool has_psi, int64_t a, int64_t r_old, int hint) {
-  if (std::getenv("TTG_NO_DECIDE") || has_psi || hint < 0 || hint > 3) return false;
+  // (a mode that kept nothing last time most likely keeps nothing again: its whole cost is
+  // trace(P C P), which the multi-CTA chain forms faster than one CTA computes C U)
+  if (std::getenv("TTG_NO_DECIDE") || has_psi || hint < (std::getenv("TTG_DECIDE_ZERO") ? 0 : 1) || hint > 3) return false;
   const int K = decide_block(hint);
   if (r_old < 1 || r_old > ttg::kDecMaxR || a > ttg::kDecMaxA || a - r_old < K) return false;
   const void* kern = K == 2 ? (const void*)ttg::k_decide<2> : (const void*)ttg::k_decide<4>;
@@ -2284,7 +2287,10 @@ SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const Sw
       if ((int)tt->mode_hint.size() < d) tt->mode_hint.assign(d, -1);
       const int hint = tt->mode_hint[i];
       // one launch for P C P, the eigen-solve and the append (ttg_decide.cuh)
-      const bool dec = raw && !o.bootstrap && !(a & 1) && decide_applies(c, src.Psi != nullptr, a, r_old, hint);
+      if ((int)tt->decide_off.size() < d) tt->decide_off.assign(d, 0);
+      const bool dec_held = tt->decide_off[i] > 0;
+      if (dec_held) --tt->decide_off[i];
+      const bool dec = raw && !o.bootstrap && !(a & 1) && !dec_held && decide_applies(c, src.Psi != nullptr, a, r_old, hint);
       bool did;
       if (dec) did = syrk(c, src.S, (int)a, L, sel, cpo, sel_frac, tsq);  // C -> c->G
       else did = raw ? gram_raw_src(c, src, n_i, r_old > 0 ? Upad : nullptr, (int)r_old, sel, cpo, sel_frac, tsq)
@@ -2337,7 +2343,8 @@ SweepOut sweep_impl(ttg_ctx* c, ttg_tt* tt, const double* Y, int64_t b, const Sw
         }
         if (er.converged) {
           decided = true;
-        } else {  // more directions than the block holds: the explicit chain from the same C
+        } else {  // more directions than the block holds, or no gap: the explicit chain from the same C
+          if (er.sweeps >= ttg::kDecIters) tt->decide_off[i] = 4;  // (a spectrum without a gap tends to stay one)
           pcp_from_c(c, src, n_i, Upad, (int)r_old, did);
           er = eig(c, (int)a, kmax, dsrc, dmult, 0, std::max(hint, decide_block(hint)));
         }

@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decide(DecideArgs p) {
     EigResult e{};
     for (int q = 0; q < 4; ++q) e.t_phase[q] = (tph[2 * q] & 0xffffffffll) | (tph[2 * q + 1] << 32);
     e.converged = ok ? 1 : 0;
-    e.sweeps = it;
+    e.sweeps = it;  // (kDecIters: no convergence -- the host does not retry with a larger block)
     e.rank = rank;
     e.tail_sq = tail;
     e.delta = delta;
